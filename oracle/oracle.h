@@ -1,0 +1,109 @@
+/*
+ * oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU reference for the hot path of
+ * arxiv 1905.01141 (uplink channel decoding of a pooled C-RAN BBU):
+ * LTE turbo decoding, int16-range fixed-point max-log-MAP, QPP interleaver,
+ * windowed recursions with next-iteration initialisation (NII), CRC24
+ * early termination, hard decision.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
+ * load this library.  The product (paper_1905_01141_b200/, libcrn) never
+ * links, imports or calls it, and shares no code, table or header with it.
+ *
+ * Citations: "PAPER.md:<line>" is /root/reference/PAPER.md (the paper text),
+ * "SPEC.md:<line>" the CPU-program spec written from it, "DESIGN.md R<n>" a
+ * reading of a passage where the paper is silent (listed in DESIGN.md).
+ *
+ * Parity pins: every function is pinned by tests/test_oracle_*.py EXCEPT the
+ * exact 3GPP (f1,f2) QPP values, which are recalled (TS 36.212 Table 5.1.3-3
+ * is not in the container): "parity unpinned" for 3GPP interop of those
+ * values; their permutation / contention-free properties are pinned.
+ */
+#ifndef CRN_ORACLE_H
+#define CRN_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORACLE_CRC_NONE = 0, ORACLE_CRC24A = 1, ORACLE_CRC24B = 2 };
+
+/* Number of supported interleaver sizes (188 sizes 40..6144). */
+int oracle_num_k(void);
+/* i-th supported K (ascending); -1 if out of range. */
+int oracle_k_at(int i);
+/* (f1, f2) for K; returns 0, or -1 if K is not a supported size. */
+int oracle_qpp_params(int K, int *f1, int *f2);
+/* Pi(i) = (f1*i + f2*i^2) mod K; -1 if K unsupported. */
+int oracle_qpp_index(int K, int i);
+
+/* CRC register after feeding nbits bits (one bit per byte, MSB-first order,
+ * zero initial register, no reflection, no final xor) through generator
+ * CRC24A (D^24+D^23+D^18+D^17+D^14+D^11+D^10+D^7+D^6+D^5+D^4+D^3+D+1) or
+ * CRC24B (D^24+D^23+D^6+D^5+D+1).  A block is valid iff the register is 0
+ * after all its bits, parity included.  DESIGN.md R7. */
+uint32_t oracle_crc24(int kind, const uint8_t *bits, int64_t nbits);
+
+/* TB -> CB segmentation (36.212 5.1.2; Algorithm 1 with
+ * CB_MAX_SIZE = 6120 = 6144 - 24; R4). B = tbs + 24. */
+typedef struct { int32_t C, Kplus, Kminus, Cplus, Cminus, F, L; } oracle_seg;
+int oracle_segment(int64_t tbs_bits, oracle_seg *out);
+
+/* Window split: M = max{M : M | K, K/M >= wmin}; returns M (W = K/M). */
+int oracle_num_windows(int K, int wmin);
+
+/* Rate-1/3 turbo encoder: c[0..K) -> d0,d1,d2[0..K+4)
+ * (36.212 5.1.3.2 stream layout incl. 12 tail bits; R11).
+ * Returns 0, -1 if K unsupported. */
+int oracle_turbo_encode(const uint8_t *c, int K, uint8_t *d0, uint8_t *d1, uint8_t *d2);
+
+/* One constituent SISO pass (one half-iteration) over a block of K steps
+ * split into M = K/W windows (R12/R13).
+ *   lsys, lpar, la : int16-range values for k in [0,K) (already clamped)
+ *   tail[6]        : (x_K, z_K, x_K+1, z_K+1, x_K+2, z_K+2)
+ *   alpha_in [M][8]: alpha_{jW} used by window j >= 1 (row 0 ignored: known start state)
+ *   beta_in  [M][8]: beta_{(j+1)W} used by window j <= M-2 (row M-1 ignored: tail)
+ *   alpha_out[M][8]: alpha_{(j+1)W} produced by window j   (may be NULL)
+ *   beta_out [M][8]: beta_{jW} produced by window j        (may be NULL)
+ *   le[K]          : extrinsic output
+ *   ops            : counted-operation accumulator (may be NULL)
+ * Returns the number of int16-range violations observed (0 expected). */
+int64_t oracle_siso(const int32_t *lsys, const int32_t *lpar, const int32_t *la,
+                    const int32_t *tail, int K, int W,
+                    const int32_t *alpha_in, const int32_t *beta_in,
+                    int32_t *alpha_out, int32_t *beta_out,
+                    int32_t *le, uint64_t *ops);
+
+/* Full iterative decode of one CB (R1-R19).
+ *   d0,d1,d2 : the K+4 received int16 LLRs of each stream (positive => bit 1)
+ *   F        : number of leading filler bits (known 0)
+ *   crc_kind : ORACLE_CRC_NONE / 24A / 24B (the check used for ET and crc_ok)
+ *   max_iters: I >= 1;  early_term: stop after the first full iteration whose
+ *              hard decision passes the CRC
+ *   wmin     : minimum window length (32 in the product definition; K forces M = 1)
+ * Outputs: bits[K] (0/1 per byte), *crc_ok, *iters_used, ext[K] (La1_next of
+ * the last iteration, natural order), *ops (counted ops, accumulated).
+ * Returns the number of int16-range violations (0 expected), or -1 if the
+ * arguments are invalid. */
+int64_t oracle_decode_cb(const int16_t *d0, const int16_t *d1, const int16_t *d2,
+                         int K, int F, int crc_kind, int max_iters, int early_term, int wmin,
+                         uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
+                         int16_t *ext, uint64_t *ops);
+
+/* Batch helper for the CPU baseline: CB i uses K[i], F[i], crc_kind[i]; its
+ * LLRs start at llr_off[i] in each of d0/d1/d2, its K bits at bit_off[i] in
+ * bits (one per byte), its ext at bit_off[i] in ext (may be NULL).
+ * Runs nthreads POSIX threads, one CB per task.  Returns total violations. */
+int64_t oracle_decode_batch(int n_cb, const int32_t *K, const int32_t *F, const int32_t *crc_kind,
+                            const int64_t *llr_off, const int64_t *bit_off,
+                            const int16_t *d0, const int16_t *d1, const int16_t *d2,
+                            int max_iters, int early_term, int nthreads,
+                            uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
+                            int16_t *ext, uint64_t *ops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
