@@ -53,6 +53,8 @@ def lib():
         L.oracle_siso.argtypes = [i32p, i32p, i32p, i32p, C.c_int, C.c_int, i32p, i32p, i32p, i32p,
                                   i32p, u64p]
         L.oracle_siso.restype = C.c_int64
+        L.oracle_nii_update.argtypes = [C.c_int, i32p, i32p, i32p, i32p]
+        L.oracle_nii_update.restype = None
         L.oracle_decode_cb.argtypes = [i16p, i16p, i16p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.c_int, u8p, u8p, u8p, i16p, u64p]
         L.oracle_decode_cb.restype = C.c_int64
@@ -184,6 +186,16 @@ def siso(lsys, lpar, la, tail, W: int, alpha_in=None, beta_in=None):
                           _p(tail, C.c_int32), K, W, _p(ai, C.c_int32), _p(bi, C.c_int32),
                           _p(ao, C.c_int32), _p(bo, C.c_int32), _p(le, C.c_int32), C.byref(ops))
     return le, ao, bo, ops.value, v
+
+
+def nii_update(alpha_out, beta_out):
+    """NII hand-over: returns (alpha_in, beta_in) for the next iteration."""
+    ao = np.ascontiguousarray(alpha_out, np.int32)
+    bo = np.ascontiguousarray(beta_out, np.int32)
+    M = ao.shape[0]
+    ai, bi = np.zeros_like(ao), np.zeros_like(bo)
+    lib().oracle_nii_update(M, _p(ao, C.c_int32), _p(bo, C.c_int32), _p(ai, C.c_int32), _p(bi, C.c_int32))
+    return ai, bi
 
 
 def decode_cb(d0, d1, d2, F: int = 0, crc_kind: int = CRC24B, max_iters: int = 8,

@@ -352,6 +352,20 @@ int64_t oracle_siso(const int32_t *lsys, const int32_t *lpar, const int32_t *la,
     return c.viol;
 }
 
+/* ---------------------------------------------------------------- NII
+ * Next-iteration initialisation (R13): in iteration t+1 window j
+ * starts its alpha recursion from alpha_{jW} that window j-1 produced in
+ * iteration t, and its beta recursion from beta_{(j+1)W} that window j+1
+ * produced in iteration t. */
+void oracle_nii_update(int M, const int32_t *alpha_out, const int32_t *beta_out,
+                       int32_t *alpha_in, int32_t *beta_in) {
+    for (int j = 0; j < M; j++)
+        for (int s = 0; s < NSTATE; s++) {
+            alpha_in[(size_t)j * NSTATE + s] = j >= 1 ? alpha_out[(size_t)(j - 1) * NSTATE + s] : 0;
+            beta_in[(size_t)j * NSTATE + s] = j + 1 < M ? beta_out[(size_t)(j + 1) * NSTATE + s] : 0;
+        }
+}
+
 /* ---------------------------------------------------------------- decoder */
 static int32_t clamp_in(int32_t v) { return v < -CLAMP_IN ? -CLAMP_IN : (v > CLAMP_IN ? CLAMP_IN : v); }
 
@@ -400,10 +414,7 @@ int64_t oracle_decode_cb(const int16_t *d0, const int16_t *d1, const int16_t *d2
         viol += oracle_siso(Ls2, Lp2, La2, tail2, K, W, a_prev[1], b_prev[1], a_new[1], b_new[1], Le2, ops);
         /* de-interleave back to DEC1 */
         for (int i = 0; i < K; i++) La1n[Pi[i]] = Le2[i];
-        for (int q = 0; q < 2; q++) {
-            memcpy(a_prev[q], a_new[q], nb * 4);
-            memcpy(b_prev[q], b_new[q], nb * 4);
-        }
+        for (int q = 0; q < 2; q++) oracle_nii_update(M, a_new[q], b_new[q], a_prev[q], b_prev[q]);
         /* hard decision on L_APP = Ls + Le1 + La1_next; tie -> 1 (R16) */
         for (int n = 0; n < K; n++) {
             int32_t lapp = Ls[n] + Le1[n] + La1n[n];

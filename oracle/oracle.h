@@ -76,6 +76,11 @@ int64_t oracle_siso(const int32_t *lsys, const int32_t *lpar, const int32_t *la,
                     int32_t *alpha_out, int32_t *beta_out,
                     int32_t *le, uint64_t *ops);
 
+/* NII hand-over between iterations (R13): alpha_in[j] <- alpha_out[j-1]
+ * (j >= 1), beta_in[j] <- beta_out[j+1] (j <= M-2); the unused rows are zeroed. */
+void oracle_nii_update(int M, const int32_t *alpha_out, const int32_t *beta_out,
+                       int32_t *alpha_in, int32_t *beta_in);
+
 /* Full iterative decode of one CB (R1-R19).
  *   d0,d1,d2 : the K+4 received int16 LLRs of each stream (positive => bit 1)
  *   F        : number of leading filler bits (known 0)

@@ -150,3 +150,24 @@ def test_siso_equals_bruteforce_maxlog(orc, n, W):
             ml = U[np.argmax(tot)]
             lapp = lsys + la + le
             assert np.array_equal((lapp > 0)[lapp != 0], ml.astype(bool)[lapp != 0])
+
+
+@pytest.mark.parametrize("n,W", [(96, 32), (12, 3), (200, 40), (64, 32)])
+def test_nii_iterations_converge_to_full_block(orc, n, W):
+    """With the inputs held fixed, repeating the windowed SISO with the oracle's
+    NII hand-over (window j starts from what window j-1 / j+1 produced in the
+    previous pass) reaches the exact full-block max-log-MAP after M passes:
+    window 0 starts from the known state and the last from the tail, so exact
+    boundary states advance one window per pass (R13)."""
+    rng = np.random.default_rng(n + W)
+    for lim in (100, 3000):
+        lsys, lpar, la = (rng.integers(-lim, lim + 1, n) for _ in range(3))
+        tail = rng.integers(-lim, lim + 1, 6)
+        full = orc.siso(lsys, lpar, la, tail, n)[0]
+        M = n // W
+        ai = bi = None
+        for t in range(M):
+            le, ao, bo, _, v = orc.siso(lsys, lpar, la, tail, W, ai, bi)
+            assert v == 0
+            ai, bi = orc.nii_update(ao, bo)
+        assert np.array_equal(le, full)
