@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: batched LTE turbo decoding on B200 (libcrn).
+
+A step = one decode of this rank's shard of BASELINE.json config 4 (65,536
+code blocks of K=6144, BPSK/AWGN at Eb/N0 = 1.0 dB, int16 LLRs, 8 fixed
+iterations; 256 cells x 256 CBs, cells sharded evenly over the ranks).
+Prints ONE JSON line on rank 0.  See DESIGN.md "measurement".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {crn,reference}]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decoded info Mbit/s (K=6144, 8 iter, int16 max-log-MAP)"
+CFG = 4
+N_CELLS = 256
+L2_BYTES = 126 * 2**20
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _cells(rank, ws):
+    per = N_CELLS // ws
+    extra = N_CELLS % ws
+    lo = rank * per + min(rank, extra)
+    return list(range(lo, lo + per + (1 if rank < extra else 0)))
+
+
+def _workload_name(iters):
+    return f"cfg4: 65536 CBs (256 cells x 256) K=6144, BPSK Eb/N0=1.0 dB, int16 LLR, {iters} fixed iterations"
+
+
+class ClockSampler:
+    """NVML SM clock + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._idx = index
+        self._t = None
+
+    def start(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self._idx)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            names = {
+                "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+                "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+                "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.reasons |= {k for k, v in names.items() if r & v and k != "gpu_idle"}
+                    except Exception:
+                        pass
+                    time.sleep(0.02)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._t = None
+        return self
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def _peak_alu(num_sms, mhz):
+    """int16 ALU roofline: 64 lanes/clk/SM on the ALU pipe
+    (B300_MICROARCH: IADD3/LOP3/... rt_SMSP = 2 -> 16 lanes/clk/SMSP) x 4 int16
+    ops per fused int16x2 lane-instruction (VIADDMNMX / VIMNMX3: 2 ops x 2 halves)."""
+    return num_sms * 64 * 4 * mhz * 1e6
+
+
+def _traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(n_sample=256, seed=0):
+    """The oracle as it stands, timed on this host's cores on a bounded sample of
+    the same workload (the first n_sample CBs of cell 0..: cfg4 CBs)."""
+    import oracle
+    from paper_1905_01141_b200 import workload as wlmod
+    from tests._inputs import oracle_llrs, offsets
+    per_cell = 256
+    cells = list(range((n_sample + per_cell - 1) // per_cell))
+    wl = wlmod.make_workload(CFG, seed=seed, cells=cells, device="cpu")
+    wl.payload = wl.payload[:n_sample]
+    wl.tbs, wl.tb_K, wl.tb_cell, wl.tb_ebn0_db = (wl.tbs[:n_sample], wl.tb_K[:n_sample],
+                                                  wl.tb_cell[:n_sample], wl.tb_ebn0_db[:n_sample])
+    cbs, ll = oracle_llrs(wl)
+    K = np.array([c["K"] for c in cbs], np.int32)
+    lo, bo = offsets(K)
+    cores = len(os.sched_getaffinity(0))
+    args = (K, np.zeros_like(K), np.full_like(K, 2), lo, bo, *(x.numpy() for x in ll))
+    t0 = time.perf_counter()
+    r = oracle.decode_batch(*args, max_iters=8, early_term=False, nthreads=cores, want_ext=False)
+    dt = time.perf_counter() - t0
+    bits = int((K - 24).sum())
+    return {"value": bits / dt / 1e6, "unit": "Mbit/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n_sample} CBs of cfg4 (cells {cells[0]}-{cells[-1]}), 8 fixed iterations, "
+                      f"{dt:.2f} s wall on {cores} threads (gcc -O2 scalar C)",
+            "ops": int(r["ops"])}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        cpu_baseline(n_sample=args.ref_sample)
+    vals, times = [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cb = cpu_baseline(n_sample=args.ref_sample)
+        times.append(time.perf_counter() - t0)
+        vals.append(cb["value"])
+    v = statistics.median(vals)
+    cb["value"] = v
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Mbit/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int16",
+           "data": "synthetic", "config": {"workload": _workload_name(8) + f" -- bounded sample of "
+                                                                         f"{args.ref_sample} CBs per step",
+                                            "parallelism": "CPU threads (oracle)"},
+           "cpu_baseline": cb, "e2e": {"value": v, "unit": "Mbit/s", "h2d_bytes_per_step": 0,
+                                       "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def run_crn(args):
+    from paper_1905_01141_b200 import batch as bmod
+    from paper_1905_01141_b200 import build as crn_build
+    from paper_1905_01141_b200 import crn
+    from paper_1905_01141_b200 import workload as wlmod
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    crn_build.build()
+    dev = crn.device_info()
+
+    cells = _cells(rank, ws)
+    wl = wlmod.make_workload(CFG, seed=args.seed, cells=cells, device="cuda")
+    b = bmod.build(wl)
+    del wl.payload
+    iters = args.iters
+    plan = crn.Plan(b.desc)
+    bits, ok, it, _ = bmod.outputs(b, want_ext=False)
+    stream = torch.cuda.current_stream()
+    l0, l1, l2 = b.llr
+    in_bytes = 3 * 2 * b.n_llr
+
+    def step():
+        plan.decode(l0, l1, l2, iters, False, bits, ok, None, None, stream=stream)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clk = ClockSampler(local).start()
+    t_all0 = torch.cuda.Event(enable_timing=True)
+    t_all1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    t_all0.record(stream)
+    for k in range(args.steps):
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    t_all1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    ms_total = t_all0.elapsed_time(t_all1)
+    launch_ms = [a.elapsed_time(z) for a, z in ev]
+
+    # outputs of the last step: counters (one NCCL reduction, DESIGN.md multi-GPU)
+    crc = ok[:b.n_cb].to(torch.int64)
+    counters = torch.tensor([b.n_cb, int(crc.sum().item()), b.info_bits(), int(b.K.sum()),
+                             crn.counted_ops(b.K, iters)], dtype=torch.float64, device="cuda")
+    tmax = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(counters, op=dist.ReduceOp.SUM)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    n_cb, n_ok, info_bits, sum_k, ops = (int(x) for x in counters.tolist())
+    ms_step = tmax.item() / args.steps
+    value = info_bits / (ms_step * 1e-3) / 1e6
+
+    # ---- e2e: host (pinned) LLRs -> device -> decode -> bits + crc back, every step
+    e2e = None
+    if not args.no_e2e:
+        host = [x.cpu().pin_memory() for x in b.llr]
+        dl = [torch.empty_like(x) for x in b.llr]
+        hb = torch.empty(bits.numel(), dtype=bits.dtype).pin_memory()
+        hok = torch.empty(ok.numel(), dtype=ok.dtype).pin_memory()
+
+        def e2e_step():
+            for d, h in zip(dl, host):
+                d.copy_(h, non_blocking=True)
+            plan.decode(dl[0], dl[1], dl[2], iters, False, bits, ok, None, None, stream=stream)
+            hb.copy_(bits, non_blocking=True)
+            hok.copy_(ok, non_blocking=True)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ne = max(1, min(args.steps, 5))
+        e0.record(stream)
+        for _ in range(ne):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": info_bits / (te.item() * 1e-3) / 1e6, "unit": "Mbit/s",
+               "h2d_bytes_per_step": in_bytes * ws, "d2h_bytes_per_step": (hb.numel() * 4 + hok.numel()) * ws,
+               "ms_per_step": te.item(), "path": "pinned host LLRs -> cudaMemcpyAsync -> crn_plan_decode -> "
+                                                   "packed bits + crc_ok -> pinned host"}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    mean_launch_ms = statistics.mean(launch_ms)
+    local_ops = crn.counted_ops(b.K, iters)
+    mhz = dev["clock_khz"] / 1e3
+    peak = _peak_alu(dev["num_sms"], mhz)
+    achieved = local_ops / (mean_launch_ms * 1e-3)
+    roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tops/s (int16)",
+            "frac": achieved / peak, "traffic": _traffic(),
+            "peak_basis": f"{dev['num_sms']} SMs x 64 lanes/clk x 4 int16 ops/lane-instr x {mhz:.0f} MHz "
+                          f"(sm max clock); counted ops = 2 x (129 K + 90) per CB-iteration",
+            "algorithmic_ops_per_launch": local_ops,
+            "frac_at_median_clock": (achieved / _peak_alu(dev["num_sms"], clocks["sm_mhz"]))
+            if clocks.get("sm_mhz") else None}
+    out = {
+        "metric": METRIC, "value": value, "unit": "Mbit/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int16", "data": "synthetic",
+        "config": {"workload": _workload_name(iters), "n_cb": n_cb, "cb_per_rank": b.n_cb,
+                   "iters": iters, "seed": args.seed,
+                   "l2": f"inputs {in_bytes / 1e9:.2f} GB per rank > L2 {L2_BYTES / 2**20:.0f} MiB: no flush needed",
+                   "parallelism": f"dp{ws} (cells sharded, no data-path collective)",
+                   "info_bits_per_step": info_bits, "sum_K": sum_k, "crc_ok": n_ok},
+        "roofline": roof, "clocks": clocks, "gpu_launches": args.steps * plan.launches,
+        "e2e": e2e, "kernel_ms_mean": mean_launch_ms, "kernel_ms": launch_ms,
+        "sum_k_mbps": sum_k / (ms_step * 1e-3) / 1e6,
+    }
+    if not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline(n_sample=args.ref_sample)
+        except Exception as e:           # the GPU number stands without it
+            out["cpu_baseline"] = {"error": repr(e)}
+    print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="crn", choices=["crn", "reference"])
+    ap.add_argument("--iters", type=int, default=8)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--ref-sample", type=int, default=256)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    return run_reference(args) if args.impl == "reference" else run_crn(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,176 @@
+/*
+ * crn.h -- C ABI of libcrn: B200-native batched LTE turbo decoding for a pooled
+ * C-RAN BBU (the uplink channel-decoding function of arxiv 1905.01141).
+ *
+ * All functions are extern "C", take plain pointers and sizes, and return a
+ * status (0 = CRN_OK, < 0 = error) unless stated otherwise.  No torch types.
+ *
+ * Citations: PAPER.md:<line> (the paper), SPEC.md:<line> (the CPU-program spec
+ * written from it, used here for interface shapes), DESIGN.md R<n> (a reading
+ * where the paper is silent).  The operation every decode entry point computes
+ * is DESIGN.md "decoder definition": per code block (CB), demultiplex the
+ * received streams, run DEC1 -> DEC2 -> de-interleave for
+ * fixed or CRC-early-terminated iterations, take the hard
+ * decision and check the CRC; int16 max-log-MAP on the 8-state
+ * LTE RSC trellis with the QPP interleaver and M_K parallel windows (R1-R19).
+ *
+ * Ownership: the caller owns every buffer.  libcrn allocates only (a) a cached
+ * per-device workspace + interleaver tables (guarded by a mutex) and (b) the
+ * device copies held by a plan.  Decode calls are asynchronous on the given
+ * CUDA stream (NULL = legacy default stream); launch errors return at once,
+ * kernel faults surface as CRN_ECUDA on a later call or at the caller's sync.
+ * Determinism: each CB's outputs depend only on that CB's inputs and
+ * descriptor -- never on batch order, composition, stream or GPU count.
+ * There is NO CPU fallback: without a usable sm_100 device every decode
+ * entry point returns CRN_ENODEV.
+ */
+#ifndef CRN_H
+#define CRN_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { CRN_OK = 0, CRN_EINVAL = -1, CRN_ECUDA = -2, CRN_ENOMEM = -3, CRN_ENODEV = -4 };
+enum { CRN_CRC_NONE = 0, CRN_CRC24A = 1, CRN_CRC24B = 2 };
+enum { CRN_DESC_ON_DEVICE = 1 };           /* flag bit 0 of crn_decode_batch_ex */
+enum { CRN_MAX_ITERS = 32, CRN_KMIN = 40, CRN_KMAX = 6144 };
+
+/* Per-CB descriptor (the paper's CCDU at CB granularity).
+ *   K        interleaver size, one of the 188 LTE sizes 40..6144
+ *   F        leading filler bits (known 0), 0 <= F <= K-25 (36.212 5.1.2; R6)
+ *   crc_kind CRN_CRC24A (TB with C=1), CRN_CRC24B (CB of a segmented TB), or
+ *            CRN_CRC_NONE (never passes; runs max iterations)          (R7)
+ *   llr_off  element offset of the CB's K+4 LLRs in each of llr_sys/p1/p2
+ *   bit_off  uint32-WORD offset of the CB's ceil(K/32) packed output words
+ *   ext_off  element offset of the CB's K extrinsic outputs in ext_out      */
+typedef struct {
+    int32_t K, F, crc_kind, reserved;
+    int64_t llr_off, bit_off, ext_off;
+} crn_cb_desc;
+
+/* 36.212 5.1.2 segmentation result (Algorithm 1; R4). */
+typedef struct { int32_t C, Kplus, Kminus, Cplus, Cminus, F, L; } crn_seg;
+
+/* ------------------------------------------------------------------ decode */
+
+/* BASELINE.json form.  iters > 0: that many fixed iterations; iters < 0:
+ * CRC early termination with at most -iters iterations (R3).
+ * CRC24B per CB, F = 0, dense layout: CB i's K_i+4 LLRs (positive => bit 1,
+ * PAPER.md:285) start at sum_{j<i}(K_j+4) in each stream (sys = d0, p1 = d1,
+ * p2 = d2 of 36.212 incl. the tail columns, R11); its hard-decision bits are
+ * packed LSB-first (bit n -> word n/32, bit n%32; R19) from word
+ * sum_{j<i} ceil(K_j/32) of out_bits; crc_ok[i] = 1 iff the final hard
+ * decision passes CRC24B.  K[] is HOST memory, every other pointer DEVICE
+ * memory.  Enqueues on the legacy default stream.  Errors: CRN_EINVAL for a K
+ * outside the table, n_cb < 0, |iters| outside [1,32] or a NULL pointer. */
+int crn_decode_batch(const int16_t *llr_sys, const int16_t *llr_p1, const int16_t *llr_p2,
+                     const int32_t *K, int32_t n_cb, int32_t iters,
+                     uint32_t *out_bits, uint8_t *crc_ok);
+
+/* General form.  desc: n_cb descriptors in HOST memory (copied during the
+ * call), or in DEVICE memory if flags & CRN_DESC_ON_DEVICE (then they are
+ * validated on the device; an invalid one yields crc_ok = 0, iters_used = 0).
+ * max_iters in [1,32]; early_term != 0 stops a CB after the first full
+ * iteration whose hard decision passes its CRC (R3, R18).
+ * Outputs (device memory): out_bits (required), crc_ok[n_cb] (required),
+ * iters_used[n_cb] (may be NULL; full iterations executed, R17), ext_out
+ * (may be NULL; int16 La1_next of the last iteration in natural order, R15).
+ * workspace: NULL -> the cached per-device workspace; else >= crn_workspace_bytes()
+ * bytes of device memory owned by the caller, used by this call only.
+ * cuda_stream: a cudaStream_t (NULL = legacy default stream).
+ * Host-side validation (descriptors in host memory) returns CRN_EINVAL for a
+ * K outside the table, F < 0 or F > K-25, an unknown crc_kind, overlapping
+ * LLR or output ranges, or unknown flag bits.  n_cb == 0 is a no-op.  Input
+ * LLRs of any int16 value are accepted (clamped to +-4096, R12). */
+int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb,
+                        const int16_t *llr_sys, const int16_t *llr_p1, const int16_t *llr_p2,
+                        int32_t max_iters, int32_t early_term, int32_t flags,
+                        uint32_t *out_bits, uint8_t *crc_ok, uint8_t *iters_used, int16_t *ext_out,
+                        void *workspace, size_t workspace_bytes, void *cuda_stream);
+
+/* Bytes of caller-provided workspace crn_decode_batch_ex needs on the current
+ * device (independent of the batch: the decoder is a persistent kernel with
+ * one slot per resident CTA). */
+size_t crn_workspace_bytes(void);
+
+/* Plans: validate + bucket + upload a descriptor set once, decode many times
+ * (the per-TTI pattern of a BBU, "CCDUs arrive in batches every
+ * millisecond").  *plan receives an opaque handle. */
+int crn_plan_create(const crn_cb_desc *desc_host, int32_t n_cb, void **plan);
+int crn_plan_decode(void *plan, const int16_t *llr_sys, const int16_t *llr_p1,
+                    const int16_t *llr_p2, int32_t max_iters, int32_t early_term,
+                    uint32_t *out_bits, uint8_t *crc_ok, uint8_t *iters_used, int16_t *ext_out,
+                    void *cuda_stream);
+/* Number of decode-kernel launches one crn_plan_decode performs (for gpu_launches). */
+int crn_plan_launches(void *plan);
+void crn_plan_destroy(void *plan);
+
+/* Counted operations of one decode (the roofline numerator, DESIGN.md "op
+ * count"): sum over CBs and executed iterations of 2 x (129 K + 90).  For a
+ * fixed-iteration batch pass iters_used = NULL and it uses max_iters. */
+int64_t crn_counted_ops(const int32_t *K_host, int32_t n_cb, const uint8_t *iters_used_host,
+                        int32_t max_iters);
+
+/* ------------------------------------------------------------------ encode (DL) */
+
+/* Rate-1/3 turbo encoding of n_cb CBs on the device.  info: one bit per byte,
+ * CB i's K_i bits at desc[i].ext_off (the whole CB content incl. fillers and
+ * CRC).  If attach_crc != 0 the last 24 bits are (re)computed as the CRC of
+ * desc[i].crc_kind over the first K-24 bits (fillers counted as 0) before
+ * encoding.  Output d0/d1/d2: one bit per byte, CB i's K_i+4 coded bits at
+ * desc[i].llr_off (36.212 5.1.3.2 layout incl. the 12 tail bits, R11).
+ * desc is HOST memory; info/d0/d1/d2 device memory. */
+int crn_encode_batch(const crn_cb_desc *desc, int32_t n_cb, const uint8_t *info, int32_t attach_crc,
+                     uint8_t *d0, uint8_t *d1, uint8_t *d2, void *cuda_stream);
+
+/* ------------------------------------------------------------------ host helpers */
+
+/* TB of tbs_bits payload bits -> 36.212 5.1.2 code-block segmentation (B = tbs+24). */
+int crn_segment_tb(int64_t tbs_bits, crn_seg *out);
+/* Build the CBs of one TB (36.212 5.1.1-5.1.2; Algorithm 1 and
+ * the CB/TB relation of PAPER.md:369): CRC24A is attached to the tbs_bits
+ * payload bits (one per byte, HOST memory), the result is segmented, CB 0 gets
+ * the F leading filler zeros and, if C > 1, every CB gets its CRC24B.
+ * cb_bits receives sum K_r bits (one per byte); desc[r] gets K, F, crc_kind
+ * (CRC24A if C == 1 else CRC24B), ext_off = bit offset inside cb_bits (plus
+ * base_bit), llr_off = sum_{s<r}(K_s+4) (plus base_llr), bit_off = word offset
+ * sum_{s<r} ceil(K_s/32) (plus base_word).  *n_cb receives C; max_cb bounds it. */
+int crn_tb_build_cbs(const uint8_t *tb_bits, int64_t tbs_bits, int32_t max_cb, int64_t base_bit,
+                     int64_t base_llr, int64_t base_word, uint8_t *cb_bits, crn_cb_desc *desc,
+                     int32_t *n_cb);
+/* TB post-processing ("a TB can be successfully decoded only when
+ * all CBs have been individually decoded", :408 "combination of CBs"): given the
+ * C decoded CBs of one TB (packed words as written by the decoder, HOST memory,
+ * CB r at desc[r].bit_off) strip fillers and CB CRCs, concatenate, check the TB
+ * CRC24A.  Returns 1 if every crc_ok[r] is set and the TB CRC passes (payload
+ * written to tb_out, one bit per byte, if non-NULL), 0 otherwise, <0 on error. */
+int crn_tb_reassemble(const uint32_t *cb_words, const crn_cb_desc *desc, const uint8_t *crc_ok,
+                      int32_t n_cb, int64_t tbs_bits, uint8_t *tb_out);
+/* QPP parameters of TS 36.212 Table 5.1.3-3 for K; CRN_EINVAL if K is not a size. */
+int crn_qpp_params(int32_t K, int32_t *f1, int32_t *f2);
+/* Window split of the decoder: M = max{M : M | K, K/M >= 32}, W = K/M (R13). */
+int crn_windows(int32_t K, int32_t *M, int32_t *W);
+/* CRC register after nbits bits (one per byte, MSB-first; zero init; 0 <=> valid). */
+uint32_t crn_crc24a(const uint8_t *bits, int64_t nbits);
+uint32_t crn_crc24b(const uint8_t *bits, int64_t nbits);
+const char *crn_strerror(int code);
+
+/* ------------------------------------------------------------------ device facts / microbench */
+
+/* SM count, SM max clock (kHz) and sm major/minor of the current device. */
+int crn_device_info(int32_t *num_sms, int32_t *clock_khz, int32_t *cc_major, int32_t *cc_minor);
+/* int16x2 ALU microbenchmark: op 0 VIADD.16x2, 1 VIMNMX.S16x2,
+ * 2 VIMNMX3.S16x2, 3 VIADDMNMX.S16x2.  Runs independent chains at full
+ * occupancy (8 CTAs x 256 threads per SM); *lane_instr = warp-instructions x 32
+ * of the opcode executed, *ms = kernel time, *max_block_cycles = the longest
+ * CTA's clock64 span (all CTAs are co-resident, so SM throughput in lane-instr
+ * per cycle = lane_instr / (num_sms x max_block_cycles)). */
+int crn_ubench_int16x2(int32_t op, int64_t *lane_instr, float *ms, int64_t *max_block_cycles);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,88 @@
+"""Product-side batch assembly for a synthetic workload: CB packing via libcrn
+(crn_tb_build_cbs / descriptors, row a1), device encoding via crn_encode_batch
+(the paper's encoding function), then the shared workload
+channel.  Used by bench.py and the GPU tests; never touches oracle/.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import crn
+from . import workload as wlmod
+
+
+@dataclass
+class Batch:
+    wl: wlmod.Workload
+    desc: np.ndarray          # crn.DESC_DTYPE [n_cb] (host)
+    cb_cell: np.ndarray
+    cb_tb: np.ndarray         # TB index per CB
+    cb_ebn0: np.ndarray
+    info: torch.Tensor        # uint8 [sum K] CB contents (device)
+    coded: tuple              # d0, d1, d2 uint8 [sum (K+4)] (device)
+    llr: tuple                # l0, l1, l2 int16 [sum (K+4)] (device)
+
+    @property
+    def n_cb(self) -> int:
+        return int(self.desc.size)
+
+    @property
+    def K(self) -> np.ndarray:
+        return self.desc["K"].astype(np.int32)
+
+    @property
+    def n_words(self) -> int:
+        return int((self.desc["bit_off"] + (self.desc["K"] + 31) // 32).max()) if self.n_cb else 0
+
+    @property
+    def n_llr(self) -> int:
+        return int((self.desc["llr_off"] + self.desc["K"] + 4).max()) if self.n_cb else 0
+
+    def info_bits(self) -> int:
+        """Decoded information bits per CB: K - F - 24 (DESIGN.md metric)."""
+        return int((self.desc["K"] - self.desc["F"] - 24).sum())
+
+
+def build(wl: wlmod.Workload, device="cuda") -> Batch:
+    dev = torch.device(device)
+    descs, infos, cells, tbs, ebn0 = [], [], [], [], []
+    bit = llr = word = 0
+    for t in range(wl.n_tb):
+        if wl.tb_kind == "cb":
+            K = int(wl.tb_K[t])
+            d = np.zeros(1, crn.DESC_DTYPE)
+            d["K"], d["F"], d["crc_kind"] = K, 0, crn.CRC24B
+            d["ext_off"], d["llr_off"], d["bit_off"] = bit, llr, word
+            infos.append(torch.cat([wl.payload[t].to(dev), torch.zeros(24, dtype=torch.uint8, device=dev)]))
+        else:
+            cbb, d = crn.tb_build_cbs(wl.payload[t].cpu().numpy(), base_bit=bit, base_llr=llr, base_word=word)
+            infos.append(torch.from_numpy(cbb).to(dev))
+        descs.append(d)
+        n = d.size
+        cells += [int(wl.tb_cell[t])] * n
+        tbs += [t] * n
+        ebn0 += [float(wl.tb_ebn0_db[t])] * n
+        bit += int(d["K"].sum())
+        llr += int((d["K"] + 4).sum())
+        word += int(((d["K"] + 31) // 32).sum())
+    desc = np.concatenate(descs) if descs else np.zeros(0, crn.DESC_DTYPE)
+    info = torch.cat(infos) if infos else torch.zeros(0, dtype=torch.uint8, device=dev)
+    coded = tuple(torch.empty(llr, dtype=torch.uint8, device=dev) for _ in range(3))
+    crn.encode_batch(desc, info, wl.tb_kind == "cb", *coded)
+    cell = np.array(cells, np.int32)
+    e = np.array(ebn0, np.float64)
+    l0, l1, l2 = wlmod.channel_llr(wl, cell, desc["K"], e, coded)
+    return Batch(wl=wl, desc=desc, cb_cell=cell, cb_tb=np.array(tbs, np.int64), cb_ebn0=e, info=info,
+                 coded=coded, llr=(l0, l1, l2))
+
+
+def outputs(b: Batch, device="cuda", want_ext: bool = True):
+    dev = torch.device(device)
+    bits = torch.zeros(max(b.n_words, 1), dtype=torch.int32, device=dev)
+    ok = torch.zeros(max(b.n_cb, 1), dtype=torch.uint8, device=dev)
+    it = torch.zeros(max(b.n_cb, 1), dtype=torch.uint8, device=dev)
+    ext = torch.zeros(max(int(b.desc["K"].sum()), 1), dtype=torch.int16, device=dev) if want_ext else None
+    return bits, ok, it, ext

@@ -1,0 +1,245 @@
+"""Thin ctypes binding of libcrn (include/crn.h) -- argument marshalling only.
+
+Every function here has the same name as its C entry point minus the ``crn_``
+prefix.  Device buffers are passed as torch CUDA tensors (``data_ptr()``),
+host buffers as numpy arrays; streams default to torch's current stream.  No
+step of the decoding path runs in Python: if libcrn.so is missing or no sm_100
+device is present the calls raise -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libcrn.so")
+
+CRN_OK, CRN_EINVAL, CRN_ECUDA, CRN_ENOMEM, CRN_ENODEV = 0, -1, -2, -3, -4
+CRC_NONE, CRC24A, CRC24B = 0, 1, 2
+DESC_ON_DEVICE = 1
+
+DESC_DTYPE = np.dtype([("K", "<i4"), ("F", "<i4"), ("crc_kind", "<i4"), ("reserved", "<i4"),
+                       ("llr_off", "<i8"), ("bit_off", "<i8"), ("ext_off", "<i8")])
+
+
+class Seg(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("C", "Kplus", "Kminus", "Cplus", "Cminus", "F", "L")]
+
+
+class CrnError(RuntimeError):
+    pass
+
+
+_lib = None
+P = C.POINTER
+vp, i16p, i32p, i64p, u8p, u32p = C.c_void_p, P(C.c_int16), P(C.c_int32), P(C.c_int64), P(C.c_uint8), P(C.c_uint32)
+
+_SIGS = {
+    "crn_decode_batch": (C.c_int, [vp, vp, vp, i32p, C.c_int32, C.c_int32, vp, vp]),
+    "crn_decode_batch_ex": (C.c_int, [vp, C.c_int32, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32,
+                                      vp, vp, vp, vp, vp, C.c_size_t, vp]),
+    "crn_workspace_bytes": (C.c_size_t, []),
+    "crn_plan_create": (C.c_int, [vp, C.c_int32, P(vp)]),
+    "crn_plan_decode": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp]),
+    "crn_plan_launches": (C.c_int, [vp]),
+    "crn_plan_destroy": (None, [vp]),
+    "crn_counted_ops": (C.c_int64, [i32p, C.c_int32, u8p, C.c_int32]),
+    "crn_encode_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp]),
+    "crn_tb_build_cbs": (C.c_int, [u8p, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_int64, u8p, vp,
+                                   i32p]),
+    "crn_tb_reassemble": (C.c_int, [u32p, vp, u8p, C.c_int32, C.c_int64, u8p]),
+    "crn_segment_tb": (C.c_int, [C.c_int64, P(Seg)]),
+    "crn_qpp_params": (C.c_int, [C.c_int32, i32p, i32p]),
+    "crn_windows": (C.c_int, [C.c_int32, i32p, i32p]),
+    "crn_crc24a": (C.c_uint32, [u8p, C.c_int64]),
+    "crn_crc24b": (C.c_uint32, [u8p, C.c_int64]),
+    "crn_strerror": (C.c_char_p, [C.c_int]),
+    "crn_device_info": (C.c_int, [i32p, i32p, i32p, i32p]),
+    "crn_ubench_int16x2": (C.c_int, [C.c_int32, i64p, P(C.c_float), i64p]),
+}
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO):
+            raise CrnError(f"{SO} is not built: run paper_1905_01141_b200.build.build() (no CPU fallback)")
+        L = C.CDLL(SO)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _chk(rc: int, what: str):
+    if rc < 0:
+        raise CrnError(f"{what}: {lib().crn_strerror(rc).decode()} ({rc})")
+    return rc
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _np(a, ct):
+    return a.ctypes.data_as(P(ct))
+
+
+def _stream(stream):
+    if stream is not None:
+        return stream if isinstance(stream, int) else stream.cuda_stream
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _cuda_dev(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise CrnError("device buffers must be CUDA tensors (no CPU fallback)")
+
+
+# ------------------------------------------------------------------ decode
+def decode_batch(l0, l1, l2, K, n_cb: int, iters: int, out_bits, crc_ok) -> None:
+    _cuda_dev(l0, l1, l2, out_bits, crc_ok)
+    Kh = np.ascontiguousarray(K, np.int32)
+    _chk(lib().crn_decode_batch(_ptr(l0), _ptr(l1), _ptr(l2), _np(Kh, C.c_int32), n_cb, iters,
+                                _ptr(out_bits), _ptr(crc_ok)), "crn_decode_batch")
+
+
+def decode_batch_ex(desc, n_cb: int, l0, l1, l2, max_iters: int, early_term: bool, flags: int, out_bits,
+                    crc_ok, iters_used=None, ext_out=None, workspace=None, workspace_bytes: int = 0,
+                    stream=None) -> None:
+    _cuda_dev(l0, l1, l2, out_bits, crc_ok, iters_used, ext_out)
+    if flags & DESC_ON_DEVICE:
+        dptr = desc.data_ptr()
+    else:
+        desc = np.ascontiguousarray(desc, DESC_DTYPE)
+        dptr = desc.ctypes.data
+    _chk(lib().crn_decode_batch_ex(dptr, n_cb, _ptr(l0), _ptr(l1), _ptr(l2), max_iters, int(early_term),
+                                   flags, _ptr(out_bits), _ptr(crc_ok), _ptr(iters_used), _ptr(ext_out),
+                                   _ptr(workspace), workspace_bytes, _stream(stream)),
+         "crn_decode_batch_ex")
+
+
+def workspace_bytes() -> int:
+    return int(lib().crn_workspace_bytes())
+
+
+class Plan:
+    """crn_plan_create / crn_plan_decode / crn_plan_destroy."""
+
+    def __init__(self, desc):
+        self.desc = np.ascontiguousarray(desc, DESC_DTYPE)
+        h = C.c_void_p()
+        _chk(lib().crn_plan_create(self.desc.ctypes.data, self.desc.size, C.byref(h)), "crn_plan_create")
+        self.h = h
+
+    def decode(self, l0, l1, l2, max_iters: int, early_term: bool, out_bits, crc_ok, iters_used=None,
+               ext_out=None, stream=None) -> None:
+        _cuda_dev(l0, l1, l2, out_bits, crc_ok, iters_used, ext_out)
+        _chk(lib().crn_plan_decode(self.h, _ptr(l0), _ptr(l1), _ptr(l2), max_iters, int(early_term),
+                                   _ptr(out_bits), _ptr(crc_ok), _ptr(iters_used), _ptr(ext_out),
+                                   _stream(stream)), "crn_plan_decode")
+
+    @property
+    def launches(self) -> int:
+        return int(lib().crn_plan_launches(self.h))
+
+    def close(self):
+        if self.h:
+            lib().crn_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def counted_ops(K, max_iters: int, iters_used=None) -> int:
+    Kh = np.ascontiguousarray(K, np.int32)
+    it = None if iters_used is None else np.ascontiguousarray(iters_used, np.uint8)
+    return int(lib().crn_counted_ops(_np(Kh, C.c_int32), Kh.size, None if it is None else _np(it, C.c_uint8),
+                                     max_iters))
+
+
+# ------------------------------------------------------------------ encode / TB helpers
+def encode_batch(desc, info, attach_crc: bool, d0, d1, d2, stream=None) -> None:
+    _cuda_dev(info, d0, d1, d2)
+    desc = np.ascontiguousarray(desc, DESC_DTYPE)
+    _chk(lib().crn_encode_batch(desc.ctypes.data, desc.size, _ptr(info), int(attach_crc), _ptr(d0), _ptr(d1),
+                                _ptr(d2), _stream(stream)), "crn_encode_batch")
+
+
+def tb_build_cbs(tb_bits, base_bit: int = 0, base_llr: int = 0, base_word: int = 0, max_cb: int = 64):
+    """-> (cb_bits uint8 [sum K], desc array [C])."""
+    tb = np.ascontiguousarray(tb_bits, np.uint8)
+    out = np.zeros(max_cb * 6144, np.uint8)
+    desc = np.zeros(max_cb, DESC_DTYPE)
+    n = C.c_int32()
+    _chk(lib().crn_tb_build_cbs(_np(tb, C.c_uint8), tb.size, max_cb, base_bit, base_llr, base_word,
+                                _np(out, C.c_uint8), desc.ctypes.data, C.byref(n)), "crn_tb_build_cbs")
+    desc = desc[:n.value].copy()
+    return out[:int(desc["K"].sum())].copy(), desc
+
+
+def tb_reassemble(cb_words, desc, crc_ok, tbs: int):
+    """-> payload (uint8 bits) or None if the TB is lost."""
+    w = np.ascontiguousarray(cb_words, np.uint32)
+    desc = np.ascontiguousarray(desc, DESC_DTYPE)
+    ok = np.ascontiguousarray(crc_ok, np.uint8)
+    out = np.zeros(tbs, np.uint8)
+    r = _chk(lib().crn_tb_reassemble(_np(w, C.c_uint32), desc.ctypes.data, _np(ok, C.c_uint8), desc.size, tbs,
+                                     _np(out, C.c_uint8)), "crn_tb_reassemble")
+    return out if r == 1 else None
+
+
+def segment_tb(tbs: int) -> dict:
+    s = Seg()
+    _chk(lib().crn_segment_tb(tbs, C.byref(s)), "crn_segment_tb")
+    return {n: getattr(s, n) for n, _ in Seg._fields_}
+
+
+def qpp_params(K: int) -> tuple[int, int]:
+    f1, f2 = C.c_int32(), C.c_int32()
+    _chk(lib().crn_qpp_params(K, C.byref(f1), C.byref(f2)), "crn_qpp_params")
+    return f1.value, f2.value
+
+
+def windows(K: int) -> tuple[int, int]:
+    M, W = C.c_int32(), C.c_int32()
+    _chk(lib().crn_windows(K, C.byref(M), C.byref(W)), "crn_windows")
+    return M.value, W.value
+
+
+def crc24a(bits) -> int:
+    b = np.ascontiguousarray(bits, np.uint8)
+    return int(lib().crn_crc24a(_np(b, C.c_uint8), b.size))
+
+
+def crc24b(bits) -> int:
+    b = np.ascontiguousarray(bits, np.uint8)
+    return int(lib().crn_crc24b(_np(b, C.c_uint8), b.size))
+
+
+def strerror(code: int) -> str:
+    return lib().crn_strerror(code).decode()
+
+
+def device_info() -> dict:
+    v = [C.c_int32() for _ in range(4)]
+    _chk(lib().crn_device_info(*(C.byref(x) for x in v)), "crn_device_info")
+    return dict(num_sms=v[0].value, clock_khz=v[1].value, cc=(v[2].value, v[3].value))
+
+
+def ubench_int16x2(op: int) -> dict:
+    li, ms, cyc = C.c_int64(), C.c_float(), C.c_int64()
+    _chk(lib().crn_ubench_int16x2(op, C.byref(li), C.byref(ms), C.byref(cyc)), "crn_ubench_int16x2")
+    return dict(lane_instr=li.value, ms=ms.value, max_block_cycles=cyc.value)

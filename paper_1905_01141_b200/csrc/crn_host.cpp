@@ -1,0 +1,517 @@
+/* crn_host.cpp -- libcrn host side: the C ABI of include/crn.h.
+ *
+ * Row a1 of the hot path (CB packing): validation of
+ * the per-CB descriptors, bucketing by K, pairing two CBs of equal K into one
+ * int16x2 lane pair, grouping pairs into CTA tasks, plus the 36.212 helpers
+ * (segmentation, CRC24A/B) and the per-device tables (QPP window-major
+ * addresses, CRC combine powers).  Everything that decodes runs in the CUDA
+ * kernels of crn_decode.cu; nothing here computes the method on the CPU.
+ */
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
+#include <vector>
+
+#include "crn_internal.h"
+#include "qpp_table.h"
+
+/* ------------------------------------------------------------------ size table */
+static int k_at(int i) {
+    if (i < 60) return 40 + 8 * i;              /* 40..512 step 8     */
+    if (i < 92) return 528 + 16 * (i - 60);     /* 528..1024 step 16  */
+    if (i < 124) return 1056 + 32 * (i - 92);   /* 1056..2048 step 32 */
+    return 2112 + 64 * (i - 124);               /* 2112..6144 step 64 */
+}
+
+extern "C" int crn_k_index(int32_t K) {
+    int lo = 0, hi = CRN_NUM_K - 1;
+    while (lo <= hi) {
+        int mid = (lo + hi) / 2, v = k_at(mid);
+        if (v == K) return mid;
+        if (v < K) lo = mid + 1; else hi = mid - 1;
+    }
+    return -1;
+}
+
+extern "C" int crn_qpp_params(int32_t K, int32_t *f1, int32_t *f2) {
+    int i = crn_k_index(K);
+    if (i < 0 || !f1 || !f2) return CRN_EINVAL;
+    *f1 = crn_qpp_f1[i];
+    *f2 = crn_qpp_f2[i];
+    return CRN_OK;
+}
+
+extern "C" int crn_windows(int32_t K, int32_t *M, int32_t *W) {
+    if (crn_k_index(K) < 0 || !M || !W) return CRN_EINVAL;
+    for (int m = K / 32; m >= 1; m--)
+        if (K % m == 0) { *M = m; *W = K / m; return CRN_OK; }
+    *M = 1; *W = K;
+    return CRN_OK;
+}
+
+/* ------------------------------------------------------------------ CRC24 (36.212 5.1.1) */
+static const uint32_t POLY_A = 0x864CFBu, POLY_B = 0x800063u;
+
+static uint32_t crc_table[2][256];
+static std::once_flag crc_once;
+static void crc_init() {
+    for (int k = 0; k < 2; k++) {
+        uint32_t poly = k ? POLY_B : POLY_A;
+        for (uint32_t b = 0; b < 256; b++) {
+            uint32_t r = b << 16;
+            for (int i = 0; i < 8; i++) r = ((r << 1) ^ ((r & 0x800000u) ? poly : 0)) & 0xFFFFFFu;
+            crc_table[k][b] = r;
+        }
+    }
+}
+
+static uint32_t crc24(int k, const uint8_t *bits, int64_t n) {
+    std::call_once(crc_once, crc_init);
+    uint32_t reg = 0;
+    int64_t i = 0;
+    for (; i + 8 <= n; i += 8) {            /* byte-at-a-time table form */
+        uint32_t byte = 0;
+        for (int b = 0; b < 8; b++) byte = (byte << 1) | (bits[i + b] & 1u);
+        reg = ((reg << 8) & 0xFFFFFFu) ^ crc_table[k][((reg >> 16) ^ byte) & 0xFFu];
+    }
+    uint32_t poly = k ? POLY_B : POLY_A;
+    for (; i < n; i++) {
+        uint32_t fb = ((reg >> 23) ^ bits[i]) & 1u;
+        reg = ((reg << 1) & 0xFFFFFFu) ^ (fb ? poly : 0u);
+    }
+    return reg;
+}
+
+extern "C" uint32_t crn_crc24a(const uint8_t *bits, int64_t nbits) { return bits ? crc24(0, bits, nbits) : 0; }
+extern "C" uint32_t crn_crc24b(const uint8_t *bits, int64_t nbits) { return bits ? crc24(1, bits, nbits) : 0; }
+
+/* ------------------------------------------------------------------ segmentation (36.212 5.1.2) */
+extern "C" int crn_segment_tb(int64_t tbs, crn_seg *o) {
+    if (!o || tbs <= 0) return CRN_EINVAL;
+    const int64_t Z = 6144;
+    int64_t B = tbs + 24, C, L, Bp;
+    if (B <= Z) { L = 0; C = 1; Bp = B; }
+    else { L = 24; C = (B + Z - L - 1) / (Z - L); Bp = B + C * L; }
+    int ip = -1;
+    for (int i = 0; i < CRN_NUM_K; i++)
+        if (C * k_at(i) >= Bp) { ip = i; break; }
+    if (ip < 0) return CRN_EINVAL;
+    int64_t Kp = k_at(ip), Km = 0, Cm = 0;
+    if (C > 1) {
+        Km = ip > 0 ? k_at(ip - 1) : 0;
+        Cm = (C * Kp - Bp) / (Kp - Km);
+    }
+    o->C = (int32_t)C; o->Kplus = (int32_t)Kp; o->Kminus = (int32_t)Km;
+    o->Cminus = (int32_t)Cm; o->Cplus = (int32_t)(C - Cm);
+    o->F = (int32_t)((C - Cm) * Kp + Cm * Km - Bp);
+    o->L = (int32_t)L;
+    return CRN_OK;
+}
+
+extern "C" const char *crn_strerror(int code) {
+    switch (code) {
+        case CRN_OK: return "ok";
+        case CRN_EINVAL: return "invalid argument";
+        case CRN_ECUDA: return "CUDA error";
+        case CRN_ENOMEM: return "out of device memory";
+        case CRN_ENODEV: return "no usable sm_100 CUDA device";
+        default: return "unknown error";
+    }
+}
+
+extern "C" int64_t crn_counted_ops(const int32_t *K, int32_t n_cb, const uint8_t *iters, int32_t max_iters) {
+    /* 129 counted ops per trellis step per SISO + 90 for the three tail steps;
+     * two SISOs per iteration (pinned against the oracle's counter) */
+    int64_t s = 0;
+    for (int i = 0; i < n_cb; i++)
+        s += 2LL * (iters ? iters[i] : max_iters) * (129LL * K[i] + 90);
+    return s;
+}
+
+/* ------------------------------------------------------------------ device context */
+static bool check_device(int *dev) {
+    if (cudaGetDevice(dev) != cudaSuccess) return false;
+    int major = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, *dev) != cudaSuccess) return false;
+    return major == 10;
+}
+
+extern "C" int crn_device_info(int32_t *num_sms, int32_t *clock_khz, int32_t *cc_major, int32_t *cc_minor) {
+    int dev;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return CRN_ENODEV; }
+    int v;
+    if (num_sms) { cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev); *num_sms = v; }
+    if (clock_khz) { cudaDeviceGetAttribute(&v, cudaDevAttrClockRate, dev); *clock_khz = v; }
+    if (cc_major) { cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMajor, dev); *cc_major = v; }
+    if (cc_minor) { cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMinor, dev); *cc_minor = v; }
+    return CRN_OK;
+}
+
+struct DevTables {
+    uint32_t *qpp_wm = nullptr, *crc_pow = nullptr;
+    int32_t *qpp_off = nullptr, *crc_off = nullptr;
+    crn_tables tab{};
+    int grid = 0;
+};
+
+static std::mutex g_mu;
+static std::map<int, DevTables> g_tables;
+static std::map<std::pair<int, void *>, std::pair<void *, size_t>> g_ws;
+
+/* x^e mod g with the register convention of crc24 (low 24 bits of g = poly). */
+static uint32_t mulx_mod(uint32_t a, uint32_t poly) { return ((a << 1) ^ ((a & 0x800000u) ? poly : 0u)) & 0xFFFFFFu; }
+
+static int build_tables(int dev, DevTables **out) {
+    auto it = g_tables.find(dev);
+    if (it != g_tables.end()) { *out = &it->second; return CRN_OK; }
+    std::vector<uint32_t> qpp, cp;
+    std::vector<int32_t> qoff(CRN_NUM_K), coff(CRN_NUM_K);
+    for (int ki = 0; ki < CRN_NUM_K; ki++) {
+        int K = k_at(ki), M, W;
+        crn_windows(K, &M, &W);
+        int64_t f1 = crn_qpp_f1[ki], f2 = crn_qpp_f2[ki];
+        qoff[ki] = (int32_t)qpp.size();
+        qpp.resize(qpp.size() + (size_t)K);
+        for (int j = 0; j < M; j++)
+            for (int i = 0; i < W; i++) {
+                int64_t x = (int64_t)j * W + i;
+                uint32_t n = (uint32_t)((f1 * x + f2 * x % K * x) % K);
+                qpp[qoff[ki] + (size_t)i * M + j] = ((n % W) << 16) | (n / W);
+            }
+        coff[ki] = (int32_t)cp.size();
+        cp.resize(cp.size() + 2 * (size_t)M);
+        for (int k = 0; k < 2; k++) {
+            uint32_t poly = k ? POLY_B : POLY_A, p = 1;     /* x^0 */
+            for (int j = M - 1; j >= 0; j--) {
+                cp[coff[ki] + (size_t)k * M + j] = p;
+                for (int s = 0; s < W; s++) p = mulx_mod(p, poly);
+            }
+        }
+    }
+    DevTables t;
+    if (cudaMalloc(&t.qpp_wm, qpp.size() * 4) != cudaSuccess ||
+        cudaMalloc(&t.crc_pow, cp.size() * 4) != cudaSuccess ||
+        cudaMalloc(&t.qpp_off, CRN_NUM_K * 4) != cudaSuccess ||
+        cudaMalloc(&t.crc_off, CRN_NUM_K * 4) != cudaSuccess) {
+        cudaGetLastError();
+        return CRN_ENOMEM;
+    }
+    cudaMemcpy(t.qpp_wm, qpp.data(), qpp.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(t.crc_pow, cp.data(), cp.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(t.qpp_off, qoff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(t.crc_off, coff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
+    if (cudaGetLastError() != cudaSuccess) return CRN_ECUDA;
+    t.tab.qpp_wm = t.qpp_wm; t.tab.crc_pow = t.crc_pow;
+    t.tab.qpp_off = t.qpp_off; t.tab.crc_off = t.crc_off;
+    t.grid = crn_decode_grid(dev);
+    if (t.grid <= 0) return CRN_ECUDA;
+    auto r = g_tables.emplace(dev, t);
+    *out = &r.first->second;
+    return CRN_OK;
+}
+
+static int get_ctx(int *dev, DevTables **t) {
+    if (!check_device(dev)) { cudaGetLastError(); return CRN_ENODEV; }
+    std::lock_guard<std::mutex> lk(g_mu);
+    return build_tables(*dev, t);
+}
+
+static int get_ws(int dev, void *stream, size_t bytes, void **ws) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto key = std::make_pair(dev, stream);
+    auto it = g_ws.find(key);
+    if (it != g_ws.end() && it->second.second >= bytes) { *ws = it->second.first; return CRN_OK; }
+    if (it != g_ws.end()) { cudaFree(it->second.first); g_ws.erase(it); }
+    void *p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); return CRN_ENOMEM; }
+    g_ws[key] = std::make_pair(p, bytes);
+    *ws = p;
+    return CRN_OK;
+}
+
+extern "C" size_t crn_workspace_bytes(void) {
+    int dev;
+    DevTables *t;
+    if (get_ctx(&dev, &t) != CRN_OK) return 0;
+    return crn_decode_ws_bytes(t->grid);
+}
+
+/* ------------------------------------------------------------------ plans (row a1) */
+struct Plan {
+    int dev = -1;
+    int n_cb = 0, n_tasks = 0;
+    crn_cb_desc *d_desc = nullptr;
+    crn_task *d_tasks = nullptr;
+    crn_pair *d_pairs = nullptr;
+    void *mem = nullptr;          /* one allocation holding the three arrays */
+};
+
+static bool ranges_overlap(std::vector<std::pair<int64_t, int64_t>> &r) {
+    std::sort(r.begin(), r.end());
+    for (size_t i = 1; i < r.size(); i++)
+        if (r[i].first < r[i - 1].second) return true;
+    return false;
+}
+
+/* Validate descriptors (crn.h: CRN_EINVAL rules). */
+static int validate(const crn_cb_desc *d, int n, bool want_ext) {
+    std::vector<std::pair<int64_t, int64_t>> lr, br, er;
+    lr.reserve(n); br.reserve(n);
+    for (int i = 0; i < n; i++) {
+        const crn_cb_desc &c = d[i];
+        if (crn_k_index(c.K) < 0 || c.F < 0 || c.F > c.K - 25 || c.crc_kind < 0 || c.crc_kind > 2 ||
+            c.llr_off < 0 || c.bit_off < 0 || (want_ext && c.ext_off < 0))
+            return CRN_EINVAL;
+        lr.emplace_back(c.llr_off, c.llr_off + c.K + 4);
+        br.emplace_back(c.bit_off, c.bit_off + (c.K + 31) / 32);
+        if (want_ext) er.emplace_back(c.ext_off, c.ext_off + c.K);
+    }
+    if (ranges_overlap(lr) || ranges_overlap(br) || (want_ext && ranges_overlap(er))) return CRN_EINVAL;
+    return CRN_OK;
+}
+
+/* Bucket by K (largest first: longest tasks start first), pair equal-K CBs in
+ * index order, group ceil-free: floor(6144/K) pairs per task. */
+static void build_tasks(const crn_cb_desc *d, int n, std::vector<crn_task> &tasks, std::vector<crn_pair> &pairs) {
+    std::vector<int> idx(n);
+    for (int i = 0; i < n; i++) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return d[a].K > d[b].K; });
+    size_t s = 0;
+    while (s < idx.size()) {
+        int K = d[idx[s]].K;
+        size_t e = s;
+        while (e < idx.size() && d[idx[e]].K == K) e++;
+        int M, W;
+        crn_windows(K, &M, &W);
+        int per = std::max(1, CRN_TASK_SUMK / K);
+        int32_t first_pair = (int32_t)pairs.size();
+        for (size_t i = s; i < e; i += 2) pairs.push_back({idx[i], i + 1 < e ? idx[i + 1] : -1});
+        int32_t np = (int32_t)pairs.size() - first_pair;
+        for (int32_t p = 0; p < np; p += per) {
+            crn_task t;
+            t.K = K; t.M = M; t.W = W; t.n_pairs = std::min(per, np - p);
+            t.pair0 = first_pair + p; t.kidx = crn_k_index(K);
+            tasks.push_back(t);
+        }
+        s = e;
+    }
+}
+
+static int plan_build(const crn_cb_desc *desc, int n, bool want_ext, cudaStream_t st, bool async, Plan *P) {
+    int rc = validate(desc, n, want_ext);
+    if (rc) return rc;
+    std::vector<crn_task> tasks;
+    std::vector<crn_pair> pairs;
+    build_tasks(desc, n, tasks, pairs);
+    size_t b0 = sizeof(crn_cb_desc) * (size_t)n, b1 = sizeof(crn_task) * tasks.size(),
+           b2 = sizeof(crn_pair) * pairs.size();
+    size_t o1 = (b0 + 255) & ~(size_t)255, o2 = (o1 + b1 + 255) & ~(size_t)255, tot = o2 + b2 + 256;
+    std::vector<uint8_t> host(tot);
+    memcpy(host.data(), desc, b0);
+    memcpy(host.data() + o1, tasks.data(), b1);
+    memcpy(host.data() + o2, pairs.data(), b2);
+    cudaError_t e = async ? cudaMallocAsync(&P->mem, tot, st) : cudaMalloc(&P->mem, tot);
+    if (e != cudaSuccess) { cudaGetLastError(); return CRN_ENOMEM; }
+    if (cudaMemcpyAsync(P->mem, host.data(), tot, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+        cudaGetLastError();
+        return CRN_ECUDA;
+    }
+    if (!async && cudaStreamSynchronize(st) != cudaSuccess) return CRN_ECUDA;
+    P->n_cb = n;
+    P->n_tasks = (int)tasks.size();
+    P->d_desc = (crn_cb_desc *)P->mem;
+    P->d_tasks = (crn_task *)((uint8_t *)P->mem + o1);
+    P->d_pairs = (crn_pair *)((uint8_t *)P->mem + o2);
+    return CRN_OK;
+}
+
+static int launch(Plan *P, DevTables *t, const int16_t *l0, const int16_t *l1, const int16_t *l2,
+                  int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
+                  void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (P->n_cb == 0) return CRN_OK;
+    if (!ws) {
+        int rc = get_ws(P->dev, (void *)st, crn_decode_ws_bytes(t->grid), &ws);
+        if (rc) return rc;
+    } else if (ws_bytes < crn_decode_ws_bytes(t->grid)) {
+        return CRN_EINVAL;
+    }
+    return crn_launch_decode(P->d_desc, P->d_tasks, P->n_tasks, P->d_pairs, l0, l1, l2, max_iters, et,
+                             bits, ok, it, ext, &t->tab, ws, (void *)st, t->grid);
+}
+
+extern "C" int crn_plan_create(const crn_cb_desc *desc, int32_t n_cb, void **plan) {
+    if (!plan || n_cb < 0 || (n_cb > 0 && !desc)) return CRN_EINVAL;
+    int dev;
+    DevTables *t;
+    int rc = get_ctx(&dev, &t);
+    if (rc) return rc;
+    Plan *P = new Plan();
+    P->dev = dev;
+    rc = plan_build(desc, n_cb, true, 0, false, P);
+    if (rc) { delete P; return rc; }
+    *plan = P;
+    return CRN_OK;
+}
+
+extern "C" int crn_plan_decode(void *plan, const int16_t *l0, const int16_t *l1, const int16_t *l2,
+                               int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it,
+                               int16_t *ext, void *stream) {
+    Plan *P = (Plan *)plan;
+    if (!P || max_iters < 1 || max_iters > CRN_MAX_ITERS) return CRN_EINVAL;
+    if (P->n_cb && (!l0 || !l1 || !l2 || !bits || !ok)) return CRN_EINVAL;
+    int dev;
+    DevTables *t;
+    int rc = get_ctx(&dev, &t);
+    if (rc) return rc;
+    if (dev != P->dev) return CRN_EINVAL;
+    return launch(P, t, l0, l1, l2, max_iters, et, bits, ok, it, ext, nullptr, 0, (cudaStream_t)stream);
+}
+
+extern "C" int crn_plan_launches(void *plan) {
+    Plan *P = (Plan *)plan;
+    return (P && P->n_cb) ? 1 : 0;
+}
+
+extern "C" void crn_plan_destroy(void *plan) {
+    Plan *P = (Plan *)plan;
+    if (!P) return;
+    if (P->mem) cudaFree(P->mem);
+    delete P;
+}
+
+extern "C" int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb, const int16_t *l0,
+                                   const int16_t *l1, const int16_t *l2, int32_t max_iters,
+                                   int32_t et, int32_t flags, uint32_t *bits, uint8_t *ok,
+                                   uint8_t *it, int16_t *ext, void *ws, size_t ws_bytes, void *stream) {
+    if (n_cb < 0 || (flags & ~CRN_DESC_ON_DEVICE) || max_iters < 1 || max_iters > CRN_MAX_ITERS)
+        return CRN_EINVAL;
+    if (n_cb == 0) return CRN_OK;
+    if (!desc || !l0 || !l1 || !l2 || !bits || !ok) return CRN_EINVAL;
+    int dev;
+    DevTables *t;
+    int rc = get_ctx(&dev, &t);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<crn_cb_desc> hd;
+    const crn_cb_desc *hdesc = desc;
+    if (flags & CRN_DESC_ON_DEVICE) {       /* descriptors are needed on the host to bucket by K */
+        hd.resize(n_cb);
+        if (cudaMemcpyAsync(hd.data(), desc, sizeof(crn_cb_desc) * n_cb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+            cudaGetLastError();
+            return CRN_ECUDA;
+        }
+        hdesc = hd.data();
+    }
+    Plan P;
+    P.dev = dev;
+    rc = plan_build(hdesc, n_cb, ext != nullptr, st, true, &P);
+    if (rc) {
+        if (P.mem) cudaFreeAsync(P.mem, st);
+        return rc;
+    }
+    rc = launch(&P, t, l0, l1, l2, max_iters, et, bits, ok, it, ext, ws, ws_bytes, st);
+    cudaFreeAsync(P.mem, st);
+    return rc;
+}
+
+extern "C" int crn_decode_batch(const int16_t *l0, const int16_t *l1, const int16_t *l2, const int32_t *K,
+                                int32_t n_cb, int32_t iters, uint32_t *bits, uint8_t *ok) {
+    if (n_cb < 0 || iters == 0 || iters > CRN_MAX_ITERS || iters < -CRN_MAX_ITERS) return CRN_EINVAL;
+    if (n_cb == 0) return CRN_OK;
+    if (!K) return CRN_EINVAL;
+    std::vector<crn_cb_desc> d(n_cb);
+    int64_t lo = 0, bo = 0;
+    for (int i = 0; i < n_cb; i++) {
+        d[i].K = K[i]; d[i].F = 0; d[i].crc_kind = CRN_CRC24B; d[i].reserved = 0;
+        d[i].llr_off = lo; d[i].bit_off = bo; d[i].ext_off = 0;
+        lo += (int64_t)K[i] + 4;
+        bo += ((int64_t)K[i] + 31) / 32;
+    }
+    return crn_decode_batch_ex(d.data(), n_cb, l0, l1, l2, iters > 0 ? iters : -iters, iters < 0, 0, bits,
+                               ok, nullptr, nullptr, nullptr, 0, nullptr);
+}
+
+/* ------------------------------------------------------------------ encode / ubench wrappers */
+extern "C" int crn_encode_batch(const crn_cb_desc *desc, int32_t n_cb, const uint8_t *info, int32_t attach_crc,
+                                uint8_t *d0, uint8_t *d1, uint8_t *d2, void *stream) {
+    if (n_cb < 0) return CRN_EINVAL;
+    if (n_cb == 0) return CRN_OK;
+    if (!desc || !info || !d0 || !d1 || !d2) return CRN_EINVAL;
+    for (int i = 0; i < n_cb; i++)
+        if (crn_k_index(desc[i].K) < 0 || desc[i].F < 0 || desc[i].F > desc[i].K - 25 ||
+            desc[i].crc_kind < 0 || desc[i].crc_kind > 2 || desc[i].llr_off < 0 || desc[i].ext_off < 0)
+            return CRN_EINVAL;
+    int dev;
+    DevTables *t;
+    int rc = get_ctx(&dev, &t);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    void *dd = nullptr;
+    size_t b = sizeof(crn_cb_desc) * (size_t)n_cb;
+    if (cudaMallocAsync(&dd, b, st) != cudaSuccess) { cudaGetLastError(); return CRN_ENOMEM; }
+    cudaMemcpyAsync(dd, desc, b, cudaMemcpyHostToDevice, st);
+    rc = crn_launch_encode((const crn_cb_desc *)dd, n_cb, info, attach_crc, d0, d1, d2, &t->tab, (void *)st);
+    cudaFreeAsync(dd, st);
+    return rc;
+}
+
+extern "C" int crn_ubench_int16x2(int32_t op, int64_t *lane_instr, float *ms, int64_t *cycles) {
+    int dev;
+    if (!check_device(&dev)) { cudaGetLastError(); return CRN_ENODEV; }
+    if (op < 0 || op > 3 || !lane_instr || !ms || !cycles) return CRN_EINVAL;
+    return crn_launch_ubench(op, lane_instr, ms, cycles);
+}
+
+/* ------------------------------------------------------------------ TB <-> CB (row a1, host) */
+extern "C" int crn_tb_build_cbs(const uint8_t *tb, int64_t tbs, int32_t max_cb, int64_t base_bit,
+                                int64_t base_llr, int64_t base_word, uint8_t *cb_bits, crn_cb_desc *desc,
+                                int32_t *n_cb) {
+    if (!tb || !cb_bits || !desc || !n_cb) return CRN_EINVAL;
+    crn_seg s;
+    if (crn_segment_tb(tbs, &s) != CRN_OK || s.C > max_cb) return CRN_EINVAL;
+    std::vector<uint8_t> b((size_t)tbs + 24);
+    for (int64_t i = 0; i < tbs; i++) b[i] = tb[i] & 1u;
+    uint32_t r = crc24(0, b.data(), tbs);
+    for (int i = 0; i < 24; i++) b[tbs + i] = (uint8_t)((r >> (23 - i)) & 1u);
+    int64_t src = 0, bit = 0, llr = 0, word = 0;
+    for (int c = 0; c < s.C; c++) {
+        int K = c < s.Cminus ? s.Kminus : s.Kplus, F = c == 0 ? s.F : 0;
+        uint8_t *o = cb_bits + bit;
+        for (int k = 0; k < F; k++) o[k] = 0;
+        for (int k = F; k < K - s.L; k++) o[k] = b[src++];
+        if (s.C > 1) {
+            uint32_t rb = crc24(1, o, K - 24);
+            for (int i = 0; i < 24; i++) o[K - 24 + i] = (uint8_t)((rb >> (23 - i)) & 1u);
+        }
+        crn_cb_desc &d = desc[c];
+        d.K = K; d.F = F; d.crc_kind = s.C > 1 ? CRN_CRC24B : CRN_CRC24A; d.reserved = 0;
+        d.ext_off = base_bit + bit; d.llr_off = base_llr + llr; d.bit_off = base_word + word;
+        bit += K; llr += K + 4; word += (K + 31) / 32;
+    }
+    *n_cb = s.C;
+    return src == tbs + 24 ? CRN_OK : CRN_EINVAL;
+}
+
+extern "C" int crn_tb_reassemble(const uint32_t *w, const crn_cb_desc *desc, const uint8_t *ok, int32_t n_cb,
+                                 int64_t tbs, uint8_t *out) {
+    if (!w || !desc || !ok || n_cb < 1) return CRN_EINVAL;
+    crn_seg s;
+    if (crn_segment_tb(tbs, &s) != CRN_OK || s.C != n_cb) return CRN_EINVAL;
+    std::vector<uint8_t> b;
+    b.reserve((size_t)tbs + 24);
+    bool all = true;
+    for (int c = 0; c < n_cb; c++) {
+        const crn_cb_desc &d = desc[c];
+        all = all && ok[c];
+        for (int k = d.F; k < d.K - s.L; k++) b.push_back((uint8_t)((w[d.bit_off + k / 32] >> (k % 32)) & 1u));
+    }
+    if ((int64_t)b.size() != tbs + 24) return CRN_EINVAL;
+    if (!all || crc24(0, b.data(), tbs + 24) != 0) return 0;
+    if (out) memcpy(out, b.data(), (size_t)tbs);
+    return 1;
+}

@@ -1,0 +1,57 @@
+/* crn_internal.h -- structures shared by libcrn's host code and its kernels.
+ * Not part of the ABI (see include/crn.h). */
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/crn.h"
+
+#define CRN_NSTATE 8
+/* Decode work unit: one CTA task = n_pairs pairs of CBs with the same K; the
+ * two CBs of a pair share every int16x2 register (lo half / hi half), so all
+ * trellis arithmetic is pair-SIMD and the 8-state butterfly is a register
+ * rename.  Thread t = p*M + j owns window j of pair p.  Sum of K over a task
+ * is <= CRN_TASK_SUMK, hence T = n_pairs*M <= CRN_TASK_SUMK/32 = CRN_CTA_THREADS. */
+#define CRN_TASK_SUMK 6144
+#define CRN_CTA_THREADS 192
+
+typedef struct {
+    int32_t K, M, W, n_pairs;
+    int32_t pair0;   /* first pair index of the task */
+    int32_t kidx;    /* index of K in the size table */
+} crn_task;
+
+typedef struct {
+    int32_t lo, hi;  /* CB indices; hi = -1 for the dummy partner of an odd bucket */
+} crn_pair;
+
+/* Per-device constant tables (built once on the host, uploaded once). */
+typedef struct {
+    const uint32_t *qpp_wm;   /* per K at qpp_off[kidx]: [i*M + j] = (Pi(jW+i) % W) << 16 | Pi(jW+i) / W */
+    const uint32_t *crc_pow;  /* per K at crc_off[kidx]: [kind(0=A,1=B)*M + j] = x^((M-1-j)W) mod g */
+    const int32_t *qpp_off;
+    const int32_t *crc_off;
+} crn_tables;
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* crn_decode.cu */
+int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_tasks, int32_t n_tasks,
+                      const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1,
+                      const int16_t *l2, int32_t max_iters, int32_t early_term,
+                      uint32_t *out_bits, uint8_t *crc_ok, uint8_t *iters_used, int16_t *ext_out,
+                      const crn_tables *tab, void *ws, void *stream, int32_t grid);
+size_t crn_decode_ws_bytes(int32_t grid);
+int crn_decode_grid(int device);
+/* crn_encode.cu */
+int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const uint8_t *info,
+                      int32_t attach_crc, uint8_t *d0, uint8_t *d1, uint8_t *d2,
+                      const crn_tables *tab, void *stream);
+/* crn_ubench.cu */
+int crn_launch_ubench(int32_t op, int64_t *lane_instr, float *ms, int64_t *cycles_per_block);
+/* crn_host.cpp */
+int crn_k_index(int32_t K);
+#ifdef __cplusplus
+}
+#endif

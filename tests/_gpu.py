@@ -1,0 +1,55 @@
+"""GPU-side helpers for the parity tests: run libcrn on a product-built batch and
+the oracle on the very same LLR buffers, then compare element by element."""
+import os
+
+import numpy as np
+import torch
+
+from paper_1905_01141_b200 import batch as bmod
+from paper_1905_01141_b200 import crn
+
+
+def run_gpu(b, max_iters, et, want_ext=True, stream=None, desc=None, l=None):
+    desc = b.desc if desc is None else desc
+    bits, ok, it, ext = bmod.outputs(b, want_ext=want_ext)
+    l0, l1, l2 = b.llr if l is None else l
+    crn.decode_batch_ex(desc, desc.size, l0, l1, l2, max_iters, et, 0, bits, ok, it, ext, stream=stream)
+    torch.cuda.synchronize()
+    return dict(words=bits.cpu().numpy().view(np.uint32), crc_ok=ok.cpu().numpy()[:desc.size],
+                iters=it.cpu().numpy()[:desc.size], ext=None if ext is None else ext.cpu().numpy())
+
+
+def unpack(words, desc, i):
+    K, o = int(desc["K"][i]), int(desc["bit_off"][i])
+    w = words[o:o + (K + 31) // 32]
+    return ((w[:, None] >> np.arange(32, dtype=np.uint32)) & 1).astype(np.uint8).reshape(-1)[:K]
+
+
+def run_oracle(b, idx, max_iters, et):
+    import oracle
+    host = [x.cpu().numpy() for x in b.llr]
+    d = b.desc[np.asarray(idx)]
+    K = d["K"].astype(np.int32)
+    lo = np.concatenate([[0], np.cumsum(K + 4)[:-1]]).astype(np.int64)
+    bo = np.concatenate([[0], np.cumsum(K)[:-1]]).astype(np.int64)
+    ll = [np.concatenate([h[o:o + k + 4] for o, k in zip(d["llr_off"], K)]) if K.size else h[:0] for h in host]
+    r = oracle.decode_batch(K, d["F"], d["crc_kind"], lo, bo, *ll, max_iters=max_iters, early_term=et,
+                            nthreads=os.cpu_count() or 1)
+    assert r["violations"] == 0
+    r["bo"], r["K"] = bo, K
+    return r
+
+
+def assert_parity(b, g, r, idx):
+    desc = b.desc
+    for n, i in enumerate(idx):
+        K = int(desc["K"][i])
+        ob = r["bits"][r["bo"][n]:r["bo"][n] + K]
+        gb = unpack(g["words"], desc, i)
+        assert np.array_equal(gb, ob), f"bits CB {i} K={K}: {np.flatnonzero(gb != ob)[:8]}"
+        assert g["crc_ok"][i] == r["crc_ok"][n], f"crc_ok CB {i}"
+        assert g["iters"][i] == r["iters"][n], f"iters CB {i}: {g['iters'][i]} vs {r['iters'][n]}"
+        if g["ext"] is not None:
+            e = int(desc["ext_off"][i])
+            ge, oe = g["ext"][e:e + K], r["ext"][r["bo"][n]:r["bo"][n] + K]
+            assert np.array_equal(ge, oe), f"ext CB {i}: {np.flatnonzero(ge != oe)[:8]}"

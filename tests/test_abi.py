@@ -1,0 +1,115 @@
+"""CPU tests of the C-ABI library: it builds, loads, exports every symbol
+include/crn.h declares, its host helpers agree with the oracle, and its decode
+entry points refuse to run without a GPU (no CPU fallback)."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1905_01141_b200 import build as crn_build
+from paper_1905_01141_b200 import crn
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    crn_build.build()
+    return crn.lib()
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "crn.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(crn_\w+)\s*\(", txt)))
+
+
+def test_exports_every_declared_symbol(L):
+    syms = header_symbols()
+    assert len(syms) >= 19
+    out = subprocess.check_output(["nm", "-D", "--defined-only", crn.SO]).decode()
+    exported = set(re.findall(r"\sT\s(crn_\w+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    for s in syms:
+        assert hasattr(L, s)
+
+
+def test_sm100a_sass_present(L):
+    out = subprocess.check_output(["cuobjdump", "--list-elf", crn.SO]).decode()
+    assert "sm_100a" in out
+
+
+def test_qpp_table_matches_oracle_copy(L, orc):
+    for K in orc.k_table():
+        assert crn.qpp_params(K) == orc.qpp_params(K)
+        M, W = crn.windows(K)
+        assert M == orc.num_windows(K, 32) and M * W == K
+    for K in (0, 39, 41, 6145, 520):
+        with pytest.raises(crn.CrnError):
+            crn.qpp_params(K)
+
+
+def test_segmentation_and_crc_match_oracle(L, orc):
+    rng = np.random.default_rng(0)
+    for tbs in list(rng.integers(1, 200000, 300)) + [16, 6120, 6121, 75376]:
+        assert crn.segment_tb(int(tbs)) == orc.segment(int(tbs))
+    for n in (1, 7, 8, 9, 64, 1000, 6143):
+        b = rng.integers(0, 2, n, dtype=np.uint8)
+        assert crn.crc24a(b) == orc.crc24a(b) and crn.crc24b(b) == orc.crc24b(b)
+
+
+def test_tb_build_and_reassemble_match_oracle(L, orc):
+    rng = np.random.default_rng(1)
+    for tbs in (16, 1000, 4000, 6121, 12000, 75376):
+        a = rng.integers(0, 2, tbs, dtype=np.uint8)
+        bits, desc = crn.tb_build_cbs(a)
+        cbs, Fs, seg = orc.segment_tb_bits(a)
+        assert np.array_equal(bits, np.concatenate(cbs))
+        assert list(desc["F"]) == Fs and list(desc["K"]) == [c.size for c in cbs]
+        # pack LSB-first as the decoder does, then reassemble
+        words = np.zeros(int((desc["bit_off"] + (desc["K"] + 31) // 32).max()), np.uint32)
+        for d, c in zip(desc, cbs):
+            for k, v in enumerate(c):
+                words[d["bit_off"] + k // 32] |= np.uint32(int(v) << (k % 32))
+        ok = np.ones(desc.size, np.uint8)
+        assert np.array_equal(crn.tb_reassemble(words, desc, ok, tbs), a)
+        ok[-1] = 0
+        assert crn.tb_reassemble(words, desc, ok, tbs) is None
+
+
+def test_counted_ops_matches_oracle_counter(L, orc):
+    rng = np.random.default_rng(2)
+    Ks = [40, 528, 1056]
+    tot = 0
+    for K in Ks:
+        ll = [rng.integers(-300, 301, K + 4).astype(np.int16) for _ in range(3)]
+        tot += orc.decode_cb(*ll, max_iters=3)["ops"]
+    assert crn.counted_ops(Ks, 3) == tot
+    assert crn.counted_ops(Ks, 8, iters_used=[3, 3, 3]) == tot
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1905_01141_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cpp", ".h")):
+                txt = open(os.path.join(dp, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), f
+                assert "oracle.h" not in txt and "liboracle" not in txt, f
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_decode_refuses_without_gpu(L):
+    import ctypes as C
+    K = np.array([1056], np.int32)
+    rc = L.crn_decode_batch(None, None, None, K.ctypes.data_as(C.POINTER(C.c_int32)), 1, 6, None, None)
+    assert rc in (crn.CRN_EINVAL, crn.CRN_ENODEV)
+    d = np.zeros(1, crn.DESC_DTYPE)
+    d["K"] = 1056
+    rc = L.crn_decode_batch_ex(d.ctypes.data, 1, 1, 1, 1, 6, 0, 0, 1, 1, None, None, None, 0, None)
+    assert rc == crn.CRN_ENODEV
+    assert L.crn_workspace_bytes() == 0

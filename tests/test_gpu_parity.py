@@ -1,0 +1,226 @@
+"""GPU parity: libcrn (CUDA, sm_100a) vs the CPU oracle, bit-exact on packed
+hard decisions, int16 extrinsics, iteration counts and CRC flags, for every
+BASELINE config (cfg4 at full size on sampled CBs) and the edge cases."""
+import numpy as np
+import pytest
+import torch
+
+from paper_1905_01141_b200 import batch as bmod
+from paper_1905_01141_b200 import build as crn_build
+from paper_1905_01141_b200 import crn
+from paper_1905_01141_b200 import workload as wlmod
+from tests._gpu import assert_parity, run_gpu, run_oracle, unpack
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    crn_build.build()
+    crn.lib()
+    assert torch.cuda.is_available()
+
+
+def _full(cfg, scale=1.0, seed=0):
+    wl = wlmod.make_workload(cfg, seed=seed, device="cuda", scale=scale)
+    return bmod.build(wl)
+
+
+def test_encoder_matches_oracle(orc):
+    for cfg, scale in ((1, 1.0), (2, 1.0), (3, 0.2), (5, 1.0)):
+        b = _full(cfg, scale)
+        info = b.info.cpu().numpy()
+        coded = [x.cpu().numpy() for x in b.coded]
+        for i in range(b.n_cb):
+            d = b.desc[i]
+            c = info[d["ext_off"]:d["ext_off"] + d["K"]].copy()
+            if b.wl.tb_kind == "cb":
+                c = orc.crc_attach(orc.CRC24B, c[:-24])
+            e = orc.turbo_encode(c)
+            for s in range(3):
+                assert np.array_equal(coded[s][d["llr_off"]:d["llr_off"] + d["K"] + 4], e[s]), (cfg, i, s)
+
+
+@pytest.mark.parametrize("cfg,scale", [(1, 1.0), (2, 1.0), (3, 0.2), (5, 1.0)])
+def test_config_parity_full(orc, cfg, scale):
+    b = _full(cfg, scale)
+    I, et = b.wl.max_iters, b.wl.early_term
+    g = run_gpu(b, I, et)
+    idx = np.arange(b.n_cb)
+    r = run_oracle(b, idx, I, et)
+    assert_parity(b, g, r, idx)
+
+
+def test_cfg4_full_size_sampled(orc):
+    """BASELINE cfg 4 at its full size (65,536 CBs, K=6144, 8 fixed iterations) in
+    the launch configuration bench.py times; the oracle checks a seeded sample."""
+    b = _full(4)
+    assert b.n_cb == 65536
+    g = run_gpu(b, 8, False)
+    rng = np.random.default_rng(0)
+    idx = np.sort(np.r_[0, 1, b.n_cb - 1, rng.choice(b.n_cb, 45, replace=False)])
+    r = run_oracle(b, idx, 8, False)
+    assert_parity(b, g, r, idx)
+    assert np.all(g["iters"] == 8)
+
+
+def _desc_for(K_list, F_list=None, kinds=None):
+    K = np.asarray(K_list, np.int64)
+    d = np.zeros(K.size, crn.DESC_DTYPE)
+    d["K"] = K
+    d["F"] = 0 if F_list is None else F_list
+    d["crc_kind"] = crn.CRC24B if kinds is None else kinds
+    d["llr_off"] = np.concatenate([[0], np.cumsum(K + 4)[:-1]])
+    d["bit_off"] = np.concatenate([[0], np.cumsum((K + 31) // 32)[:-1]])
+    d["ext_off"] = np.concatenate([[0], np.cumsum(K)[:-1]])
+    return d
+
+
+class _B:
+    """A raw batch (descriptor + LLR buffers) not produced by the workload."""
+
+    def __init__(self, desc, llr):
+        self.desc, self.llr = desc, llr
+        self.n_cb = desc.size
+        self.n_words = int((desc["bit_off"] + (desc["K"] + 31) // 32).max())
+        self.wl = None
+
+
+def _random_llr(desc, rng, lim):
+    n = int((desc["llr_off"] + desc["K"] + 4).max())
+    return tuple(torch.from_numpy(rng.integers(-lim, lim + 1, n).astype(np.int16)).cuda() for _ in range(3))
+
+
+def _raw_parity(desc, llr, I, et):
+    b = _B(desc, llr)
+    bits = torch.zeros(b.n_words, dtype=torch.int32, device="cuda")
+    ok = torch.zeros(desc.size, dtype=torch.uint8, device="cuda")
+    it = torch.zeros(desc.size, dtype=torch.uint8, device="cuda")
+    ext = torch.zeros(int(desc["K"].sum()), dtype=torch.int16, device="cuda")
+    crn.decode_batch_ex(desc, desc.size, *llr, I, et, 0, bits, ok, it, ext)
+    torch.cuda.synchronize()
+    g = dict(words=bits.cpu().numpy().view(np.uint32), crc_ok=ok.cpu().numpy(), iters=it.cpu().numpy(),
+             ext=ext.cpu().numpy())
+    idx = np.arange(desc.size)
+    r = run_oracle(b, idx, I, et)
+    assert_parity(b, g, r, idx)
+    return g
+
+
+def test_every_k_ragged_and_adversarial(orc):
+    """All 188 sizes once (odd buckets -> dummy partner lanes, every window
+    length 32..62), random fillers up to K-25, all CRC kinds, saturated and
+    out-of-range LLRs (clamp path)."""
+    rng = np.random.default_rng(7)
+    Ks = orc.k_table()
+    F = [int(rng.integers(0, K - 24)) if i % 3 == 0 else 0 for i, K in enumerate(Ks)]
+    kinds = [i % 3 for i in range(len(Ks))]
+    d = _desc_for(Ks, F, kinds)
+    for lim in (300, 32767):
+        _raw_parity(d, _random_llr(d, rng, lim), 3, False)
+
+
+def test_many_small_blocks_multi_pair_tasks(orc):
+    rng = np.random.default_rng(8)
+    Ks = [40] * 301 + [48] * 7 + [64] * 130 + [1056] * 5
+    d = _desc_for(list(rng.permutation(Ks)))
+    _raw_parity(d, _random_llr(d, rng, 200), 4, False)
+
+
+def test_iteration_extremes_and_et(orc):
+    rng = np.random.default_rng(9)
+    d = _desc_for([6144, 6144, 6144, 512, 40])
+    llr = _random_llr(d, rng, 100)
+    _raw_parity(d, llr, 1, False)
+    _raw_parity(d, llr, 32, True)
+
+
+def test_zero_llrs_fail_at_max(orc):
+    d = _desc_for([40, 1056, 6144], [0, 8, 100], [2, 1, 2])
+    n = int((d["llr_off"] + d["K"] + 4).max())
+    z = tuple(torch.zeros(n, dtype=torch.int16, device="cuda") for _ in range(3))
+    g = _raw_parity(d, z, 5, True)
+    assert np.all(g["crc_ok"] == 0) and np.all(g["iters"] == 5)
+
+
+def test_batch_order_and_composition_invariance(orc):
+    b = _full(5)
+    g = run_gpu(b, 8, True)
+    rng = np.random.default_rng(3)
+    perm = rng.permutation(b.n_cb)
+    d2 = b.desc[perm].copy()
+    g2 = run_gpu(b, 8, True, desc=d2)
+    for i in range(b.n_cb):
+        assert np.array_equal(unpack(g["words"], b.desc, i), unpack(g2["words"], b.desc, i))
+    assert np.array_equal(g["crc_ok"][perm], g2["crc_ok"]) and np.array_equal(g["iters"][perm], g2["iters"])
+    sub = b.desc[perm[:37]].copy()
+    g3 = run_gpu(b, 8, True, desc=sub)
+    assert np.array_equal(g3["iters"], g["iters"][perm[:37]])
+    g4 = run_gpu(b, 8, True)                                    # run twice: identical
+    assert np.array_equal(g4["words"], g["words"]) and np.array_equal(g4["ext"], g["ext"])
+
+
+def test_plan_simple_api_and_device_descriptors(orc):
+    b = _full(1)
+    g = run_gpu(b, 6, False)
+    # plan API
+    bits, ok, it, ext = bmod.outputs(b)
+    p = crn.Plan(b.desc)
+    assert p.launches == 1
+    p.decode(*b.llr, 6, False, bits, ok, it, ext)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits.cpu().numpy().view(np.uint32), g["words"])
+    assert np.array_equal(ext.cpu().numpy(), g["ext"])
+    p.close()
+    # BASELINE.json form (dense layout, CRC24B, fixed iterations)
+    bits2 = torch.zeros_like(bits)
+    ok2 = torch.zeros_like(ok)
+    crn.decode_batch(*b.llr, b.K, b.n_cb, 6, bits2, ok2)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits2.cpu().numpy().view(np.uint32), g["words"])
+    assert np.array_equal(ok2.cpu().numpy()[:b.n_cb], g["crc_ok"])
+    # descriptors in device memory
+    dd = torch.from_numpy(b.desc.view(np.uint8).copy()).cuda()
+    bits3 = torch.zeros_like(bits)
+    crn.decode_batch_ex(dd, b.n_cb, *b.llr, 6, False, crn.DESC_ON_DEVICE, bits3, ok)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits3.cpu().numpy().view(np.uint32), g["words"])
+
+
+def test_streams_and_invalid_args(orc):
+    b = _full(5)
+    g = run_gpu(b, 8, True)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        g2 = run_gpu(b, 8, True, stream=s)
+    assert np.array_equal(g["words"], g2["words"])
+    bits, ok, it, ext = bmod.outputs(b)
+    bad = b.desc.copy()
+    bad["K"][0] = 41
+    with pytest.raises(crn.CrnError):
+        crn.decode_batch_ex(bad, bad.size, *b.llr, 8, True, 0, bits, ok)
+    bad = b.desc.copy()
+    bad["llr_off"][1] = bad["llr_off"][0]          # overlapping inputs
+    with pytest.raises(crn.CrnError):
+        crn.decode_batch_ex(bad, bad.size, *b.llr, 8, True, 0, bits, ok)
+    with pytest.raises(crn.CrnError):
+        crn.decode_batch_ex(b.desc, b.n_cb, *b.llr, 33, True, 0, bits, ok)
+    crn.decode_batch_ex(b.desc[:0], 0, *b.llr, 8, True, 0, bits, ok)   # n_cb == 0 no-op
+
+
+def test_tb_configs_tb_verdict(orc):
+    """cfg2/cfg3 transport blocks: TB success iff all CBs pass and the TB CRC24A
+    passes; successful TBs reproduce the payload."""
+    for cfg, scale in ((2, 1.0), (3, 0.1)):
+        b = _full(cfg, scale)
+        g = run_gpu(b, 8, True)
+        n_ok = 0
+        for t in range(b.wl.n_tb):
+            idx = np.flatnonzero(b.cb_tb == t)
+            pay = crn.tb_reassemble(g["words"], b.desc[idx], g["crc_ok"][idx], int(b.wl.tbs[t]))
+            if pay is not None:
+                n_ok += 1
+                assert np.array_equal(pay, b.wl.payload[t].cpu().numpy())
+            else:
+                assert not np.all(g["crc_ok"][idx])
+        assert n_ok >= 1
