@@ -38,13 +38,6 @@ def _dist():
     return ws, rank, local
 
 
-def _cells(rank, ws):
-    per = N_CELLS // ws
-    extra = N_CELLS % ws
-    lo = rank * per + min(rank, extra)
-    return list(range(lo, lo + per + (1 if rank < extra else 0)))
-
-
 def _workload_name(iters):
     return f"cfg4: 65536 CBs (256 cells x 256) K=6144, BPSK Eb/N0=1.0 dB, int16 LLR, {iters} fixed iterations"
 
@@ -167,6 +160,7 @@ def run_crn(args):
     from paper_1905_01141_b200 import batch as bmod
     from paper_1905_01141_b200 import build as crn_build
     from paper_1905_01141_b200 import crn
+    from paper_1905_01141_b200 import shard
     from paper_1905_01141_b200 import workload as wlmod
 
     ws, rank, local = _dist()
@@ -178,7 +172,7 @@ def run_crn(args):
     crn_build.build()
     dev = crn.device_info()
 
-    cells = _cells(rank, ws)
+    cells = shard.cells_for_rank(rank, ws, N_CELLS)
     wl = wlmod.make_workload(CFG, seed=args.seed, cells=cells, device="cuda")
     b = bmod.build(wl)
     del wl.payload
@@ -205,6 +199,7 @@ def run_crn(args):
     t_all0 = torch.cuda.Event(enable_timing=True)
     t_all1 = torch.cuda.Event(enable_timing=True)
     barrier()
+    torch.cuda.nvtx.range_push("timed")
     t_all0.record(stream)
     for k in range(args.steps):
         ev[k][0].record(stream)
@@ -212,20 +207,17 @@ def run_crn(args):
         ev[k][1].record(stream)
     t_all1.record(stream)
     barrier()
+    torch.cuda.nvtx.range_pop()
     clocks = clk.stop()
     ms_total = t_all0.elapsed_time(t_all1)
     launch_ms = [a.elapsed_time(z) for a, z in ev]
 
     # outputs of the last step: counters (one NCCL reduction, DESIGN.md multi-GPU)
-    crc = ok[:b.n_cb].to(torch.int64)
-    counters = torch.tensor([b.n_cb, int(crc.sum().item()), b.info_bits(), int(b.K.sum()),
-                             crn.counted_ops(b.K, iters)], dtype=torch.float64, device="cuda")
-    tmax = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(counters, op=dist.ReduceOp.SUM)
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    n_cb, n_ok, info_bits, sum_k, ops = (int(x) for x in counters.tolist())
-    ms_step = tmax.item() / args.steps
+    n_ok_local = int(ok[:b.n_cb].to(torch.int64).sum().item())
+    c, tmax = shard.reduce_counters([b.n_cb, n_ok_local, b.info_bits(), int(b.K.sum()),
+                                     crn.counted_ops(b.K, iters)], ms_total, dist, device="cuda")
+    n_cb, n_ok, info_bits, sum_k, ops = (c[k] for k in shard.COUNTERS)
+    ms_step = tmax / args.steps
     value = info_bits / (ms_step * 1e-3) / 1e6
 
     # ---- e2e: host (pinned) LLRs -> device -> decode -> bits + crc back, every step

@@ -38,7 +38,8 @@ constexpr u32 POLY_A = 0x864CFBu, POLY_B = 0x800063u;
 
 /* workspace slot (u32 words) */
 constexpr int A_LS = 0, A_LP1 = SUMK, A_LP2 = 2 * SUMK, A_LSI = 3 * SUMK, A_X = 4 * SUMK, A_Y = 5 * SUMK;
-constexpr int A_NII = 6 * SUMK;                 /* [c][parity][alpha/beta][s][TMAX] */
+constexpr int A_Z = 6 * SUMK;                   /* fast path: Le2 in interleaved order */
+constexpr int A_NII = 7 * SUMK;                 /* [c][parity][alpha/beta][s][TMAX] */
 constexpr int NII_WORDS = 2 * 2 * 2 * NS * TMAX;
 constexpr int A_TAIL = A_NII + NII_WORDS;       /* [pair][12] */
 constexpr int SLOT_WORDS = A_TAIL + MAXP * 12;
@@ -236,6 +237,320 @@ __device__ __forceinline__ void siso(const Ctx &c) {
     for (int s = 0; s < NS; s++) *nii_at(0, wr, s, t) = a[s];          /* alpha_{(j+1)W} -> window j+1 */
 }
 
+/* ======================================================================
+ * Fast path: W = 32 (every K that is a multiple of 32: all K >= 1056 and 15
+ * of the smaller sizes).  Compile-time window length, so every per-step
+ * index is an immediate.  The window's inputs are loaded into registers at
+ * the start of each half-iteration (window-major workspace, row stride TS);
+ * the alpha and beta recursions run concurrently ("crossing": alpha forward
+ * from the window start, beta backward from its end; the first half stores
+ * both, the second half pairs each new metric with the stored one of the
+ * other sweep and emits two extrinsics per step); stored metrics live in
+ * shared memory at (slot*16 + k)*TS + t.  State metrics are kept biased by
+ * -1 (a~ = a - 1), which turns the normaliser's negation into one NOT:
+ * ~(m - 1) = -m.  Exact: every value stays within int16.
+ * ====================================================================== */
+constexpr int TS = TMAX;                       /* fast-path row stride (words) */
+constexpr u32 M1 = 0xFFFFFFFFu;               /* (-1, -1): biased 0           */
+constexpr u32 FLOORB = 0xDFFFDFFFu;           /* (-8193, -8193): biased floor */
+constexpr u32 NEG4097 = 0xEFFFEFFFu, ONE2 = 0x00010001u;
+
+__device__ __forceinline__ void norm8b(u32 v[NS]) {
+    u32 m0 = __vimax3_s16x2(v[0], v[1], v[2]);
+    u32 m1 = __vimax3_s16x2(v[3], v[4], v[5]);
+    u32 m = __vimax3_s16x2(v[6], v[7], m0);
+    m = __vmaxs2(m, m1);
+    const u32 nm = ~m;                         /* biased: ~(m - 1) = -m */
+#pragma unroll
+    for (int s = 0; s < NS; s++) v[s] = vaddmax(v[s], nm, FLOORB);
+}
+
+__device__ __forceinline__ void alpha_step_b(u32 a[NS], u32 Lu, u32 Lp, u32 Lup) {
+    u32 an[NS];
+#pragma unroll
+    for (int Sp = 0; Sp < NS; Sp++) {
+        const int S0 = 2 * (Sp & 3), S1 = S0 + 1;
+        const int u0 = (nxt(S0, 0) == Sp) ? 0 : 1, u1 = (nxt(S1, 0) == Sp) ? 0 : 1;
+        const int z0 = par(S0, u0), z1 = par(S1, u1);
+        if (!u0 && !z0) an[Sp] = vaddmax(a[S1], gsel(u1, z1, Lu, Lp, Lup), a[S0]);
+        else if (!u1 && !z1) an[Sp] = vaddmax(a[S0], gsel(u0, z0, Lu, Lp, Lup), a[S1]);
+        else an[Sp] = vaddmax(a[S1], gsel(u1, z1, Lu, Lp, Lup), vadd(a[S0], gsel(u0, z0, Lu, Lp, Lup)));
+    }
+    norm8b(an);
+#pragma unroll
+    for (int s = 0; s < NS; s++) a[s] = an[s];
+}
+
+__device__ __forceinline__ void beta_step_b(u32 b[NS], u32 Lu, u32 Lp, u32 Lup) {
+    u32 v[NS];
+#pragma unroll
+    for (int S = 0; S < NS; S++) {
+        const int n0 = nxt(S, 0), n1 = nxt(S, 1), z0 = par(S, 0), z1 = par(S, 1);
+        if (!z0) v[S] = vaddmax(b[n1], gsel(1, z1, Lu, Lp, Lup), b[n0]);
+        else v[S] = vaddmax(b[n1], gsel(1, z1, Lu, Lp, Lup), vadd(b[n0], Lp));
+    }
+    norm8b(v);
+#pragma unroll
+    for (int s = 0; s < NS; s++) b[s] = v[s];
+}
+
+/* Le = clamp(L1 - L0, +-4096) computed as min(max(L1 + ~L0, -4097) + 1, 4096) */
+__device__ __forceinline__ u32 lambda_le_b(const u32 a[NS], const u32 bn[NS], u32 Lp) {
+    u32 lam[2];
+#pragma unroll
+    for (int u = 0; u < 2; u++) {
+        u32 m[2] = {0, 0};
+        bool first[2] = {true, true};
+#pragma unroll
+        for (int S = 0; S < NS; S++) {
+            const int z = par(S, u), Sn = nxt(S, u);
+            m[z] = first[z] ? vadd(a[S], bn[Sn]) : vaddmax(a[S], bn[Sn], m[z]);
+            first[z] = false;
+        }
+        lam[u] = vaddmax(m[1], Lp, m[0]);
+    }
+    return __viaddmin_s16x2(vaddmax(lam[1], ~lam[0], NEG4097), ONE2, CLIP_HI);
+}
+
+__device__ __forceinline__ void tail_beta_b(const u32 *tail, u32 b[NS]) {
+    b[0] = M1;
+#pragma unroll
+    for (int s = 1; s < NS; s++) b[s] = FLOORB;
+#pragma unroll
+    for (int tau = 2; tau >= 0; tau--) {
+        u32 x = tail[2 * tau], z = tail[2 * tau + 1], xz = vadd(x, z);
+        u32 v[NS];
+#pragma unroll
+        for (int S = 0; S < NS; S++) {
+            const int r1 = (S >> 2) & 1, r2 = (S >> 1) & 1, r3 = S & 1;
+            const int uS = r2 ^ r3, zS = r1 ^ r3;
+            v[S] = (uS | zS) ? vadd(b[S >> 1], gsel(uS, zS, x, z, xz)) : b[S >> 1];
+        }
+        norm8b(v);
+#pragma unroll
+        for (int s = 0; s < NS; s++) b[s] = v[s];
+    }
+}
+
+/* One half-iteration of thread t = (pair p, window j) on the W = 32 path.
+ * C = 0: DEC1: Ls, Lp1 natural; La1[n] = Le2[Pi^-1(n)] gathered from Z
+ *         (zeros in iteration 1); Le1 -> Y, natural order.
+ * C = 1: DEC2: Ls[Pi], Lp2 natural-in-interleaved-order; La2[i] = Le1[Pi(i)]
+ *         gathered from Y; Le2 -> Z in interleaved order.
+ * Both gathers are row-local (contention-free): at step i every window of
+ * the pair reads one row of the window-major array. */
+template <int C>
+__device__ __forceinline__ void siso_w32(u32 *slot, const u32 *qg, u32 *sm, int t, int p, int pM, int j, int M,
+                                         int it) {
+    constexpr int W = 32, H = 16;
+    u32 Lu[W], Lp[W];
+    const u32 *Lsrc = slot + (C ? A_LSI : A_LS), *Psrc = slot + (C ? A_LP2 : A_LP1), *Asrc = slot + (C ? A_Y : A_Z);
+    if (C == 0 && it == 1) {
+#pragma unroll
+        for (int i = 0; i < W; i++) {
+            Lp[i] = Psrc[i * TS + t];
+            Lu[i] = Lsrc[i * TS + t];
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; i++) {
+            Lp[i] = Psrc[i * TS + t];
+            Lu[i] = vadd(Lsrc[i * TS + t], Asrc[pM + (int)qg[i * M + j]]);
+        }
+    }
+
+    u32 *nii = slot + A_NII;
+    const int rd = (it - 1) & 1, wr = it & 1;
+    u32 a[NS], b[NS];
+    if (j == 0) {
+        a[0] = M1;
+#pragma unroll
+        for (int s = 1; s < NS; s++) a[s] = FLOORB;
+    } else if (it == 1) {
+#pragma unroll
+        for (int s = 0; s < NS; s++) a[s] = M1;
+    } else {
+#pragma unroll
+        for (int s = 0; s < NS; s++) a[s] = nii[(((C * 2 + rd) * 2 + 0) * NS + s) * TMAX + t - 1];
+    }
+    if (j == M - 1) tail_beta_b(slot + A_TAIL + p * 12 + C * 6, b);
+    else if (it == 1) {
+#pragma unroll
+        for (int s = 0; s < NS; s++) b[s] = M1;
+    } else {
+#pragma unroll
+        for (int s = 0; s < NS; s++) b[s] = nii[(((C * 2 + rd) * 2 + 1) * NS + s) * TMAX + t + 1];
+    }
+
+    u32 *st = sm + t;
+    /* first half: store alpha_s and beta_{W-s}, advance both (rows a5, a6) */
+#pragma unroll
+    for (int s = 0; s < H; s++) {
+#pragma unroll
+        for (int k = 0; k < NS; k++) {
+            st[(s * 16 + k) * TS] = a[k];
+            st[(s * 16 + 8 + k) * TS] = b[k];
+        }
+        const int sl = W - 1 - s;
+        alpha_step_b(a, Lu[s], Lp[s], vadd(Lu[s], Lp[s]));
+        beta_step_b(b, Lu[sl], Lp[sl], vadd(Lu[sl], Lp[sl]));
+    }
+    /* second half: alpha_s meets stored beta_{s+1}, beta_{W-s} meets stored
+     * alpha_{W-1-s}; two extrinsics per step (row a7) */
+    u32 *Le = slot + (C ? A_Z : A_Y) + t;
+#pragma unroll
+    for (int s = H; s < W; s++) {
+        const int sl = W - 1 - s;
+        u32 bs[NS], as[NS];
+        asm volatile("" ::: "memory");      /* keep the stored-metric loads of one step together:
+                                               hoisting all 16 steps' loads costs ~130 registers */
+#pragma unroll
+        for (int k = 0; k < NS; k++) {
+            bs[k] = st[(sl * 16 + 8 + k) * TS];
+            as[k] = st[(sl * 16 + k) * TS];
+        }
+        Le[s * TS] = lambda_le_b(a, bs, Lp[s]);
+        Le[sl * TS] = lambda_le_b(as, b, Lp[sl]);
+        alpha_step_b(a, Lu[s], Lp[s], vadd(Lu[s], Lp[s]));
+        beta_step_b(b, Lu[sl], Lp[sl], vadd(Lu[sl], Lp[sl]));
+    }
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+        nii[(((C * 2 + wr) * 2 + 0) * NS + s) * TMAX + t] = a[s];     /* alpha_{(j+1)W} -> window j+1 */
+        nii[(((C * 2 + wr) * 2 + 1) * NS + s) * TMAX + t] = b[s];     /* beta_{jW}      -> window j-1 */
+    }
+}
+
+struct TaskSh {
+    int *cb, *F, *kind;
+    uint8_t *done, *fin;
+    u32 *crc;
+    int *left;
+};
+
+__device__ __forceinline__ void run_task_w32(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
+                                          const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
+                                          const int16_t *__restrict__ l2, int max_iters, int et,
+                                          uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok,
+                                          uint8_t *__restrict__ iters_used, int16_t *__restrict__ ext_out,
+                                          const crn_tables &tab, u32 *slot, u32 *sm, TaskSh sh) {
+    constexpr int W = 32;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int M = tk.M, NP = tk.n_pairs, T = NP * M;
+    const bool active = tid < T;
+    const int p = active ? tid / M : 0, j = active ? tid - p * M : 0, pM = p * M;
+    const u32 *qts = tab.qpp_ts + tab.qpp_off[tk.kidx];     /* natural pos of Pi(jW+i)   */
+    const u32 *qinv = tab.qinv_ts + tab.qpp_off[tk.kidx];   /* interleaved pos of jW+i   */
+    const u32 *cpow = tab.crc_pow + tab.crc_off[tk.kidx];
+
+    /* ---- row a2: each thread stages its own window of both CBs of its pair */
+    if (active) {
+        const int clo = sh.cb[2 * p], chi = sh.cb[2 * p + 1];
+        const int Flo = sh.F[2 * p], Fhi = sh.F[2 * p + 1];
+        const int64_t olo = clo >= 0 ? desc[clo].llr_off : 0, ohi = chi >= 0 ? desc[chi].llr_off : 0;
+#pragma unroll 4
+        for (int i = 0; i < W; i++) {
+            const int n = j * W + i;
+            int16_t vs0 = 0, vs1 = 0, va0 = 0, va1 = 0, vq0 = 0, vq1 = 0;
+            if (clo >= 0) { vs0 = l0[olo + n]; va0 = l1[olo + n]; vq0 = l2[olo + n]; }
+            if (chi >= 0) { vs1 = l0[ohi + n]; va1 = l1[ohi + n]; vq1 = l2[ohi + n]; }
+            if (n < Flo) { vs0 = -4096; va0 = -4096; }            /* known filler 0 */
+            if (n < Fhi) { vs1 = -4096; va1 = -4096; }
+            slot[A_LS + i * TS + tid] = clamp_pack(vs0, vs1);
+            slot[A_LP1 + i * TS + tid] = clamp_pack(va0, va1);
+            slot[A_LP2 + i * TS + tid] = clamp_pack(vq0, vq1);
+        }
+        if (j == M - 1) {
+            const int K = tk.K;
+#pragma unroll
+            for (int m = 0; m < 12; m++) {     /* tails: DESIGN.md R11 column order */
+                const int col = K + m / 3;
+                const int16_t *src = (m % 3 == 0) ? l0 : (m % 3 == 1) ? l1 : l2;
+                const int16_t v0 = clo >= 0 ? src[olo + col] : 0;
+                const int16_t v1 = chi >= 0 ? src[ohi + col] : 0;
+                slot[A_TAIL + p * 12 + m] = clamp_pack(v0, v1);
+            }
+        }
+    }
+    __syncthreads();
+    if (active) {       /* interleaved systematic Ls[Pi(jW+i)] for DEC2 */
+#pragma unroll 8
+        for (int i = 0; i < W; i++) slot[A_LSI + i * TS + tid] = slot[A_LS + pM + (int)qts[i * M + j]];
+    }
+    __syncthreads();
+
+    for (int it = 1; it <= max_iters; it++) {
+        if (active) siso_w32<0>(slot, qinv, sm, tid, p, pM, j, M, it);
+        __syncthreads();
+        if (active) siso_w32<1>(slot, qts, sm, tid, p, pM, j, M, it);
+        __syncthreads();
+        if (!et && it != max_iters) continue;     /* fixed mode: decide only at the end */
+
+        /* ---- row a9: one packed word per window and CB lane, windowed CRC */
+        u32 wlo = 0, whi = 0;
+        if (active) {
+#pragma unroll
+            for (int i = 0; i < W; i++) {
+                const u32 la1n = slot[A_Z + pM + (int)qinv[i * M + j]];     /* La1_next[n] = Le2[Pi^-1(n)] */
+                const u32 lapp = vadd(vadd(slot[A_LS + i * TS + tid], slot[A_Y + i * TS + tid]), la1n);
+                const u32 ge = __vcmpges2(lapp, 0u);         /* tie -> 1 (R16) */
+                wlo |= (ge & 1u) << i;
+                whi |= ((ge >> 16) & 1u) << i;
+            }
+            const int n0 = j * W, Flo = sh.F[2 * p], Fhi = sh.F[2 * p + 1];
+            if (Flo > n0) wlo &= (Flo >= n0 + 32) ? 0u : (0xFFFFFFFFu << (Flo - n0));
+            if (Fhi > n0) whi &= (Fhi >= n0 + 32) ? 0u : (0xFFFFFFFFu << (Fhi - n0));
+#pragma unroll
+            for (int l = 0; l < 2; l++) {
+                const int kind = sh.kind[2 * p + l];
+                if (kind == CRN_CRC_NONE) continue;
+                const u32 w = l ? whi : wlo, poly = kind == CRN_CRC24A ? POLY_A : POLY_B;
+                u32 r = 0;
+#pragma unroll
+                for (int i = 0; i < W; i++) r = crc_bit(r, (w >> i) & 1u, poly);
+                atomicXor(&sh.crc[2 * p + l], crc_mulmod(r, cpow[(kind == CRN_CRC24A ? 0 : M) + j], poly));
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < 2 * NP; e += nth) {
+            if (sh.done[e]) continue;
+            const bool pass = sh.kind[e] != CRN_CRC_NONE && sh.crc[e] == 0;
+            if ((et && pass) || it == max_iters) {
+                sh.fin[e] = 1;
+                sh.done[e] = 1;
+                crc_ok[sh.cb[e]] = pass;
+                if (iters_used) iters_used[sh.cb[e]] = (uint8_t)it;
+            }
+        }
+        __syncthreads();
+        if (active) {
+#pragma unroll
+            for (int l = 0; l < 2; l++) {
+                if (!sh.fin[2 * p + l]) continue;
+                const crn_cb_desc &d = desc[sh.cb[2 * p + l]];
+                out_bits[d.bit_off + j] = l ? whi : wlo;
+                if (ext_out) {
+#pragma unroll 8
+                    for (int i = 0; i < W; i++) {
+                        const u32 x = slot[A_Z + pM + (int)qinv[i * M + j]];
+                        ext_out[d.ext_off + j * W + i] = (int16_t)(l ? (x >> 16) : (x & 0xFFFFu));
+                    }
+                }
+            }
+        }
+        if (tid == 0) {
+            int left = 0;
+            for (int e = 0; e < 2 * NP; e++) left += !sh.done[e];
+            *sh.left = left;
+        }
+        __syncthreads();
+        for (int e = tid; e < 2 * NP; e += nth) { sh.fin[e] = 0; sh.crc[e] = 0; }
+        const int left = *sh.left;
+        __syncthreads();
+        if (left == 0) break;
+    }
+}
+
 __global__ void __launch_bounds__(TMAX, 1)
 decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__ tasks, int n_tasks,
               const crn_pair *__restrict__ pairs, const int16_t *__restrict__ l0,
@@ -276,7 +591,13 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
         }
         for (int e = tid; e < 2 * NP * nw; e += nth) s_bits[e] = 0;
         __syncthreads();
+        if (W == 32) {
+            TaskSh sh{s_cb, s_F, s_kind, s_done, s_fin, s_crc, &s_left};
+            run_task_w32(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab, slot, bst, sh);
+            continue;
+        }
 
+        /* ===== generic path (W in 33..62, small K only): runtime W, stride T ===== */
         /* ---- row a2: demux, clamp to +-4096, filler override, window-major pair packing */
         for (int e = tid; e < NP * K; e += nth) {
             const int p = e / K, n = e - p * K;

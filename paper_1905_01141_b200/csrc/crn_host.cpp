@@ -152,7 +152,7 @@ extern "C" int crn_device_info(int32_t *num_sms, int32_t *clock_khz, int32_t *cc
 }
 
 struct DevTables {
-    uint32_t *qpp_wm = nullptr, *crc_pow = nullptr;
+    uint32_t *qpp_wm = nullptr, *qpp_ts = nullptr, *qinv_ts = nullptr, *crc_pow = nullptr;
     int32_t *qpp_off = nullptr, *crc_off = nullptr;
     crn_tables tab{};
     int grid = 0;
@@ -168,7 +168,7 @@ static uint32_t mulx_mod(uint32_t a, uint32_t poly) { return ((a << 1) ^ ((a & 0
 static int build_tables(int dev, DevTables **out) {
     auto it = g_tables.find(dev);
     if (it != g_tables.end()) { *out = &it->second; return CRN_OK; }
-    std::vector<uint32_t> qpp, cp;
+    std::vector<uint32_t> qpp, qts, qin, cp;
     std::vector<int32_t> qoff(CRN_NUM_K), coff(CRN_NUM_K);
     for (int ki = 0; ki < CRN_NUM_K; ki++) {
         int K = k_at(ki), M, W;
@@ -176,11 +176,16 @@ static int build_tables(int dev, DevTables **out) {
         int64_t f1 = crn_qpp_f1[ki], f2 = crn_qpp_f2[ki];
         qoff[ki] = (int32_t)qpp.size();
         qpp.resize(qpp.size() + (size_t)K);
+        qts.resize(qpp.size());
+        qin.resize(qpp.size());
         for (int j = 0; j < M; j++)
             for (int i = 0; i < W; i++) {
                 int64_t x = (int64_t)j * W + i;
                 uint32_t n = (uint32_t)((f1 * x + f2 * x % K * x) % K);
                 qpp[qoff[ki] + (size_t)i * M + j] = ((n % W) << 16) | (n / W);
+                qts[qoff[ki] + (size_t)i * M + j] = (n % W) * CRN_CTA_THREADS + n / W;
+                /* inverse: natural position n = Pi(x) is read back from interleaved position x */
+                qin[qoff[ki] + (size_t)(n % W) * M + n / W] = (uint32_t)((x % W) * CRN_CTA_THREADS + x / W);
             }
         coff[ki] = (int32_t)cp.size();
         cp.resize(cp.size() + 2 * (size_t)M);
@@ -194,6 +199,8 @@ static int build_tables(int dev, DevTables **out) {
     }
     DevTables t;
     if (cudaMalloc(&t.qpp_wm, qpp.size() * 4) != cudaSuccess ||
+        cudaMalloc(&t.qpp_ts, qts.size() * 4) != cudaSuccess ||
+        cudaMalloc(&t.qinv_ts, qin.size() * 4) != cudaSuccess ||
         cudaMalloc(&t.crc_pow, cp.size() * 4) != cudaSuccess ||
         cudaMalloc(&t.qpp_off, CRN_NUM_K * 4) != cudaSuccess ||
         cudaMalloc(&t.crc_off, CRN_NUM_K * 4) != cudaSuccess) {
@@ -201,11 +208,13 @@ static int build_tables(int dev, DevTables **out) {
         return CRN_ENOMEM;
     }
     cudaMemcpy(t.qpp_wm, qpp.data(), qpp.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(t.qpp_ts, qts.data(), qts.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(t.qinv_ts, qin.data(), qin.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.crc_pow, cp.data(), cp.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.qpp_off, qoff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.crc_off, coff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
     if (cudaGetLastError() != cudaSuccess) return CRN_ECUDA;
-    t.tab.qpp_wm = t.qpp_wm; t.tab.crc_pow = t.crc_pow;
+    t.tab.qpp_wm = t.qpp_wm; t.tab.qpp_ts = t.qpp_ts; t.tab.qinv_ts = t.qinv_ts; t.tab.crc_pow = t.crc_pow;
     t.tab.qpp_off = t.qpp_off; t.tab.crc_off = t.crc_off;
     t.grid = crn_decode_grid(dev);
     if (t.grid <= 0) return CRN_ECUDA;

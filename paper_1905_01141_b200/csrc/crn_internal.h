@@ -28,6 +28,8 @@ typedef struct {
 /* Per-device constant tables (built once on the host, uploaded once). */
 typedef struct {
     const uint32_t *qpp_wm;   /* per K at qpp_off[kidx]: [i*M + j] = (Pi(jW+i) % W) << 16 | Pi(jW+i) / W */
+    const uint32_t *qpp_ts;   /* same index: (Pi(jW+i) % W) * CRN_CTA_THREADS + Pi(jW+i) / W (fast path) */
+    const uint32_t *qinv_ts;  /* same index, inverse permutation: m = Pi^-1(jW+i) -> (m % W) * CRN_CTA_THREADS + m / W */
     const uint32_t *crc_pow;  /* per K at crc_off[kidx]: [kind(0=A,1=B)*M + j] = x^((M-1-j)W) mod g */
     const int32_t *qpp_off;
     const int32_t *crc_off;

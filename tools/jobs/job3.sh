@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/rc.txt
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/rc.txt
+timeout 900 python bench.py --steps 10 --warmup 3 --no-e2e > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/rc.txt
