@@ -157,11 +157,16 @@ int crn_windows(int32_t K, int32_t *M, int32_t *W);
 uint32_t crn_crc24a(const uint8_t *bits, int64_t nbits);
 uint32_t crn_crc24b(const uint8_t *bits, int64_t nbits);
 const char *crn_strerror(int code);
+/* Text of the last CUDA failure seen by this thread inside libcrn ("" if none). */
+const char *crn_last_error(void);
 
 /* ------------------------------------------------------------------ device facts / microbench */
 
 /* SM count, SM max clock (kHz) and sm major/minor of the current device. */
 int crn_device_info(int32_t *num_sms, int32_t *clock_khz, int32_t *cc_major, int32_t *cc_minor);
+/* Decode kernel resources: static / dynamic shared memory (bytes), the kernel's
+ * current max dynamic shared memory attribute, registers per thread. */
+int crn_decode_kernel_info(int32_t *static_smem, int32_t *dyn_smem, int32_t *max_dyn, int32_t *regs);
 /* int16x2 ALU microbenchmark: op 0 VIADD.16x2, 1 VIMNMX.S16x2,
  * 2 VIMNMX3.S16x2, 3 VIADDMNMX.S16x2.  Runs independent chains at full
  * occupancy (8 CTAs x 256 threads per SM); *lane_instr = warp-instructions x 32

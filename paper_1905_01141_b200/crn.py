@@ -56,7 +56,9 @@ _SIGS = {
     "crn_crc24a": (C.c_uint32, [u8p, C.c_int64]),
     "crn_crc24b": (C.c_uint32, [u8p, C.c_int64]),
     "crn_strerror": (C.c_char_p, [C.c_int]),
+    "crn_last_error": (C.c_char_p, []),
     "crn_device_info": (C.c_int, [i32p, i32p, i32p, i32p]),
+    "crn_decode_kernel_info": (C.c_int, [i32p, i32p, i32p, i32p]),
     "crn_ubench_int16x2": (C.c_int, [C.c_int32, i64p, P(C.c_float), i64p]),
 }
 
@@ -77,7 +79,8 @@ def lib():
 
 def _chk(rc: int, what: str):
     if rc < 0:
-        raise CrnError(f"{what}: {lib().crn_strerror(rc).decode()} ({rc})")
+        detail = lib().crn_last_error().decode()
+        raise CrnError(f"{what}: {lib().crn_strerror(rc).decode()} ({rc})" + (f" [{detail}]" if detail else ""))
     return rc
 
 
@@ -237,6 +240,12 @@ def device_info() -> dict:
     v = [C.c_int32() for _ in range(4)]
     _chk(lib().crn_device_info(*(C.byref(x) for x in v)), "crn_device_info")
     return dict(num_sms=v[0].value, clock_khz=v[1].value, cc=(v[2].value, v[3].value))
+
+
+def decode_kernel_info() -> dict:
+    v = [C.c_int32() for _ in range(4)]
+    _chk(lib().crn_decode_kernel_info(*(C.byref(x) for x in v)), "crn_decode_kernel_info")
+    return dict(static_smem=v[0].value, dyn_smem=v[1].value, max_dyn_attr=v[2].value, regs=v[3].value)
 
 
 def ubench_int16x2(op: int) -> dict:

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -159,6 +160,16 @@ struct DevTables {
 };
 
 static std::mutex g_mu;
+static thread_local char g_err[256] = "";
+
+/* Records the CUDA error behind a CRN_ECUDA / CRN_ENOMEM for crn_last_error(). */
+static int cuda_fail(cudaError_t e, const char *where, int code) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    cudaGetLastError();
+    return code;
+}
+
+extern "C" const char *crn_last_error(void) { return g_err; }
 static std::map<int, DevTables> g_tables;
 static std::map<std::pair<int, void *>, std::pair<void *, size_t>> g_ws;
 
@@ -213,11 +224,15 @@ static int build_tables(int dev, DevTables **out) {
     cudaMemcpy(t.crc_pow, cp.data(), cp.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.qpp_off, qoff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.crc_off, coff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
-    if (cudaGetLastError() != cudaSuccess) return CRN_ECUDA;
+    if (cudaError_t e = cudaGetLastError()) return cuda_fail(e, "table upload", CRN_ECUDA);
     t.tab.qpp_wm = t.qpp_wm; t.tab.qpp_ts = t.qpp_ts; t.tab.qinv_ts = t.qinv_ts; t.tab.crc_pow = t.crc_pow;
     t.tab.qpp_off = t.qpp_off; t.tab.crc_off = t.crc_off;
     t.grid = crn_decode_grid(dev);
-    if (t.grid <= 0) return CRN_ECUDA;
+    if (t.grid <= 0) {
+        char where[96];
+        snprintf(where, sizeof(where), "decode kernel configuration (code %d; needs exactly 1 CTA/SM)", t.grid);
+        return cuda_fail(cudaGetLastError(), where, CRN_ECUDA);
+    }
     auto r = g_tables.emplace(dev, t);
     *out = &r.first->second;
     return CRN_OK;
@@ -296,7 +311,7 @@ static void build_tasks(const crn_cb_desc *d, int n, std::vector<crn_task> &task
         while (e < idx.size() && d[idx[e]].K == K) e++;
         int M, W;
         crn_windows(K, &M, &W);
-        int per = std::max(1, CRN_TASK_SUMK / K);
+        int per = std::max(1, std::min(CRN_TASK_SUMK / K, CRN_MAX_PAIRS));
         int32_t first_pair = (int32_t)pairs.size();
         for (size_t i = s; i < e; i += 2) pairs.push_back({idx[i], i + 1 < e ? idx[i + 1] : -1});
         int32_t np = (int32_t)pairs.size() - first_pair;

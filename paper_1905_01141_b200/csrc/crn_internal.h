@@ -14,6 +14,8 @@
  * is <= CRN_TASK_SUMK, hence T = n_pairs*M <= CRN_TASK_SUMK/32 = CRN_CTA_THREADS. */
 #define CRN_TASK_SUMK 6144
 #define CRN_CTA_THREADS 192
+/* At most this many CB pairs per task (bounds the per-task shared arrays). */
+#define CRN_MAX_PAIRS 96
 
 typedef struct {
     int32_t K, M, W, n_pairs;
