@@ -8,17 +8,20 @@
  * two CBs of a pair live in the low / high int16 half of every 32-bit register
  * and word (pair-SIMD: VIADD.16x2, VIMNMX(3).S16x2, VIADDMNMX.S16x2), so the
  * 8-state butterfly is a compile-time register rename.  Window t = p*M + j is
- * window j of pair p, owned by thread t of a 192-thread CTA (one per SM).
+ * window j of pair p.  On the W = 32 path (every K >= 1056) a window is split
+ * between a head thread (steps 0..15) and a tail thread (steps 16..31) of a
+ * 384-thread CTA (one per SM): 12 warps, three per SM sub-partition.
  *
- * On-chip residency (fast path, W = 32, i.e. every K >= 1056): a CB pair never
- * leaves the SM while it is decoded.  Shared memory holds the window-major
- * inputs (Ls, Lp1, Ls[Pi], Lp2), both extrinsic buffers (Le1 natural, Le2
- * interleaved), the NII boundary states and the per-half-iteration input
- * chunks; tensor memory (TMEM, 512 columns, otherwise idle in this kernel)
- * holds the alpha/beta metrics the crossing recursions store.  Element (step
- * i, window t) of a per-step array is at i*192 + t: a warp's access at one
- * step is contiguous, and because W divides K the QPP is contention-free per
- * window, so every interleaved gather at step i hits one row.
+ * On-chip residency (W = 32): a CB pair never leaves the SM while it is
+ * decoded.  Registers hold each thread's static Ls - Lp sums; shared memory
+ * holds the parity planes, both extrinsic buffers (Le1 natural, Le2
+ * interleaved), the NII boundary states and the per-half-iteration branch-
+ * metric chunks; tensor memory (TMEM, otherwise idle in this kernel) holds the
+ * alpha/beta metrics each thread stores in its first sweep and reads back in
+ * its second.  Element (step i, window t) of a per-step array is at i*192 + t:
+ * a warp's access at one step is contiguous, and because W divides K the QPP
+ * is contention-free per window, so every interleaved gather at step i hits
+ * one row.
  *
  * Exactness.  Every intermediate provably fits int16 (DESIGN.md "int16
  * safety", checked by the oracle on adversarial inputs), so wrapping int16x2
@@ -38,9 +41,10 @@ namespace {
 
 constexpr int NS = CRN_NSTATE;
 constexpr int WMAX = CRN_CTA_THREADS;           /* max windows per task (192) */
-constexpr int BLOCK = CRN_CTA_THREADS;          /* threads per CTA (192) */
+constexpr int BLOCK = 2 * CRN_CTA_THREADS;      /* threads per CTA (384): a head and a tail thread per window */
 constexpr int SUMK = CRN_TASK_SUMK;
 constexpr int TS = WMAX;                        /* fast-path row stride (words) */
+constexpr int HW = 16;                          /* trellis steps per half-window thread (W = 32) */
 constexpr int MAXP = CRN_MAX_PAIRS;             /* max pairs per task */
 constexpr u32 M1 = 0xFFFFFFFFu;                 /* (-1, -1): biased 0 */
 constexpr u32 FLOORB = 0xDFFFDFFFu;             /* (-8193, -8193): biased state-metric floor */
@@ -57,17 +61,25 @@ constexpr int A_TAIL = A_NII + NII_WORDS;       /* [pair][12] */
 constexpr int SLOT_WORDS = A_TAIL + MAXP * 12;
 constexpr size_t WS_HEAD = 256;                 /* task counter */
 
-/* fast-path shared-memory layout (u32 words) */
-constexpr int F_LS = 0, F_LP1 = 6144, F_LSI = 2 * 6144, F_LP2 = 3 * 6144, F_Y = 4 * 6144, F_Z = 5 * 6144;
-constexpr int F_CH = 6 * 6144;                  /* [16 chunks][192][4]: (Lu[s], Lp[s], Lu[31-s], Lp[31-s]) */
-constexpr int F_NII = F_CH + 16 * BLOCK * 4;    /* [c][alpha/beta][s][192], single-buffered */
-constexpr int F_NII_WORDS = 2 * 2 * NS * WMAX;
-constexpr int F_TAIL = F_NII + F_NII_WORDS;     /* [pair][12] */
-constexpr int F_WORDS = F_TAIL + MAXP * 12;
+/* fast-path shared-memory layout (u32 words).  Y = Le1 (natural order), Z =
+ * Le2 (interleaved order), both window-major [step][window]; NII boundary
+ * states [c][alpha/beta][s][window]; X = the mid-window hand-over between the
+ * head and tail thread of a window [alpha/beta][s][window] (reused for the
+ * hard-decision half-words); LP = the static parity LLRs Lp1 (natural) and
+ * Lp2 (interleaved order), window-major; CH = per-thread branch-metric chunk
+ * [step][thread] of uint2 (Lu+Lp, Lu-Lp); tails [pair][12]. */
+constexpr int S_Y = 0, S_Z = SUMK, S_NII = 2 * SUMK;
+constexpr int S_NII_WORDS = 2 * 2 * NS * WMAX;
+constexpr int S_X = S_NII + S_NII_WORDS;
+constexpr int S_LP = S_X + 2 * NS * WMAX;       /* [c][step][window] */
+constexpr int S_CH = S_LP + 2 * SUMK;
+constexpr int S_TAIL = S_CH + HW * BLOCK * 2;
+constexpr int S_WORDS = S_TAIL + MAXP * 12;
+static_assert(S_CH % 2 == 0, "chunk array must be 8-byte aligned");
 /* generic path: beta storage (W+1)*8*T words, then the packed output bits */
 constexpr int G_BITS = (SUMK + WMAX) * NS;
 constexpr int G_WORDS = G_BITS + 2 * (SUMK / 32 + MAXP);
-constexpr int SMEM_WORDS = F_WORDS > G_WORDS ? F_WORDS : G_WORDS;
+constexpr int SMEM_WORDS = S_WORDS > G_WORDS ? S_WORDS : G_WORDS;
 static_assert(SMEM_WORDS * 4 + 3584 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
 
 /* ---- RSC trellis, S = 4 r1 + 2 r2 + r3 (R1), evaluated at compile time */
@@ -120,6 +132,76 @@ __device__ __forceinline__ void beta_step(u32 b[NS], u32 Lu, u32 Lp, u32 Lup) {
     norm8(v);
 #pragma unroll
     for (int s = 0; s < NS; s++) b[s] = v[s];
+}
+
+/* ---- Branch-difference form of the recursions (fast path).  The two branches
+ * into (alpha) or out of (beta) a state carry complementary (u, z) labels
+ * (R1): type A = {(0,0), (1,1)}, type B = {(0,1), (1,0)}.  A type-A
+ * candidate pair is max(m0, m1 + Lup); a type-B pair is
+ * max(m0 + Lp, m1 + Lu) = Lp + max(m0, m1 + D), D = Lu - Lp, so one fused
+ * VIADDMNMX forms every state and the common "+ Lp" of the type-B states is
+ * folded into the maximum and into the normaliser's offset.  Exact: every
+ * value below is the oracle's integer, and all fit int16. */
+__host__ __device__ constexpr int pred_u(int S, int Sp) { return nxt(S, 0) == Sp ? 0 : 1; }
+/* alpha: type of state S' (1 = B) and which predecessor carries the unmodified branch */
+__host__ __device__ constexpr bool a_isB(int Sp) {
+    return !((pred_u(2 * (Sp & 3), Sp) == 0 && par(2 * (Sp & 3), 0) == 0) ||
+             (pred_u(2 * (Sp & 3) + 1, Sp) == 0 && par(2 * (Sp & 3) + 1, 0) == 0));
+}
+/* the predecessor whose branch is (0,0) [type A] or (0,1) [type B] */
+__host__ __device__ constexpr int a_base(int Sp) {
+    return pred_u(2 * (Sp & 3), Sp) == 0 ? 2 * (Sp & 3) : 2 * (Sp & 3) + 1;
+}
+__host__ __device__ constexpr bool b_isB(int S) { return par(S, 0) == 1; }
+/* group member lists (compile-time): the k-th type-A / type-B state */
+__host__ __device__ constexpr int nth_state(bool alpha, bool B, int k) {
+    int c = 0;
+    for (int s = 0; s < NS; s++)
+        if ((alpha ? a_isB(s) : b_isB(s)) == B) {
+            if (c == k) return s;
+            c++;
+        }
+    return -1;
+}
+static_assert(!a_isB(0) && a_isB(1) && a_isB(2) && !a_isB(3) && !a_isB(4) && a_isB(5) && a_isB(6) && !a_isB(7),
+              "alpha state types (SURVEY 8c.1: {0,3,4,7} receive (0,0)/(1,1))");
+static_assert(nth_state(true, true, 3) >= 0 && nth_state(false, true, 3) >= 0 && nth_state(false, false, 3) >= 0,
+              "four states of each type");
+
+/* v[] holds type-A values and type-B differences w (v_B = w + Lp).  Writes
+ * N(v) (biased) into out[]: m = max(max_A v, max_B w + Lp); out = max(v - m, F). */
+template <bool ALPHA>
+__device__ __forceinline__ void norm_ab(const u32 v[NS], u32 Lp, u32 out[NS]) {
+    constexpr int a0 = nth_state(ALPHA, false, 0), a1 = nth_state(ALPHA, false, 1), a2 = nth_state(ALPHA, false, 2),
+                  a3 = nth_state(ALPHA, false, 3);
+    constexpr int b0 = nth_state(ALPHA, true, 0), b1 = nth_state(ALPHA, true, 1), b2 = nth_state(ALPHA, true, 2),
+                  b3 = nth_state(ALPHA, true, 3);
+    const u32 tA = __vimax3_s16x2(v[a0], v[a1], v[a2]);
+    const u32 tB = __vmaxs2(__vimax3_s16x2(v[b0], v[b1], v[b2]), v[b3]);
+    const u32 m = __vmaxs2(vaddmax(tB, Lp, tA), v[a3]);
+    const u32 nm = ~m;                          /* ~(m - 1) = -m (biased values) */
+    const u32 lpm = vadd(Lp, nm);               /* Lp - m */
+#pragma unroll
+    for (int s = 0; s < NS; s++) out[s] = vaddmax(v[s], (ALPHA ? a_isB(s) : b_isB(s)) ? lpm : nm, FLOORB);
+}
+
+/* alpha_{k+1} = N(max over predecessors of alpha_k + gamma_k)  (row a6) */
+__device__ __forceinline__ void alpha_step_d(u32 a[NS], u32 Lp, u32 Lup, u32 D) {
+    u32 v[NS];
+#pragma unroll
+    for (int Sp = 0; Sp < NS; Sp++) {
+        const int x = a_base(Sp), y = x ^ 1;    /* y carries (1,1) [A] or (1,0) [B] */
+        v[Sp] = vaddmax(a[y], a_isB(Sp) ? D : Lup, a[x]);
+    }
+    norm_ab<true>(v, Lp, a);
+}
+
+/* beta_k = N(max over successors of beta_{k+1} + gamma_k)  (row a5) */
+__device__ __forceinline__ void beta_step_d(u32 b[NS], u32 Lp, u32 Lup, u32 D) {
+    u32 v[NS];
+#pragma unroll
+    for (int S = 0; S < NS; S++) v[S] = vaddmax(b[nxt(S, 1)], b_isB(S) ? D : Lup, b[nxt(S, 0)]);
+    norm_ab<false>(v, Lp, b);
 }
 
 /* Row a7: Lambda_u = max over the 8 transitions with input u of alpha_k(S) +
@@ -262,115 +344,167 @@ __device__ __forceinline__ int finish_iteration(TaskSh sh, int NP) {
 }
 
 /* ---- tensor memory (tcgen05) helpers.  A warp may touch only the TMEM lanes
- * of its quadrant (warp % 4); warps 4 and 5 use the upper 256 columns. */
+ * of its quadrant (warp % 4); warps 4-7 use columns 128-255, warps 8-11 256-383. */
 __device__ __forceinline__ u32 smem_addr(const void *p) { return (u32)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ void tm_store16(u32 ta, const u32 a[NS], const u32 b[NS]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
-                 :: "r"(ta), "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]),
-                    "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]), "r"(b[6]), "r"(b[7])
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+/* ======================================================================
+ * Fast path: W = 32 (every K that is a multiple of 32: all K >= 1056 and 15
+ * smaller sizes).  Window t of the task is split between two threads: the
+ * head thread (tid = t, warps 0-5) owns steps 0..15, the tail thread (tid =
+ * 192 + t, warps 6-11) steps 16..31, so a 192-window CB pair runs on 12 warps,
+ * three per SM sub-partition.  Per half-iteration:
+ *   phase 0  each thread forms its 16 branch-metric triples (Lp, Lu+Lp, Lu-Lp)
+ *            from register-resident static sums and the gathered a-priori LLR;
+ *   phase 1  head: alpha forward over steps 0..15, tail: beta backward over
+ *            31..16, each storing its metrics in its own TMEM lane;
+ *   hand-over  alpha_16 and beta_16 swap through shared memory (one barrier);
+ *   phase 2  head: beta backward over 15..0, tail: alpha forward over 16..31;
+ *            each step meets the thread's own stored metric of the other
+ *            sweep and emits one extrinsic (rows a5-a7);
+ *   NII      head: beta_{jW} -> window j-1, tail: alpha_{(j+1)W} -> window
+ *            j+1, for the next iteration (row a8).
+ * ====================================================================== */
+struct SCtx {
+    u32 *sm;        /* shared-memory base (fast layout) */
+    u32 ta;         /* this thread's TMEM base: lane quadrant + 128-column block */
+    int tid, t, p, j, M, pM, k0;
+};
+
+__device__ __forceinline__ void tm_store8(u32 ta, const u32 v[NS]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                  : "memory");
 }
 
-__device__ __forceinline__ void tm_load16(u32 ta, u32 v[16]) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+__device__ __forceinline__ void tm_load8(u32 ta, u32 v[NS]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                  : "r"(ta)
                  : "memory");
 }
 
 /* Waits for outstanding TMEM loads; v is an in/out operand so no use of the
  * loaded registers can be scheduled before the wait. */
-__device__ __forceinline__ void tm_wait_ld(u32 v[16]) {
+__device__ __forceinline__ void tm_wait_ld8(u32 v[NS]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
-                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7])
                  :: "memory");
 }
 
-__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-/* ======================================================================
- * Fast path: W = 32 (every K that is a multiple of 32: all K >= 1056 and 15
- * smaller sizes).  Per half-iteration a thread first builds its window's 16
- * input chunks (Lu = Ls + La with La gathered through the interleaver, and
- * Lp), then runs the alpha and beta recursions concurrently ("crossing":
- * alpha forward from the window start, beta backward from its end).  In the
- * first 16 steps both sweeps store their metrics in TMEM; in the last 16 each
- * new metric meets the stored metric of the other sweep and two extrinsics
- * per step are emitted.  The TMEM load of the next slot is issued one step
- * ahead and lands while the alpha/beta steps run.  The step loops are rolled
- * (one body per half), so the instruction footprint stays in the i-cache.
- * ====================================================================== */
-struct FastCtx {
-    u32 *sm;        /* shared-memory base (fast layout) */
-    u32 ta;         /* this thread's TMEM base: lane quadrant + column block */
-    int t, p, j, M, pM;
-};
-
-/* Row a4 inputs of one half-iteration: chunk s = (Lu[s], Lp[s], Lu[31-s], Lp[31-s]). */
-__device__ __forceinline__ void build_chunks(const FastCtx &f, const u32 *ls, const u32 *lp, const u32 *la,
-                                             const u32 *__restrict__ qg, bool zero_la) {
-    uint4 *ch = reinterpret_cast<uint4 *>(f.sm + F_CH) + f.t;
-#pragma unroll 4
-    for (int s = 0; s < 16; s++) {
-        const int i0 = s, i1 = 31 - s;
-        u32 a0 = 0, a1 = 0;
-        if (!zero_la) {
-            a0 = la[f.pM + (int)qg[i0 * f.M + f.j]];
-            a1 = la[f.pM + (int)qg[i1 * f.M + f.j]];
-        }
-        ch[s * BLOCK] = make_uint4(vadd(ls[i0 * TS + f.t], a0), lp[i0 * TS + f.t],
-                                   vadd(ls[i1 * TS + f.t], a1), lp[i1 * TS + f.t]);
+/* Phase 0 (row a4): chunk[s] = (Lu+Lp, Lu-Lp) with Lu = Ls + La for the
+ * thread's 16 steps, from the static Ls-Lp (registers), Lp (shared plane) and
+ * the a-priori La gathered through a QPP table (zero in DEC1 of iteration 1). */
+__device__ __forceinline__ void build_chunk(const SCtx &f, const u32 (&sn)[HW], const u32 *lp, const u32 *la,
+                                            const u32 *__restrict__ q, bool zero_la) {
+    uint2 *ch = reinterpret_cast<uint2 *>(f.sm + S_CH) + f.tid;
+    const u32 *qq = q + f.k0 * f.M + f.j;
+    lp += f.k0 * TS + f.t;
+#pragma unroll
+    for (int s = 0; s < HW; s++) {
+        const u32 a = zero_la ? 0u : la[f.pM + (int)qq[s * f.M]];
+        const u32 d = vadd(sn[s], a);                       /* Lu - Lp */
+        const u32 p = lp[s * TS];
+        ch[s * BLOCK] = make_uint2(vadd(vadd(d, p), p), d);
     }
 }
 
-/* One half-iteration (rows a5-a8) of window t.  c = 0: DEC1, Le1 -> Y
- * (natural order); c = 1: DEC2, Le2 -> Z (interleaved order). */
-__device__ __noinline__ void siso_fast(const FastCtx &f, int c, int it) {
-    const uint4 *ch = reinterpret_cast<const uint4 *>(f.sm + F_CH) + f.t;
-    u32 *nii = f.sm + F_NII;
-    u32 *le = f.sm + (c ? F_Z : F_Y) + f.t;
-    u32 a[NS], b[NS];
-    init_metrics<true>(nii, f.sm + F_TAIL + f.p * 12 + c * 6, c, it, f.j, f.M, f.t, a, b);
-    __syncthreads();                   /* every window has read its NII inputs before any is overwritten */
-
-    /* steps 0..15: store alpha_s and beta_{32-s} in TMEM slot s, advance both sweeps */
+/* One half-iteration of constituent c (rows a5-a8).  Le -> Y (c = 0, natural
+ * order) or Z (c = 1, interleaved order). */
+__device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, int it) {
+    const uint2 *ch = reinterpret_cast<const uint2 *>(f.sm + S_CH) + f.tid;
+    const u32 *lp = f.sm + S_LP + c * SUMK + f.k0 * TS + f.t;
+    u32 *nii = f.sm + S_NII;
+    u32 *X = f.sm + S_X;
+    u32 *le = f.sm + (c ? S_Z : S_Y) + f.t;
+    u32 m[NS];
+    if (!tail_thr) {
+        /* alpha_0 of window j: known start state, zero in iteration 1, NII afterwards (R13) */
+        if (f.j == 0) {
+            m[0] = M1;
+#pragma unroll
+            for (int s = 1; s < NS; s++) m[s] = FLOORB;
+        } else if (it == 1) {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = M1;
+        } else {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = nii[nii1_ix(c, 0, s, f.t - 1)];
+        }
 #pragma unroll 1
-    for (int s = 0; s < 16; s++) {
-        const uint4 in = ch[s * BLOCK];
-        tm_store16(f.ta + s * 16, a, b);
-        alpha_step(a, in.x, in.y, vadd(in.x, in.y));
-        beta_step(b, in.z, in.w, vadd(in.z, in.w));
+        for (int s = 0; s < HW; s++) {          /* store alpha_s, advance to alpha_{s+1} */
+            const uint2 g = ch[s * BLOCK];
+            tm_store8(f.ta + s * 8, m);
+            alpha_step_d(m, lp[s * TS], g.x, g.y);
+        }
+#pragma unroll
+        for (int s = 0; s < NS; s++) X[s * TS + f.t] = m[s];             /* alpha_16 -> tail thread */
+    } else {
+        /* beta_32 of window j: tail termination, zero in iteration 1, NII afterwards */
+        if (f.j == f.M - 1) tail_beta(f.sm + S_TAIL + f.p * 12 + c * 6, m);
+        else if (it == 1) {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = M1;
+        } else {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = nii[nii1_ix(c, 1, s, f.t + 1)];
+        }
+#pragma unroll 1
+        for (int s = HW - 1; s >= 0; s--) {     /* store beta_{17+s}, advance to beta_{16+s} */
+            const uint2 g = ch[s * BLOCK];
+            tm_store8(f.ta + s * 8, m);
+            beta_step_d(m, lp[s * TS], g.x, g.y);
+        }
+#pragma unroll
+        for (int s = 0; s < NS; s++) X[(NS + s) * TS + f.t] = m[s];      /* beta_16 -> head thread */
     }
     tm_wait_st();
-    /* steps 16..31: alpha_s meets beta_{s+1} and beta_{32-s} meets alpha_{31-s},
-     * both from slot 31-s; two buffers so the next slot loads one step ahead */
-    u32 bufA[16], bufB[16];
-    tm_load16(f.ta + 15 * 16, bufA);
+    __syncthreads();        /* hand-over; also orders this half-iteration's NII reads before its writes */
+
+    u32 bufA[NS], bufB[NS];
+    if (!tail_thr) {
+        u32 b[NS];
+#pragma unroll
+        for (int s = 0; s < NS; s++) b[s] = X[(NS + s) * TS + f.t];      /* beta_16 */
+        tm_load8(f.ta + (HW - 1) * 8, bufA);
 #pragma unroll 1
-    for (int s = 16; s < 32; s += 2) {
+        for (int s = HW - 1; s >= 0; s -= 2) {
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int ss = s + h, sl = 31 - ss;
-            u32 *cur = h ? bufB : bufA, *nxt = h ? bufA : bufB;
-            const uint4 in = ch[sl * BLOCK];          /* (Lu[sl], Lp[sl], Lu[ss], Lp[ss]) */
-            tm_wait_ld(cur);
-            if (sl > 0) tm_load16(f.ta + (sl - 1) * 16, nxt);
-            u32 ao[NS], bo[NS];
-#pragma unroll
-            for (int k = 0; k < NS; k++) { ao[k] = a[k]; bo[k] = b[k]; }
-            alpha_step(a, in.z, in.w, vadd(in.z, in.w));
-            beta_step(b, in.x, in.y, vadd(in.x, in.y));
-            le[ss * TS] = lambda_le(ao, cur + 8, in.w);   /* alpha_ss + beta_{ss+1} */
-            le[sl * TS] = lambda_le(cur, bo, in.y);       /* alpha_sl + beta_{sl+1} */
+            for (int h = 0; h < 2; h++) {
+                const int ss = s - h;
+                u32 *cur = h ? bufB : bufA, *nx = h ? bufA : bufB;
+                const uint2 g = ch[ss * BLOCK];
+                const u32 p = lp[ss * TS];
+                tm_wait_ld8(cur);
+                if (ss > 0) tm_load8(f.ta + (ss - 1) * 8, nx);
+                le[ss * TS] = lambda_le(cur, b, p);                /* alpha_ss (stored) + beta_{ss+1} */
+                beta_step_d(b, p, g.x, g.y);
+            }
         }
-    }
 #pragma unroll
-    for (int s = 0; s < NS; s++) {
-        nii[nii1_ix(c, 0, s, f.t)] = a[s];        /* alpha_{(j+1)W} -> window j+1, next iteration */
-        nii[nii1_ix(c, 1, s, f.t)] = b[s];        /* beta_{jW}      -> window j-1, next iteration */
+        for (int s = 0; s < NS; s++) nii[nii1_ix(c, 1, s, f.t)] = b[s];  /* beta_{jW} -> window j-1 */
+    } else {
+        u32 a[NS];
+#pragma unroll
+        for (int s = 0; s < NS; s++) a[s] = X[s * TS + f.t];             /* alpha_16 */
+        tm_load8(f.ta, bufA);
+#pragma unroll 1
+        for (int s = 0; s < HW; s += 2) {
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int ss = s + h;
+                u32 *cur = h ? bufB : bufA, *nx = h ? bufA : bufB;
+                const uint2 g = ch[ss * BLOCK];
+                const u32 p = lp[ss * TS];
+                tm_wait_ld8(cur);
+                if (ss < HW - 1) tm_load8(f.ta + (ss + 1) * 8, nx);
+                le[(HW + ss) * TS] = lambda_le(a, cur, p);         /* alpha_{16+ss} + beta_{17+ss} (stored) */
+                alpha_step_d(a, p, g.x, g.y);
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < NS; s++) nii[nii1_ix(c, 0, s, f.t)] = a[s];  /* alpha_{(j+1)W} -> window j+1 */
     }
 }
 
@@ -383,106 +517,133 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
     constexpr int W = 32;
     const int M = tk.M, NP = tk.n_pairs, T = NP * M;
     const int tid = threadIdx.x, warp = tid >> 5;
-    const bool active = tid < T;
-    FastCtx f;
+    const bool tail_thr = tid >= WMAX;          /* warp-uniform: WMAX = 6 warps */
+    SCtx f;
     f.sm = sm;
-    f.ta = tmem + ((u32)((warp & 3) * 32) << 16) + (u32)((warp >> 2) * 256);
-    f.t = tid;
+    f.ta = tmem + ((u32)((warp & 3) * 32) << 16) + (u32)((warp >> 2) * 128);
+    f.tid = tid;
+    f.t = tid - (tail_thr ? WMAX : 0);
+    const bool active = f.t < T;
     f.M = M;
-    f.p = active ? tid / M : 0;         /* inactive threads run on pair 0 window 0 data; outputs unused */
-    f.j = active ? tid - f.p * M : 0;
+    f.p = active ? f.t / M : 0;         /* inactive threads run on pair 0 window 0 data; outputs unused */
+    f.j = active ? f.t - f.p * M : 0;
     f.pM = f.p * M;
+    f.k0 = tail_thr ? HW : 0;
     const u32 *qts = tab.qpp_ts + tab.qpp_off[tk.kidx];     /* natural position of Pi(jW+i)  */
     const u32 *qinv = tab.qinv_ts + tab.qpp_off[tk.kidx];   /* interleaved position of jW+i */
     const u32 *cpow = tab.crc_pow + tab.crc_off[tk.kidx];
 
-    /* ---- row a2: stage own window of both CBs of the pair into shared memory */
-    if (active) {
+    /* ---- row a2: stage own half-window of both CBs of the pair into registers:
+     * Ls-Lp1 (natural) and Ls[Pi]-Lp2 (interleaved); Lp1, Lp2 into the shared planes */
+    u32 sn1[HW], sn2[HW];
+    {
         const int p = f.p, j = f.j;
         const int clo = sh.cb[2 * p], chi = sh.cb[2 * p + 1];
         const int Flo = sh.F[2 * p], Fhi = sh.F[2 * p + 1];
         const int64_t olo = clo >= 0 ? desc[clo].llr_off : 0, ohi = chi >= 0 ? desc[chi].llr_off : 0;
-#pragma unroll 4
-        for (int i = 0; i < W; i++) {
-            const int n = j * W + i;
+        u32 *tmp = sm + S_CH;                 /* natural Ls, window-major, for the interleaved gather */
+#pragma unroll
+        for (int s = 0; s < HW; s++) {
+            const int n = j * W + f.k0 + s;
             int16_t vs0 = 0, vs1 = 0, va0 = 0, va1 = 0, vq0 = 0, vq1 = 0;
             if (clo >= 0) { vs0 = l0[olo + n]; va0 = l1[olo + n]; vq0 = l2[olo + n]; }
             if (chi >= 0) { vs1 = l0[ohi + n]; va1 = l1[ohi + n]; vq1 = l2[ohi + n]; }
             if (n < Flo) { vs0 = -4096; va0 = -4096; }            /* known filler 0 */
             if (n < Fhi) { vs1 = -4096; va1 = -4096; }
-            sm[F_LS + i * TS + tid] = clamp_pack(vs0, vs1);
-            sm[F_LP1 + i * TS + tid] = clamp_pack(va0, va1);
-            sm[F_LP2 + i * TS + tid] = clamp_pack(vq0, vq1);
-        }
-        if (j == M - 1) {
-#pragma unroll
-            for (int m = 0; m < 12; m++) {     /* tails: DESIGN.md R11 column order */
-                const int col = tk.K + m / 3;
-                const int16_t *src = (m % 3 == 0) ? l0 : (m % 3 == 1) ? l1 : l2;
-                const int16_t v0 = clo >= 0 ? src[olo + col] : 0;
-                const int16_t v1 = chi >= 0 ? src[ohi + col] : 0;
-                sm[F_TAIL + p * 12 + m] = clamp_pack(v0, v1);
+            const u32 ls = clamp_pack(vs0, vs1), p1 = clamp_pack(va0, va1);
+            sn1[s] = __vsub2(ls, p1);
+            if (active) {
+                tmp[(f.k0 + s) * TS + f.t] = ls;
+                sm[S_LP + (f.k0 + s) * TS + f.t] = p1;
+                sm[S_LP + SUMK + (f.k0 + s) * TS + f.t] = clamp_pack(vq0, vq1);
             }
         }
+        if (active && tail_thr && j == M - 1) {
+#pragma unroll
+            for (int mm = 0; mm < 12; mm++) {     /* tails: DESIGN.md R11 column order */
+                const int col = tk.K + mm / 3;
+                const int16_t *src = (mm % 3 == 0) ? l0 : (mm % 3 == 1) ? l1 : l2;
+                const int16_t v0 = clo >= 0 ? src[olo + col] : 0;
+                const int16_t v1 = chi >= 0 ? src[ohi + col] : 0;
+                sm[S_TAIL + p * 12 + mm] = clamp_pack(v0, v1);
+            }
+        }
+        __syncthreads();
+        const u32 *qq = qts + f.k0 * M + j;
+#pragma unroll
+        for (int s = 0; s < HW; s++) {       /* interleaved systematic Ls[Pi(jW+k)] */
+            const u32 lsi = tmp[f.pM + (int)qq[s * M]];
+            sn2[s] = __vsub2(lsi, sm[S_LP + SUMK + (f.k0 + s) * TS + f.t]);
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    if (active) {    /* interleaved systematic Ls[Pi(jW+i)] for DEC2 */
-#pragma unroll 8
-        for (int i = 0; i < W; i++) sm[F_LSI + i * TS + tid] = sm[F_LS + f.pM + (int)qts[i * M + f.j]];
-    }
-    __syncthreads();
 
     for (int it = 1; it <= max_iters; it++) {
         /* DEC1: La1[n] = Le2[Pi^-1(n)] gathered from Z (zero in iteration 1) */
-        build_chunks(f, sm + F_LS, sm + F_LP1, sm + F_Z, qinv, it == 1);
-        siso_fast(f, 0, it);
+        build_chunk(f, sn1, sm + S_LP, sm + S_Z, qinv, it == 1);
+        siso_split(f, tail_thr, 0, it);
         __syncthreads();
         /* DEC2: La2[i] = Le1[Pi(i)] gathered from Y */
-        build_chunks(f, sm + F_LSI, sm + F_LP2, sm + F_Y, qts, false);
-        siso_fast(f, 1, it);
+        build_chunk(f, sn2, sm + S_LP + SUMK, sm + S_Y, qts, false);
+        siso_split(f, tail_thr, 1, it);
         __syncthreads();
         if (!et && it != max_iters) continue;     /* fixed mode: decide only at the end */
 
-        /* ---- row a9: one packed word per window and CB lane, windowed CRC */
-        u32 wlo = 0, whi = 0;
-        if (active) {
-            const int p = f.p, j = f.j;
-#pragma unroll 8
-            for (int i = 0; i < W; i++) {
-                const u32 la1n = sm[F_Z + f.pM + (int)qinv[i * M + j]];     /* La1_next[n] = Le2[Pi^-1(n)] */
-                const u32 lapp = vadd(vadd(sm[F_LS + i * TS + tid], sm[F_Y + i * TS + tid]), la1n);
-                const u32 ge = __vcmpges2(lapp, 0u);         /* L_APP >= 0 -> 1, tie -> 1 (R16) */
-                wlo |= (ge & 1u) << i;
-                whi |= ((ge >> 16) & 1u) << i;
+        /* ---- row a9: L_APP = Ls + Le1 + La1_next (tie -> 1, R16); 16 bits per
+         * thread and CB lane, merged per window; windowed CRC */
+        {
+            u32 wlo = 0, whi = 0;
+            const u32 *qq = qinv + f.k0 * M + f.j;
+#pragma unroll
+            for (int s = 0; s < HW; s++) {
+                const u32 la1n = sm[S_Z + f.pM + (int)qq[s * M]];     /* La1_next[n] = Le2[Pi^-1(n)] */
+                const u32 ls = vadd(sn1[s], sm[S_LP + (f.k0 + s) * TS + f.t]);
+                const u32 lapp = vadd(vadd(ls, sm[S_Y + (f.k0 + s) * TS + f.t]), la1n);
+                const u32 ge = __vcmpges2(lapp, 0u);
+                wlo |= (ge & 1u) << s;
+                whi |= ((ge >> 16) & 1u) << s;
             }
-            const int n0 = j * W, Flo = sh.F[2 * p], Fhi = sh.F[2 * p + 1];
-            if (Flo > n0) wlo &= (Flo >= n0 + 32) ? 0u : (0xFFFFFFFFu << (Flo - n0));
-            if (Fhi > n0) whi &= (Fhi >= n0 + 32) ? 0u : (0xFFFFFFFFu << (Fhi - n0));
-#pragma unroll
-            for (int l = 0; l < 2; l++) {
-                const int kind = sh.kind[2 * p + l];
-                if (kind == CRN_CRC_NONE) continue;
-                const u32 w = l ? whi : wlo, poly = kind == CRN_CRC24A ? POLY_A : POLY_B;
-                u32 r = 0;
-#pragma unroll
-                for (int i = 0; i < W; i++) r = crc_bit(r, (w >> i) & 1u, poly);
-                atomicXor(&sh.crc[2 * p + l], crc_mulmod(r, cpow[(kind == CRN_CRC24A ? 0 : M) + j], poly));
+            u32 *hb = sm + S_X;               /* [half][lo/hi][window] */
+            if (active) {
+                hb[((tail_thr ? 2 : 0) + 0) * TS + f.t] = wlo;
+                hb[((tail_thr ? 2 : 0) + 1) * TS + f.t] = whi;
             }
-        }
-        __syncthreads();
-        decide(sh, NP, it, max_iters, et, crc_ok, iters_used);
-        if (active) {
-            const int p = f.p, j = f.j;
+            __syncthreads();
+            if (active && !tail_thr) {
+                const int p = f.p, j = f.j;
+                wlo = hb[0 * TS + f.t] | (hb[2 * TS + f.t] << 16);
+                whi = hb[1 * TS + f.t] | (hb[3 * TS + f.t] << 16);
+                const int n0 = j * W, Flo = sh.F[2 * p], Fhi = sh.F[2 * p + 1];
+                if (Flo > n0) wlo &= (Flo >= n0 + 32) ? 0u : (0xFFFFFFFFu << (Flo - n0));
+                if (Fhi > n0) whi &= (Fhi >= n0 + 32) ? 0u : (0xFFFFFFFFu << (Fhi - n0));
+                hb[0 * TS + f.t] = wlo;
+                hb[1 * TS + f.t] = whi;
 #pragma unroll
-            for (int l = 0; l < 2; l++) {
-                if (!sh.fin[2 * p + l]) continue;
-                const crn_cb_desc &d = desc[sh.cb[2 * p + l]];
-                out_bits[d.bit_off + j] = l ? whi : wlo;
-                if (ext_out) {
-#pragma unroll 8
-                    for (int i = 0; i < W; i++) {
-                        const u32 x = sm[F_Z + f.pM + (int)qinv[i * M + j]];
-                        ext_out[d.ext_off + j * W + i] = (int16_t)(l ? (x >> 16) : (x & 0xFFFFu));
+                for (int l = 0; l < 2; l++) {
+                    const int kind = sh.kind[2 * p + l];
+                    if (kind == CRN_CRC_NONE) continue;
+                    const u32 w = l ? whi : wlo, poly = kind == CRN_CRC24A ? POLY_A : POLY_B;
+                    u32 r = 0;
+#pragma unroll
+                    for (int i = 0; i < W; i++) r = crc_bit(r, (w >> i) & 1u, poly);
+                    atomicXor(&sh.crc[2 * p + l], crc_mulmod(r, cpow[(kind == CRN_CRC24A ? 0 : M) + j], poly));
+                }
+            }
+            __syncthreads();
+            decide(sh, NP, it, max_iters, et, crc_ok, iters_used);
+            if (active) {
+                const int p = f.p, j = f.j;
+#pragma unroll
+                for (int l = 0; l < 2; l++) {
+                    if (!sh.fin[2 * p + l]) continue;
+                    const crn_cb_desc &d = desc[sh.cb[2 * p + l]];
+                    if (!tail_thr) out_bits[d.bit_off + j] = hb[l * TS + f.t];
+                    if (ext_out) {
+#pragma unroll
+                        for (int s = 0; s < HW; s++) {
+                            const u32 x = sm[S_Z + f.pM + (int)qq[s * M]];
+                            ext_out[d.ext_off + j * W + f.k0 + s] = (int16_t)(l ? (x >> 16) : (x & 0xFFFFu));
+                        }
                     }
                 }
             }
