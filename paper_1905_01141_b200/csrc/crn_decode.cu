@@ -401,9 +401,12 @@ __device__ __forceinline__ void build_chunk(const SCtx &f, const u32 (&sn)[HW], 
     uint2 *ch = reinterpret_cast<uint2 *>(f.sm + S_CH) + f.tid;
     const u32 *qq = q + f.k0 * f.M + f.j;
     lp += f.k0 * TS + f.t;
+    u32 qv[HW];             /* all table entries first: one L2 round trip, not 16 */
+#pragma unroll
+    for (int s = 0; s < HW; s++) qv[s] = zero_la ? 0u : __ldg(qq + s * f.M);
 #pragma unroll
     for (int s = 0; s < HW; s++) {
-        const u32 a = zero_la ? 0u : la[f.pM + (int)qq[s * f.M]];
+        const u32 a = zero_la ? 0u : la[f.pM + (int)qv[s]];
         const u32 d = vadd(sn[s], a);                       /* Lu - Lp */
         const u32 p = lp[s * TS];
         ch[s * BLOCK] = make_uint2(vadd(vadd(d, p), p), d);
@@ -570,9 +573,12 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         }
         __syncthreads();
         const u32 *qq = qts + f.k0 * M + j;
+        u32 qv[HW];
+#pragma unroll
+        for (int s = 0; s < HW; s++) qv[s] = __ldg(qq + s * M);
 #pragma unroll
         for (int s = 0; s < HW; s++) {       /* interleaved systematic Ls[Pi(jW+k)] */
-            const u32 lsi = tmp[f.pM + (int)qq[s * M]];
+            const u32 lsi = tmp[f.pM + (int)qv[s]];
             sn2[s] = __vsub2(lsi, sm[S_LP + SUMK + (f.k0 + s) * TS + f.t]);
         }
         __syncthreads();
@@ -594,9 +600,12 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         {
             u32 wlo = 0, whi = 0;
             const u32 *qq = qinv + f.k0 * M + f.j;
+            u32 qv[HW];
+#pragma unroll
+            for (int s = 0; s < HW; s++) qv[s] = __ldg(qq + s * M);
 #pragma unroll
             for (int s = 0; s < HW; s++) {
-                const u32 la1n = sm[S_Z + f.pM + (int)qq[s * M]];     /* La1_next[n] = Le2[Pi^-1(n)] */
+                const u32 la1n = sm[S_Z + f.pM + (int)qv[s]];        /* La1_next[n] = Le2[Pi^-1(n)] */
                 const u32 ls = vadd(sn1[s], sm[S_LP + (f.k0 + s) * TS + f.t]);
                 const u32 lapp = vadd(vadd(ls, sm[S_Y + (f.k0 + s) * TS + f.t]), la1n);
                 const u32 ge = __vcmpges2(lapp, 0u);
@@ -641,7 +650,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                     if (ext_out) {
 #pragma unroll
                         for (int s = 0; s < HW; s++) {
-                            const u32 x = sm[S_Z + f.pM + (int)qq[s * M]];
+                            const u32 x = sm[S_Z + f.pM + (int)qv[s]];
                             ext_out[d.ext_off + j * W + f.k0 + s] = (int16_t)(l ? (x >> 16) : (x & 0xFFFFu));
                         }
                     }
