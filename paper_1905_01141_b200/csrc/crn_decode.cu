@@ -368,7 +368,8 @@ __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sy
  * ====================================================================== */
 struct SCtx {
     u32 *sm;        /* shared-memory base (fast layout) */
-    u32 ta;         /* this thread's TMEM base: lane quadrant + 128-column block */
+    u32 ta;         /* this thread's TMEM metric slots: lane quadrant + 128-column block */
+    u32 ts;         /* this thread's TMEM statics: Ls-Lp1 (16 columns), Ls[Pi]-Lp2 (16) */
     int tid, t, p, j, M, pM, k0;
 };
 
@@ -393,23 +394,57 @@ __device__ __forceinline__ void tm_wait_ld8(u32 v[NS]) {
                  :: "memory");
 }
 
+__device__ __forceinline__ void tm_store16(u32 ta, const u32 v[HW]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 :: "r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                    "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+                 : "memory");
+}
+
+/* Loads 16 columns and waits for them (used outside the recursion loops). */
+__device__ __forceinline__ void tm_load16_wait(u32 ta, u32 v[HW]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+                 "tcgen05.wait::ld.sync.aligned;"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                 : "r"(ta)
+                 : "memory");
+}
+
 /* Phase 0 (row a4): chunk[s] = (Lu+Lp, Lu-Lp) with Lu = Ls + La for the
- * thread's 16 steps, from the static Ls-Lp (registers), Lp (shared plane) and
- * the a-priori La gathered through a QPP table (zero in DEC1 of iteration 1). */
-__device__ __forceinline__ void build_chunk(const SCtx &f, const u32 (&sn)[HW], const u32 *lp, const u32 *la,
-                                            const u32 *__restrict__ q, bool zero_la) {
+ * thread's 16 steps, from the static Ls-Lp (TMEM), Lp (shared plane) and the
+ * a-priori La gathered at the thread's QPP word indices q[] (registers; zero
+ * in DEC1 of iteration 1). */
+__device__ __forceinline__ void build_chunk(const SCtx &f, int c, const u32 (&q)[HW], const u32 *lp, const u32 *la,
+                                            bool zero_la) {
     uint2 *ch = reinterpret_cast<uint2 *>(f.sm + S_CH) + f.tid;
-    const u32 *qq = q + f.k0 * f.M + f.j;
     lp += f.k0 * TS + f.t;
-    u32 qv[HW];             /* all table entries first: one L2 round trip, not 16 */
-#pragma unroll
-    for (int s = 0; s < HW; s++) qv[s] = zero_la ? 0u : __ldg(qq + s * f.M);
+    u32 sn[HW];
+    tm_load16_wait(f.ts + c * HW, sn);
 #pragma unroll
     for (int s = 0; s < HW; s++) {
-        const u32 a = zero_la ? 0u : la[f.pM + (int)qv[s]];
+        const u32 a = zero_la ? 0u : la[q[s]];
         const u32 d = vadd(sn[s], a);                       /* Lu - Lp */
         const u32 p = lp[s * TS];
         ch[s * BLOCK] = make_uint2(vadd(vadd(d, p), p), d);
+    }
+}
+
+/* 16 consecutive int16 LLRs of one stream: 8-byte vector loads when aligned.
+ * Returned as 8 words of (element 2i, element 2i+1). */
+__device__ __forceinline__ void load16(const int16_t *__restrict__ src, u32 w[HW / 2]) {
+    if ((reinterpret_cast<uintptr_t>(src) & 7) == 0) {
+        const uint2 *v = reinterpret_cast<const uint2 *>(src);
+#pragma unroll
+        for (int k = 0; k < HW / 4; k++) {
+            const uint2 x = __ldg(v + k);
+            w[2 * k] = x.x;
+            w[2 * k + 1] = x.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < HW / 2; k++)
+            w[k] = (u32)(uint16_t)__ldg(src + 2 * k) | ((u32)(uint16_t)__ldg(src + 2 * k + 1) << 16);
     }
 }
 
@@ -524,6 +559,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
     SCtx f;
     f.sm = sm;
     f.ta = tmem + ((u32)((warp & 3) * 32) << 16) + (u32)((warp >> 2) * 128);
+    f.ts = tmem + ((u32)((warp & 3) * 32) << 16) + (u32)(3 * 128 + (warp >> 2) * 2 * HW);
     f.tid = tid;
     f.t = tid - (tail_thr ? WMAX : 0);
     const bool active = f.t < T;
@@ -536,31 +572,53 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
     const u32 *qinv = tab.qinv_ts + tab.qpp_off[tk.kidx];   /* interleaved position of jW+i */
     const u32 *cpow = tab.crc_pow + tab.crc_off[tk.kidx];
 
-    /* ---- row a2: stage own half-window of both CBs of the pair into registers:
-     * Ls-Lp1 (natural) and Ls[Pi]-Lp2 (interleaved); Lp1, Lp2 into the shared planes */
-    u32 sn1[HW], sn2[HW];
+    /* ---- row a2: stage own half-window of both CBs of the pair: Lp1, Lp2 into
+     * the shared planes, Ls-Lp1 (natural) and Ls[Pi]-Lp2 (interleaved) into
+     * TMEM; the thread's QPP word indices stay in registers for the task */
+    u32 q1[HW], q2[HW];     /* pM + position of Pi^-1(jW+k) (DEC1 gather) / Pi(jW+k) (DEC2 gather) */
     {
         const int p = f.p, j = f.j;
         const int clo = sh.cb[2 * p], chi = sh.cb[2 * p + 1];
         const int Flo = sh.F[2 * p], Fhi = sh.F[2 * p + 1];
         const int64_t olo = clo >= 0 ? desc[clo].llr_off : 0, ohi = chi >= 0 ? desc[chi].llr_off : 0;
+        const int n0 = j * W + f.k0;
         u32 *tmp = sm + S_CH;                 /* natural Ls, window-major, for the interleaved gather */
+        u32 sn[HW];
 #pragma unroll
-        for (int s = 0; s < HW; s++) {
-            const int n = j * W + f.k0 + s;
-            int16_t vs0 = 0, vs1 = 0, va0 = 0, va1 = 0, vq0 = 0, vq1 = 0;
-            if (clo >= 0) { vs0 = l0[olo + n]; va0 = l1[olo + n]; vq0 = l2[olo + n]; }
-            if (chi >= 0) { vs1 = l0[ohi + n]; va1 = l1[ohi + n]; vq1 = l2[ohi + n]; }
-            if (n < Flo) { vs0 = -4096; va0 = -4096; }            /* known filler 0 */
-            if (n < Fhi) { vs1 = -4096; va1 = -4096; }
-            const u32 ls = clamp_pack(vs0, vs1), p1 = clamp_pack(va0, va1);
-            sn1[s] = __vsub2(ls, p1);
-            if (active) {
-                tmp[(f.k0 + s) * TS + f.t] = ls;
-                sm[S_LP + (f.k0 + s) * TS + f.t] = p1;
-                sm[S_LP + SUMK + (f.k0 + s) * TS + f.t] = clamp_pack(vq0, vq1);
+        for (int x = 0; x < 3; x++) {
+            const int16_t *src = x == 0 ? l0 : x == 1 ? l1 : l2;
+            u32 wl[HW / 2], wh[HW / 2];
+            if (clo >= 0) load16(src + olo + n0, wl);
+            else {
+#pragma unroll
+                for (int k = 0; k < HW / 2; k++) wl[k] = 0;
+            }
+            if (chi >= 0) load16(src + ohi + n0, wh);
+            else {
+#pragma unroll
+                for (int k = 0; k < HW / 2; k++) wh[k] = 0;
+            }
+#pragma unroll
+            for (int s = 0; s < HW; s++) {
+                u32 v = __byte_perm(wl[s / 2], wh[s / 2], (s & 1) ? 0x7632 : 0x5410);
+                if (x < 2) {                                       /* known filler 0: Ls = Lp1 = -4096 */
+                    if (n0 + s < Flo) v = (v & 0xFFFF0000u) | 0xF000u;
+                    if (n0 + s < Fhi) v = (v & 0x0000FFFFu) | 0xF0000000u;
+                }
+                v = __vmins2(__vmaxs2(v, CLIP_LO), CLIP_HI);
+                const int ix = (f.k0 + s) * TS + f.t;
+                if (x == 0) {
+                    sn[s] = v;
+                    if (active) tmp[ix] = v;
+                } else if (x == 1) {
+                    sn[s] = __vsub2(sn[s], v);
+                    if (active) sm[S_LP + ix] = v;
+                } else if (active) {
+                    sm[S_LP + SUMK + ix] = v;
+                }
             }
         }
+        tm_store16(f.ts, sn);
         if (active && tail_thr && j == M - 1) {
 #pragma unroll
             for (int mm = 0; mm < 12; mm++) {     /* tails: DESIGN.md R11 column order */
@@ -571,26 +629,27 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                 sm[S_TAIL + p * 12 + mm] = clamp_pack(v0, v1);
             }
         }
-        __syncthreads();
-        const u32 *qq = qts + f.k0 * M + j;
-        u32 qv[HW];
 #pragma unroll
-        for (int s = 0; s < HW; s++) qv[s] = __ldg(qq + s * M);
-#pragma unroll
-        for (int s = 0; s < HW; s++) {       /* interleaved systematic Ls[Pi(jW+k)] */
-            const u32 lsi = tmp[f.pM + (int)qv[s]];
-            sn2[s] = __vsub2(lsi, sm[S_LP + SUMK + (f.k0 + s) * TS + f.t]);
+        for (int s = 0; s < HW; s++) {
+            q1[s] = f.pM + __ldg(qinv + (f.k0 + s) * M + j);
+            q2[s] = f.pM + __ldg(qts + (f.k0 + s) * M + j);
         }
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < HW; s++)          /* interleaved systematic Ls[Pi(jW+k)] */
+            sn[s] = __vsub2(tmp[q2[s]], sm[S_LP + SUMK + (f.k0 + s) * TS + f.t]);
+        tm_store16(f.ts + HW, sn);
+        tm_wait_st();
         __syncthreads();
     }
 
     for (int it = 1; it <= max_iters; it++) {
         /* DEC1: La1[n] = Le2[Pi^-1(n)] gathered from Z (zero in iteration 1) */
-        build_chunk(f, sn1, sm + S_LP, sm + S_Z, qinv, it == 1);
+        build_chunk(f, 0, q1, sm + S_LP, sm + S_Z, it == 1);
         siso_split(f, tail_thr, 0, it);
         __syncthreads();
         /* DEC2: La2[i] = Le1[Pi(i)] gathered from Y */
-        build_chunk(f, sn2, sm + S_LP + SUMK, sm + S_Y, qts, false);
+        build_chunk(f, 1, q2, sm + S_LP + SUMK, sm + S_Y, false);
         siso_split(f, tail_thr, 1, it);
         __syncthreads();
         if (!et && it != max_iters) continue;     /* fixed mode: decide only at the end */
@@ -599,14 +658,12 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
          * thread and CB lane, merged per window; windowed CRC */
         {
             u32 wlo = 0, whi = 0;
-            const u32 *qq = qinv + f.k0 * M + f.j;
-            u32 qv[HW];
-#pragma unroll
-            for (int s = 0; s < HW; s++) qv[s] = __ldg(qq + s * M);
+            u32 sn[HW];
+            tm_load16_wait(f.ts, sn);
 #pragma unroll
             for (int s = 0; s < HW; s++) {
-                const u32 la1n = sm[S_Z + f.pM + (int)qv[s]];        /* La1_next[n] = Le2[Pi^-1(n)] */
-                const u32 ls = vadd(sn1[s], sm[S_LP + (f.k0 + s) * TS + f.t]);
+                const u32 la1n = sm[S_Z + q1[s]];                    /* La1_next[n] = Le2[Pi^-1(n)] */
+                const u32 ls = vadd(sn[s], sm[S_LP + (f.k0 + s) * TS + f.t]);
                 const u32 lapp = vadd(vadd(ls, sm[S_Y + (f.k0 + s) * TS + f.t]), la1n);
                 const u32 ge = __vcmpges2(lapp, 0u);
                 wlo |= (ge & 1u) << s;
@@ -650,7 +707,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                     if (ext_out) {
 #pragma unroll
                         for (int s = 0; s < HW; s++) {
-                            const u32 x = sm[S_Z + f.pM + (int)qv[s]];
+                            const u32 x = sm[S_Z + q1[s]];
                             ext_out[d.ext_off + j * W + f.k0 + s] = (int16_t)(l ? (x >> 16) : (x & 0xFFFFu));
                         }
                     }
