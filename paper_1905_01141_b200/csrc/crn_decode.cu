@@ -419,14 +419,17 @@ __device__ __forceinline__ void build_chunk(const SCtx &f, int c, const u32 (&q)
                                             bool zero_la) {
     uint2 *ch = reinterpret_cast<uint2 *>(f.sm + S_CH) + f.tid;
     lp += f.k0 * TS + f.t;
-    u32 sn[HW];
+    u32 a[HW], pv[HW], sn[HW];
+#pragma unroll
+    for (int s = 0; s < HW; s++) {          /* shared loads first: the TMEM load below is a compiler barrier */
+        a[s] = zero_la ? 0u : la[q[s]];
+        pv[s] = lp[s * TS];
+    }
     tm_load16_wait(f.ts + c * HW, sn);
 #pragma unroll
     for (int s = 0; s < HW; s++) {
-        const u32 a = zero_la ? 0u : la[q[s]];
-        const u32 d = vadd(sn[s], a);                       /* Lu - Lp */
-        const u32 p = lp[s * TS];
-        ch[s * BLOCK] = make_uint2(vadd(vadd(d, p), p), d);
+        const u32 d = vadd(sn[s], a[s]);                    /* Lu - Lp */
+        ch[s * BLOCK] = make_uint2(vadd(vadd(d, pv[s]), pv[s]), d);
     }
 }
 
@@ -515,7 +518,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
                 const uint2 g = ch[ss * BLOCK];
                 const u32 p = lp[ss * TS];
                 tm_wait_ld8(cur);
-                if (ss > 0) tm_load8(f.ta + (ss - 1) * 8, nx);
+                tm_load8(f.ta + (ss > 0 ? ss - 1 : 0) * 8, nx);      /* unconditional: no branch around the load */
                 le[ss * TS] = lambda_le(cur, b, p);                /* alpha_ss (stored) + beta_{ss+1} */
                 beta_step_d(b, p, g.x, g.y);
             }
@@ -536,7 +539,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
                 const uint2 g = ch[ss * BLOCK];
                 const u32 p = lp[ss * TS];
                 tm_wait_ld8(cur);
-                if (ss < HW - 1) tm_load8(f.ta + (ss + 1) * 8, nx);
+                tm_load8(f.ta + (ss < HW - 1 ? ss + 1 : ss) * 8, nx);
                 le[(HW + ss) * TS] = lambda_le(a, cur, p);         /* alpha_{16+ss} + beta_{17+ss} (stored) */
                 alpha_step_d(a, p, g.x, g.y);
             }
