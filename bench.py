@@ -95,6 +95,8 @@ def _peak_alu(num_sms, mhz):
 
 
 def _traffic():
+    """DRAM bytes per decode launch from the committed ncu --set full capture
+    (profiles/ncu_decode_summary.json, written by tools/ncu_summary.py)."""
     p = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
     try:
         with open(p) as f:
@@ -103,10 +105,9 @@ def _traffic():
         return None
 
 
-def cpu_baseline(n_sample=256, seed=0):
-    """The oracle as it stands, timed on this host's cores on a bounded sample of
-    the same workload (the first n_sample CBs of cell 0..: cfg4 CBs)."""
-    import oracle
+def _cpu_sample(n_sample, seed=0):
+    """A bounded sample of the bench workload for the oracle: the first n_sample
+    CBs of cfg4 (cells 0.., 256 CBs per cell), inputs built by the oracle side."""
     from paper_1905_01141_b200 import workload as wlmod
     from tests._inputs import oracle_llrs, offsets
     per_cell = 256
@@ -118,42 +119,102 @@ def cpu_baseline(n_sample=256, seed=0):
     cbs, ll = oracle_llrs(wl)
     K = np.array([c["K"] for c in cbs], np.int32)
     lo, bo = offsets(K)
+    return dict(K=K, args=(K, np.zeros_like(K), np.full_like(K, 2), lo, bo, *(x.numpy() for x in ll)),
+                cells=cells, n=n_sample)
+
+
+def cpu_baseline(sample, iters=8):
+    """The oracle as it stands, timed on this host's cores on a bounded sample
+    of the same workload (decode only; inputs prepared beforehand)."""
+    import oracle
     cores = len(os.sched_getaffinity(0))
-    args = (K, np.zeros_like(K), np.full_like(K, 2), lo, bo, *(x.numpy() for x in ll))
     t0 = time.perf_counter()
-    r = oracle.decode_batch(*args, max_iters=8, early_term=False, nthreads=cores, want_ext=False)
+    r = oracle.decode_batch(*sample["args"], max_iters=iters, early_term=False, nthreads=cores, want_ext=False)
     dt = time.perf_counter() - t0
-    bits = int((K - 24).sum())
+    bits = int((sample["K"] - 24).sum())
+    c = sample["cells"]
     return {"value": bits / dt / 1e6, "unit": "Mbit/s", "cores": cores, "kind": "oracle",
-            "sample": f"{n_sample} CBs of cfg4 (cells {cells[0]}-{cells[-1]}), 8 fixed iterations, "
-                      f"{dt:.2f} s wall on {cores} threads (gcc -O2 scalar C)",
-            "ops": int(r["ops"])}
+            "sample": f"{sample['n']} CBs of cfg4 (cells {c[0]}-{c[-1]}), {iters} fixed iterations, "
+                      f"{dt:.2f} s wall x {cores} threads = {dt * cores:.1f} CPU-s (gcc -O2 scalar C)",
+            "ops": int(r["ops"]), "seconds": dt}
 
 
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
+    sample = _cpu_sample(args.ref_sample, args.seed)
     for _ in range(args.warmup):
-        cpu_baseline(n_sample=args.ref_sample)
+        cpu_baseline(sample, args.iters)
     vals, times = [], []
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        cb = cpu_baseline(n_sample=args.ref_sample)
-        times.append(time.perf_counter() - t0)
+        cb = cpu_baseline(sample, args.iters)
+        times.append(cb["seconds"])
         vals.append(cb["value"])
     v = statistics.median(vals)
     cb["value"] = v
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Mbit/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int16",
-           "data": "synthetic", "config": {"workload": _workload_name(8) + f" -- bounded sample of "
-                                                                         f"{args.ref_sample} CBs per step",
+           "data": "synthetic", "config": {"workload": _workload_name(args.iters) + f" -- bounded sample of "
+                                                                              f"{args.ref_sample} CBs per step",
                                             "parallelism": "CPU threads (oracle)"},
            "cpu_baseline": cb, "e2e": {"value": v, "unit": "Mbit/s", "h2d_bytes_per_step": 0,
                                        "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
+
+
+def run_latency(args, seed=0):
+    """BASELINE cfg5: paced 1 ms TTIs of 200 CBs (20 cells x 10 CBs, K uniform over
+    the 188 sizes, Eb/N0 ~ U[0.5, 3] dB per CB, CRC ET at max 8 iterations), 4 cell
+    groups -> 4 CUDA streams, through crn_stream_run (host buffers in, host
+    results out).  TTI t uses cells 20t..20t+19 of cfg5; args.lat_distinct distinct
+    TTIs are generated and cycled over args.lat_ttis releases."""
+    from paper_1905_01141_b200 import batch as bmod
+    from paper_1905_01141_b200 import crn
+    from paper_1905_01141_b200 import workload as wlmod
+    n_groups, cells_per_tti = 4, 20
+    t_gen = time.perf_counter()
+    distinct = []
+    for t in range(args.lat_distinct):
+        wl = wlmod.make_workload(5, seed=seed, cells=range(cells_per_tti * t, cells_per_tti * (t + 1)), device="cuda")
+        b = bmod.build(wl)
+        grp = []
+        for gi in range(n_groups):
+            sel = np.flatnonzero(((b.cb_cell % cells_per_tti) // (cells_per_tti // n_groups)) == gi)
+            d = b.desc[sel].copy()
+            K = d["K"].astype(np.int64)
+            d["llr_off"] = np.concatenate([[0], np.cumsum(K + 4)[:-1]]) if K.size else K
+            d["bit_off"] = np.concatenate([[0], np.cumsum((K + 31) // 32)[:-1]]) if K.size else K
+            src = torch.from_numpy(np.concatenate([np.arange(int(o), int(o) + int(k) + 4)
+                                                   for o, k in zip(b.desc["llr_off"][sel], K)])).cuda()
+            hl = [x[src].cpu().pin_memory() for x in b.llr]
+            nw = max(int(((K + 31) // 32).sum()), 1)
+            grp.append(dict(desc=d, l0=hl[0], l1=hl[1], l2=hl[2],
+                            bits=torch.zeros(nw, dtype=torch.int32).pin_memory(),
+                            ok=torch.zeros(max(sel.size, 1), dtype=torch.uint8).pin_memory(),
+                            it=torch.zeros(max(sel.size, 1), dtype=torch.uint8).pin_memory(),
+                            sum_k=int(K.sum()), n_cb=int(sel.size), info=int((d["K"] - d["F"] - 24).sum())))
+        distinct.append(grp)
+    t_gen = time.perf_counter() - t_gen
+    groups = [g for t in range(args.lat_ttis) for g in distinct[t % args.lat_distinct]]
+    tim = crn.stream_run(groups, args.lat_ttis, n_groups, 1000.0, 8, True)
+    skip = min(10, args.lat_ttis // 10)
+    lat, dev = tim["latency_us"][skip:], tim["device_us"][skip:]
+    its = np.concatenate([g["it"].numpy()[:g["n_cb"]] for grp in distinct for g in grp])
+    sum_k = [sum(g["sum_k"] for g in grp) for grp in distinct]
+    return {"workload": "cfg5: 1 ms TTIs of 200 CBs (20 cells x 10), K ~ U(188 sizes), QPSK Eb/N0 ~ U[0.5,3] dB "
+                        "per CB, CRC24B ET max 8 iterations, 4 cell groups = 4 CUDA streams, host buffers in/out "
+                        "(crn_stream_run)",
+            "n_tti": args.lat_ttis, "distinct_ttis": args.lat_distinct, "period_us": 1000.0,
+            "measured_ttis": int(lat.size), "p50_us": float(np.percentile(lat, 50)),
+            "p99_us": float(np.percentile(lat, 99)), "max_us": float(lat.max()), "mean_us": float(lat.mean()),
+            "device_p50_us": float(np.percentile(dev, 50)), "device_p99_us": float(np.percentile(dev, 99)),
+            "deadline_us": 2000.0, "deadline_misses": int((lat > 2000.0).sum()),
+            "mean_iters": float(its.mean()), "mean_sum_k_per_tti": float(np.mean(sum_k)),
+            "gen_s": round(t_gen, 1),
+            "latency": "release (pacer) -> last group's results in pinned host memory (completion thread)"}
 
 
 def run_crn(args):
@@ -220,24 +281,21 @@ def run_crn(args):
     ms_step = tmax / args.steps
     value = info_bits / (ms_step * 1e-3) / 1e6
 
-    # ---- e2e: host (pinned) LLRs -> device -> decode -> bits + crc back, every step
+    # ---- e2e: pinned host LLRs -> crn_plan_decode_host (chunked upload / decode /
+    # download overlap inside libcrn) -> packed bits + crc_ok in pinned host memory
     e2e = None
     if not args.no_e2e:
         host = [x.cpu().pin_memory() for x in b.llr]
-        dl = [torch.empty_like(x) for x in b.llr]
         hb = torch.empty(bits.numel(), dtype=bits.dtype).pin_memory()
         hok = torch.empty(ok.numel(), dtype=ok.dtype).pin_memory()
 
         def e2e_step():
-            for d, h in zip(dl, host):
-                d.copy_(h, non_blocking=True)
-            plan.decode(dl[0], dl[1], dl[2], iters, False, bits, ok, None, None, stream=stream)
-            hb.copy_(bits, non_blocking=True)
-            hok.copy_(ok, non_blocking=True)
+            plan.decode_host(host[0], host[1], host[2], iters, False, hb, hok, None, stream=stream)
 
         for _ in range(max(1, args.warmup)):
             e2e_step()
         barrier()
+        hb.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ne = max(1, min(args.steps, 5))
         e0.record(stream)
@@ -248,10 +306,13 @@ def run_crn(args):
         te = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device="cuda")
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        n_ok_host = int(hok[:b.n_cb].to(torch.int64).sum())
         e2e = {"value": info_bits / (te.item() * 1e-3) / 1e6, "unit": "Mbit/s",
-               "h2d_bytes_per_step": in_bytes * ws, "d2h_bytes_per_step": (hb.numel() * 4 + hok.numel()) * ws,
-               "ms_per_step": te.item(), "path": "pinned host LLRs -> cudaMemcpyAsync -> crn_plan_decode -> "
-                                                   "packed bits + crc_ok -> pinned host"}
+               "h2d_bytes_per_step": in_bytes * ws, "d2h_bytes_per_step": (b.n_words * 4 + b.n_cb) * ws,
+               "ms_per_step": te.item(), "chunks": plan.chunks, "crc_ok_host": n_ok_host,
+               "path": "pinned host LLRs -> crn_plan_decode_host (chunked H2D / decode / D2H overlap) -> "
+                       "packed bits + crc_ok in pinned host memory"}
+        del host
 
     if rank != 0:
         if dist:
@@ -279,12 +340,18 @@ def run_crn(args):
                    "parallelism": f"dp{ws} (cells sharded, no data-path collective)",
                    "info_bits_per_step": info_bits, "sum_K": sum_k, "crc_ok": n_ok},
         "roofline": roof, "clocks": clocks, "gpu_launches": args.steps * plan.launches,
+        "gpu_launches_note": "one persistent decode_kernel launch per step (+1 cudaMemsetAsync of the task counter)",
         "e2e": e2e, "kernel_ms_mean": mean_launch_ms, "kernel_ms": launch_ms,
         "sum_k_mbps": sum_k / (ms_step * 1e-3) / 1e6,
     }
+    if not args.no_latency and ws == 1:
+        try:
+            out["latency"] = run_latency(args, seed=args.seed)
+        except Exception as e:           # the throughput number stands without it
+            out["latency"] = {"error": repr(e)}
     if not args.no_cpu_baseline:
         try:
-            out["cpu_baseline"] = cpu_baseline(n_sample=args.ref_sample)
+            out["cpu_baseline"] = cpu_baseline(_cpu_sample(args.ref_sample, args.seed), iters)
         except Exception as e:           # the GPU number stands without it
             out["cpu_baseline"] = {"error": repr(e)}
     print(json.dumps(out), flush=True)
@@ -301,7 +368,11 @@ def main():
     ap.add_argument("--impl", default="crn", choices=["crn", "reference"])
     ap.add_argument("--iters", type=int, default=8)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--ref-sample", type=int, default=256)
+    ap.add_argument("--ref-sample", type=int, default=2048,
+                    help="CBs of the oracle's bounded sample (cpu_baseline / --impl reference)")
+    ap.add_argument("--lat-ttis", type=int, default=1000)
+    ap.add_argument("--lat-distinct", type=int, default=100)
+    ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -108,6 +108,65 @@ int crn_plan_decode(void *plan, const int16_t *llr_sys, const int16_t *llr_p1,
 int crn_plan_launches(void *plan);
 void crn_plan_destroy(void *plan);
 
+/* Host-buffer decode (the end-to-end path: LLRs arrive in host memory from the
+ * fronthaul).  h_llr_* are HOST arrays laid out exactly as
+ * the plan's descriptors say (llr_off), h_out_bits / h_crc_ok / h_iters_used
+ * (may be NULL) HOST outputs (bit_off, CB index).  Pinned (page-locked) host
+ * memory is required for the copies to overlap the decode; pageable memory
+ * works but serialises.  The plan's CBs are cut into n_chunks chunks of
+ * consecutive CB indices (0 = automatic: about 4 waves of the persistent grid
+ * per chunk, at most 16); chunk c's upload, chunk c-1's decode and chunk c-2's
+ * download run concurrently on two internal copy streams and cuda_stream.
+ * Asynchronous: every step is ordered after prior work on cuda_stream and
+ * cuda_stream waits for the last download, so synchronising cuda_stream makes
+ * the host outputs valid.  The plan owns the device staging buffers (sized
+ * once, on the first call).  Errors as crn_plan_decode, CRN_EINVAL for
+ * n_chunks outside [0, 64]; ext_out is not offered on this path. */
+int crn_plan_decode_host(void *plan, const int16_t *h_llr_sys, const int16_t *h_llr_p1,
+                         const int16_t *h_llr_p2, int32_t max_iters, int32_t early_term,
+                         uint32_t *h_out_bits, uint8_t *h_crc_ok, uint8_t *h_iters_used,
+                         int32_t n_chunks, void *cuda_stream);
+/* Chunks the last crn_plan_decode_host of this plan used (0 if none yet). */
+int crn_plan_chunks(void *plan);
+
+/* ------------------------------------------------------------------ streaming TTIs */
+
+/* One cell group's share of one TTI (the CCDUs of PAPER.md:326 that arrive
+ * together every millisecond).  All pointers are HOST memory (pinned for
+ * overlap): desc[n_cb] as in crn_decode_batch_ex (llr_off / bit_off relative
+ * to this group's own arrays), llr_* of n_llr elements each, out_bits of
+ * n_words words, crc_ok[n_cb], iters_used[n_cb] (may be NULL).  n_cb may be 0. */
+typedef struct {
+    const crn_cb_desc *desc;
+    int32_t n_cb, reserved;
+    const int16_t *llr_sys, *llr_p1, *llr_p2;
+    int64_t n_llr;
+    uint32_t *out_bits;
+    int64_t n_words;
+    uint8_t *crc_ok, *iters_used;
+} crn_tti_group;
+
+/* Per-TTI timestamps in microseconds from the run's start (steady clock):
+ * release (the pacer's release instant), submitted (all groups enqueued),
+ * complete (the last group's downloads observed done by the completion
+ * thread), latency = complete - release, device = span of the TTI's GPU work
+ * (first upload start .. last download end, CUDA events). */
+typedef struct {
+    double release_us, submitted_us, complete_us, latency_us, device_us;
+} crn_tti_timing;
+
+/* Paced streaming decode (Algorithm 2 as a GPU executor;
+ * the timestamps play the paper's performance captor, :398-411).  groups[t *
+ * n_groups + g] is group g of TTI t.  TTI t is released at t0 + t * period_us
+ * (period_us = 0: back to back); at release the host buckets each group's CBs
+ * into tasks (row a1) and enqueues upload -> decode -> download on the
+ * group's own CUDA stream (created by the call).  A completion thread records
+ * when each group's downloads finish.  Blocks until every TTI is done and
+ * fills timing[n_tti].  Every group is validated before the first release
+ * (CRN_EINVAL as crn_decode_batch_ex, or n_llr / n_words too small). */
+int crn_stream_run(const crn_tti_group *groups, int32_t n_tti, int32_t n_groups, double period_us,
+                   int32_t max_iters, int32_t early_term, crn_tti_timing *timing);
+
 /* Counted operations of one decode (the roofline numerator, DESIGN.md "op
  * count"): sum over CBs and executed iterations of 2 x (129 K + 90).  For a
  * fixed-iteration batch pass iters_used = NULL and it uses max_iters. */

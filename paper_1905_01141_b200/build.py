@@ -12,8 +12,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libcrn.so")
-SOURCES = ["crn_host.cpp", "crn_decode.cu", "crn_encode.cu", "crn_ubench.cu"]
-HEADERS = ["crn_internal.h", "qpp_table.h", os.path.join("..", "..", "include", "crn.h")]
+SOURCES = ["crn_host.cpp", "crn_runtime.cpp", "crn_decode.cu", "crn_encode.cu", "crn_ubench.cu"]
+HEADERS = ["crn_internal.h", "crn_plan.h", "qpp_table.h", os.path.join("..", "..", "include", "crn.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr"]

@@ -28,6 +28,18 @@ class Seg(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("C", "Kplus", "Kminus", "Cplus", "Cminus", "F", "L")]
 
 
+class TtiGroup(C.Structure):
+    _fields_ = [("desc", C.c_void_p), ("n_cb", C.c_int32), ("reserved", C.c_int32),
+                ("llr_sys", C.c_void_p), ("llr_p1", C.c_void_p), ("llr_p2", C.c_void_p),
+                ("n_llr", C.c_int64), ("out_bits", C.c_void_p), ("n_words", C.c_int64),
+                ("crc_ok", C.c_void_p), ("iters_used", C.c_void_p)]
+
+
+class TtiTiming(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("release_us", "submitted_us", "complete_us", "latency_us",
+                                          "device_us")]
+
+
 class CrnError(RuntimeError):
     pass
 
@@ -44,6 +56,9 @@ _SIGS = {
     "crn_plan_create": (C.c_int, [vp, C.c_int32, P(vp)]),
     "crn_plan_decode": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp]),
     "crn_plan_launches": (C.c_int, [vp]),
+    "crn_plan_decode_host": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, C.c_int32, vp]),
+    "crn_plan_chunks": (C.c_int, [vp]),
+    "crn_stream_run": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int32, vp]),
     "crn_plan_destroy": (None, [vp]),
     "crn_counted_ops": (C.c_int64, [i32p, C.c_int32, u8p, C.c_int32]),
     "crn_encode_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp]),
@@ -150,6 +165,20 @@ class Plan:
                                    _ptr(out_bits), _ptr(crc_ok), _ptr(iters_used), _ptr(ext_out),
                                    _stream(stream)), "crn_plan_decode")
 
+    def decode_host(self, h0, h1, h2, max_iters: int, early_term: bool, h_bits, h_ok, h_iters=None,
+                    n_chunks: int = 0, stream=None) -> None:
+        """crn_plan_decode_host: every buffer is a HOST (CPU, ideally pinned) torch tensor."""
+        for t in (h0, h1, h2, h_bits, h_ok, h_iters):
+            if t is not None and t.is_cuda:
+                raise CrnError("crn_plan_decode_host takes host buffers")
+        _chk(lib().crn_plan_decode_host(self.h, _ptr(h0), _ptr(h1), _ptr(h2), max_iters, int(early_term),
+                                        _ptr(h_bits), _ptr(h_ok), _ptr(h_iters), n_chunks, _stream(stream)),
+             "crn_plan_decode_host")
+
+    @property
+    def chunks(self) -> int:
+        return int(lib().crn_plan_chunks(self.h))
+
     @property
     def launches(self) -> int:
         return int(lib().crn_plan_launches(self.h))
@@ -164,6 +193,31 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+def stream_run(groups, n_tti: int, n_groups: int, period_us: float, max_iters: int, early_term: bool):
+    """crn_stream_run.  groups: list (length n_tti * n_groups, TTI-major) of dicts with
+    HOST arrays desc (numpy DESC_DTYPE), l0/l1/l2 (int16 tensors, pinned), bits (int32 tensor),
+    ok (uint8 tensor), it (uint8 tensor or None).  Returns a numpy structured array of timings."""
+    arr = (TtiGroup * len(groups))()
+    keep = []
+    for x, g in enumerate(groups):
+        d = np.ascontiguousarray(g["desc"], DESC_DTYPE)
+        keep.append(d)
+        for k in ("l0", "l1", "l2", "bits", "ok", "it"):
+            if g.get(k) is not None and g[k].is_cuda:
+                raise CrnError("crn_stream_run takes host buffers")
+        arr[x] = TtiGroup(d.ctypes.data if d.size else None, d.size, 0, _ptr(g["l0"]), _ptr(g["l1"]),
+                          _ptr(g["l2"]), g["l0"].numel(), _ptr(g["bits"]), g["bits"].numel(), _ptr(g["ok"]),
+                          _ptr(g.get("it")))
+    tim = (TtiTiming * n_tti)()
+    _chk(lib().crn_stream_run(arr, n_tti, n_groups, period_us, max_iters, int(early_term), tim),
+         "crn_stream_run")
+    out = np.zeros(n_tti, [(n, "f8") for n, _ in TtiTiming._fields_])
+    for i in range(n_tti):
+        for n, _ in TtiTiming._fields_:
+            out[n][i] = getattr(tim[i], n)
+    return out
 
 
 def counted_ops(K, max_iters: int, iters_used=None) -> int:

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "crn_internal.h"
+#include "crn_plan.h"
 #include "qpp_table.h"
 
 /* ------------------------------------------------------------------ size table */
@@ -152,18 +153,10 @@ extern "C" int crn_device_info(int32_t *num_sms, int32_t *clock_khz, int32_t *cc
     return CRN_OK;
 }
 
-struct DevTables {
-    uint32_t *qpp_wm = nullptr, *qpp_ts = nullptr, *qinv_ts = nullptr, *crc_pow = nullptr;
-    int32_t *qpp_off = nullptr, *crc_off = nullptr;
-    crn_tables tab{};
-    int grid = 0;
-};
-
 static std::mutex g_mu;
 static thread_local char g_err[256] = "";
 
-/* Records the CUDA error behind a CRN_ECUDA / CRN_ENOMEM for crn_last_error(). */
-static int cuda_fail(cudaError_t e, const char *where, int code) {
+int crn_cuda_fail(cudaError_t e, const char *where, int code) {
     snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
     cudaGetLastError();
     return code;
@@ -224,27 +217,27 @@ static int build_tables(int dev, DevTables **out) {
     cudaMemcpy(t.crc_pow, cp.data(), cp.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.qpp_off, qoff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.crc_off, coff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
-    if (cudaError_t e = cudaGetLastError()) return cuda_fail(e, "table upload", CRN_ECUDA);
+    if (cudaError_t e = cudaGetLastError()) return crn_cuda_fail(e, "table upload", CRN_ECUDA);
     t.tab.qpp_wm = t.qpp_wm; t.tab.qpp_ts = t.qpp_ts; t.tab.qinv_ts = t.qinv_ts; t.tab.crc_pow = t.crc_pow;
     t.tab.qpp_off = t.qpp_off; t.tab.crc_off = t.crc_off;
     t.grid = crn_decode_grid(dev);
     if (t.grid <= 0) {
         char where[96];
         snprintf(where, sizeof(where), "decode kernel configuration (code %d; needs exactly 1 CTA/SM)", t.grid);
-        return cuda_fail(cudaGetLastError(), where, CRN_ECUDA);
+        return crn_cuda_fail(cudaGetLastError(), where, CRN_ECUDA);
     }
     auto r = g_tables.emplace(dev, t);
     *out = &r.first->second;
     return CRN_OK;
 }
 
-static int get_ctx(int *dev, DevTables **t) {
+int crn_get_ctx(int *dev, DevTables **t) {
     if (!check_device(dev)) { cudaGetLastError(); return CRN_ENODEV; }
     std::lock_guard<std::mutex> lk(g_mu);
     return build_tables(*dev, t);
 }
 
-static int get_ws(int dev, void *stream, size_t bytes, void **ws) {
+int crn_get_ws(int dev, void *stream, size_t bytes, void **ws) {
     std::lock_guard<std::mutex> lk(g_mu);
     auto key = std::make_pair(dev, stream);
     auto it = g_ws.find(key);
@@ -260,20 +253,11 @@ static int get_ws(int dev, void *stream, size_t bytes, void **ws) {
 extern "C" size_t crn_workspace_bytes(void) {
     int dev;
     DevTables *t;
-    if (get_ctx(&dev, &t) != CRN_OK) return 0;
+    if (crn_get_ctx(&dev, &t) != CRN_OK) return 0;
     return crn_decode_ws_bytes(t->grid);
 }
 
 /* ------------------------------------------------------------------ plans (row a1) */
-struct Plan {
-    int dev = -1;
-    int n_cb = 0, n_tasks = 0;
-    crn_cb_desc *d_desc = nullptr;
-    crn_task *d_tasks = nullptr;
-    crn_pair *d_pairs = nullptr;
-    void *mem = nullptr;          /* one allocation holding the three arrays */
-};
-
 static bool ranges_overlap(std::vector<std::pair<int64_t, int64_t>> &r) {
     std::sort(r.begin(), r.end());
     for (size_t i = 1; i < r.size(); i++)
@@ -282,7 +266,7 @@ static bool ranges_overlap(std::vector<std::pair<int64_t, int64_t>> &r) {
 }
 
 /* Validate descriptors (crn.h: CRN_EINVAL rules). */
-static int validate(const crn_cb_desc *d, int n, bool want_ext) {
+int crn_validate(const crn_cb_desc *d, int n, bool want_ext) {
     std::vector<std::pair<int64_t, int64_t>> lr, br, er;
     lr.reserve(n); br.reserve(n);
     for (int i = 0; i < n; i++) {
@@ -299,10 +283,10 @@ static int validate(const crn_cb_desc *d, int n, bool want_ext) {
 }
 
 /* Bucket by K (largest first: longest tasks start first), pair equal-K CBs in
- * index order, group ceil-free: floor(6144/K) pairs per task. */
-static void build_tasks(const crn_cb_desc *d, int n, std::vector<crn_task> &tasks, std::vector<crn_pair> &pairs) {
-    std::vector<int> idx(n);
-    for (int i = 0; i < n; i++) idx[i] = i;
+ * index order, group floor(6144/K) pairs per task. */
+void crn_build_tasks(const crn_cb_desc *d, const int *sel, int n, std::vector<crn_task> &tasks,
+                     std::vector<crn_pair> &pairs) {
+    std::vector<int> idx(sel, sel + n);
     std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return d[a].K > d[b].K; });
     size_t s = 0;
     while (s < idx.size()) {
@@ -326,11 +310,13 @@ static void build_tasks(const crn_cb_desc *d, int n, std::vector<crn_task> &task
 }
 
 static int plan_build(const crn_cb_desc *desc, int n, bool want_ext, cudaStream_t st, bool async, Plan *P) {
-    int rc = validate(desc, n, want_ext);
+    int rc = crn_validate(desc, n, want_ext);
     if (rc) return rc;
     std::vector<crn_task> tasks;
     std::vector<crn_pair> pairs;
-    build_tasks(desc, n, tasks, pairs);
+    std::vector<int> all(n);
+    for (int i = 0; i < n; i++) all[i] = i;
+    crn_build_tasks(desc, all.data(), n, tasks, pairs);
     size_t b0 = sizeof(crn_cb_desc) * (size_t)n, b1 = sizeof(crn_task) * tasks.size(),
            b2 = sizeof(crn_pair) * pairs.size();
     size_t o1 = (b0 + 255) & ~(size_t)255, o2 = (o1 + b1 + 255) & ~(size_t)255, tot = o2 + b2 + 256;
@@ -353,30 +339,40 @@ static int plan_build(const crn_cb_desc *desc, int n, bool want_ext, cudaStream_
     return CRN_OK;
 }
 
-static int launch(Plan *P, DevTables *t, const int16_t *l0, const int16_t *l1, const int16_t *l2,
-                  int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
-                  void *ws, size_t ws_bytes, cudaStream_t st) {
-    if (P->n_cb == 0) return CRN_OK;
+int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn_task *d_tasks, int n_tasks,
+                     const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,
+                     int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
+                     void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (n_tasks == 0) return CRN_OK;
     if (!ws) {
-        int rc = get_ws(P->dev, (void *)st, crn_decode_ws_bytes(t->grid), &ws);
+        int rc = crn_get_ws(dev, (void *)st, crn_decode_ws_bytes(t->grid), &ws);
         if (rc) return rc;
     } else if (ws_bytes < crn_decode_ws_bytes(t->grid)) {
         return CRN_EINVAL;
     }
-    return crn_launch_decode(P->d_desc, P->d_tasks, P->n_tasks, P->d_pairs, l0, l1, l2, max_iters, et,
-                             bits, ok, it, ext, &t->tab, ws, (void *)st, t->grid);
+    return crn_launch_decode(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits, ok, it, ext,
+                             &t->tab, ws, (void *)st, t->grid);
+}
+
+static int launch(Plan *P, DevTables *t, const int16_t *l0, const int16_t *l1, const int16_t *l2,
+                  int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
+                  void *ws, size_t ws_bytes, cudaStream_t st) {
+    if (P->n_cb == 0) return CRN_OK;
+    return crn_launch_tasks(P->dev, t, P->d_desc, P->d_tasks, P->n_tasks, P->d_pairs, l0, l1, l2, max_iters, et,
+                            bits, ok, it, ext, ws, ws_bytes, st);
 }
 
 extern "C" int crn_plan_create(const crn_cb_desc *desc, int32_t n_cb, void **plan) {
     if (!plan || n_cb < 0 || (n_cb > 0 && !desc)) return CRN_EINVAL;
     int dev;
     DevTables *t;
-    int rc = get_ctx(&dev, &t);
+    int rc = crn_get_ctx(&dev, &t);
     if (rc) return rc;
     Plan *P = new Plan();
     P->dev = dev;
     rc = plan_build(desc, n_cb, true, 0, false, P);
     if (rc) { delete P; return rc; }
+    P->h_desc.assign(desc, desc + n_cb);
     *plan = P;
     return CRN_OK;
 }
@@ -389,7 +385,7 @@ extern "C" int crn_plan_decode(void *plan, const int16_t *l0, const int16_t *l1,
     if (P->n_cb && (!l0 || !l1 || !l2 || !bits || !ok)) return CRN_EINVAL;
     int dev;
     DevTables *t;
-    int rc = get_ctx(&dev, &t);
+    int rc = crn_get_ctx(&dev, &t);
     if (rc) return rc;
     if (dev != P->dev) return CRN_EINVAL;
     return launch(P, t, l0, l1, l2, max_iters, et, bits, ok, it, ext, nullptr, 0, (cudaStream_t)stream);
@@ -403,6 +399,7 @@ extern "C" int crn_plan_launches(void *plan) {
 extern "C" void crn_plan_destroy(void *plan) {
     Plan *P = (Plan *)plan;
     if (!P) return;
+    if (P->pipe) crn_pipe_destroy(P->pipe);
     if (P->mem) cudaFree(P->mem);
     delete P;
 }
@@ -417,7 +414,7 @@ extern "C" int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb, const 
     if (!desc || !l0 || !l1 || !l2 || !bits || !ok) return CRN_EINVAL;
     int dev;
     DevTables *t;
-    int rc = get_ctx(&dev, &t);
+    int rc = crn_get_ctx(&dev, &t);
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     std::vector<crn_cb_desc> hd;
@@ -472,7 +469,7 @@ extern "C" int crn_encode_batch(const crn_cb_desc *desc, int32_t n_cb, const uin
             return CRN_EINVAL;
     int dev;
     DevTables *t;
-    int rc = get_ctx(&dev, &t);
+    int rc = crn_get_ctx(&dev, &t);
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     void *dd = nullptr;

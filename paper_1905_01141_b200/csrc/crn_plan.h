@@ -1,0 +1,49 @@
+/* crn_plan.h -- host-side internals shared by crn_host.cpp (plans, tables,
+ * validation, task building) and crn_runtime.cpp (host-buffer pipeline, TTI
+ * stream runner).  Not part of the ABI (see include/crn.h). */
+#pragma once
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "crn_internal.h"
+
+struct DevTables {
+    uint32_t *qpp_wm = nullptr, *qpp_ts = nullptr, *qinv_ts = nullptr, *crc_pow = nullptr;
+    int32_t *qpp_off = nullptr, *crc_off = nullptr;
+    crn_tables tab{};
+    int grid = 0;
+};
+
+struct HostPipe;      /* crn_runtime.cpp: staging buffers + streams of crn_plan_decode_host */
+
+struct Plan {
+    int dev = -1;
+    int n_cb = 0, n_tasks = 0;
+    crn_cb_desc *d_desc = nullptr;
+    crn_task *d_tasks = nullptr;
+    crn_pair *d_pairs = nullptr;
+    void *mem = nullptr;          /* one allocation holding the three arrays */
+    std::vector<crn_cb_desc> h_desc;   /* host copy (kept for the host-buffer pipeline) */
+    HostPipe *pipe = nullptr;
+};
+
+/* Device context: checks for an sm_100 device and builds the per-device tables once. */
+int crn_get_ctx(int *dev, DevTables **t);
+/* Cached per-(device, stream) decode workspace. */
+int crn_get_ws(int dev, void *stream, size_t bytes, void **ws);
+/* Descriptor validation (include/crn.h CRN_EINVAL rules). */
+int crn_validate(const crn_cb_desc *d, int n, bool want_ext);
+/* Bucket by K (largest first), pair equal-K CBs, group pairs into CTA tasks.
+ * Only the CBs idx[0..n_idx) take part; pair0 of the tasks indexes `pairs`. */
+void crn_build_tasks(const crn_cb_desc *d, const int *idx, int n_idx, std::vector<crn_task> &tasks,
+                     std::vector<crn_pair> &pairs);
+/* Launch the decode kernel over n_tasks tasks (device arrays), workspace from the cache if ws == NULL. */
+int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn_task *d_tasks, int n_tasks,
+                     const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,
+                     int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
+                     void *ws, size_t ws_bytes, cudaStream_t st);
+/* Records the CUDA error behind a CRN_ECUDA / CRN_ENOMEM for crn_last_error(). */
+int crn_cuda_fail(cudaError_t e, const char *where, int code);
+/* Frees the host pipeline of a plan (crn_runtime.cpp). */
+void crn_pipe_destroy(HostPipe *p);

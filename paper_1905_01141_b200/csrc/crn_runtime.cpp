@@ -1,0 +1,414 @@
+/* crn_runtime.cpp -- libcrn's host runtime around the decode kernel:
+ *
+ *  (1) crn_plan_decode_host: decode from HOST buffers.  The plan's CBs are cut
+ *      into chunks of consecutive CB indices; chunk c's LLRs are copied in on a
+ *      copy stream while chunk c-1 decodes on the caller's stream and chunk
+ *      c-2's results are copied out on a third stream, so the PCIe transfers
+ *      overlap the decode (the end-to-end path of a BBU whose LLRs arrive from
+ *      the fronthaul into host memory).
+ *
+ *  (2) crn_stream_run: the paper's per-TTI operation ("CCDUs
+ *      arrive in batches every millisecond"; Algorithm 2, :372-393) as a paced
+ *      streaming executor: TTI i is released at t0 + i * period; each cell
+ *      group has its own CUDA stream (H2D -> decode -> D2H); a completion
+ *      thread time-stamps every (TTI, group) the moment its last copy lands,
+ *      like the paper's performance captor which records
+ *      the stage timestamps outside the real-time path.
+ *
+ * Nothing here computes the method: all decoding runs in crn_decode.cu.
+ */
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "crn_internal.h"
+#include "crn_plan.h"
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+double us_since(Clock::time_point t0, Clock::time_point t) {
+    return std::chrono::duration<double, std::micro>(t - t0).count();
+}
+
+struct Chunk {
+    int32_t cb0 = 0, cb1 = 0;             /* CB index range [cb0, cb1) */
+    int64_t llr0 = 0, llr1 = 0;           /* element range of the chunk's LLRs */
+    int64_t w0 = 0, w1 = 0;               /* output word range */
+    int32_t task0 = 0, n_tasks = 0;       /* slice of the pipe's task array */
+};
+
+}  // namespace
+
+struct HostPipe {
+    int requested = 0;                    /* chunk count asked for (n_chunks may be smaller) */
+    int n_chunks = 0;
+    std::vector<Chunk> ch;
+    void *mem = nullptr;                  /* device: tasks, pairs, LLR staging, outputs */
+    crn_task *d_tasks = nullptr;
+    crn_pair *d_pairs = nullptr;
+    int16_t *d_l[3] = {nullptr, nullptr, nullptr};
+    uint32_t *d_bits = nullptr;
+    uint8_t *d_ok = nullptr, *d_it = nullptr;
+    int64_t n_llr = 0, n_words = 0;
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_comp;
+    cudaEvent_t ev_start = nullptr, ev_end = nullptr;
+};
+
+void crn_pipe_destroy(HostPipe *p) {
+    if (!p) return;
+    if (p->s_in) cudaStreamSynchronize(p->s_in);
+    if (p->s_out) cudaStreamSynchronize(p->s_out);
+    for (auto e : p->ev_in) cudaEventDestroy(e);
+    for (auto e : p->ev_comp) cudaEventDestroy(e);
+    if (p->ev_start) cudaEventDestroy(p->ev_start);
+    if (p->ev_end) cudaEventDestroy(p->ev_end);
+    if (p->s_in) cudaStreamDestroy(p->s_in);
+    if (p->s_out) cudaStreamDestroy(p->s_out);
+    if (p->mem) cudaFree(p->mem);
+    delete p;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+/* Cut the plan into n chunks of consecutive CB indices with about equal sum K,
+ * build each chunk's tasks, allocate staging + outputs, create streams/events. */
+static int pipe_build(Plan *P, int n_chunks, HostPipe **out) {
+    const crn_cb_desc *d = P->h_desc.data();
+    const int n = P->n_cb;
+    HostPipe *p = new HostPipe();
+    int64_t sumk = 0;
+    for (int i = 0; i < n; i++) sumk += d[i].K;
+    std::vector<crn_task> tasks;
+    std::vector<crn_pair> pairs;
+    int64_t acc = 0;
+    int cb0 = 0;
+    for (int c = 0; c < n_chunks && cb0 < n; c++) {
+        int cb1 = cb0;
+        const int64_t target = (sumk * (c + 1) + n_chunks - 1) / n_chunks;
+        while (cb1 < n && (acc < target || cb1 == cb0)) acc += d[cb1++].K;
+        if (c == n_chunks - 1) while (cb1 < n) acc += d[cb1++].K;
+        Chunk k;
+        k.cb0 = cb0; k.cb1 = cb1;
+        k.llr0 = INT64_MAX; k.w0 = INT64_MAX;
+        for (int i = cb0; i < cb1; i++) {
+            k.llr0 = std::min(k.llr0, d[i].llr_off);
+            k.llr1 = std::max(k.llr1, d[i].llr_off + d[i].K + 4);
+            k.w0 = std::min(k.w0, d[i].bit_off);
+            k.w1 = std::max(k.w1, d[i].bit_off + (d[i].K + 31) / 32);
+        }
+        std::vector<int> sel(cb1 - cb0);
+        for (int i = cb0; i < cb1; i++) sel[i - cb0] = i;
+        k.task0 = (int32_t)tasks.size();
+        crn_build_tasks(d, sel.data(), (int)sel.size(), tasks, pairs);
+        k.n_tasks = (int32_t)tasks.size() - k.task0;
+        p->n_llr = std::max(p->n_llr, k.llr1);
+        p->n_words = std::max(p->n_words, k.w1);
+        p->ch.push_back(k);
+        cb0 = cb1;
+    }
+    p->n_chunks = (int)p->ch.size();
+    p->requested = n_chunks;
+    const size_t bt = sizeof(crn_task) * tasks.size(), bp = sizeof(crn_pair) * pairs.size();
+    const size_t o_p = align256(bt), o_l = o_p + align256(bp), bl = align256(sizeof(int16_t) * p->n_llr);
+    const size_t o_b = o_l + 3 * bl, o_ok = o_b + align256(4 * p->n_words), o_it = o_ok + align256(n);
+    const size_t tot = o_it + align256(n);
+    if (cudaMalloc(&p->mem, tot) != cudaSuccess) {
+        cudaGetLastError();
+        delete p;
+        return CRN_ENOMEM;
+    }
+    uint8_t *m = (uint8_t *)p->mem;
+    p->d_tasks = (crn_task *)m;
+    p->d_pairs = (crn_pair *)(m + o_p);
+    for (int s = 0; s < 3; s++) p->d_l[s] = (int16_t *)(m + o_l + s * bl);
+    p->d_bits = (uint32_t *)(m + o_b);
+    p->d_ok = m + o_ok;
+    p->d_it = m + o_it;
+    cudaMemcpy(p->d_tasks, tasks.data(), bt, cudaMemcpyHostToDevice);
+    cudaMemcpy(p->d_pairs, pairs.data(), bp, cudaMemcpyHostToDevice);
+    cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking);
+    p->ev_in.resize(p->n_chunks);
+    p->ev_comp.resize(p->n_chunks);
+    for (int c = 0; c < p->n_chunks; c++) {
+        cudaEventCreateWithFlags(&p->ev_in[c], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&p->ev_comp[c], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&p->ev_end, cudaEventDisableTiming);
+    if (cudaError_t e = cudaGetLastError()) {
+        crn_pipe_destroy(p);
+        return crn_cuda_fail(e, "host pipeline setup", CRN_ECUDA);
+    }
+    *out = p;
+    return CRN_OK;
+}
+
+extern "C" int crn_plan_decode_host(void *plan, const int16_t *h0, const int16_t *h1, const int16_t *h2,
+                                    int32_t max_iters, int32_t et, uint32_t *h_bits, uint8_t *h_ok,
+                                    uint8_t *h_it, int32_t n_chunks, void *stream) {
+    Plan *P = (Plan *)plan;
+    if (!P || max_iters < 1 || max_iters > CRN_MAX_ITERS || n_chunks < 0 || n_chunks > 64) return CRN_EINVAL;
+    if (P->n_cb == 0) return CRN_OK;
+    if (!h0 || !h1 || !h2 || !h_bits || !h_ok) return CRN_EINVAL;
+    int dev;
+    DevTables *t;
+    int rc = crn_get_ctx(&dev, &t);
+    if (rc) return rc;
+    if (dev != P->dev) return CRN_EINVAL;
+    if (n_chunks == 0) /* auto: >= 4 waves of the persistent grid per chunk, at most 16 chunks */
+        n_chunks = std::max(1, std::min(16, P->n_tasks / (4 * t->grid)));
+    if (!P->pipe || P->pipe->requested != n_chunks) {
+        if (P->pipe) crn_pipe_destroy(P->pipe);
+        P->pipe = nullptr;
+        rc = pipe_build(P, n_chunks, &P->pipe);
+        if (rc) return rc;
+    }
+    HostPipe *p = P->pipe;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaEventRecord(p->ev_start, st);
+    cudaStreamWaitEvent(p->s_in, p->ev_start, 0);
+    cudaStreamWaitEvent(p->s_out, p->ev_start, 0);
+    const int16_t *hs[3] = {h0, h1, h2};
+    for (int c = 0; c < p->n_chunks; c++) {
+        const Chunk &k = p->ch[c];
+        const size_t nb = sizeof(int16_t) * (size_t)(k.llr1 - k.llr0);
+        for (int s = 0; s < 3; s++)
+            cudaMemcpyAsync(p->d_l[s] + k.llr0, hs[s] + k.llr0, nb, cudaMemcpyHostToDevice, p->s_in);
+        cudaEventRecord(p->ev_in[c], p->s_in);
+        cudaStreamWaitEvent(st, p->ev_in[c], 0);
+        rc = crn_launch_tasks(dev, t, P->d_desc, p->d_tasks + k.task0, k.n_tasks, p->d_pairs, p->d_l[0], p->d_l[1],
+                              p->d_l[2], max_iters, et, p->d_bits, p->d_ok, h_it ? p->d_it : nullptr, nullptr,
+                              nullptr, 0, st);
+        if (rc) return rc;
+        cudaEventRecord(p->ev_comp[c], st);
+        cudaStreamWaitEvent(p->s_out, p->ev_comp[c], 0);
+        cudaMemcpyAsync(h_bits + k.w0, p->d_bits + k.w0, 4 * (size_t)(k.w1 - k.w0), cudaMemcpyDeviceToHost, p->s_out);
+        cudaMemcpyAsync(h_ok + k.cb0, p->d_ok + k.cb0, (size_t)(k.cb1 - k.cb0), cudaMemcpyDeviceToHost, p->s_out);
+        if (h_it)
+            cudaMemcpyAsync(h_it + k.cb0, p->d_it + k.cb0, (size_t)(k.cb1 - k.cb0), cudaMemcpyDeviceToHost,
+                            p->s_out);
+    }
+    cudaEventRecord(p->ev_end, p->s_out);
+    cudaStreamWaitEvent(st, p->ev_end, 0);
+    cudaStreamWaitEvent(p->s_in, p->ev_end, 0);    /* the next call's uploads follow this call's downloads */
+    if (cudaError_t e = cudaGetLastError()) return crn_cuda_fail(e, "crn_plan_decode_host", CRN_ECUDA);
+    return CRN_OK;
+}
+
+extern "C" int crn_plan_chunks(void *plan) {
+    Plan *P = (Plan *)plan;
+    return (P && P->pipe) ? P->pipe->n_chunks : 0;
+}
+
+/* ------------------------------------------------------------------ TTI stream runner */
+namespace {
+
+struct GroupRes {
+    cudaStream_t st = nullptr;
+    void *dmem = nullptr;          /* device: plan blob + LLRs + outputs */
+    size_t dbytes = 0;
+    void *hblob[2] = {nullptr, nullptr};  /* pinned host plan blobs, double-buffered by TTI parity */
+    size_t hbytes = 0;
+    cudaEvent_t ev_blob[2] = {nullptr, nullptr};
+    void *ws = nullptr;
+};
+
+struct Layout {
+    size_t o_desc, o_tasks, o_pairs, o_l, bl, o_bits, o_ok, o_it, tot;
+};
+
+Layout layout(int n_cb, int n_tasks, int n_pairs, int64_t n_llr, int64_t n_words) {
+    Layout L;
+    L.o_desc = 0;
+    L.o_tasks = align256(sizeof(crn_cb_desc) * n_cb);
+    L.o_pairs = L.o_tasks + align256(sizeof(crn_task) * n_tasks);
+    L.o_l = L.o_pairs + align256(sizeof(crn_pair) * n_pairs);
+    L.bl = align256(sizeof(int16_t) * n_llr);
+    L.o_bits = L.o_l + 3 * L.bl;
+    L.o_ok = L.o_bits + align256(4 * n_words);
+    L.o_it = L.o_ok + align256(n_cb);
+    L.tot = L.o_it + align256(n_cb);
+    return L;
+}
+
+}  // namespace
+
+extern "C" int crn_stream_run(const crn_tti_group *g, int32_t n_tti, int32_t n_groups, double period_us,
+                              int32_t max_iters, int32_t et, crn_tti_timing *timing) {
+    if (!g || !timing || n_tti < 1 || n_groups < 1 || n_groups > 64 || period_us < 0 || max_iters < 1 ||
+        max_iters > CRN_MAX_ITERS)
+        return CRN_EINVAL;
+    int dev;
+    DevTables *t;
+    int rc = crn_get_ctx(&dev, &t);
+    if (rc) return rc;
+    const int64_t NG = (int64_t)n_tti * n_groups;
+    /* validate every group up front (host), size the per-group device buffers */
+    std::vector<size_t> need(n_groups, 0), hneed(n_groups, 0);
+    for (int64_t x = 0; x < NG; x++) {
+        const crn_tti_group &q = g[x];
+        if (q.n_cb < 0 || (q.n_cb > 0 && (!q.desc || !q.llr_sys || !q.llr_p1 || !q.llr_p2 || !q.out_bits ||
+                                          !q.crc_ok)))
+            return CRN_EINVAL;
+        if ((rc = crn_validate(q.desc, q.n_cb, false))) return rc;
+        int64_t n_llr = 0, n_words = 0;
+        for (int i = 0; i < q.n_cb; i++) {
+            n_llr = std::max(n_llr, q.desc[i].llr_off + q.desc[i].K + 4);
+            n_words = std::max(n_words, q.desc[i].bit_off + (q.desc[i].K + 31) / 32);
+        }
+        if (n_llr > q.n_llr || n_words > q.n_words) return CRN_EINVAL;
+        /* upper bounds: tasks <= CBs, pairs <= CBs */
+        const Layout L = layout(q.n_cb, q.n_cb, q.n_cb, n_llr, n_words);
+        const int gi = (int)(x % n_groups);
+        need[gi] = std::max(need[gi], L.tot);
+        hneed[gi] = std::max(hneed[gi], L.o_l);
+    }
+    std::vector<GroupRes> G(n_groups);
+    auto cleanup = [&]() {
+        for (auto &r : G) {
+            if (r.st) cudaStreamSynchronize(r.st);
+            for (int b = 0; b < 2; b++) {
+                if (r.hblob[b]) cudaFreeHost(r.hblob[b]);
+                if (r.ev_blob[b]) cudaEventDestroy(r.ev_blob[b]);
+            }
+            if (r.dmem) cudaFree(r.dmem);
+            if (r.ws) cudaFree(r.ws);
+            if (r.st) cudaStreamDestroy(r.st);
+        }
+    };
+    for (int gi = 0; gi < n_groups; gi++) {
+        GroupRes &r = G[gi];
+        if (cudaStreamCreateWithFlags(&r.st, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaMalloc(&r.dmem, std::max<size_t>(need[gi], 256)) != cudaSuccess ||
+            cudaMallocHost(&r.hblob[0], std::max<size_t>(hneed[gi], 256)) != cudaSuccess ||
+            cudaMallocHost(&r.hblob[1], std::max<size_t>(hneed[gi], 256)) != cudaSuccess ||
+            cudaEventCreateWithFlags(&r.ev_blob[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&r.ev_blob[1], cudaEventDisableTiming) != cudaSuccess ||
+            cudaMalloc(&r.ws, crn_decode_ws_bytes(t->grid)) != cudaSuccess) {
+            cudaGetLastError();
+            cleanup();
+            return CRN_ENOMEM;
+        }
+    }
+    /* per (TTI, group): timing events (start before the uploads, end after the downloads) */
+    std::vector<cudaEvent_t> ev0(NG), ev1(NG);
+    for (int64_t x = 0; x < NG; x++) {
+        cudaEventCreate(&ev0[x]);
+        cudaEventCreate(&ev1[x]);
+    }
+    std::vector<double> done_us(NG, 0.0), rel_us(n_tti, 0.0), sub_us(n_tti, 0.0);
+    std::atomic<int64_t> submitted{0};
+    std::atomic<bool> abort_flag{false};
+    const Clock::time_point t0 = Clock::now() + std::chrono::milliseconds(2);
+
+    /* completion thread (the "captor"): time-stamps each (TTI, group) when its end event fires */
+    std::thread watcher([&]() {
+        for (int64_t x = 0; x < NG; x++) {
+            while (submitted.load(std::memory_order_acquire) <= x) {
+                if (abort_flag.load()) return;
+                std::this_thread::yield();
+            }
+            for (;;) {
+                cudaError_t q = cudaEventQuery(ev1[x]);
+                if (q == cudaSuccess) break;
+                if (q != cudaErrorNotReady || abort_flag.load()) return;
+            }
+            done_us[x] = us_since(t0, Clock::now());
+        }
+    });
+
+    for (int ti = 0; ti < n_tti && rc == CRN_OK; ti++) {
+        const Clock::time_point rel = t0 + std::chrono::duration_cast<Clock::duration>(
+                                               std::chrono::duration<double, std::micro>(period_us * ti));
+        while (Clock::now() < rel) { /* pacer: release TTI ti at t0 + ti * period */ }
+        rel_us[ti] = us_since(t0, rel);
+        for (int gi = 0; gi < n_groups && rc == CRN_OK; gi++) {
+            const int64_t x = (int64_t)ti * n_groups + gi;
+            const crn_tti_group &q = g[x];
+            GroupRes &r = G[gi];
+            cudaEventRecord(ev0[x], r.st);
+            if (q.n_cb > 0) {
+                /* row a1 per TTI: bucket / pair / task the group's CBs (host) */
+                std::vector<crn_task> tasks;
+                std::vector<crn_pair> pairs;
+                std::vector<int> sel(q.n_cb);
+                for (int i = 0; i < q.n_cb; i++) sel[i] = i;
+                crn_build_tasks(q.desc, sel.data(), q.n_cb, tasks, pairs);
+                int64_t n_llr = 0, n_words = 0;
+                for (int i = 0; i < q.n_cb; i++) {
+                    n_llr = std::max(n_llr, q.desc[i].llr_off + q.desc[i].K + 4);
+                    n_words = std::max(n_words, q.desc[i].bit_off + (q.desc[i].K + 31) / 32);
+                }
+                const Layout L = layout(q.n_cb, (int)tasks.size(), (int)pairs.size(), n_llr, n_words);
+                const int b = ti & 1;
+                cudaEventSynchronize(r.ev_blob[b]);              /* blob slot from TTI ti-2 uploaded */
+                uint8_t *hb = (uint8_t *)r.hblob[b];
+                memcpy(hb + L.o_desc, q.desc, sizeof(crn_cb_desc) * q.n_cb);
+                memcpy(hb + L.o_tasks, tasks.data(), sizeof(crn_task) * tasks.size());
+                memcpy(hb + L.o_pairs, pairs.data(), sizeof(crn_pair) * pairs.size());
+                uint8_t *dm = (uint8_t *)r.dmem;
+                cudaMemcpyAsync(dm, hb, L.o_l, cudaMemcpyHostToDevice, r.st);
+                cudaEventRecord(r.ev_blob[b], r.st);
+                const int16_t *hs[3] = {q.llr_sys, q.llr_p1, q.llr_p2};
+                int16_t *dl[3];
+                for (int s = 0; s < 3; s++) {
+                    dl[s] = (int16_t *)(dm + L.o_l + s * L.bl);
+                    cudaMemcpyAsync(dl[s], hs[s], sizeof(int16_t) * n_llr, cudaMemcpyHostToDevice, r.st);
+                }
+                uint32_t *dbits = (uint32_t *)(dm + L.o_bits);
+                uint8_t *dok = dm + L.o_ok, *dit = dm + L.o_it;
+                rc = crn_launch_tasks(dev, t, (const crn_cb_desc *)(dm + L.o_desc), (const crn_task *)(dm + L.o_tasks),
+                                      (int)tasks.size(), (const crn_pair *)(dm + L.o_pairs), dl[0], dl[1], dl[2],
+                                      max_iters, et, dbits, dok, q.iters_used ? dit : nullptr, nullptr, r.ws,
+                                      crn_decode_ws_bytes(t->grid), r.st);
+                cudaMemcpyAsync(q.out_bits, dbits, 4 * (size_t)n_words, cudaMemcpyDeviceToHost, r.st);
+                cudaMemcpyAsync(q.crc_ok, dok, (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
+                if (q.iters_used) cudaMemcpyAsync(q.iters_used, dit, (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
+            }
+            cudaEventRecord(ev1[x], r.st);
+            submitted.store(x + 1, std::memory_order_release);
+        }
+        sub_us[ti] = us_since(t0, Clock::now());
+    }
+    if (rc != CRN_OK) abort_flag.store(true);
+    watcher.join();
+    cudaError_t e = cudaSuccess;
+    for (auto &r : G)
+        if (cudaStreamSynchronize(r.st) != cudaSuccess) e = cudaGetLastError();
+    if (rc == CRN_OK && e != cudaSuccess) rc = crn_cuda_fail(e, "crn_stream_run", CRN_ECUDA);
+    if (rc == CRN_OK) {
+        for (int ti = 0; ti < n_tti; ti++) {
+            crn_tti_timing &o = timing[ti];
+            o.release_us = rel_us[ti];
+            o.submitted_us = sub_us[ti];
+            o.complete_us = 0;
+            float smin = 0, emax = 0;
+            for (int gi = 0; gi < n_groups; gi++) {
+                const int64_t x = (int64_t)ti * n_groups + gi;
+                o.complete_us = std::max(o.complete_us, done_us[x]);
+                float s = 0, en = 0;
+                cudaEventElapsedTime(&s, ev0[(int64_t)ti * n_groups], ev0[x]);
+                cudaEventElapsedTime(&en, ev0[(int64_t)ti * n_groups], ev1[x]);
+                smin = std::min(smin, s);
+                emax = std::max(emax, en);
+            }
+            o.latency_us = o.complete_us - o.release_us;
+            o.device_us = 1e3 * (double)(emax - smin);
+        }
+    }
+    for (int64_t x = 0; x < NG; x++) {
+        cudaEventDestroy(ev0[x]);
+        cudaEventDestroy(ev1[x]);
+    }
+    cleanup();
+    return rc;
+}

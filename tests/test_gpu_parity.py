@@ -224,3 +224,67 @@ def test_tb_configs_tb_verdict(orc):
             else:
                 assert not np.all(g["crc_ok"][idx])
         assert n_ok >= 1
+
+
+def _host(t):
+    return t.cpu().pin_memory()
+
+
+@pytest.mark.parametrize("n_chunks", [0, 1, 3, 7])
+def test_plan_decode_host_pipeline(orc, n_chunks):
+    """crn_plan_decode_host (host buffers, chunked upload/decode/download overlap)
+    equals the oracle on a mixed-K, filler-carrying TB batch for any chunking."""
+    b = _full(3, 0.1)
+    idx = np.arange(b.n_cb)
+    r = run_oracle(b, idx, 8, True)
+    p = crn.Plan(b.desc)
+    hl = [_host(x) for x in b.llr]
+    hb = torch.zeros(b.n_words, dtype=torch.int32).pin_memory()
+    hok = torch.full((b.n_cb,), 7, dtype=torch.uint8).pin_memory()
+    hit = torch.zeros(b.n_cb, dtype=torch.uint8).pin_memory()
+    for rep in range(2):                        # second call reuses the staging buffers
+        hb.zero_()
+        p.decode_host(*hl, 8, True, hb, hok, hit, n_chunks=n_chunks)
+        torch.cuda.synchronize()
+        g = dict(words=hb.numpy().view(np.uint32), crc_ok=hok.numpy(), iters=hit.numpy(), ext=None)
+        assert_parity(b, g, r, idx)
+    assert p.chunks >= 1 and (n_chunks == 0 or p.chunks <= n_chunks)
+    with pytest.raises(crn.CrnError):
+        p.decode_host(*b.llr, 8, True, hb, hok)            # device tensors refused
+    p.close()
+
+
+def test_stream_run_cfg5(orc):
+    """crn_stream_run: paced TTIs of cfg5, one stream per cell group; every CB of
+    every TTI bit-exact against the oracle; timestamps ordered."""
+    n_tti, n_groups = 3, 4
+    groups, checks = [], []
+    for t in range(n_tti):
+        b = _full(5, seed=100 + t)
+        r = run_oracle(b, np.arange(b.n_cb), 8, True)
+        cells = np.unique(b.cb_cell)
+        for gi in range(n_groups):
+            sel = np.flatnonzero(np.isin(b.cb_cell, cells[gi::n_groups]))
+            d = b.desc[sel].copy()
+            K = d["K"].astype(np.int64)
+            d["llr_off"] = np.concatenate([[0], np.cumsum(K + 4)[:-1]])
+            d["bit_off"] = np.concatenate([[0], np.cumsum((K + 31) // 32)[:-1]])
+            hl = [torch.cat([x[int(o):int(o) + int(k) + 4] for o, k in zip(b.desc["llr_off"][sel], K)]).cpu()
+                  .pin_memory() if sel.size else torch.zeros(1, dtype=torch.int16).pin_memory() for x in b.llr]
+            nw = int(((K + 31) // 32).sum())
+            g = dict(desc=d, l0=hl[0], l1=hl[1], l2=hl[2], bits=torch.zeros(max(nw, 1), dtype=torch.int32).pin_memory(),
+                     ok=torch.zeros(max(sel.size, 1), dtype=torch.uint8).pin_memory(),
+                     it=torch.zeros(max(sel.size, 1), dtype=torch.uint8).pin_memory())
+            groups.append(g)
+            checks.append((b, r, sel, d, g))
+    tim = crn.stream_run(groups, n_tti, n_groups, 1000.0, 8, True)
+    for b, r, sel, d, g in checks:
+        words = g["bits"].numpy().view(np.uint32)
+        for n, i in enumerate(sel):
+            K = int(d["K"][n])
+            ob = r["bits"][r["bo"][i]:r["bo"][i] + K]
+            assert np.array_equal(unpack(words, d, n), ob)
+            assert g["ok"].numpy()[n] == r["crc_ok"][i] and g["it"].numpy()[n] == r["iters"][i]
+    assert np.all(tim["latency_us"] > 0) and np.all(tim["device_us"] > 0)
+    assert np.all(np.diff(tim["release_us"]) > 900)
+    assert np.all(tim["complete_us"] > tim["release_us"])

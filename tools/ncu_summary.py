@@ -21,6 +21,13 @@ hdr, units, vals = rows[0], rows[1], rows[2]
 d = dict(zip(hdr, vals))
 u = dict(zip(hdr, units))
 out = {k: f"{d[k]} {u[k]}".strip() for k in KEYS if k in d}
+_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+try:   # roofline "traffic": DRAM bytes of the captured launch (read + write)
+    out["dram_bytes_per_launch"] = int(sum(float(d[k].replace(",", "")) * _SCALE[u[k]]
+                                           for k in ("dram__bytes_read.sum", "dram__bytes_write.sum")))
+    out["report"] = rep
+except (KeyError, ValueError):
+    pass
 st = {k[len(STALL):].replace("_per_issue_active.ratio", ""): float(d[k]) for k in hdr
       if k.startswith(STALL) and k.endswith("_per_issue_active.ratio")}
 out["stalls_per_issue"] = dict(sorted(((k, round(v, 3)) for k, v in st.items() if v > 0.01), key=lambda x: -x[1]))
