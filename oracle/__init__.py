@@ -58,9 +58,17 @@ def lib():
         L.oracle_decode_cb.argtypes = [i16p, i16p, i16p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.c_int, u8p, u8p, u8p, i16p, u64p]
         L.oracle_decode_cb.restype = C.c_int64
+        L.oracle_decode_cb_v.argtypes = [i16p, i16p, i16p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, C.c_int, u8p, u8p, u8p, i16p, u64p]
+        L.oracle_decode_cb_v.restype = C.c_int64
+        L.oracle_ext_scale.argtypes = [C.c_int32]
+        L.oracle_ext_scale.restype = C.c_int32
         L.oracle_decode_batch.argtypes = [C.c_int, i32p, i32p, i32p, i64p, i64p, i16p, i16p, i16p,
                                           C.c_int, C.c_int, C.c_int, u8p, u8p, u8p, i16p, u64p]
         L.oracle_decode_batch.restype = C.c_int64
+        L.oracle_decode_batch_v.argtypes = [C.c_int, i32p, i32p, i32p, i64p, i64p, i16p, i16p, i16p,
+                                            C.c_int, C.c_int, C.c_int, C.c_int, u8p, u8p, u8p, i16p, u64p]
+        L.oracle_decode_batch_v.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -198,15 +206,23 @@ def nii_update(alpha_out, beta_out):
     return ai, bi
 
 
+VAR_MAXLOG, VAR_SCALED = 0, 1
+
+
+def ext_scale(x: int) -> int:
+    """The scaled variant's extrinsic map floor(3x/4) (R28)."""
+    return int(lib().oracle_ext_scale(int(x)))
+
+
 def decode_cb(d0, d1, d2, F: int = 0, crc_kind: int = CRC24B, max_iters: int = 8,
-              early_term: bool = False, wmin: int = 32) -> dict:
+              early_term: bool = False, wmin: int = 32, variant: int = VAR_MAXLOG) -> dict:
     d0, d1, d2 = (np.ascontiguousarray(x, np.int16) for x in (d0, d1, d2))
     K = d0.size - 4
     bits = np.zeros(K, np.uint8)
     ext = np.zeros(K, np.int16)
     ok, it, ops = C.c_uint8(), C.c_uint8(), C.c_uint64(0)
-    v = lib().oracle_decode_cb(_p(d0, C.c_int16), _p(d1, C.c_int16), _p(d2, C.c_int16), K, F,
-                               crc_kind, max_iters, int(early_term), wmin, _p(bits, C.c_uint8),
+    v = lib().oracle_decode_cb_v(_p(d0, C.c_int16), _p(d1, C.c_int16), _p(d2, C.c_int16), K, F,
+                                 crc_kind, max_iters, int(early_term), wmin, variant, _p(bits, C.c_uint8),
                                C.byref(ok), C.byref(it), _p(ext, C.c_int16), C.byref(ops))
     if v < 0:
         raise ValueError("invalid arguments")
@@ -215,7 +231,7 @@ def decode_cb(d0, d1, d2, F: int = 0, crc_kind: int = CRC24B, max_iters: int = 8
 
 
 def decode_batch(K, F, crc_kind, llr_off, bit_off, d0, d1, d2, max_iters: int, early_term: bool,
-                 nthreads: int, want_ext: bool = True) -> dict:
+                 nthreads: int, want_ext: bool = True, variant: int = VAR_MAXLOG) -> dict:
     K = np.ascontiguousarray(K, np.int32)
     n = K.size
     F = np.ascontiguousarray(F, np.int32)
@@ -229,10 +245,10 @@ def decode_batch(K, F, crc_kind, llr_off, bit_off, d0, d1, d2, max_iters: int, e
     ok = np.zeros(n, np.uint8)
     it = np.zeros(n, np.uint8)
     ops = C.c_uint64(0)
-    v = lib().oracle_decode_batch(n, _p(K, C.c_int32), _p(F, C.c_int32), _p(crc_kind, C.c_int32),
-                                  _p(llr_off, C.c_int64), _p(bit_off, C.c_int64),
-                                  _p(d0, C.c_int16), _p(d1, C.c_int16), _p(d2, C.c_int16),
-                                  max_iters, int(early_term), nthreads, _p(bits, C.c_uint8),
+    v = lib().oracle_decode_batch_v(n, _p(K, C.c_int32), _p(F, C.c_int32), _p(crc_kind, C.c_int32),
+                                    _p(llr_off, C.c_int64), _p(bit_off, C.c_int64),
+                                    _p(d0, C.c_int16), _p(d1, C.c_int16), _p(d2, C.c_int16),
+                                    max_iters, int(early_term), variant, nthreads, _p(bits, C.c_uint8),
                                   _p(ok, C.c_uint8), _p(it, C.c_uint8),
                                   _p(ext, C.c_int16) if want_ext else None, C.byref(ops))
     return {"bits": bits, "crc_ok": ok, "iters": it, "ext": ext, "ops": ops.value, "violations": v}

@@ -369,11 +369,29 @@ void oracle_nii_update(int M, const int32_t *alpha_out, const int32_t *beta_out,
 /* ---------------------------------------------------------------- decoder */
 static int32_t clamp_in(int32_t v) { return v < -CLAMP_IN ? -CLAMP_IN : (v > CLAMP_IN ? CLAMP_IN : v); }
 
+/* Extrinsic scaling of the scaled max-log-MAP variant (R28):
+ * s(x) = floor(3x / 4), written as the floor of a quotient, not as a shift. */
+static int32_t scale34(int32_t x) {
+    int32_t n = 3 * x;
+    return n >= 0 ? n / 4 : -((-n + 3) / 4);
+}
+
+int32_t oracle_ext_scale(int32_t x) { return scale34(x); }
+
 int64_t oracle_decode_cb(const int16_t *d0, const int16_t *d1, const int16_t *d2,
                          int K, int F, int crc_kind, int max_iters, int early_term, int wmin,
                          uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
                          int16_t *ext, uint64_t *ops) {
-    if (k_row(K) < 0 || F < 0 || F > K - 25 || max_iters < 1 || crc_kind < 0 || crc_kind > 2)
+    return oracle_decode_cb_v(d0, d1, d2, K, F, crc_kind, max_iters, early_term, wmin, ORACLE_VAR_MAXLOG,
+                              bits, crc_ok, iters_used, ext, ops);
+}
+
+int64_t oracle_decode_cb_v(const int16_t *d0, const int16_t *d1, const int16_t *d2,
+                           int K, int F, int crc_kind, int max_iters, int early_term, int wmin, int variant,
+                           uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
+                           int16_t *ext, uint64_t *ops) {
+    if (k_row(K) < 0 || F < 0 || F > K - 25 || max_iters < 1 || crc_kind < 0 || crc_kind > 2 ||
+        variant < 0 || variant > 1)
         return -1;
     int64_t viol = 0;
     int W = K / oracle_num_windows(K, wmin), M = K / W;
@@ -409,9 +427,13 @@ int64_t oracle_decode_cb(const int16_t *d0, const int16_t *d1, const int16_t *d2
         t_used = it;
         /* DEC1: R(b_i), R(b_i)' and the a-priori La1 -> extrinsic Le1 */
         viol += oracle_siso(Ls, Lp1, La1, tail1, K, W, a_prev[0], b_prev[0], a_new[0], b_new[0], Le1, ops);
+        if (variant == ORACLE_VAR_SCALED)     /* extrinsic handed on = floor(3 Le / 4) (R28) */
+            for (int k = 0; k < K; k++) Le1[k] = scale34(Le1[k]);
         /* DEC2: interleaved R(b_i), R(b_i)'' and La2 = interleaved Le1 */
         for (int i = 0; i < K; i++) La2[i] = Le1[Pi[i]];
         viol += oracle_siso(Ls2, Lp2, La2, tail2, K, W, a_prev[1], b_prev[1], a_new[1], b_new[1], Le2, ops);
+        if (variant == ORACLE_VAR_SCALED)
+            for (int i = 0; i < K; i++) Le2[i] = scale34(Le2[i]);
         /* de-interleave back to DEC1 */
         for (int i = 0; i < K; i++) La1n[Pi[i]] = Le2[i];
         for (int q = 0; q < 2; q++) oracle_nii_update(M, a_new[q], b_new[q], a_prev[q], b_prev[q]);
@@ -439,7 +461,7 @@ int64_t oracle_decode_cb(const int16_t *d0, const int16_t *d1, const int16_t *d2
 /* ---------------------------------------------------------------- batch (CPU baseline) */
 typedef struct {
     int n_cb; const int32_t *K, *F, *crc; const int64_t *lo, *bo;
-    const int16_t *d0, *d1, *d2; int I, et;
+    const int16_t *d0, *d1, *d2; int I, et, variant;
     uint8_t *bits, *ok, *it; int16_t *ext;
     atomic_int next; atomic_llong viol; atomic_ullong ops;
 } batch_t;
@@ -451,8 +473,8 @@ static void *batch_worker(void *p) {
         int i = atomic_fetch_add(&b->next, 1);
         if (i >= b->n_cb) break;
         int64_t lo = b->lo[i], bo = b->bo[i];
-        int64_t v = oracle_decode_cb(b->d0 + lo, b->d1 + lo, b->d2 + lo, b->K[i], b->F[i], b->crc[i],
-                                     b->I, b->et, 32, b->bits + bo, b->ok + i, b->it + i,
+        int64_t v = oracle_decode_cb_v(b->d0 + lo, b->d1 + lo, b->d2 + lo, b->K[i], b->F[i], b->crc[i],
+                                       b->I, b->et, 32, b->variant, b->bits + bo, b->ok + i, b->it + i,
                                      b->ext ? b->ext + bo : NULL, &ops);
         viol += v < 0 ? 1 : v;
     }
@@ -467,9 +489,19 @@ int64_t oracle_decode_batch(int n_cb, const int32_t *K, const int32_t *F, const 
                             int max_iters, int early_term, int nthreads,
                             uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
                             int16_t *ext, uint64_t *ops) {
+    return oracle_decode_batch_v(n_cb, K, F, crc_kind, llr_off, bit_off, d0, d1, d2, max_iters, early_term,
+                                 ORACLE_VAR_MAXLOG, nthreads, bits, crc_ok, iters_used, ext, ops);
+}
+
+int64_t oracle_decode_batch_v(int n_cb, const int32_t *K, const int32_t *F, const int32_t *crc_kind,
+                              const int64_t *llr_off, const int64_t *bit_off,
+                              const int16_t *d0, const int16_t *d1, const int16_t *d2,
+                              int max_iters, int early_term, int variant, int nthreads,
+                              uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
+                              int16_t *ext, uint64_t *ops) {
     batch_t b;
     b.n_cb = n_cb; b.K = K; b.F = F; b.crc = crc_kind; b.lo = llr_off; b.bo = bit_off;
-    b.d0 = d0; b.d1 = d1; b.d2 = d2; b.I = max_iters; b.et = early_term;
+    b.d0 = d0; b.d1 = d1; b.d2 = d2; b.I = max_iters; b.et = early_term; b.variant = variant;
     b.bits = bits; b.ok = crc_ok; b.it = iters_used; b.ext = ext;
     atomic_init(&b.next, 0); atomic_init(&b.viol, 0); atomic_init(&b.ops, 0);
     if (nthreads < 1) nthreads = 1;

@@ -29,6 +29,10 @@ extern "C" {
 #endif
 
 enum { ORACLE_CRC_NONE = 0, ORACLE_CRC24A = 1, ORACLE_CRC24B = 2 };
+/* Decoder variants: plain max-log-MAP (the product definition, R2) and
+ * the scaled-extrinsic max-log-MAP of SURVEY.md §8(f) f2 (R28): each
+ * SISO's extrinsic Le = clamp(L1 - L0, +-4096) is handed on as floor(3 Le / 4). */
+enum { ORACLE_VAR_MAXLOG = 0, ORACLE_VAR_SCALED = 1 };
 
 /* Number of supported interleaver sizes (188 sizes 40..6144). */
 int oracle_num_k(void);
@@ -97,6 +101,17 @@ int64_t oracle_decode_cb(const int16_t *d0, const int16_t *d1, const int16_t *d2
                          uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
                          int16_t *ext, uint64_t *ops);
 
+/* The variant's extrinsic scaling s(x) = floor(3x / 4) (R28). */
+int32_t oracle_ext_scale(int32_t x);
+
+/* Same with a decoder variant (ORACLE_VAR_*): with ORACLE_VAR_SCALED, Le1 and
+ * Le2 are replaced by floor(3 Le / 4) right after each SISO, so the a-priori
+ * inputs, L_APP and ext all use the scaled values.  -1 for an unknown variant. */
+int64_t oracle_decode_cb_v(const int16_t *d0, const int16_t *d1, const int16_t *d2,
+                           int K, int F, int crc_kind, int max_iters, int early_term, int wmin, int variant,
+                           uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
+                           int16_t *ext, uint64_t *ops);
+
 /* Batch helper for the CPU baseline: CB i uses K[i], F[i], crc_kind[i]; its
  * LLRs start at llr_off[i] in each of d0/d1/d2, its K bits at bit_off[i] in
  * bits (one per byte), its ext at bit_off[i] in ext (may be NULL).
@@ -107,6 +122,12 @@ int64_t oracle_decode_batch(int n_cb, const int32_t *K, const int32_t *F, const 
                             int max_iters, int early_term, int nthreads,
                             uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
                             int16_t *ext, uint64_t *ops);
+int64_t oracle_decode_batch_v(int n_cb, const int32_t *K, const int32_t *F, const int32_t *crc_kind,
+                              const int64_t *llr_off, const int64_t *bit_off,
+                              const int16_t *d0, const int16_t *d1, const int16_t *d2,
+                              int max_iters, int early_term, int variant, int nthreads,
+                              uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
+                              int16_t *ext, uint64_t *ops);
 
 #ifdef __cplusplus
 }

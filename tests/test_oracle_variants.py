@@ -1,0 +1,92 @@
+"""Pins of the oracle's scaled-extrinsic max-log-MAP variant (SURVEY.md §8(f)
+f2, R28): the extrinsic each SISO hands on is floor(3 Le / 4).
+CPU only.
+
+* the scaling map against the definition of the floor (4 s <= 3x < 4 s + 4);
+* one iteration equals the composition of the brute-force-pinned SISO
+  (tests/test_oracle_encoder_siso.py) with that map and the QPP permutation;
+* noiseless round trips, zero-evidence failure, int16 safety, ET prefix;
+* the known behaviour of scaling max-log-MAP extrinsics (it offsets the
+  max-log over-estimate): fewer block errors and iterations at the same Eb/N0.
+"""
+import numpy as np
+import pytest
+
+from paper_1905_01141_b200 import workload as wlmod
+from tests._inputs import offsets, oracle_llrs
+
+
+def test_ext_scale_is_floor_of_three_quarters(orc):
+    xs = np.arange(-4096, 4097)
+    s = np.array([orc.ext_scale(int(x)) for x in xs])
+    assert np.all(4 * s <= 3 * xs) and np.all(3 * xs < 4 * s + 4)     # s = floor(3x/4) by definition
+    assert np.all(np.diff(s) >= 0) and s[0] == -3072 and s[-1] == 3072
+    assert [orc.ext_scale(x) for x in (-1, 0, 1, 2, -2)] == [-1, 0, 0, 1, -2]
+
+
+@pytest.mark.parametrize("K", [40, 1056])
+def test_one_iteration_is_composition_of_pinned_parts(orc, K):
+    """DEC1 -> scale -> interleave -> DEC2 -> scale -> de-interleave."""
+    rng = np.random.default_rng(K)
+    d = [rng.integers(-5000, 5001, K + 4).astype(np.int16) for _ in range(3)]
+    r = orc.decode_cb(*d, max_iters=1, variant=orc.VAR_SCALED)
+    W = K // orc.num_windows(K)
+    cl = [np.clip(x.astype(np.int32), -4096, 4096) for x in d]
+    Ls, Lp1, Lp2 = cl[0][:K], cl[1][:K], cl[2][:K]
+    t1 = [cl[0][K], cl[1][K], cl[2][K], cl[0][K + 1], cl[1][K + 1], cl[2][K + 1]]
+    t2 = [cl[0][K + 2], cl[1][K + 2], cl[2][K + 2], cl[0][K + 3], cl[1][K + 3], cl[2][K + 3]]
+    Pi = orc.qpp_perm(K)
+    sc = np.vectorize(orc.ext_scale)
+    le1 = sc(orc.siso(Ls, Lp1, np.zeros(K), t1, W)[0])
+    le2 = sc(orc.siso(Ls[Pi], Lp2, le1[Pi], t2, W)[0])
+    la1n = np.zeros(K, np.int64)
+    la1n[Pi] = le2
+    assert np.array_equal(r["ext"].astype(np.int64), la1n)
+    lapp = Ls + le1 + la1n
+    assert np.array_equal(r["bits"], (lapp >= 0).astype(np.uint8))
+
+
+def _noiseless(orc, c, amp):
+    return [((2 * x.astype(np.int32) - 1) * amp).astype(np.int16) for x in orc.turbo_encode(c)]
+
+
+@pytest.mark.parametrize("K", [40, 104, 1056, 6144])
+def test_scaled_noiseless_zero_and_range(orc, K):
+    rng = np.random.default_rng(K + 1)
+    c = orc.crc_attach(orc.CRC24B, rng.integers(0, 2, K - 24, dtype=np.uint8))
+    for amp in (4096, 8):
+        r = orc.decode_cb(*_noiseless(orc, c, amp), max_iters=8, early_term=True, variant=orc.VAR_SCALED)
+        assert np.array_equal(r["bits"], c) and r["crc_ok"] == 1 and r["violations"] == 0
+    z = [np.zeros(K + 4, np.int16)] * 3
+    r = orc.decode_cb(*z, max_iters=4, early_term=True, variant=orc.VAR_SCALED)
+    assert r["crc_ok"] == 0 and r["iters"] == 4 and np.all(r["bits"] == 1)
+    ll = [rng.integers(-32768, 32768, K + 4).astype(np.int16) for _ in range(3)]
+    r = orc.decode_cb(*ll, max_iters=4, variant=orc.VAR_SCALED)
+    assert r["violations"] == 0 and np.all(np.abs(r["ext"]) <= 3072)
+
+
+def test_scaled_et_is_prefix_of_fixed(orc):
+    wl = wlmod.make_workload(5, seed=4)
+    cbs, ll = oracle_llrs(wl)
+    lo, _ = offsets([cb["K"] for cb in cbs])
+    for cb, o in list(zip(cbs, lo))[:60]:
+        K = cb["K"]
+        x = [t[o:o + K + 4].numpy() for t in ll]
+        r = orc.decode_cb(*x, F=cb["F"], crc_kind=cb["crc"], max_iters=8, early_term=True, variant=orc.VAR_SCALED)
+        f = orc.decode_cb(*x, F=cb["F"], crc_kind=cb["crc"], max_iters=r["iters"], variant=orc.VAR_SCALED)
+        assert np.array_equal(r["bits"], f["bits"]) and np.array_equal(r["ext"], f["ext"])
+
+
+def test_scaling_lowers_bler_and_iterations(orc):
+    """128 CBs of K=1056 at Eb/N0 = 0.9 dB, CRC ET at max 8 (seeded)."""
+    wl = wlmod.make_workload(1, seed=5, scale=4.0)
+    wl.tb_ebn0_db[:] = 0.9
+    cbs, ll = oracle_llrs(wl)
+    K = np.array([c["K"] for c in cbs], np.int32)
+    lo, bo = offsets(K)
+    res = []
+    for v in (orc.VAR_MAXLOG, orc.VAR_SCALED):
+        r = orc.decode_batch(K, np.zeros_like(K), np.full_like(K, 2), lo, bo, *(x.numpy() for x in ll),
+                             max_iters=8, early_term=True, nthreads=4, variant=v, want_ext=False)
+        res.append((1 - r["crc_ok"].mean(), r["iters"].mean()))
+    assert res[1][0] < res[0][0] and res[1][1] < res[0][1], res
