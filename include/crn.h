@@ -36,6 +36,12 @@ extern "C" {
 enum { CRN_OK = 0, CRN_EINVAL = -1, CRN_ECUDA = -2, CRN_ENOMEM = -3, CRN_ENODEV = -4 };
 enum { CRN_CRC_NONE = 0, CRN_CRC24A = 1, CRN_CRC24B = 2 };
 enum { CRN_DESC_ON_DEVICE = 1 };           /* flag bit 0 of crn_decode_batch_ex */
+enum { CRN_EXT_SCALED = 2 };               /* flag bit 1: scaled-extrinsic variant (below) */
+/* Decoder variants: CRN_VARIANT_MAXLOG is the definition
+ * every entry point computes by default (R2); CRN_VARIANT_SCALED
+ * hands on floor(3 Le / 4) instead of each SISO's extrinsic Le, so the
+ * a-priori inputs, L_APP and ext_out all use the scaled value (R28). */
+enum { CRN_VARIANT_MAXLOG = 0, CRN_VARIANT_SCALED = 1 };
 enum { CRN_MAX_ITERS = 32, CRN_KMIN = 40, CRN_KMAX = 6144 };
 
 /* Per-CB descriptor (the paper's CCDU at CB granularity).
@@ -83,7 +89,8 @@ int crn_decode_batch(const int16_t *llr_sys, const int16_t *llr_p1, const int16_
  * cuda_stream: a cudaStream_t (NULL = legacy default stream).
  * Host-side validation (descriptors in host memory) returns CRN_EINVAL for a
  * K outside the table, F < 0 or F > K-25, an unknown crc_kind, overlapping
- * LLR or output ranges, or unknown flag bits.  n_cb == 0 is a no-op.  Input
+ * LLR or output ranges, or unknown flag bits.  flags & CRN_EXT_SCALED selects
+ * CRN_VARIANT_SCALED.  n_cb == 0 is a no-op.  Input
  * LLRs of any int16 value are accepted (clamped to +-4096, R12). */
 int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb,
                         const int16_t *llr_sys, const int16_t *llr_p1, const int16_t *llr_p2,
@@ -104,6 +111,9 @@ int crn_plan_decode(void *plan, const int16_t *llr_sys, const int16_t *llr_p1,
                     const int16_t *llr_p2, int32_t max_iters, int32_t early_term,
                     uint32_t *out_bits, uint8_t *crc_ok, uint8_t *iters_used, int16_t *ext_out,
                     void *cuda_stream);
+/* Decoder variant of later crn_plan_decode / crn_plan_decode_host calls of this
+ * plan (CRN_VARIANT_*; default CRN_VARIANT_MAXLOG).  CRN_EINVAL otherwise. */
+int crn_plan_set_variant(void *plan, int32_t variant);
 /* Number of decode-kernel launches one crn_plan_decode performs (for gpu_launches). */
 int crn_plan_launches(void *plan);
 void crn_plan_destroy(void *plan);
@@ -208,6 +218,28 @@ int crn_tb_build_cbs(const uint8_t *tb_bits, int64_t tbs_bits, int32_t max_cb, i
  * written to tb_out, one bit per byte, if non-NULL), 0 otherwise, <0 on error. */
 int crn_tb_reassemble(const uint32_t *cb_words, const crn_cb_desc *desc, const uint8_t *crc_ok,
                       int32_t n_cb, int64_t tbs_bits, uint8_t *tb_out);
+/* Transport block of a decoded batch: its C = n_cb code blocks are
+ * desc[cb0 .. cb0+n_cb) in segment order (as crn_tb_build_cbs emits them),
+ * tbs payload bits; its payload words go to tb_words[word_off ..]. */
+typedef struct {
+    int32_t cb0, n_cb;
+    int64_t tbs, word_off;
+} crn_tb_desc;
+
+/* TB post-processing on the DEVICE for a whole batch (PAPER.md:408
+ * "combination of CBs", :369 TB success rule): for each TB
+ * strip fillers and CB CRC24Bs, concatenate, check the TB CRC24A;
+ * tb_ok[i] = 1 iff every CB's crc_ok is set and the TB CRC passes.  tb_words
+ * (may be NULL) receives the ceil(tbs/32) payload words LSB-first from
+ * word_off (written whatever the verdict).  tb and desc are HOST arrays
+ * (copied; n_cb = the length of desc, TBs index into it); cb_words
+ * (the decoder's out_bits), crc_ok, tb_ok, tb_words are DEVICE memory.
+ * Asynchronous on cuda_stream.  CRN_EINVAL if a TB's CB range is outside desc,
+ * its CBs do not match the 36.212 segmentation of tbs (C, K+/K-, F, crc_kind)
+ * or C > 128. */
+int crn_tb_verdict_batch(const crn_tb_desc *tb, int32_t n_tb, const crn_cb_desc *desc, int32_t n_cb,
+                         const uint32_t *cb_words, const uint8_t *crc_ok, uint8_t *tb_ok,
+                         uint32_t *tb_words, void *cuda_stream);
 /* QPP parameters of TS 36.212 Table 5.1.3-3 for K; CRN_EINVAL if K is not a size. */
 int crn_qpp_params(int32_t K, int32_t *f1, int32_t *f2);
 /* Window split of the decoder: M = max{M : M | K, K/M >= 32}, W = K/M (R13). */

@@ -19,6 +19,8 @@ SO = os.path.join(HERE, "libcrn.so")
 CRN_OK, CRN_EINVAL, CRN_ECUDA, CRN_ENOMEM, CRN_ENODEV = 0, -1, -2, -3, -4
 CRC_NONE, CRC24A, CRC24B = 0, 1, 2
 DESC_ON_DEVICE = 1
+EXT_SCALED = 2
+VARIANT_MAXLOG, VARIANT_SCALED = 0, 1
 
 DESC_DTYPE = np.dtype([("K", "<i4"), ("F", "<i4"), ("crc_kind", "<i4"), ("reserved", "<i4"),
                        ("llr_off", "<i8"), ("bit_off", "<i8"), ("ext_off", "<i8")])
@@ -56,6 +58,7 @@ _SIGS = {
     "crn_plan_create": (C.c_int, [vp, C.c_int32, P(vp)]),
     "crn_plan_decode": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp]),
     "crn_plan_launches": (C.c_int, [vp]),
+    "crn_plan_set_variant": (C.c_int, [vp, C.c_int32]),
     "crn_plan_decode_host": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, C.c_int32, vp]),
     "crn_plan_chunks": (C.c_int, [vp]),
     "crn_stream_run": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int32, vp]),
@@ -64,6 +67,7 @@ _SIGS = {
     "crn_encode_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp]),
     "crn_tb_build_cbs": (C.c_int, [u8p, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_int64, u8p, vp,
                                    i32p]),
+    "crn_tb_verdict_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp, vp]),
     "crn_tb_reassemble": (C.c_int, [u32p, vp, u8p, C.c_int32, C.c_int64, u8p]),
     "crn_segment_tb": (C.c_int, [C.c_int64, P(Seg)]),
     "crn_qpp_params": (C.c_int, [C.c_int32, i32p, i32p]),
@@ -175,6 +179,9 @@ class Plan:
                                         _ptr(h_bits), _ptr(h_ok), _ptr(h_iters), n_chunks, _stream(stream)),
              "crn_plan_decode_host")
 
+    def set_variant(self, variant: int) -> None:
+        _chk(lib().crn_plan_set_variant(self.h, variant), "crn_plan_set_variant")
+
     @property
     def chunks(self) -> int:
         return int(lib().crn_plan_chunks(self.h))
@@ -245,6 +252,19 @@ def tb_build_cbs(tb_bits, base_bit: int = 0, base_llr: int = 0, base_word: int =
                                 _np(out, C.c_uint8), desc.ctypes.data, C.byref(n)), "crn_tb_build_cbs")
     desc = desc[:n.value].copy()
     return out[:int(desc["K"].sum())].copy(), desc
+
+
+TB_DTYPE = np.dtype([("cb0", "<i4"), ("n_cb", "<i4"), ("tbs", "<i8"), ("word_off", "<i8")])
+
+
+def tb_verdict_batch(tbs, desc, cb_words, crc_ok, tb_ok, tb_words=None, stream=None) -> None:
+    """crn_tb_verdict_batch: tbs (TB_DTYPE) and desc host arrays; the rest CUDA tensors."""
+    _cuda_dev(cb_words, crc_ok, tb_ok, tb_words)
+    tbs = np.ascontiguousarray(tbs, TB_DTYPE)
+    desc = np.ascontiguousarray(desc, DESC_DTYPE)
+    _chk(lib().crn_tb_verdict_batch(tbs.ctypes.data, tbs.size, desc.ctypes.data, desc.size, _ptr(cb_words),
+                                    _ptr(crc_ok), _ptr(tb_ok), _ptr(tb_words), _stream(stream)),
+         "crn_tb_verdict_batch")
 
 
 def tb_reassemble(cb_words, desc, crc_ok, tbs: int):

@@ -224,6 +224,19 @@ __device__ __forceinline__ u32 lambda_le(const u32 a[NS], const u32 bn[NS], u32 
     return __viaddmin_s16x2(vaddmax(lam[1], ~lam[0], NEG4097), ONE2, CLIP_HI);
 }
 
+/* Row f2 variant (R28): the extrinsic handed on is floor(3 Le / 4),
+ * per int16 half: 3 Le fits int16 (|Le| <= 4096), then an arithmetic shift by 2
+ * (logical shift of the word, each half's low 14 bits kept, its sign copied
+ * into its top two bits). */
+__device__ __forceinline__ u32 scale34(u32 x) {
+    const u32 t = vadd(vadd(x, x), x);
+    const u32 s = t & 0x80008000u;
+    return ((t >> 2) & 0x3FFF3FFFu) | s | (s >> 1);
+}
+
+template <bool SCALE>
+__device__ __forceinline__ u32 ext_out_map(u32 le) { return SCALE ? scale34(le) : le; }
+
 /* beta_K from the tail: beta_{K+3} = (0, -F x7), three forced steps (R11) */
 __device__ __forceinline__ void tail_beta(const u32 *tail, u32 b[NS]) {
     b[0] = M1;
@@ -453,6 +466,7 @@ __device__ __forceinline__ void load16(const int16_t *__restrict__ src, u32 w[HW
 
 /* One half-iteration of constituent c (rows a5-a8).  Le -> Y (c = 0, natural
  * order) or Z (c = 1, interleaved order). */
+template <bool SCALE>
 __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, int it) {
     const uint2 *ch = reinterpret_cast<const uint2 *>(f.sm + S_CH) + f.tid;
     const u32 *lp = f.sm + S_LP + c * SUMK + f.k0 * TS + f.t;
@@ -519,7 +533,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
                 const u32 p = lp[ss * TS];
                 tm_wait_ld8(cur);
                 tm_load8(f.ta + (ss > 0 ? ss - 1 : 0) * 8, nx);      /* unconditional: no branch around the load */
-                le[ss * TS] = lambda_le(cur, b, p);                /* alpha_ss (stored) + beta_{ss+1} */
+                le[ss * TS] = ext_out_map<SCALE>(lambda_le(cur, b, p));   /* alpha_ss (stored) + beta_{ss+1} */
                 beta_step_d(b, p, g.x, g.y);
             }
         }
@@ -540,7 +554,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
                 const u32 p = lp[ss * TS];
                 tm_wait_ld8(cur);
                 tm_load8(f.ta + (ss < HW - 1 ? ss + 1 : ss) * 8, nx);
-                le[(HW + ss) * TS] = lambda_le(a, cur, p);         /* alpha_{16+ss} + beta_{17+ss} (stored) */
+                le[(HW + ss) * TS] = ext_out_map<SCALE>(lambda_le(a, cur, p));   /* alpha_{16+ss} + beta_{17+ss} (stored) */
                 alpha_step_d(a, p, g.x, g.y);
             }
         }
@@ -549,6 +563,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
     }
 }
 
+template <bool SCALE>
 __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
                                               const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
                                               const int16_t *__restrict__ l2, int max_iters, int et,
@@ -649,11 +664,11 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
     for (int it = 1; it <= max_iters; it++) {
         /* DEC1: La1[n] = Le2[Pi^-1(n)] gathered from Z (zero in iteration 1) */
         build_chunk(f, 0, q1, sm + S_LP, sm + S_Z, it == 1);
-        siso_split(f, tail_thr, 0, it);
+        siso_split<SCALE>(f, tail_thr, 0, it);
         __syncthreads();
         /* DEC2: La2[i] = Le1[Pi(i)] gathered from Y */
         build_chunk(f, 1, q2, sm + S_LP + SUMK, sm + S_Y, false);
-        siso_split(f, tail_thr, 1, it);
+        siso_split<SCALE>(f, tail_thr, 1, it);
         __syncthreads();
         if (!et && it != max_iters) continue;     /* fixed mode: decide only at the end */
 
@@ -735,7 +750,7 @@ struct GCtx {
 
 /* C = 0: DEC1 (La from X natural, Le1 -> Y); C = 1: DEC2 (interleaved
  * systematic, Lp2, La2 = Y[Pi(i)], Le2 scattered to X[Pi(i)] = La1_next). */
-template <int C>
+template <int C, bool SCALE>
 __device__ __forceinline__ void siso_generic(const GCtx &c) {
     const int T = c.T, t = c.t, W = c.W;
     const u32 *Ls = c.slot + (C ? A_LSI : A_LS);
@@ -771,13 +786,14 @@ __device__ __forceinline__ void siso_generic(const GCtx &c) {
         u32 bn[NS];
 #pragma unroll
         for (int s = 0; s < NS; s++) bn[s] = c.bst[((i + 1) * NS + s) * T + t];
-        Le[ax] = lambda_le(a, bn, lp);
+        Le[ax] = ext_out_map<SCALE>(lambda_le(a, bn, lp));
         alpha_step(a, lu, lp, vadd(lu, lp));
     }
 #pragma unroll
     for (int s = 0; s < NS; s++) c.slot[A_NII + nii_ix(C, wr, 0, s, t)] = a[s];     /* alpha_{(j+1)W} -> window j+1 */
 }
 
+template <bool SCALE>
 __device__ __noinline__ void run_task_generic(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
                                               const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
                                               const int16_t *__restrict__ l2, int max_iters, int et,
@@ -829,9 +845,9 @@ __device__ __noinline__ void run_task_generic(const crn_task &tk, const crn_cb_d
     c.M = M; c.W = W; c.slot = slot; c.qtab = qtab; c.bst = bst;
     for (int it = 1; it <= max_iters; it++) {
         c.it = it;
-        if (active) siso_generic<0>(c);
+        if (active) siso_generic<0, SCALE>(c);
         __syncthreads();
-        if (active) siso_generic<1>(c);
+        if (active) siso_generic<1, SCALE>(c);
         __syncthreads();
         if (!et && it != max_iters) continue;
         /* ---- row a9: L_APP = Ls + Le1 + La1_next, hard decision (tie -> 1),
@@ -889,7 +905,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
               const crn_pair *__restrict__ pairs, const int16_t *__restrict__ l0,
               const int16_t *__restrict__ l1, const int16_t *__restrict__ l2, int max_iters, int et,
               uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok, uint8_t *__restrict__ iters_used,
-              int16_t *__restrict__ ext_out, crn_tables tab, uint8_t *ws) {
+              int16_t *__restrict__ ext_out, crn_tables tab, uint8_t *ws, int variant) {
     extern __shared__ __align__(16) u32 smem[];
     __shared__ int s_task, s_left;
     __shared__ u32 s_tmem;
@@ -929,11 +945,21 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             s_crc[e] = 0;
         }
         __syncthreads();
-        if (tk.W == 32)
-            run_task_fast(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab, smem, tmem, sh);
-        else
-            run_task_generic(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab, slot, smem,
-                             sh, smem + G_BITS);
+        if (tk.W == 32) {
+            if (variant == CRN_VARIANT_SCALED)
+                run_task_fast<true>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab, smem,
+                                    tmem, sh);
+            else
+                run_task_fast<false>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
+                                     smem, tmem, sh);
+        } else {
+            if (variant == CRN_VARIANT_SCALED)
+                run_task_generic<true>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
+                                       slot, smem, sh, smem + G_BITS);
+            else
+                run_task_generic<false>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
+                                        slot, smem, sh, smem + G_BITS);
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -977,11 +1003,12 @@ extern "C" int crn_decode_kernel_info(int32_t *static_smem, int32_t *dyn_smem, i
 extern "C" int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_tasks, int32_t n_tasks,
                                  const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,
                                  int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it,
-                                 int16_t *ext, const crn_tables *tab, void *ws, void *stream, int32_t grid) {
+                                 int16_t *ext, const crn_tables *tab, void *ws, void *stream, int32_t grid,
+                                 int32_t variant) {
     cudaStream_t st = (cudaStream_t)stream;
     if (cudaMemsetAsync(ws, 0, WS_HEAD, st) != cudaSuccess) return CRN_ECUDA;
     const int g = grid < n_tasks ? grid : n_tasks;
     decode_kernel<<<g, BLOCK, smem_bytes(), st>>>(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits,
-                                                  ok, it, ext, *tab, (uint8_t *)ws);
+                                                  ok, it, ext, *tab, (uint8_t *)ws, variant);
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
 }

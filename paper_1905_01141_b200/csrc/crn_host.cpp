@@ -342,7 +342,7 @@ static int plan_build(const crn_cb_desc *desc, int n, bool want_ext, cudaStream_
 int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn_task *d_tasks, int n_tasks,
                      const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,
                      int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
-                     void *ws, size_t ws_bytes, cudaStream_t st) {
+                     void *ws, size_t ws_bytes, cudaStream_t st, int variant) {
     if (n_tasks == 0) return CRN_OK;
     if (!ws) {
         int rc = crn_get_ws(dev, (void *)st, crn_decode_ws_bytes(t->grid), &ws);
@@ -351,7 +351,7 @@ int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn
         return CRN_EINVAL;
     }
     return crn_launch_decode(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits, ok, it, ext,
-                             &t->tab, ws, (void *)st, t->grid);
+                             &t->tab, ws, (void *)st, t->grid, variant);
 }
 
 static int launch(Plan *P, DevTables *t, const int16_t *l0, const int16_t *l1, const int16_t *l2,
@@ -359,7 +359,7 @@ static int launch(Plan *P, DevTables *t, const int16_t *l0, const int16_t *l1, c
                   void *ws, size_t ws_bytes, cudaStream_t st) {
     if (P->n_cb == 0) return CRN_OK;
     return crn_launch_tasks(P->dev, t, P->d_desc, P->d_tasks, P->n_tasks, P->d_pairs, l0, l1, l2, max_iters, et,
-                            bits, ok, it, ext, ws, ws_bytes, st);
+                            bits, ok, it, ext, ws, ws_bytes, st, P->variant);
 }
 
 extern "C" int crn_plan_create(const crn_cb_desc *desc, int32_t n_cb, void **plan) {
@@ -391,6 +391,13 @@ extern "C" int crn_plan_decode(void *plan, const int16_t *l0, const int16_t *l1,
     return launch(P, t, l0, l1, l2, max_iters, et, bits, ok, it, ext, nullptr, 0, (cudaStream_t)stream);
 }
 
+extern "C" int crn_plan_set_variant(void *plan, int32_t variant) {
+    Plan *P = (Plan *)plan;
+    if (!P || (variant != CRN_VARIANT_MAXLOG && variant != CRN_VARIANT_SCALED)) return CRN_EINVAL;
+    P->variant = variant;
+    return CRN_OK;
+}
+
 extern "C" int crn_plan_launches(void *plan) {
     Plan *P = (Plan *)plan;
     return (P && P->n_cb) ? 1 : 0;
@@ -408,7 +415,7 @@ extern "C" int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb, const 
                                    const int16_t *l1, const int16_t *l2, int32_t max_iters,
                                    int32_t et, int32_t flags, uint32_t *bits, uint8_t *ok,
                                    uint8_t *it, int16_t *ext, void *ws, size_t ws_bytes, void *stream) {
-    if (n_cb < 0 || (flags & ~CRN_DESC_ON_DEVICE) || max_iters < 1 || max_iters > CRN_MAX_ITERS)
+    if (n_cb < 0 || (flags & ~(CRN_DESC_ON_DEVICE | CRN_EXT_SCALED)) || max_iters < 1 || max_iters > CRN_MAX_ITERS)
         return CRN_EINVAL;
     if (n_cb == 0) return CRN_OK;
     if (!desc || !l0 || !l1 || !l2 || !bits || !ok) return CRN_EINVAL;
@@ -430,6 +437,7 @@ extern "C" int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb, const 
     }
     Plan P;
     P.dev = dev;
+    P.variant = (flags & CRN_EXT_SCALED) ? CRN_VARIANT_SCALED : CRN_VARIANT_MAXLOG;
     rc = plan_build(hdesc, n_cb, ext != nullptr, st, true, &P);
     if (rc) {
         if (P.mem) cudaFreeAsync(P.mem, st);
@@ -535,4 +543,43 @@ extern "C" int crn_tb_reassemble(const uint32_t *w, const crn_cb_desc *desc, con
     if (!all || crc24(0, b.data(), tbs + 24) != 0) return 0;
     if (out) memcpy(out, b.data(), (size_t)tbs);
     return 1;
+}
+
+extern "C" int crn_tb_verdict_batch(const crn_tb_desc *tb, int32_t n_tb, const crn_cb_desc *desc, int32_t n_cb,
+                                    const uint32_t *cb_words, const uint8_t *crc_ok, uint8_t *tb_ok,
+                                    uint32_t *tb_words, void *stream) {
+    if (n_tb < 0 || n_cb < 0) return CRN_EINVAL;
+    if (n_tb == 0) return CRN_OK;
+    if (!tb || !desc || !cb_words || !crc_ok || !tb_ok) return CRN_EINVAL;
+    for (int i = 0; i < n_tb; i++) {
+        const crn_tb_desc &t = tb[i];
+        crn_seg s;
+        if (t.cb0 < 0 || t.n_cb < 1 || t.n_cb > CRN_TB_MAX_CB || (int64_t)t.cb0 + t.n_cb > n_cb ||
+            t.word_off < 0 || crn_segment_tb(t.tbs, &s) != CRN_OK || s.C != t.n_cb)
+            return CRN_EINVAL;
+        for (int r = 0; r < t.n_cb; r++) {
+            const crn_cb_desc &d = desc[t.cb0 + r];
+            if (d.K != (r < s.Cminus ? s.Kminus : s.Kplus) || d.F != (r == 0 ? s.F : 0) ||
+                d.crc_kind != (s.C > 1 ? CRN_CRC24B : CRN_CRC24A) || d.bit_off < 0)
+                return CRN_EINVAL;
+        }
+    }
+    int dev;
+    DevTables *t;
+    int rc = crn_get_ctx(&dev, &t);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t b0 = sizeof(crn_tb_desc) * (size_t)n_tb, o1 = (b0 + 255) & ~(size_t)255;
+    const size_t tot = o1 + sizeof(crn_cb_desc) * (size_t)n_cb;
+    std::vector<uint8_t> host(tot);
+    memcpy(host.data(), tb, b0);
+    memcpy(host.data() + o1, desc, sizeof(crn_cb_desc) * (size_t)n_cb);
+    void *dm = nullptr;
+    if (cudaMallocAsync(&dm, tot, st) != cudaSuccess) { cudaGetLastError(); return CRN_ENOMEM; }
+    cudaMemcpyAsync(dm, host.data(), tot, cudaMemcpyHostToDevice, st);
+    rc = crn_launch_tb((const crn_tb_desc *)dm, n_tb, (const crn_cb_desc *)((uint8_t *)dm + o1), cb_words, crc_ok,
+                       tb_ok, tb_words, (void *)st);
+    cudaFreeAsync(dm, st);
+    if (cudaError_t e = cudaGetLastError()) return crn_cuda_fail(e, "crn_tb_verdict_batch", CRN_ECUDA);
+    return rc;
 }

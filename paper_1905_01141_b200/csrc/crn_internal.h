@@ -27,6 +27,9 @@ typedef struct {
     int32_t lo, hi;  /* CB indices; hi = -1 for the dummy partner of an odd bucket */
 } crn_pair;
 
+/* Max CBs per TB accepted by crn_tb_verdict_batch (LTE needs <= 64). */
+#define CRN_TB_MAX_CB 128
+
 /* Per-device constant tables (built once on the host, uploaded once). */
 typedef struct {
     const uint32_t *qpp_wm;   /* per K at qpp_off[kidx]: [i*M + j] = (Pi(jW+i) % W) << 16 | Pi(jW+i) / W */
@@ -45,13 +48,16 @@ int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_tasks, int32_
                       const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1,
                       const int16_t *l2, int32_t max_iters, int32_t early_term,
                       uint32_t *out_bits, uint8_t *crc_ok, uint8_t *iters_used, int16_t *ext_out,
-                      const crn_tables *tab, void *ws, void *stream, int32_t grid);
+                      const crn_tables *tab, void *ws, void *stream, int32_t grid, int32_t variant);
 size_t crn_decode_ws_bytes(int32_t grid);
 int crn_decode_grid(int device);
 /* crn_encode.cu */
 int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const uint8_t *info,
                       int32_t attach_crc, uint8_t *d0, uint8_t *d1, uint8_t *d2,
                       const crn_tables *tab, void *stream);
+/* crn_tb.cu */
+int crn_launch_tb(const crn_tb_desc *d_tbs, int32_t n_tb, const crn_cb_desc *d_desc, const uint32_t *cb_words,
+                  const uint8_t *crc_ok, uint8_t *tb_ok, uint32_t *tb_words, void *stream);
 /* crn_ubench.cu */
 int crn_launch_ubench(int32_t op, int64_t *lane_instr, float *ms, int64_t *cycles_per_block);
 /* crn_host.cpp */

@@ -186,3 +186,18 @@ def channel_llr(wl: Workload, cb_cell: np.ndarray, cb_K: np.ndarray, cb_ebn0_db:
             L = -2.0 * amp * y / sig2                                      # positive => bit 1
             out[s][lo:hi] = quantise(L)
     return tuple(out)
+
+
+def make_cb_workload(Ks, ebn0_db=1.0, seed=0, modulation="qpsk", device="cpu", max_iters=8,
+                     early_term=False, cfg=9) -> Workload:
+    """Standalone CBs of the given sizes (K-24 random bits + CRC24B each), all on
+    one synthetic cell, one Eb/N0 for all: probes and tests of single sizes."""
+    Ks = [int(k) for k in Ks]
+    dev = torch.device(device)
+    gb = generator(cfg, seed, 0, 1, dev)
+    payload = [torch.randint(0, 2, (k - 24,), generator=gb, device=dev, dtype=torch.uint8) for k in Ks]
+    n = len(Ks)
+    return Workload(name=f"cb{n}", cfg=cfg, seed=seed, max_iters=max_iters, early_term=early_term,
+                    modulation=modulation, cells=[0], tb_kind="cb", tbs=np.array([k - 24 for k in Ks], np.int64),
+                    tb_cell=np.zeros(n, np.int32), tb_ebn0_db=np.full(n, float(ebn0_db)),
+                    tb_K=np.array(Ks, np.int32), payload=payload)

@@ -9,11 +9,11 @@ from paper_1905_01141_b200 import batch as bmod
 from paper_1905_01141_b200 import crn
 
 
-def run_gpu(b, max_iters, et, want_ext=True, stream=None, desc=None, l=None):
+def run_gpu(b, max_iters, et, want_ext=True, stream=None, desc=None, l=None, flags=0):
     desc = b.desc if desc is None else desc
     bits, ok, it, ext = bmod.outputs(b, want_ext=want_ext)
     l0, l1, l2 = b.llr if l is None else l
-    crn.decode_batch_ex(desc, desc.size, l0, l1, l2, max_iters, et, 0, bits, ok, it, ext, stream=stream)
+    crn.decode_batch_ex(desc, desc.size, l0, l1, l2, max_iters, et, flags, bits, ok, it, ext, stream=stream)
     torch.cuda.synchronize()
     return dict(words=bits.cpu().numpy().view(np.uint32), crc_ok=ok.cpu().numpy()[:desc.size],
                 iters=it.cpu().numpy()[:desc.size], ext=None if ext is None else ext.cpu().numpy())
@@ -25,7 +25,7 @@ def unpack(words, desc, i):
     return ((w[:, None] >> np.arange(32, dtype=np.uint32)) & 1).astype(np.uint8).reshape(-1)[:K]
 
 
-def run_oracle(b, idx, max_iters, et):
+def run_oracle(b, idx, max_iters, et, variant=0):
     import oracle
     host = [x.cpu().numpy() for x in b.llr]
     d = b.desc[np.asarray(idx)]
@@ -34,7 +34,7 @@ def run_oracle(b, idx, max_iters, et):
     bo = np.concatenate([[0], np.cumsum(K)[:-1]]).astype(np.int64)
     ll = [np.concatenate([h[o:o + k + 4] for o, k in zip(d["llr_off"], K)]) if K.size else h[:0] for h in host]
     r = oracle.decode_batch(K, d["F"], d["crc_kind"], lo, bo, *ll, max_iters=max_iters, early_term=et,
-                            nthreads=os.cpu_count() or 1)
+                            nthreads=os.cpu_count() or 1, variant=variant)
     assert r["violations"] == 0
     r["bo"], r["K"] = bo, K
     return r

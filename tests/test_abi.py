@@ -113,3 +113,28 @@ def test_decode_refuses_without_gpu(L):
     rc = L.crn_decode_batch_ex(d.ctypes.data, 1, 1, 1, 1, 6, 0, 0, 1, 1, None, None, None, 0, None)
     assert rc == crn.CRN_ENODEV
     assert L.crn_workspace_bytes() == 0
+
+
+def test_tb_verdict_batch_validation():
+    """crn_tb_verdict_batch rejects TB tables that do not match 36.212 segmentation
+    before touching a device (host-side validation)."""
+    import ctypes as C
+    tb_bits = np.random.default_rng(1).integers(0, 2, 12000, dtype=np.uint8)
+    cbb, desc = crn.tb_build_cbs(tb_bits)
+    tbs = np.zeros(1, crn.TB_DTYPE)
+    tbs[0] = (0, desc.size, 12000, 0)
+    fake = C.c_void_p(16)
+    def call(t, d):
+        t = np.ascontiguousarray(t, crn.TB_DTYPE)
+        d = np.ascontiguousarray(d, crn.DESC_DTYPE)
+        return crn.lib().crn_tb_verdict_batch(t.ctypes.data, t.size, d.ctypes.data, d.size, fake, fake, fake,
+                                              None, None)
+    assert call(tbs, desc) in (crn.CRN_ENODEV, crn.CRN_OK)        # valid (no device here)
+    bad = tbs.copy(); bad["tbs"] = 12001
+    assert call(bad, desc) == crn.CRN_EINVAL                       # wrong segmentation
+    bad = tbs.copy(); bad["n_cb"] = 3
+    assert call(bad, desc) == crn.CRN_EINVAL                       # range outside desc
+    d2 = desc.copy(); d2["F"][0] += 1
+    assert call(tbs, d2) == crn.CRN_EINVAL                         # filler mismatch
+    d2 = desc.copy(); d2["crc_kind"][1] = crn.CRC24A
+    assert call(tbs, d2) == crn.CRN_EINVAL

@@ -288,3 +288,78 @@ def test_stream_run_cfg5(orc):
     assert np.all(tim["latency_us"] > 0) and np.all(tim["device_us"] > 0)
     assert np.all(np.diff(tim["release_us"]) > 900)
     assert np.all(tim["complete_us"] > tim["release_us"])
+
+
+def _tb_table(b):
+    """TB descriptors of a TB-config batch (CBs of TB t are contiguous, in segment order)."""
+    tbs = np.zeros(b.wl.n_tb, crn.TB_DTYPE)
+    w = 0
+    for t in range(b.wl.n_tb):
+        idx = np.flatnonzero(b.cb_tb == t)
+        tbs[t] = (idx[0], idx.size, int(b.wl.tbs[t]), w)
+        w += (int(b.wl.tbs[t]) + 31) // 32
+    return tbs, w
+
+
+@pytest.mark.parametrize("cfg,scale,kill", [(2, 1.0, False), (3, 0.2, False), (3, 0.1, True)])
+def test_tb_verdict_batch_matches_oracle(orc, cfg, scale, kill):
+    """Row f1: device TB post-processing (strip fillers + CB CRCs, concatenate, TB
+    CRC24A, all-CBs rule of PAPER.md:369) equals the oracle's reassembly of the
+    oracle's own decoded bits, payload words included."""
+    b = _full(cfg, scale)
+    if kill:                                     # zero the LLRs of every 3rd CB's systematic stream
+        for i in range(0, b.n_cb, 3):
+            o, K = int(b.desc["llr_off"][i]), int(b.desc["K"][i])
+            for x in b.llr:
+                x[o:o + K + 4] = 0
+    g = run_gpu(b, 8, True, want_ext=False)
+    idx = np.arange(b.n_cb)
+    r = run_oracle(b, idx, 8, True)
+    tbs, nw = _tb_table(b)
+    words = torch.from_numpy(g["words"].view(np.int32).copy()).cuda()
+    ok = torch.from_numpy(g["crc_ok"].copy()).cuda()
+    tb_ok = torch.full((tbs.size,), 9, dtype=torch.uint8, device="cuda")
+    tb_words = torch.zeros(max(nw, 1), dtype=torch.int32, device="cuda")
+    crn.tb_verdict_batch(tbs, b.desc, words, ok, tb_ok, tb_words)
+    torch.cuda.synchronize()
+    tb_ok, tb_words = tb_ok.cpu().numpy(), tb_words.cpu().numpy().view(np.uint32)
+    n_fail = 0
+    for t in range(tbs.size):
+        cb = np.arange(tbs["cb0"][t], tbs["cb0"][t] + tbs["n_cb"][t])
+        seg = orc.segment(int(tbs["tbs"][t]))
+        bits = [r["bits"][r["bo"][i]:r["bo"][i] + r["K"][i]] for i in cb]
+        Fs = [int(b.desc["F"][i]) for i in cb]
+        pay = orc.reassemble_tb(bits, Fs, seg)
+        want = bool(np.all(r["crc_ok"][cb]) and pay is not None)
+        assert bool(tb_ok[t]) == want, t
+        n_fail += not want
+        L = seg["L"]
+        full = np.concatenate([c[F:c.size - L] for c, F in zip(bits, Fs)])[:int(tbs["tbs"][t])]
+        w0 = int(tbs["word_off"][t])
+        got = ((tb_words[w0:w0 + (full.size + 31) // 32, None] >> np.arange(32, dtype=np.uint32)) & 1)
+        assert np.array_equal(got.astype(np.uint8).reshape(-1)[:full.size], full), t
+        if want:
+            assert np.array_equal(full, b.wl.payload[t].cpu().numpy())
+    if kill:
+        assert n_fail >= 1
+
+
+@pytest.mark.parametrize("cfg,scale,I,et", [(1, 1.0, 6, False), (5, 1.0, 8, True), (3, 0.1, 8, True)])
+def test_scaled_variant_parity(orc, cfg, scale, I, et):
+    """Row f2: the scaled-extrinsic variant (CRN_EXT_SCALED, R28) is
+    bit-exact against the oracle's variant on both kernel paths (W = 32 and
+    generic W), and the plan API selects it too."""
+    b = _full(cfg, scale)
+    g = run_gpu(b, I, et, flags=crn.EXT_SCALED)
+    idx = np.arange(b.n_cb)
+    r = run_oracle(b, idx, I, et, variant=orc.VAR_SCALED)
+    assert_parity(b, g, r, idx)
+    p = crn.Plan(b.desc)
+    p.set_variant(crn.VARIANT_SCALED)
+    bits, ok, it, ext = bmod.outputs(b)
+    p.decode(*b.llr, I, et, bits, ok, it, ext)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits.cpu().numpy().view(np.uint32), g["words"])
+    assert np.array_equal(ext.cpu().numpy(), g["ext"])
+    with pytest.raises(crn.CrnError):
+        p.set_variant(7)
