@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(HERE, "libcrn.so")
+SO = os.environ.get("CRN_LIB") or os.path.join(HERE, "libcrn.so")   # CRN_LIB: A/B experiments only
 
 CRN_OK, CRN_EINVAL, CRN_ECUDA, CRN_ENOMEM, CRN_ENODEV = 0, -1, -2, -3, -4
 CRC_NONE, CRC24A, CRC24B = 0, 1, 2

@@ -73,14 +73,50 @@ constexpr int S_NII_WORDS = 2 * 2 * NS * WMAX;
 constexpr int S_X = S_NII + S_NII_WORDS;
 constexpr int S_LP = S_X + 2 * NS * WMAX;       /* [c][step][window] */
 constexpr int S_CH = S_LP + 2 * SUMK;
-constexpr int S_TAIL = S_CH + HW * BLOCK * 2;
-constexpr int S_WORDS = S_TAIL + MAXP * 12;
+constexpr int S_TAIL = S_CH + HW * BLOCK * 2;   /* per pair: beta_K of DEC1 (8 words), of DEC2 (8 words) */
+constexpr int S_WORDS = S_TAIL + MAXP * 16;
 static_assert(S_CH % 2 == 0, "chunk array must be 8-byte aligned");
 /* generic path: beta storage (W+1)*8*T words, then the packed output bits */
 constexpr int G_BITS = (SUMK + WMAX) * NS;
 constexpr int G_WORDS = G_BITS + 2 * (SUMK / 32 + MAXP);
 constexpr int SMEM_WORDS = S_WORDS > G_WORDS ? S_WORDS : G_WORDS;
-static_assert(SMEM_WORDS * 4 + 3584 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
+static_assert(SMEM_WORDS * 4 + 6400 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
+
+/* ---- optional phase profiler (build with -DCRN_PHASE_PROF; never in the product
+ * build): lane 0 of warp 0 (a head warp) and of warp 6 (a tail warp) attribute
+ * clock64 intervals to the phase that just ended; summed over CTAs. */
+enum { P_FETCH, P_STAGE, P_CHUNK, P_PH1, P_BAR1, P_PH2, P_BAR2, P_HD, P_N };
+#ifdef CRN_PHASE_PROF
+__device__ unsigned long long g_prof[2 * P_N];
+__shared__ unsigned long long s_pacc[2][P_N];
+__shared__ long long s_plast[2];
+__device__ __forceinline__ void prof_mark(int ph) {
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0 && (w == 0 || w == 6)) {
+        const int k = w ? 1 : 0;
+        const long long t = clock64();
+        s_pacc[k][ph] += (unsigned long long)(t - s_plast[k]);
+        s_plast[k] = t;
+    }
+}
+__device__ __forceinline__ void prof_init() {
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0 && (w == 0 || w == 6)) {
+        const int k = w ? 1 : 0;
+        for (int i = 0; i < P_N; i++) s_pacc[k][i] = 0;
+        s_plast[k] = clock64();
+    }
+}
+__device__ __forceinline__ void prof_flush() {
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0 && (w == 0 || w == 6))
+        for (int i = 0; i < P_N; i++) atomicAdd(&g_prof[(w ? 1 : 0) * P_N + i], s_pacc[w ? 1 : 0][i]);
+}
+#else
+__device__ __forceinline__ void prof_mark(int) {}
+__device__ __forceinline__ void prof_init() {}
+__device__ __forceinline__ void prof_flush() {}
+#endif
 
 /* ---- RSC trellis, S = 4 r1 + 2 r2 + r3 (R1), evaluated at compile time */
 __host__ __device__ constexpr int nxt(int S, int u) { return (((u ^ (S >> 1) ^ S) & 1) << 2) | (S >> 1); }
@@ -424,28 +460,6 @@ __device__ __forceinline__ void tm_load16_wait(u32 ta, u32 v[HW]) {
                  : "memory");
 }
 
-/* Phase 0 (row a4): chunk[s] = (Lu+Lp, Lu-Lp) with Lu = Ls + La for the
- * thread's 16 steps, from the static Ls-Lp (TMEM), Lp (shared plane) and the
- * a-priori La gathered at the thread's QPP word indices q[] (registers; zero
- * in DEC1 of iteration 1). */
-__device__ __forceinline__ void build_chunk(const SCtx &f, int c, const u32 (&q)[HW], const u32 *lp, const u32 *la,
-                                            bool zero_la) {
-    uint2 *ch = reinterpret_cast<uint2 *>(f.sm + S_CH) + f.tid;
-    lp += f.k0 * TS + f.t;
-    u32 a[HW], pv[HW], sn[HW];
-#pragma unroll
-    for (int s = 0; s < HW; s++) {          /* shared loads first: the TMEM load below is a compiler barrier */
-        a[s] = zero_la ? 0u : la[q[s]];
-        pv[s] = lp[s * TS];
-    }
-    tm_load16_wait(f.ts + c * HW, sn);
-#pragma unroll
-    for (int s = 0; s < HW; s++) {
-        const u32 d = vadd(sn[s], a[s]);                    /* Lu - Lp */
-        ch[s * BLOCK] = make_uint2(vadd(vadd(d, pv[s]), pv[s]), d);
-    }
-}
-
 /* 16 consecutive int16 LLRs of one stream: 8-byte vector loads when aligned.
  * Returned as 8 words of (element 2i, element 2i+1). */
 __device__ __forceinline__ void load16(const int16_t *__restrict__ src, u32 w[HW / 2]) {
@@ -467,9 +481,20 @@ __device__ __forceinline__ void load16(const int16_t *__restrict__ src, u32 w[HW
 /* One half-iteration of constituent c (rows a5-a8).  Le -> Y (c = 0, natural
  * order) or Z (c = 1, interleaved order). */
 template <bool SCALE>
-__device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, int it) {
-    const uint2 *ch = reinterpret_cast<const uint2 *>(f.sm + S_CH) + f.tid;
+__device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, int it, const u32 (&q)[HW],
+                                           const u32 *la, bool zero_la) {
+    uint2 *ch = reinterpret_cast<uint2 *>(f.sm + S_CH) + f.tid;
     const u32 *lp = f.sm + S_LP + c * SUMK + f.k0 * TS + f.t;
+    /* row a4 fused into phase 1: this thread's 16 (Lu+Lp, Lu-Lp) pairs are formed
+     * step by step from the TMEM static sums, the parity plane and the a-priori
+     * LLRs gathered at its QPP indices, used at once and kept in smem for phase 2 */
+    u32 av[HW], pv[HW], sn[HW];
+#pragma unroll
+    for (int s = 0; s < HW; s++) {
+        av[s] = zero_la ? 0u : la[q[s]];
+        pv[s] = lp[s * TS];
+    }
+    tm_load16_wait(f.ts + c * HW, sn);
     u32 *nii = f.sm + S_NII;
     u32 *X = f.sm + S_X;
     u32 *le = f.sm + (c ? S_Z : S_Y) + f.t;
@@ -487,35 +512,43 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
 #pragma unroll
             for (int s = 0; s < NS; s++) m[s] = nii[nii1_ix(c, 0, s, f.t - 1)];
         }
-#pragma unroll 1
+#pragma unroll
         for (int s = 0; s < HW; s++) {          /* store alpha_s, advance to alpha_{s+1} */
-            const uint2 g = ch[s * BLOCK];
+            const u32 d = vadd(sn[s], av[s]);                /* Lu - Lp */
+            const u32 x = vadd(vadd(d, pv[s]), pv[s]);       /* Lu + Lp */
+            ch[s * BLOCK] = make_uint2(x, d);
             tm_store8(f.ta + s * 8, m);
-            alpha_step_d(m, lp[s * TS], g.x, g.y);
+            alpha_step_d(m, pv[s], x, d);
         }
 #pragma unroll
         for (int s = 0; s < NS; s++) X[s * TS + f.t] = m[s];             /* alpha_16 -> tail thread */
     } else {
         /* beta_32 of window j: tail termination, zero in iteration 1, NII afterwards */
-        if (f.j == f.M - 1) tail_beta(f.sm + S_TAIL + f.p * 12 + c * 6, m);
-        else if (it == 1) {
+        if (f.j == f.M - 1) {               /* beta_K from the tail, precomputed at staging (static) */
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = f.sm[S_TAIL + f.p * 16 + c * 8 + s];
+        } else if (it == 1) {
 #pragma unroll
             for (int s = 0; s < NS; s++) m[s] = M1;
         } else {
 #pragma unroll
             for (int s = 0; s < NS; s++) m[s] = nii[nii1_ix(c, 1, s, f.t + 1)];
         }
-#pragma unroll 1
+#pragma unroll
         for (int s = HW - 1; s >= 0; s--) {     /* store beta_{17+s}, advance to beta_{16+s} */
-            const uint2 g = ch[s * BLOCK];
+            const u32 d = vadd(sn[s], av[s]);
+            const u32 x = vadd(vadd(d, pv[s]), pv[s]);
+            ch[s * BLOCK] = make_uint2(x, d);
             tm_store8(f.ta + s * 8, m);
-            beta_step_d(m, lp[s * TS], g.x, g.y);
+            beta_step_d(m, pv[s], x, d);
         }
 #pragma unroll
         for (int s = 0; s < NS; s++) X[(NS + s) * TS + f.t] = m[s];      /* beta_16 -> head thread */
     }
+    prof_mark(P_PH1);
     tm_wait_st();
     __syncthreads();        /* hand-over; also orders this half-iteration's NII reads before its writes */
+    prof_mark(P_BAR1);
 
     u32 bufA[NS], bufB[NS];
     if (!tail_thr) {
@@ -523,7 +556,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
 #pragma unroll
         for (int s = 0; s < NS; s++) b[s] = X[(NS + s) * TS + f.t];      /* beta_16 */
         tm_load8(f.ta + (HW - 1) * 8, bufA);
-#pragma unroll 1
+#pragma unroll 2
         for (int s = HW - 1; s >= 0; s -= 2) {
 #pragma unroll
             for (int h = 0; h < 2; h++) {
@@ -544,7 +577,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
 #pragma unroll
         for (int s = 0; s < NS; s++) a[s] = X[s * TS + f.t];             /* alpha_16 */
         tm_load8(f.ta, bufA);
-#pragma unroll 1
+#pragma unroll 2
         for (int s = 0; s < HW; s += 2) {
 #pragma unroll
             for (int h = 0; h < 2; h++) {
@@ -638,13 +671,23 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         }
         tm_store16(f.ts, sn);
         if (active && tail_thr && j == M - 1) {
+            /* tails (R11 column order) -> beta_K of both constituents: it
+             * depends on the tail LLRs only, so it is formed once per task */
+            u32 tl[12];
 #pragma unroll
-            for (int mm = 0; mm < 12; mm++) {     /* tails: DESIGN.md R11 column order */
+            for (int mm = 0; mm < 12; mm++) {
                 const int col = tk.K + mm / 3;
                 const int16_t *src = (mm % 3 == 0) ? l0 : (mm % 3 == 1) ? l1 : l2;
                 const int16_t v0 = clo >= 0 ? src[olo + col] : 0;
                 const int16_t v1 = chi >= 0 ? src[ohi + col] : 0;
-                sm[S_TAIL + p * 12 + mm] = clamp_pack(v0, v1);
+                tl[mm] = clamp_pack(v0, v1);
+            }
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                u32 b[NS];
+                tail_beta(tl + 6 * c, b);
+#pragma unroll
+                for (int s = 0; s < NS; s++) sm[S_TAIL + p * 16 + c * 8 + s] = b[s];
             }
         }
 #pragma unroll
@@ -659,17 +702,22 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         tm_store16(f.ts + HW, sn);
         tm_wait_st();
         __syncthreads();
+        prof_mark(P_STAGE);
     }
 
     for (int it = 1; it <= max_iters; it++) {
         /* DEC1: La1[n] = Le2[Pi^-1(n)] gathered from Z (zero in iteration 1) */
-        build_chunk(f, 0, q1, sm + S_LP, sm + S_Z, it == 1);
-        siso_split<SCALE>(f, tail_thr, 0, it);
+        prof_mark(P_CHUNK);
+        siso_split<SCALE>(f, tail_thr, 0, it, q1, sm + S_Z, it == 1);
+        prof_mark(P_PH2);
         __syncthreads();
+        prof_mark(P_BAR2);
         /* DEC2: La2[i] = Le1[Pi(i)] gathered from Y */
-        build_chunk(f, 1, q2, sm + S_LP + SUMK, sm + S_Y, false);
-        siso_split<SCALE>(f, tail_thr, 1, it);
+        prof_mark(P_CHUNK);
+        siso_split<SCALE>(f, tail_thr, 1, it, q2, sm + S_Y, false);
+        prof_mark(P_PH2);
         __syncthreads();
+        prof_mark(P_BAR2);
         if (!et && it != max_iters) continue;     /* fixed mode: decide only at the end */
 
         /* ---- row a9: L_APP = Ls + Le1 + La1_next (tie -> 1, R16); 16 bits per
@@ -732,7 +780,9 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                 }
             }
         }
+        prof_mark(P_HD);
         if (finish_iteration(sh, NP) == 0) break;
+        prof_mark(P_HD);
     }
 }
 
@@ -900,6 +950,50 @@ __device__ __noinline__ void run_task_generic(const crn_task &tk, const crn_cb_d
     }
 }
 
+/* Claim the CTA's next task (warp 0): its descriptor and CB list go to the
+ * shared "next" slots, and its input LLRs (3 streams x K+4 int16 per CB) are
+ * bulk-prefetched into L2, so the task starts from on-chip metadata and its
+ * staging loads hit L2 instead of waiting on HBM. */
+struct NextSh {
+    int *task;
+    crn_task *tk;
+    int *cb, *F, *kind;
+};
+
+__device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks, const crn_task *__restrict__ tasks,
+                                           const crn_pair *__restrict__ pairs, const crn_cb_desc *__restrict__ desc,
+                                           const int16_t *l0, const int16_t *l1, const int16_t *l2, int lane) {
+    int nt = 0;
+    if (lane == 0) nt = atomicAdd(counter, 1);
+    nt = __shfl_sync(0xFFFFFFFFu, nt, 0);
+    if (lane == 0) *nx.task = nt;
+    if (nt >= n_tasks) return;
+    const crn_task t = tasks[nt];
+    if (lane == 0) *nx.tk = t;
+    for (int e = lane; e < 2 * t.n_pairs; e += 32) {
+        const crn_pair pr = pairs[t.pair0 + (e >> 1)];
+        const int cb = (e & 1) ? pr.hi : pr.lo;
+        nx.cb[e] = cb;
+        if (cb < 0) {
+            nx.F[e] = 0;
+            nx.kind[e] = 0;
+            continue;
+        }
+        const crn_cb_desc &d = desc[cb];
+        nx.F[e] = d.F;
+        nx.kind[e] = d.crc_kind;
+        const int64_t off = d.llr_off;
+        const uint32_t bytes = 2u * (uint32_t)(t.K + 4);
+#pragma unroll
+        for (int x = 0; x < 3; x++) {
+            const uintptr_t a = reinterpret_cast<uintptr_t>((x == 0 ? l0 : x == 1 ? l1 : l2) + off);
+            const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (a + bytes + 15) & ~(uintptr_t)15;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
+                         : "memory");
+        }
+    }
+}
+
 __global__ void __launch_bounds__(BLOCK, 1)
 decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__ tasks, int n_tasks,
               const crn_pair *__restrict__ pairs, const int16_t *__restrict__ l0,
@@ -907,7 +1001,9 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
               uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok, uint8_t *__restrict__ iters_used,
               int16_t *__restrict__ ext_out, crn_tables tab, uint8_t *ws, int variant) {
     extern __shared__ __align__(16) u32 smem[];
-    __shared__ int s_task, s_left;
+    __shared__ int s_ntask, s_left;
+    __shared__ crn_task s_ntk;
+    __shared__ int s_ncb[2 * MAXP], s_nF[2 * MAXP], s_nkind[2 * MAXP];
     __shared__ u32 s_tmem;
     __shared__ u32 s_crc[2 * MAXP];
     __shared__ int s_cb[2 * MAXP], s_F[2 * MAXP], s_kind[2 * MAXP];
@@ -928,23 +1024,28 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     asm volatile("tcgen05.fence::after_thread_sync;");
     const u32 tmem = s_tmem;
 
+    /* Tasks are claimed one ahead (claim_next): task t+1's metadata and LLRs
+     * move on-chip / into L2 while task t decodes. */
+    const NextSh nx{&s_ntask, &s_ntk, s_ncb, s_nF, s_nkind};
+    prof_init();
+    if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid);
     for (;;) {
-        if (tid == 0) s_task = atomicAdd(counter, 1);
-        __syncthreads();
-        const int task = s_task;
+        __syncthreads();                        /* next slots filled */
+        const int task = s_ntask;
         if (task >= n_tasks) break;
-        const crn_task tk = tasks[task];
+        const crn_task tk = s_ntk;
         for (int e = tid; e < 2 * tk.n_pairs; e += BLOCK) {
-            const crn_pair pr = pairs[tk.pair0 + (e >> 1)];
-            const int cb = (e & 1) ? pr.hi : pr.lo;
+            const int cb = s_ncb[e];
             s_cb[e] = cb;
-            s_F[e] = cb >= 0 ? desc[cb].F : 0;
-            s_kind[e] = cb >= 0 ? desc[cb].crc_kind : 0;
+            s_F[e] = s_nF[e];
+            s_kind[e] = s_nkind[e];
             s_done[e] = cb < 0;
             s_fin[e] = 0;
             s_crc[e] = 0;
         }
-        __syncthreads();
+        __syncthreads();                        /* next slots consumed */
+        if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid);
+        prof_mark(P_FETCH);
         if (tk.W == 32) {
             if (variant == CRN_VARIANT_SCALED)
                 run_task_fast<true>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab, smem,
@@ -961,6 +1062,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
                                         slot, smem, sh, smem + G_BITS);
         }
     }
+    prof_flush();
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if ((tid >> 5) == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tmem));
@@ -1012,3 +1114,13 @@ extern "C" int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_ta
                                                   ok, it, ext, *tab, (uint8_t *)ws, variant);
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
 }
+
+#ifdef CRN_PHASE_PROF
+/* phase profiler readout (profiling builds only): 2 x P_N cycle sums, then reset */
+extern "C" int crn_prof_read(unsigned long long *out) {
+    if (cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 2 * P_N) != cudaSuccess) return CRN_ECUDA;
+    static const unsigned long long z[2 * P_N] = {};
+    cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+    return CRN_OK;
+}
+#endif
