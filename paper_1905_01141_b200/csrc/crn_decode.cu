@@ -621,7 +621,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
     f.k0 = tail_thr ? HW : 0;
     const u32 *qts = tab.qpp_ts + tab.qpp_off[tk.kidx];     /* natural position of Pi(jW+i)  */
     const u32 *qinv = tab.qinv_ts + tab.qpp_off[tk.kidx];   /* interleaved position of jW+i */
-    const u32 *cpow = tab.crc_pow + tab.crc_off[tk.kidx];
+    const u32 *cbit = tab.crc_bit + tab.crcb_off[tk.kidx] + f.j;        /* + kind*K + i*M */
 
     /* ---- row a2: stage own half-window of both CBs of the pair: Lp1, Lp2 into
      * the shared planes, Ls-Lp1 (natural) and Ls[Pi]-Lp2 (interleaved) into
@@ -634,24 +634,46 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         const int64_t olo = clo >= 0 ? desc[clo].llr_off : 0, ohi = chi >= 0 ? desc[chi].llr_off : 0;
         const int n0 = j * W + f.k0;
         u32 *tmp = sm + S_CH;                 /* natural Ls, window-major, for the interleaved gather */
-        u32 sn[HW];
+        /* every global load of the staging first (one round trip): the thread's 16
+         * LLRs of each stream and CB, its QPP word indices and, for the last
+         * window's tail thread, the 12 tail columns */
+        u32 wl[3][HW / 2], wh[3][HW / 2];
 #pragma unroll
         for (int x = 0; x < 3; x++) {
             const int16_t *src = x == 0 ? l0 : x == 1 ? l1 : l2;
-            u32 wl[HW / 2], wh[HW / 2];
-            if (clo >= 0) load16(src + olo + n0, wl);
+            if (clo >= 0) load16(src + olo + n0, wl[x]);
             else {
 #pragma unroll
-                for (int k = 0; k < HW / 2; k++) wl[k] = 0;
+                for (int k = 0; k < HW / 2; k++) wl[x][k] = 0;
             }
-            if (chi >= 0) load16(src + ohi + n0, wh);
+            if (chi >= 0) load16(src + ohi + n0, wh[x]);
             else {
 #pragma unroll
-                for (int k = 0; k < HW / 2; k++) wh[k] = 0;
+                for (int k = 0; k < HW / 2; k++) wh[x][k] = 0;
             }
+        }
+#pragma unroll
+        for (int s = 0; s < HW; s++) {
+            q1[s] = __ldg(qinv + (f.k0 + s) * M + j);
+            q2[s] = __ldg(qts + (f.k0 + s) * M + j);
+        }
+        const bool tail_owner = active && tail_thr && j == M - 1;
+        int16_t t0[12], t1[12];
+        if (tail_owner) {
+#pragma unroll
+            for (int mm = 0; mm < 12; mm++) {     /* tails: DESIGN.md R11 column order */
+                const int col = tk.K + mm / 3;
+                const int16_t *src = (mm % 3 == 0) ? l0 : (mm % 3 == 1) ? l1 : l2;
+                t0[mm] = clo >= 0 ? __ldg(src + olo + col) : (int16_t)0;
+                t1[mm] = chi >= 0 ? __ldg(src + ohi + col) : (int16_t)0;
+            }
+        }
+        u32 sn[HW];
+#pragma unroll
+        for (int x = 0; x < 3; x++) {
 #pragma unroll
             for (int s = 0; s < HW; s++) {
-                u32 v = __byte_perm(wl[s / 2], wh[s / 2], (s & 1) ? 0x7632 : 0x5410);
+                u32 v = __byte_perm(wl[x][s / 2], wh[x][s / 2], (s & 1) ? 0x7632 : 0x5410);
                 if (x < 2) {                                       /* known filler 0: Ls = Lp1 = -4096 */
                     if (n0 + s < Flo) v = (v & 0xFFFF0000u) | 0xF000u;
                     if (n0 + s < Fhi) v = (v & 0x0000FFFFu) | 0xF0000000u;
@@ -670,18 +692,11 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             }
         }
         tm_store16(f.ts, sn);
-        if (active && tail_thr && j == M - 1) {
-            /* tails (R11 column order) -> beta_K of both constituents: it
-             * depends on the tail LLRs only, so it is formed once per task */
+        if (tail_owner) {
+            /* beta_K of both constituents depends on the tail LLRs only: formed once per task */
             u32 tl[12];
 #pragma unroll
-            for (int mm = 0; mm < 12; mm++) {
-                const int col = tk.K + mm / 3;
-                const int16_t *src = (mm % 3 == 0) ? l0 : (mm % 3 == 1) ? l1 : l2;
-                const int16_t v0 = clo >= 0 ? src[olo + col] : 0;
-                const int16_t v1 = chi >= 0 ? src[ohi + col] : 0;
-                tl[mm] = clamp_pack(v0, v1);
-            }
+            for (int mm = 0; mm < 12; mm++) tl[mm] = clamp_pack(t0[mm], t1[mm]);
 #pragma unroll
             for (int c = 0; c < 2; c++) {
                 u32 b[NS];
@@ -692,8 +707,8 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         }
 #pragma unroll
         for (int s = 0; s < HW; s++) {
-            q1[s] = f.pM + __ldg(qinv + (f.k0 + s) * M + j);
-            q2[s] = f.pM + __ldg(qts + (f.k0 + s) * M + j);
+            q1[s] += f.pM;
+            q2[s] += f.pM;
         }
         __syncthreads();
 #pragma unroll
@@ -751,14 +766,15 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                 hb[0 * TS + f.t] = wlo;
                 hb[1 * TS + f.t] = whi;
 #pragma unroll
-                for (int l = 0; l < 2; l++) {
+                for (int l = 0; l < 2; l++) {     /* CRC register = XOR of the constants of the set bits */
                     const int kind = sh.kind[2 * p + l];
                     if (kind == CRN_CRC_NONE) continue;
-                    const u32 w = l ? whi : wlo, poly = kind == CRN_CRC24A ? POLY_A : POLY_B;
-                    u32 r = 0;
+                    const u32 w = l ? whi : wlo;
+                    const u32 *cb = cbit + (kind == CRN_CRC24A ? 0 : tk.K);
+                    u32 acc = 0;
 #pragma unroll
-                    for (int i = 0; i < W; i++) r = crc_bit(r, (w >> i) & 1u, poly);
-                    atomicXor(&sh.crc[2 * p + l], crc_mulmod(r, cpow[(kind == CRN_CRC24A ? 0 : M) + j], poly));
+                    for (int i = 0; i < W; i++) acc ^= __ldg(cb + i * M) & (0u - ((w >> i) & 1u));
+                    atomicXor(&sh.crc[2 * p + l], acc);
                 }
             }
             __syncthreads();

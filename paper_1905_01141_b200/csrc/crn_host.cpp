@@ -172,8 +172,8 @@ static uint32_t mulx_mod(uint32_t a, uint32_t poly) { return ((a << 1) ^ ((a & 0
 static int build_tables(int dev, DevTables **out) {
     auto it = g_tables.find(dev);
     if (it != g_tables.end()) { *out = &it->second; return CRN_OK; }
-    std::vector<uint32_t> qpp, qts, qin, cp;
-    std::vector<int32_t> qoff(CRN_NUM_K), coff(CRN_NUM_K);
+    std::vector<uint32_t> qpp, qts, qin, cp, cb;
+    std::vector<int32_t> qoff(CRN_NUM_K), coff(CRN_NUM_K), cboff(CRN_NUM_K);
     for (int ki = 0; ki < CRN_NUM_K; ki++) {
         int K = k_at(ki), M, W;
         crn_windows(K, &M, &W);
@@ -191,6 +191,15 @@ static int build_tables(int dev, DevTables **out) {
                 /* inverse: natural position n = Pi(x) is read back from interleaved position x */
                 qin[qoff[ki] + (size_t)(n % W) * M + n / W] = (uint32_t)((x % W) * CRN_CTA_THREADS + x / W);
             }
+        cboff[ki] = (int32_t)cb.size();            /* per-bit CRC constants, window-major */
+        cb.resize(cb.size() + 2 * (size_t)K);
+        for (int k = 0; k < 2; k++) {
+            uint32_t poly = k ? POLY_B : POLY_A, c = poly;        /* x^24 mod g for n = K-1 */
+            for (int n = K - 1; n >= 0; n--) {
+                cb[cboff[ki] + (size_t)k * K + (size_t)(n % W) * M + n / W] = c;
+                c = mulx_mod(c, poly);
+            }
+        }
         coff[ki] = (int32_t)cp.size();
         cp.resize(cp.size() + 2 * (size_t)M);
         for (int k = 0; k < 2; k++) {
@@ -207,7 +216,9 @@ static int build_tables(int dev, DevTables **out) {
         cudaMalloc(&t.qinv_ts, qin.size() * 4) != cudaSuccess ||
         cudaMalloc(&t.crc_pow, cp.size() * 4) != cudaSuccess ||
         cudaMalloc(&t.qpp_off, CRN_NUM_K * 4) != cudaSuccess ||
-        cudaMalloc(&t.crc_off, CRN_NUM_K * 4) != cudaSuccess) {
+        cudaMalloc(&t.crc_off, CRN_NUM_K * 4) != cudaSuccess ||
+        cudaMalloc(&t.crc_bit, cb.size() * 4) != cudaSuccess ||
+        cudaMalloc(&t.crcb_off, CRN_NUM_K * 4) != cudaSuccess) {
         cudaGetLastError();
         return CRN_ENOMEM;
     }
@@ -217,9 +228,12 @@ static int build_tables(int dev, DevTables **out) {
     cudaMemcpy(t.crc_pow, cp.data(), cp.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.qpp_off, qoff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.crc_off, coff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(t.crc_bit, cb.data(), cb.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(t.crcb_off, cboff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
     if (cudaError_t e = cudaGetLastError()) return crn_cuda_fail(e, "table upload", CRN_ECUDA);
     t.tab.qpp_wm = t.qpp_wm; t.tab.qpp_ts = t.qpp_ts; t.tab.qinv_ts = t.qinv_ts; t.tab.crc_pow = t.crc_pow;
     t.tab.qpp_off = t.qpp_off; t.tab.crc_off = t.crc_off;
+    t.tab.crc_bit = t.crc_bit; t.tab.crcb_off = t.crcb_off;
     t.grid = crn_decode_grid(dev);
     if (t.grid <= 0) {
         char where[96];

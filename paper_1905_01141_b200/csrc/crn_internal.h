@@ -36,8 +36,11 @@ typedef struct {
     const uint32_t *qpp_ts;   /* same index: (Pi(jW+i) % W) * CRN_CTA_THREADS + Pi(jW+i) / W (fast path) */
     const uint32_t *qinv_ts;  /* same index, inverse permutation: m = Pi^-1(jW+i) -> (m % W) * CRN_CTA_THREADS + m / W */
     const uint32_t *crc_pow;  /* per K at crc_off[kidx]: [kind(0=A,1=B)*M + j] = x^((M-1-j)W) mod g */
+    const uint32_t *crc_bit;  /* per K at crcb_off[kidx]: [kind(0=A,1=B)*K + i*M + j] = x^(K-1-n+24) mod g, n = jW+i:
+                                 the CRC register contribution of a 1 at bit n (register = XOR over the set bits) */
     const int32_t *qpp_off;
     const int32_t *crc_off;
+    const int32_t *crcb_off;
 } crn_tables;
 
 #ifdef __cplusplus
