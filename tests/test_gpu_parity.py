@@ -363,3 +363,53 @@ def test_scaled_variant_parity(orc, cfg, scale, I, et):
     assert np.array_equal(ext.cpu().numpy(), g["ext"])
     with pytest.raises(crn.CrnError):
         p.set_variant(7)
+
+
+def test_outputs_write_only_their_ranges(orc):
+    """Memcheck substitute (compute-sanitizer is unavailable on this pool): CBs are
+    laid out with gaps between their LLR, output-word and ext ranges, every output
+    buffer is pre-filled with a sentinel, and after decoding (fast + generic paths,
+    ET, ext_out) everything outside the described ranges still holds the sentinel
+    while every CB is bit-exact against the oracle."""
+    b = _full(5, 1.0)
+    rng = np.random.default_rng(11)
+    K = b.desc["K"].astype(np.int64)
+    gl = rng.integers(1, 40, b.n_cb)
+    gw = rng.integers(1, 5, b.n_cb)
+    ge = rng.integers(1, 40, b.n_cb)
+    d = b.desc.copy()
+    lo = np.zeros(b.n_cb, np.int64); wo = np.zeros(b.n_cb, np.int64); eo = np.zeros(b.n_cb, np.int64)
+    a = c = e = 0
+    for i in range(b.n_cb):
+        a += gl[i]; lo[i] = a; a += K[i] + 4
+        c += gw[i]; wo[i] = c; c += (K[i] + 31) // 32
+        e += ge[i]; eo[i] = e; e += K[i]
+    d["llr_off"], d["bit_off"], d["ext_off"] = lo, wo, eo
+    n_llr, n_w, n_e = a + 17, c + 9, e + 23
+    ll = [torch.full((n_llr,), 0x5A5A, dtype=torch.int16, device="cuda") for _ in range(3)]
+    for s in range(3):
+        for i in range(b.n_cb):
+            o = int(b.desc["llr_off"][i])
+            ll[s][int(lo[i]):int(lo[i]) + int(K[i]) + 4] = b.llr[s][o:o + int(K[i]) + 4]
+    SENT = 0x3C3C3C3C
+    bits = torch.full((n_w,), SENT, dtype=torch.int64, device="cuda").to(torch.int32)
+    ok = torch.full((b.n_cb + 7,), 0xA5, dtype=torch.uint8, device="cuda")
+    it = torch.full((b.n_cb + 7,), 0xA5, dtype=torch.uint8, device="cuda")
+    ext = torch.full((n_e,), 0x7B7B, dtype=torch.int16, device="cuda")
+    crn.decode_batch_ex(d, b.n_cb, *ll, 8, True, 0, bits, ok, it, ext)
+    torch.cuda.synchronize()
+    words = bits.cpu().numpy().view(np.uint32)
+    r = run_oracle(b, np.arange(b.n_cb), 8, True)
+    g = dict(words=words, crc_ok=ok.cpu().numpy()[:b.n_cb], iters=it.cpu().numpy()[:b.n_cb], ext=ext.cpu().numpy())
+
+    class _B:
+        desc = d
+    assert_parity(_B, g, r, np.arange(b.n_cb))
+    wmask = np.ones(n_w, bool)
+    emask = np.ones(n_e, bool)
+    for i in range(b.n_cb):
+        wmask[wo[i]:wo[i] + (K[i] + 31) // 32] = False
+        emask[eo[i]:eo[i] + K[i]] = False
+    assert np.all(words[wmask] == SENT)
+    assert np.all(g["ext"][emask] == 0x7B7B)
+    assert np.all(ok.cpu().numpy()[b.n_cb:] == 0xA5) and np.all(it.cpu().numpy()[b.n_cb:] == 0xA5)
