@@ -99,8 +99,8 @@ int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb,
                         void *workspace, size_t workspace_bytes, void *cuda_stream);
 
 /* Bytes of caller-provided workspace crn_decode_batch_ex needs on the current
- * device (independent of the batch: the decoder is a persistent kernel with
- * one slot per resident CTA). */
+ * device (independent of the batch: the persistent decoder keeps every CB's
+ * state on chip; the workspace holds its task counter). */
 size_t crn_workspace_bytes(void);
 
 /* Plans: validate + bucket + upload a descriptor set once, decode many times

@@ -51,14 +51,7 @@ constexpr u32 FLOORB = 0xDFFFDFFFu;             /* (-8193, -8193): biased state-
 constexpr u32 CLIP_HI = 0x10001000u;            /* ( 4096,  4096): channel / extrinsic clamp */
 constexpr u32 CLIP_LO = 0xF000F000u;            /* (-4096, -4096) */
 constexpr u32 NEG4097 = 0xEFFFEFFFu, ONE2 = 0x00010001u;
-constexpr u32 POLY_A = 0x864CFBu, POLY_B = 0x800063u;
 
-/* generic-path workspace slot in global memory (u32 words, stride T) */
-constexpr int A_LS = 0, A_LP1 = SUMK, A_LP2 = 2 * SUMK, A_LSI = 3 * SUMK, A_X = 4 * SUMK, A_Y = 5 * SUMK;
-constexpr int A_NII = 6 * SUMK;                 /* [c][parity][alpha/beta][s][WMAX] */
-constexpr int NII_WORDS = 2 * 2 * 2 * NS * WMAX;
-constexpr int A_TAIL = A_NII + NII_WORDS;       /* [pair][12] */
-constexpr int SLOT_WORDS = A_TAIL + MAXP * 12;
 constexpr size_t WS_HEAD = 256;                 /* task counter */
 
 /* fast-path shared-memory layout (u32 words).  Y = Le1 (natural order), Z =
@@ -76,10 +69,8 @@ constexpr int S_CH = S_LP + 2 * SUMK;
 constexpr int S_TAIL = S_CH + HW * BLOCK * 2;   /* per pair: beta_K of DEC1 (8 words), of DEC2 (8 words) */
 constexpr int S_WORDS = S_TAIL + MAXP * 16;
 static_assert(S_CH % 2 == 0, "chunk array must be 8-byte aligned");
-/* generic path: beta storage (W+1)*8*T words, then the packed output bits */
-constexpr int G_BITS = (SUMK + WMAX) * NS;
-constexpr int G_WORDS = G_BITS + 2 * (SUMK / 32 + MAXP);
-constexpr int SMEM_WORDS = S_WORDS > G_WORDS ? S_WORDS : G_WORDS;
+constexpr int SMEM_WORDS = S_WORDS;
+static_assert(SMEM_WORDS == CRN_SMEM_WORDS, "split-window sizing (crn_internal.h) must see the same shared memory");
 static_assert(SMEM_WORDS * 4 + 6400 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
 
 /* ---- optional phase profiler (build with -DCRN_PHASE_PROF; never in the product
@@ -137,37 +128,6 @@ __device__ __forceinline__ void norm8(u32 v[NS]) {
     const u32 nm = ~m;                          /* ~(m - 1) = -m */
 #pragma unroll
     for (int s = 0; s < NS; s++) v[s] = vaddmax(v[s], nm, FLOORB);
-}
-
-/* alpha_{k+1}(S') = N(max over the two predecessors S of alpha_k(S) + gamma_k)  (row a6) */
-__device__ __forceinline__ void alpha_step(u32 a[NS], u32 Lu, u32 Lp, u32 Lup) {
-    u32 an[NS];
-#pragma unroll
-    for (int Sp = 0; Sp < NS; Sp++) {
-        const int S0 = 2 * (Sp & 3), S1 = S0 + 1;
-        const int u0 = (nxt(S0, 0) == Sp) ? 0 : 1, u1 = (nxt(S1, 0) == Sp) ? 0 : 1;
-        const int z0 = par(S0, u0), z1 = par(S1, u1);
-        if (!u0 && !z0) an[Sp] = vaddmax(a[S1], gsel(u1, z1, Lu, Lp, Lup), a[S0]);
-        else if (!u1 && !z1) an[Sp] = vaddmax(a[S0], gsel(u0, z0, Lu, Lp, Lup), a[S1]);
-        else an[Sp] = vaddmax(a[S1], gsel(u1, z1, Lu, Lp, Lup), vadd(a[S0], gsel(u0, z0, Lu, Lp, Lup)));
-    }
-    norm8(an);
-#pragma unroll
-    for (int s = 0; s < NS; s++) a[s] = an[s];
-}
-
-/* beta_k(S) = N(max over u of beta_{k+1}(next(S,u)) + gamma_k(u, z(S,u)))  (row a5) */
-__device__ __forceinline__ void beta_step(u32 b[NS], u32 Lu, u32 Lp, u32 Lup) {
-    u32 v[NS];
-#pragma unroll
-    for (int S = 0; S < NS; S++) {
-        const int n0 = nxt(S, 0), n1 = nxt(S, 1), z0 = par(S, 0), z1 = par(S, 1);
-        if (!z0) v[S] = vaddmax(b[n1], gsel(1, z1, Lu, Lp, Lup), b[n0]);
-        else v[S] = vaddmax(b[n1], gsel(1, z1, Lu, Lp, Lup), vadd(b[n0], Lp));
-    }
-    norm8(v);
-#pragma unroll
-    for (int s = 0; s < NS; s++) b[s] = v[s];
 }
 
 /* ---- Branch-difference form of the recursions (fast path).  The two branches
@@ -299,60 +259,8 @@ __device__ __forceinline__ u32 clamp_pack(int16_t lo, int16_t hi) {
     return __vmins2(__vmaxs2(v, CLIP_LO), CLIP_HI);
 }
 
-__device__ __forceinline__ u32 crc_bit(u32 reg, u32 bit, u32 poly) {
-    const u32 fb = ((reg >> 23) ^ bit) & 1u;
-    return ((reg << 1) & 0xFFFFFFu) ^ (fb ? poly : 0u);
-}
-
-/* a(x) * b(x) mod g(x), 24-bit polynomials (Horner over the bits of b) */
-__device__ __forceinline__ u32 crc_mulmod(u32 a, u32 b, u32 poly) {
-    u32 acc = 0;
-    for (int k = 23; k >= 0; k--) {
-        acc = ((acc << 1) & 0xFFFFFFu) ^ ((acc & 0x800000u) ? poly : 0u);
-        if ((b >> k) & 1u) acc ^= a;
-    }
-    return acc;
-}
-
-/* NII words: [c][parity][alpha(0)/beta(1)][s][WMAX] */
-__device__ __forceinline__ int nii_ix(int c, int parity, int ab, int s, int t) {
-    return (((c * 2 + parity) * 2 + ab) * NS + s) * WMAX + t;
-}
-
 /* fast path (shared memory, single-buffered): [c][alpha(0)/beta(1)][s][WMAX] */
 __device__ __forceinline__ int nii1_ix(int c, int ab, int s, int t) { return ((c * 2 + ab) * NS + s) * WMAX + t; }
-
-/* Initial alpha / beta of window j in iteration it (biased), R13:
- * window 0 starts at the known state, the last window's beta comes from the
- * tail, other boundaries are zero in iteration 1 and the neighbour's metric
- * from the previous iteration afterwards.  SINGLE: the shared-memory NII
- * buffer of the fast path (one copy; the caller separates reads from the
- * writes of this half-iteration with a barrier); else the double-buffered
- * global one, indexed by iteration parity. */
-template <bool SINGLE>
-__device__ __forceinline__ void init_metrics(const u32 *nii, const u32 *tail, int c, int it, int j, int M, int t,
-                                             u32 a[NS], u32 b[NS]) {
-    const int rd = (it - 1) & 1;
-    if (j == 0) {
-        a[0] = M1;
-#pragma unroll
-        for (int s = 1; s < NS; s++) a[s] = FLOORB;
-    } else if (it == 1) {
-#pragma unroll
-        for (int s = 0; s < NS; s++) a[s] = M1;
-    } else {
-#pragma unroll
-        for (int s = 0; s < NS; s++) a[s] = nii[SINGLE ? nii1_ix(c, 0, s, t - 1) : nii_ix(c, rd, 0, s, t - 1)];
-    }
-    if (j == M - 1) tail_beta(tail, b);
-    else if (it == 1) {
-#pragma unroll
-        for (int s = 0; s < NS; s++) b[s] = M1;
-    } else {
-#pragma unroll
-        for (int s = 0; s < NS; s++) b[s] = nii[SINGLE ? nii1_ix(c, 1, s, t + 1) : nii_ix(c, rd, 1, s, t + 1)];
-    }
-}
 
 struct TaskSh {
     int *cb, *F, *kind;
@@ -803,163 +711,294 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
 }
 
 /* ======================================================================
- * Generic path: W in 33..62 (only K <= 1008 with K not a multiple of 32).
- * Runtime W, T <= 192 windows, window-major stride T in the global workspace, beta
- * stored for the whole window, then alpha + Lambda.
+ * Split-window path: W in 33..62 (K <= 1008 that is not a multiple of 32).
+ * The W = 32 design with runtime sizes: a window's head thread (tid < Tp)
+ * owns steps [0, hw), hw = ceil(W/2), its tail thread (tid = Tp + t) steps
+ * [hw, W); everything the CB pairs of the task need stays on chip:
+ * extrinsics, parity planes, per-thread QPP word indices and branch-metric
+ * pairs, NII states in shared memory (row stride Tp, crn_split_smem_words),
+ * stored alpha/beta and the static Ls-Lp sums in TMEM (10*hw columns per
+ * thread).  The host sizes n_pairs so both fit (crn_split_fits).  Rolled
+ * loops (runtime W); one TMEM column per static sum and step.
  * ====================================================================== */
-struct GCtx {
-    int T, t, p, j, M, W, it;
-    u32 *slot;
-    const u32 *qtab;
-    u32 *bst;   /* shared: beta storage (i*NS + s)*T + t */
+struct GSplit {
+    u32 *Y, *Z, *LP, *Q, *CH, *NII, *X, *TB;
+    int W, M, T, Tp, hw_h;     /* geometry */
+    int tid2;                  /* position in the per-thread arrays: tid for head, Tp + t for tail */
+    int t, p, j, pM, k0, hw;   /* window, pair, window in CB, steps owned */
+    u32 ta, ts;                /* TMEM: 8*hw_h stored-metric columns, then 2*hw_h static columns */
 };
 
-/* C = 0: DEC1 (La from X natural, Le1 -> Y); C = 1: DEC2 (interleaved
- * systematic, Lp2, La2 = Y[Pi(i)], Le2 scattered to X[Pi(i)] = La1_next). */
-template <int C, bool SCALE>
-__device__ __forceinline__ void siso_generic(const GCtx &c) {
-    const int T = c.T, t = c.t, W = c.W;
-    const u32 *Ls = c.slot + (C ? A_LSI : A_LS);
-    const u32 *Lp = c.slot + (C ? A_LP2 : A_LP1);
-    const u32 *La = c.slot + (C ? A_Y : A_X);
-    u32 *Le = c.slot + (C ? A_X : A_Y);
-    auto addr = [&](int i) -> int {
-        if (C == 0) return i * T + t;
-        const u32 q = c.qtab[i * c.M + c.j];
-        return (int)(q >> 16) * T + c.p * c.M + (int)(q & 0xFFFFu);
-    };
-    u32 a[NS], b[NS];
-    init_metrics<false>(c.slot + A_NII, c.slot + A_TAIL + c.p * 12 + C * 6, C, c.it, c.j, c.M, t, a, b);
+__device__ __forceinline__ void tm_store1(u32 ta, u32 v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(ta), "r"(v) : "memory");
+}
+__device__ __forceinline__ u32 tm_load1_wait(u32 ta) {
+    u32 v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\ttcgen05.wait::ld.sync.aligned;"
+                 : "=r"(v) : "r"(ta) : "memory");
+    return v;
+}
+
+/* One half-iteration of constituent c on the split-window path (rows a4-a8). */
+template <bool SCALE>
+__device__ __forceinline__ void siso_gsplit(const GSplit &g, bool tail_thr, int c, int it) {
+    const int Tp = g.Tp, W = g.W, hw = g.hw, t = g.t, st2 = 2 * Tp;
+    const u32 *lp = g.LP + c * W * Tp + g.k0 * Tp + t;           /* this thread's steps, stride Tp */
+    const u32 *Qc = g.Q + c * g.hw_h * st2 + g.tid2;              /* QPP word indices (stride 2Tp) */
+    const u32 *la = c ? g.Y : g.Z;
+    const bool zero_la = c == 0 && it == 1;
+    uint2 *ch = reinterpret_cast<uint2 *>(g.CH) + g.tid2;
+    u32 *le = (c ? g.Z : g.Y) + g.k0 * Tp + t;
+    const u32 ts = g.ts + c * g.hw_h;
+    u32 m[NS];
+    /* ---- phase 1: head alpha forward over [0, hw), tail beta backward over [hw_h, W) */
+    if (!tail_thr) {
+        if (g.j == 0) {
+            m[0] = M1;
 #pragma unroll
-    for (int s = 0; s < NS; s++) c.bst[(W * NS + s) * T + t] = b[s];
-#pragma unroll 2
-    for (int i = W - 1; i >= 0; i--) {
-        const int ix = i * T + t;
-        const u32 lp = Lp[ix], lu = vadd(Ls[ix], La[addr(i)]);
-        beta_step(b, lu, lp, vadd(lu, lp));
-        if (i > 0) {
+            for (int s = 1; s < NS; s++) m[s] = FLOORB;
+        } else if (it == 1) {
 #pragma unroll
-            for (int s = 0; s < NS; s++) c.bst[(i * NS + s) * T + t] = b[s];
+            for (int s = 0; s < NS; s++) m[s] = M1;
+        } else {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = g.NII[((c * 2 + 0) * NS + s) * Tp + t - 1];
         }
+#pragma unroll 1
+        for (int s = 0; s < hw; s++) {
+            const u32 av = zero_la ? 0u : la[Qc[s * st2]];
+            const u32 pv = lp[s * Tp];
+            const u32 sn = tm_load1_wait(ts + s);
+            const u32 d = vadd(sn, av), x = vadd(vadd(d, pv), pv);
+            ch[s * st2] = make_uint2(x, d);
+            tm_store8(g.ta + s * 8, m);
+            alpha_step_d(m, pv, x, d);
+        }
+#pragma unroll
+        for (int s = 0; s < NS; s++) g.X[s * Tp + t] = m[s];                 /* alpha_hw -> tail thread */
+    } else {
+        if (g.j == g.M - 1) {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = g.TB[g.p * 16 + c * 8 + s];
+        } else if (it == 1) {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = M1;
+        } else {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = g.NII[((c * 2 + 1) * NS + s) * Tp + t + 1];
+        }
+#pragma unroll 1
+        for (int s = hw - 1; s >= 0; s--) {
+            const u32 av = zero_la ? 0u : la[Qc[s * st2]];
+            const u32 pv = lp[s * Tp];
+            const u32 sn = tm_load1_wait(ts + s);
+            const u32 d = vadd(sn, av), x = vadd(vadd(d, pv), pv);
+            ch[s * st2] = make_uint2(x, d);
+            tm_store8(g.ta + s * 8, m);
+            beta_step_d(m, pv, x, d);
+        }
+#pragma unroll
+        for (int s = 0; s < NS; s++) g.X[(NS + s) * Tp + t] = m[s];          /* beta_hw_h -> head thread */
     }
-    const int wr = c.it & 1;
+    tm_wait_st();
+    __syncthreads();        /* hand-over; also orders this half-iteration's NII reads before its writes */
+    /* ---- phase 2: head beta backward over [0, hw) + Lambda, tail alpha forward + Lambda */
+    u32 nx[NS], cur[NS];
+    if (!tail_thr) {
+        u32 b[NS];
 #pragma unroll
-    for (int s = 0; s < NS; s++) c.slot[A_NII + nii_ix(C, wr, 1, s, t)] = b[s];     /* beta_{jW} -> window j-1 */
-#pragma unroll 2
-    for (int i = 0; i < W; i++) {
-        const int ix = i * T + t, ax = addr(i);
-        const u32 lp = Lp[ix], lu = vadd(Ls[ix], La[ax]);
-        u32 bn[NS];
+        for (int s = 0; s < NS; s++) b[s] = g.X[(NS + s) * Tp + t];
+        tm_load8(g.ta + (hw - 1) * 8, nx);
+#pragma unroll 1
+        for (int s = hw - 1; s >= 0; s--) {
+            const uint2 gg = ch[s * st2];
+            const u32 pv = lp[s * Tp];
+            tm_wait_ld8(nx);
 #pragma unroll
-        for (int s = 0; s < NS; s++) bn[s] = c.bst[((i + 1) * NS + s) * T + t];
-        Le[ax] = ext_out_map<SCALE>(lambda_le(a, bn, lp));
-        alpha_step(a, lu, lp, vadd(lu, lp));
+            for (int k = 0; k < NS; k++) cur[k] = nx[k];
+            tm_load8(g.ta + (s > 0 ? s - 1 : 0) * 8, nx);
+            le[s * Tp] = ext_out_map<SCALE>(lambda_le(cur, b, pv));
+            beta_step_d(b, pv, gg.x, gg.y);
+        }
+        tm_wait_ld8(nx);
+#pragma unroll
+        for (int s = 0; s < NS; s++) g.NII[((c * 2 + 1) * NS + s) * Tp + t] = b[s];   /* beta_{jW} -> window j-1 */
+    } else {
+        u32 a[NS];
+#pragma unroll
+        for (int s = 0; s < NS; s++) a[s] = g.X[s * Tp + t];
+        tm_load8(g.ta, nx);
+#pragma unroll 1
+        for (int s = 0; s < hw; s++) {
+            const uint2 gg = ch[s * st2];
+            const u32 pv = lp[s * Tp];
+            tm_wait_ld8(nx);
+#pragma unroll
+            for (int k = 0; k < NS; k++) cur[k] = nx[k];
+            tm_load8(g.ta + (s + 1 < hw ? s + 1 : s) * 8, nx);
+            le[s * Tp] = ext_out_map<SCALE>(lambda_le(a, cur, pv));
+            alpha_step_d(a, pv, gg.x, gg.y);
+        }
+        tm_wait_ld8(nx);
+#pragma unroll
+        for (int s = 0; s < NS; s++) g.NII[((c * 2 + 0) * NS + s) * Tp + t] = a[s];   /* alpha_{(j+1)W} -> window j+1 */
     }
-#pragma unroll
-    for (int s = 0; s < NS; s++) c.slot[A_NII + nii_ix(C, wr, 0, s, t)] = a[s];     /* alpha_{(j+1)W} -> window j+1 */
 }
 
 template <bool SCALE>
-__device__ __noinline__ void run_task_generic(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
-                                              const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
-                                              const int16_t *__restrict__ l2, int max_iters, int et,
-                                              uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok,
-                                              uint8_t *__restrict__ iters_used, int16_t *__restrict__ ext_out,
-                                              const crn_tables &tab, u32 *slot, u32 *bst, TaskSh sh, u32 *s_bits) {
-    const int tid = threadIdx.x;
-    const int K = tk.K, M = tk.M, W = tk.W, NP = tk.n_pairs, T = NP * M;
+__device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
+                                            const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
+                                            const int16_t *__restrict__ l2, int max_iters, int et,
+                                            uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok,
+                                            uint8_t *__restrict__ iters_used, int16_t *__restrict__ ext_out,
+                                            const crn_tables &tab, u32 *sm, u32 tmem, TaskSh sh) {
+    const int tid = threadIdx.x, warp = tid >> 5;
+    GSplit g;
+    g.W = tk.W;
+    g.M = tk.M;
+    g.T = tk.n_pairs * tk.M;
+    g.Tp = (g.T + 31) & ~31;
+    g.hw_h = (g.W + 1) / 2;
+    const int W = g.W, M = g.M, T = g.T, Tp = g.Tp, NP = tk.n_pairs, K = tk.K;
+    g.Y = sm;
+    g.Z = g.Y + W * Tp;
+    g.LP = g.Z + W * Tp;
+    g.Q = g.LP + 2 * W * Tp;
+    g.CH = g.Q + 2 * g.hw_h * 2 * Tp;
+    g.NII = g.CH + 2 * g.hw_h * 2 * Tp;
+    g.X = g.NII + 32 * Tp;
+    g.TB = g.X + 16 * Tp;
+    const bool working = tid < 2 * Tp;          /* whole warps: Tp is a multiple of 32 */
+    const bool tail_thr = tid >= Tp;
+    g.tid2 = tid;
+    g.t = tid - (tail_thr ? Tp : 0);
+    const bool active = working && g.t < T;
+    g.p = active ? g.t / M : 0;
+    g.j = active ? g.t - g.p * M : 0;
+    g.pM = g.p * M;
+    g.k0 = tail_thr ? g.hw_h : 0;
+    g.hw = tail_thr ? W - g.hw_h : g.hw_h;
+    g.ta = tmem + ((u32)((warp & 3) * 32) << 16) + (u32)((warp >> 2) * 10 * g.hw_h);
+    g.ts = g.ta + 8 * g.hw_h;
+    const u32 *qw = tab.qpp_wm + tab.qpp_off[tk.kidx];      /* (row << 16) | col of Pi(jW+i) */
+    const u32 *qi = tab.qinv_wm + tab.qpp_off[tk.kidx];     /* same for Pi^-1(jW+i) */
+    const u32 *cbit = tab.crc_bit + tab.crcb_off[tk.kidx] + g.j;
+    const int p = g.p, j = g.j, t = g.t, hw = g.hw, k0 = g.k0, st2 = 2 * Tp;
+    const int clo = sh.cb[2 * p], chi = sh.cb[2 * p + 1];
+    const int Flo = sh.F[2 * p], Fhi = sh.F[2 * p + 1];
+
+    /* ---- row a2: stage this thread's steps of both CBs of the pair */
+    if (working) {
+        const int64_t olo = clo >= 0 ? desc[clo].llr_off : 0, ohi = chi >= 0 ? desc[chi].llr_off : 0;
+        u32 *tmp = g.CH;                        /* natural Ls, window-major, for the interleaved gather */
+#pragma unroll 1
+        for (int s = 0; s < hw; s++) {
+            const int n = j * W + k0 + s, ix = (k0 + s) * Tp + t;
+            u32 v[3];
+#pragma unroll
+            for (int x = 0; x < 3; x++) {
+                const int16_t *src = x == 0 ? l0 : x == 1 ? l1 : l2;
+                int16_t a = clo >= 0 ? __ldg(src + olo + n) : (int16_t)0;
+                int16_t b = chi >= 0 ? __ldg(src + ohi + n) : (int16_t)0;
+                if (x < 2) {                                   /* known filler 0: Ls = Lp1 = -4096 */
+                    if (n < Flo) a = -4096;
+                    if (n < Fhi) b = -4096;
+                }
+                v[x] = clamp_pack(a, b);
+            }
+            tmp[ix] = v[0];
+            g.LP[ix] = v[1];
+            g.LP[W * Tp + ix] = v[2];
+            tm_store1(g.ts + s, __vsub2(v[0], v[1]));              /* Ls - Lp1 */
+            const u32 q1 = __ldg(qi + (k0 + s) * M + j), q2 = __ldg(qw + (k0 + s) * M + j);
+            g.Q[s * st2 + tid] = (q1 >> 16) * Tp + g.pM + (q1 & 0xFFFFu);                  /* DEC1 gather: Z */
+            g.Q[g.hw_h * st2 + s * st2 + tid] = (q2 >> 16) * Tp + g.pM + (q2 & 0xFFFFu);   /* DEC2 gather: Y */
+        }
+        if (active && tail_thr && j == M - 1) {      /* beta_K of both constituents from the tails */
+            u32 tl[12];
+#pragma unroll
+            for (int mm = 0; mm < 12; mm++) {
+                const int col = K + mm / 3;
+                const int16_t *src = (mm % 3 == 0) ? l0 : (mm % 3 == 1) ? l1 : l2;
+                tl[mm] = clamp_pack(clo >= 0 ? __ldg(src + olo + col) : (int16_t)0,
+                                    chi >= 0 ? __ldg(src + ohi + col) : (int16_t)0);
+            }
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                u32 b[NS];
+                tail_beta(tl + 6 * c, b);
+#pragma unroll
+                for (int s = 0; s < NS; s++) g.TB[p * 16 + c * 8 + s] = b[s];
+            }
+        }
+    }
+    __syncthreads();
+    if (working) {
+#pragma unroll 1
+        for (int s = 0; s < hw; s++)            /* Ls[Pi(i)] - Lp2 */
+            tm_store1(g.ts + g.hw_h + s, __vsub2(g.CH[g.Q[g.hw_h * st2 + s * st2 + tid]], g.LP[W * Tp + (k0 + s) * Tp + t]));
+        tm_wait_st();
+    }
+    __syncthreads();
+
     const int nw = (K + 31) >> 5;
-    const u32 *qtab = tab.qpp_wm + tab.qpp_off[tk.kidx];
-    const u32 *cpow = tab.crc_pow + tab.crc_off[tk.kidx];
-    for (int e = tid; e < 2 * NP * nw; e += BLOCK) s_bits[e] = 0;
-
-    /* ---- row a2: demux, clamp to +-4096, filler override, window-major pair packing */
-    for (int e = tid; e < NP * K; e += BLOCK) {
-        const int p = e / K, n = e - p * K;
-        const int clo = sh.cb[2 * p], chi = sh.cb[2 * p + 1];
-        int16_t s0 = 0, s1 = 0, a0 = 0, a1 = 0, q0 = 0, q1 = 0;
-        if (clo >= 0) { const int64_t o = desc[clo].llr_off + n; s0 = l0[o]; a0 = l1[o]; q0 = l2[o]; }
-        if (chi >= 0) { const int64_t o = desc[chi].llr_off + n; s1 = l0[o]; a1 = l1[o]; q1 = l2[o]; }
-        if (n < sh.F[2 * p]) { s0 = -4096; a0 = -4096; }           /* known filler 0 */
-        if (n < sh.F[2 * p + 1]) { s1 = -4096; a1 = -4096; }
-        const int ix = (n % W) * T + p * M + n / W;
-        slot[A_LS + ix] = clamp_pack(s0, s1);
-        slot[A_LP1 + ix] = clamp_pack(a0, a1);
-        slot[A_LP2 + ix] = clamp_pack(q0, q1);
-    }
-    for (int e = tid; e < NP * 12; e += BLOCK) {
-        const int p = e / 12, m = e - p * 12;
-        const int col = K + m / 3;                                  /* tails: DESIGN.md R11 */
-        const int16_t *src = (m % 3 == 0) ? l0 : (m % 3 == 1) ? l1 : l2;
-        const int clo = sh.cb[2 * p], chi = sh.cb[2 * p + 1];
-        const int16_t v0 = clo >= 0 ? src[desc[clo].llr_off + col] : 0;
-        const int16_t v1 = chi >= 0 ? src[desc[chi].llr_off + col] : 0;
-        slot[A_TAIL + p * 12 + m] = clamp_pack(v0, v1);
-    }
-    __syncthreads();
-    for (int e = tid; e < T * W; e += BLOCK) {                      /* Ls[Pi(i)] for DEC2, La1 = 0 */
-        const int i = e / T, tt = e - i * T, p = tt / M, j = tt - p * M;
-        const u32 q = qtab[i * M + j];
-        slot[A_LSI + e] = slot[A_LS + (int)(q >> 16) * T + p * M + (int)(q & 0xFFFFu)];
-        slot[A_X + e] = 0;
-    }
-    __syncthreads();
-
-    const bool active = tid < T;
-    GCtx c;
-    c.T = T; c.t = tid; c.p = active ? tid / M : 0; c.j = active ? tid - c.p * M : 0;
-    c.M = M; c.W = W; c.slot = slot; c.qtab = qtab; c.bst = bst;
     for (int it = 1; it <= max_iters; it++) {
-        c.it = it;
-        if (active) siso_generic<0, SCALE>(c);
+        if (working) siso_gsplit<SCALE>(g, tail_thr, 0, it);
+        else __syncthreads();                   /* the hand-over barrier inside siso_gsplit */
         __syncthreads();
-        if (active) siso_generic<1, SCALE>(c);
+        if (working) siso_gsplit<SCALE>(g, tail_thr, 1, it);
+        else __syncthreads();
         __syncthreads();
         if (!et && it != max_iters) continue;
-        /* ---- row a9: L_APP = Ls + Le1 + La1_next, hard decision (tie -> 1),
-         * fillers 0, LSB-first packing, windowed CRC with GF(2) combine */
-        if (active) {
-            const int p = c.p, j = c.j;
-            const int Flo = sh.F[2 * p], Fhi = sh.F[2 * p + 1];
-            const int klo = sh.kind[2 * p], khi = sh.kind[2 * p + 1];
-            const u32 plo = klo == CRN_CRC24A ? POLY_A : POLY_B, phi = khi == CRN_CRC24A ? POLY_A : POLY_B;
-            u64 vlo = 0, vhi = 0;
-            u32 rlo = 0, rhi = 0;
-            for (int i = 0; i < W; i++) {
-                const int ix = i * T + tid, n = j * W + i;
-                const u32 lapp = vadd(vadd(slot[A_LS + ix], slot[A_Y + ix]), slot[A_X + ix]);
+        /* ---- row a9: L_APP = Ls + Le1 + La1_next, hard decision (tie -> 1), fillers 0,
+         * LSB-first packing into shared words, CRC as the XOR of per-bit constants */
+        u32 *bits = g.X;                        /* [pair lane][nw] words, free after the hand-over */
+        for (int e = tid; e < 2 * NP * nw; e += BLOCK) bits[e] = 0;
+        __syncthreads();
+        u32 blo = 0, bhi = 0;
+        if (working) {                          /* TMEM loads are warp-collective: every lane of a working warp */
+#pragma unroll 1
+            for (int s = 0; s < hw; s++) {
+                const int ix = (k0 + s) * Tp + t, n = j * W + k0 + s;
+                const u32 ls = vadd(tm_load1_wait(g.ts + s), g.LP[ix]);
+                const u32 lapp = vadd(vadd(ls, g.Y[ix]), g.Z[g.Q[s * st2 + tid]]);
                 const u32 ge = __vcmpges2(lapp, 0u);
-                const u32 blo = (n < Flo) ? 0u : (ge & 1u), bhi = (n < Fhi) ? 0u : ((ge >> 16) & 1u);
-                vlo |= (u64)blo << i;
-                vhi |= (u64)bhi << i;
-                rlo = crc_bit(rlo, blo, plo);
-                rhi = crc_bit(rhi, bhi, phi);
+                blo |= (n < Flo ? 0u : (ge & 1u)) << s;
+                bhi |= (n < Fhi ? 0u : ((ge >> 16) & 1u)) << s;
             }
-            const int start = j * W, w0 = start >> 5, off = start & 31;
-            const u64 vv[2] = {vlo, vhi};
+        }
+        if (active) {
+            const int n0 = j * W + k0, w0 = n0 >> 5, off = n0 & 31;
 #pragma unroll
             for (int l = 0; l < 2; l++) {
-                u32 *bb = s_bits + (2 * p + l) * nw;
-                atomicOr(&bb[w0], (u32)(vv[l] << off));
-                if (w0 + 1 < nw) atomicOr(&bb[w0 + 1], (u32)(vv[l] >> (32 - off)));
-                if (off && w0 + 2 < nw) atomicOr(&bb[w0 + 2], (u32)(vv[l] >> (64 - off)));
+                const u32 b = l ? bhi : blo;
+                u32 *bb = bits + (2 * p + l) * nw;
+                atomicOr(&bb[w0], b << off);
+                if (off && w0 + 1 < nw) atomicOr(&bb[w0 + 1], b >> (32 - off));
+                const int kind = sh.kind[2 * p + l];
+                if (kind == CRN_CRC_NONE) continue;
+                const u32 *cb = cbit + (kind == CRN_CRC24A ? 0 : K) + k0 * M;
+                u32 acc = 0;
+#pragma unroll 1
+                for (int s = 0; s < hw; s++) acc ^= __ldg(cb + s * M) & (0u - ((b >> s) & 1u));
+                atomicXor(&sh.crc[2 * p + l], acc);
             }
-            if (klo != CRN_CRC_NONE) atomicXor(&sh.crc[2 * p], crc_mulmod(rlo, cpow[(klo == CRN_CRC24A ? 0 : M) + j], plo));
-            if (khi != CRN_CRC_NONE) atomicXor(&sh.crc[2 * p + 1], crc_mulmod(rhi, cpow[(khi == CRN_CRC24A ? 0 : M) + j], phi));
         }
         __syncthreads();
         decide(sh, NP, it, max_iters, et, crc_ok, iters_used);
         for (int e = tid; e < 2 * NP * nw; e += BLOCK) {
             const int pl = e / nw, w = e - pl * nw;
-            if (sh.fin[pl]) out_bits[desc[sh.cb[pl]].bit_off + w] = s_bits[e];
-            s_bits[e] = 0;
+            if (sh.fin[pl]) out_bits[desc[sh.cb[pl]].bit_off + w] = bits[e];
         }
-        if (ext_out) {
-            for (int e = tid; e < 2 * NP * K; e += BLOCK) {
-                const int pl = e / K, n = e - pl * K, p = pl >> 1;
-                if (!sh.fin[pl]) continue;
-                const u32 x = slot[A_X + (n % W) * T + p * M + n / W];
-                ext_out[desc[sh.cb[pl]].ext_off + n] = (int16_t)((pl & 1) ? (x >> 16) : (x & 0xFFFFu));
+        if (ext_out && active) {
+#pragma unroll
+            for (int l = 0; l < 2; l++) {
+                if (!sh.fin[2 * p + l]) continue;
+                const crn_cb_desc &d = desc[sh.cb[2 * p + l]];
+                for (int s = 0; s < hw; s++) {
+                    const u32 x = g.Z[g.Q[s * st2 + tid]];
+                    ext_out[d.ext_off + j * W + k0 + s] = (int16_t)(l ? (x >> 16) : (x & 0xFFFFu));
+                }
             }
         }
         if (finish_iteration(sh, NP) == 0) break;
@@ -1026,7 +1065,6 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     __shared__ uint8_t s_done[2 * MAXP], s_fin[2 * MAXP];
 
     int *counter = (int *)ws;
-    u32 *slot = (u32 *)(ws + WS_HEAD) + (size_t)blockIdx.x * SLOT_WORDS;
     const int tid = threadIdx.x;
     const TaskSh sh{s_cb, s_F, s_kind, s_done, s_fin, s_crc, &s_left};
 
@@ -1071,11 +1109,11 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
                                      smem, tmem, sh);
         } else {
             if (variant == CRN_VARIANT_SCALED)
-                run_task_generic<true>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
-                                       slot, smem, sh, smem + G_BITS);
+                run_task_split<true>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
+                                     smem, tmem, sh);
             else
-                run_task_generic<false>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
-                                        slot, smem, sh, smem + G_BITS);
+                run_task_split<false>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
+                                      smem, tmem, sh);
         }
     }
     prof_flush();
@@ -1088,7 +1126,7 @@ size_t smem_bytes() { return (size_t)SMEM_WORDS * 4; }
 
 }  // namespace
 
-extern "C" size_t crn_decode_ws_bytes(int32_t grid) { return WS_HEAD + (size_t)grid * SLOT_WORDS * 4; }
+extern "C" size_t crn_decode_ws_bytes(int32_t) { return WS_HEAD; }   /* the task counter; all decode state is on chip */
 
 extern "C" int crn_decode_grid(int device) {
     /* returns the persistent grid (one CTA per SM), or a negative code:

@@ -172,8 +172,8 @@ static uint32_t mulx_mod(uint32_t a, uint32_t poly) { return ((a << 1) ^ ((a & 0
 static int build_tables(int dev, DevTables **out) {
     auto it = g_tables.find(dev);
     if (it != g_tables.end()) { *out = &it->second; return CRN_OK; }
-    std::vector<uint32_t> qpp, qts, qin, cp, cb;
-    std::vector<int32_t> qoff(CRN_NUM_K), coff(CRN_NUM_K), cboff(CRN_NUM_K);
+    std::vector<uint32_t> qpp, qts, qin, qiw, cb;
+    std::vector<int32_t> qoff(CRN_NUM_K), cboff(CRN_NUM_K);
     for (int ki = 0; ki < CRN_NUM_K; ki++) {
         int K = k_at(ki), M, W;
         crn_windows(K, &M, &W);
@@ -182,6 +182,7 @@ static int build_tables(int dev, DevTables **out) {
         qpp.resize(qpp.size() + (size_t)K);
         qts.resize(qpp.size());
         qin.resize(qpp.size());
+        qiw.resize(qpp.size());
         for (int j = 0; j < M; j++)
             for (int i = 0; i < W; i++) {
                 int64_t x = (int64_t)j * W + i;
@@ -190,6 +191,7 @@ static int build_tables(int dev, DevTables **out) {
                 qts[qoff[ki] + (size_t)i * M + j] = (n % W) * CRN_CTA_THREADS + n / W;
                 /* inverse: natural position n = Pi(x) is read back from interleaved position x */
                 qin[qoff[ki] + (size_t)(n % W) * M + n / W] = (uint32_t)((x % W) * CRN_CTA_THREADS + x / W);
+                qiw[qoff[ki] + (size_t)(n % W) * M + n / W] = (uint32_t)(((x % W) << 16) | (x / W));
             }
         cboff[ki] = (int32_t)cb.size();            /* per-bit CRC constants, window-major */
         cb.resize(cb.size() + 2 * (size_t)K);
@@ -200,23 +202,13 @@ static int build_tables(int dev, DevTables **out) {
                 c = mulx_mod(c, poly);
             }
         }
-        coff[ki] = (int32_t)cp.size();
-        cp.resize(cp.size() + 2 * (size_t)M);
-        for (int k = 0; k < 2; k++) {
-            uint32_t poly = k ? POLY_B : POLY_A, p = 1;     /* x^0 */
-            for (int j = M - 1; j >= 0; j--) {
-                cp[coff[ki] + (size_t)k * M + j] = p;
-                for (int s = 0; s < W; s++) p = mulx_mod(p, poly);
-            }
-        }
     }
     DevTables t;
     if (cudaMalloc(&t.qpp_wm, qpp.size() * 4) != cudaSuccess ||
         cudaMalloc(&t.qpp_ts, qts.size() * 4) != cudaSuccess ||
         cudaMalloc(&t.qinv_ts, qin.size() * 4) != cudaSuccess ||
-        cudaMalloc(&t.crc_pow, cp.size() * 4) != cudaSuccess ||
+        cudaMalloc(&t.qinv_wm, qiw.size() * 4) != cudaSuccess ||
         cudaMalloc(&t.qpp_off, CRN_NUM_K * 4) != cudaSuccess ||
-        cudaMalloc(&t.crc_off, CRN_NUM_K * 4) != cudaSuccess ||
         cudaMalloc(&t.crc_bit, cb.size() * 4) != cudaSuccess ||
         cudaMalloc(&t.crcb_off, CRN_NUM_K * 4) != cudaSuccess) {
         cudaGetLastError();
@@ -225,15 +217,15 @@ static int build_tables(int dev, DevTables **out) {
     cudaMemcpy(t.qpp_wm, qpp.data(), qpp.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.qpp_ts, qts.data(), qts.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.qinv_ts, qin.data(), qin.size() * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(t.crc_pow, cp.data(), cp.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(t.qinv_wm, qiw.data(), qiw.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.qpp_off, qoff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
-    cudaMemcpy(t.crc_off, coff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.crc_bit, cb.data(), cb.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.crcb_off, cboff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
     if (cudaError_t e = cudaGetLastError()) return crn_cuda_fail(e, "table upload", CRN_ECUDA);
-    t.tab.qpp_wm = t.qpp_wm; t.tab.qpp_ts = t.qpp_ts; t.tab.qinv_ts = t.qinv_ts; t.tab.crc_pow = t.crc_pow;
-    t.tab.qpp_off = t.qpp_off; t.tab.crc_off = t.crc_off;
+    t.tab.qpp_wm = t.qpp_wm; t.tab.qpp_ts = t.qpp_ts; t.tab.qinv_ts = t.qinv_ts;
+    t.tab.qpp_off = t.qpp_off;
     t.tab.crc_bit = t.crc_bit; t.tab.crcb_off = t.crcb_off;
+    t.tab.qinv_wm = t.qinv_wm;
     t.grid = crn_decode_grid(dev);
     if (t.grid <= 0) {
         char where[96];
@@ -300,6 +292,7 @@ int crn_validate(const crn_cb_desc *d, int n, bool want_ext) {
  * index order, group floor(6144/K) pairs per task. */
 void crn_build_tasks(const crn_cb_desc *d, const int *sel, int n, std::vector<crn_task> &tasks,
                      std::vector<crn_pair> &pairs) {
+    const size_t t0 = tasks.size();
     std::vector<int> idx(sel, sel + n);
     std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return d[a].K > d[b].K; });
     size_t s = 0;
@@ -310,6 +303,8 @@ void crn_build_tasks(const crn_cb_desc *d, const int *sel, int n, std::vector<cr
         int M, W;
         crn_windows(K, &M, &W);
         int per = std::max(1, std::min(CRN_TASK_SUMK / K, CRN_MAX_PAIRS));
+        if (W != 32)                        /* split-window path: shared memory and TMEM bound the task */
+            while (per > 1 && !crn_split_fits(W, M, per)) per--;
         int32_t first_pair = (int32_t)pairs.size();
         for (size_t i = s; i < e; i += 2) pairs.push_back({idx[i], i + 1 < e ? idx[i + 1] : -1});
         int32_t np = (int32_t)pairs.size() - first_pair;
@@ -321,6 +316,12 @@ void crn_build_tasks(const crn_cb_desc *d, const int *sel, int n, std::vector<cr
         }
         s = e;
     }
+    /* longest tasks first (LPT order for the persistent grid): a task's critical
+     * path is the trellis steps one thread runs per half-iteration -- 16 on the
+     * W = 32 path (split windows), W on the generic path (one thread per window) */
+    auto steps = [](const crn_task &t) { return t.W == 32 ? 16 : t.W; };
+    std::stable_sort(tasks.begin() + (std::ptrdiff_t)t0, tasks.end(),
+                     [&](const crn_task &a, const crn_task &b) { return steps(a) > steps(b); });
 }
 
 static int plan_build(const crn_cb_desc *desc, int n, bool want_ext, cudaStream_t st, bool async, Plan *P) {

@@ -27,6 +27,31 @@ typedef struct {
     int32_t lo, hi;  /* CB indices; hi = -1 for the dummy partner of an odd bucket */
 } crn_pair;
 
+/* Split-window path for W in 33..62 (crn_decode.cu run_task_split): a task of
+ * n_pairs pairs has T = n_pairs*M windows, Tp = T rounded up to 32; the head
+ * thread of a window owns steps [0, hw) with hw = ceil(W/2), the tail thread
+ * [hw, W).  Shared-memory words of its layout (row stride Tp):
+ *   Y, Z (extrinsics) W*Tp each | Lp1, Lp2 W*Tp each | Q1, Q2 (per-thread QPP
+ *   word indices) hw*2Tp each | CH (branch-metric pairs) 2*hw*2Tp |
+ *   NII 32*Tp | X (hand-over / hard-decision bits) 16*Tp | tail beta 16*n_pairs
+ * and TMEM columns per thread 10*hw (8 per stored step + 2 static sums), one
+ * 10*hw block per group of 4 warps.  The host sizes n_pairs so both fit. */
+#define CRN_SMEM_WORDS 47616
+#define CRN_TMEM_COLS 512
+static inline int crn_split_tp(int T) { return (T + 31) & ~31; }
+static inline int crn_split_smem_words(int W, int M, int n_pairs) {
+    const int T = n_pairs * M, Tp = crn_split_tp(T), hw = (W + 1) / 2;
+    return 4 * W * Tp + 8 * hw * Tp + 48 * Tp + 16 * n_pairs;
+}
+static inline int crn_split_tmem_cols(int W, int M, int n_pairs) {
+    const int Tp = crn_split_tp(n_pairs * M), hw = (W + 1) / 2;
+    return ((2 * Tp + 127) / 128) * 10 * hw;
+}
+static inline int crn_split_fits(int W, int M, int n_pairs) {
+    return n_pairs * M <= CRN_CTA_THREADS && crn_split_smem_words(W, M, n_pairs) <= CRN_SMEM_WORDS &&
+           crn_split_tmem_cols(W, M, n_pairs) <= CRN_TMEM_COLS;
+}
+
 /* Max CBs per TB accepted by crn_tb_verdict_batch (LTE needs <= 64). */
 #define CRN_TB_MAX_CB 128
 
@@ -35,11 +60,10 @@ typedef struct {
     const uint32_t *qpp_wm;   /* per K at qpp_off[kidx]: [i*M + j] = (Pi(jW+i) % W) << 16 | Pi(jW+i) / W */
     const uint32_t *qpp_ts;   /* same index: (Pi(jW+i) % W) * CRN_CTA_THREADS + Pi(jW+i) / W (fast path) */
     const uint32_t *qinv_ts;  /* same index, inverse permutation: m = Pi^-1(jW+i) -> (m % W) * CRN_CTA_THREADS + m / W */
-    const uint32_t *crc_pow;  /* per K at crc_off[kidx]: [kind(0=A,1=B)*M + j] = x^((M-1-j)W) mod g */
+    const uint32_t *qinv_wm;  /* same index, inverse permutation in the qpp_wm format: (m % W) << 16 | m / W */
     const uint32_t *crc_bit;  /* per K at crcb_off[kidx]: [kind(0=A,1=B)*K + i*M + j] = x^(K-1-n+24) mod g, n = jW+i:
                                  the CRC register contribution of a 1 at bit n (register = XOR over the set bits) */
     const int32_t *qpp_off;
-    const int32_t *crc_off;
     const int32_t *crcb_off;
 } crn_tables;
 

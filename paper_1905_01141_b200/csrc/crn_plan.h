@@ -9,8 +9,9 @@
 #include "crn_internal.h"
 
 struct DevTables {
-    uint32_t *qpp_wm = nullptr, *qpp_ts = nullptr, *qinv_ts = nullptr, *crc_pow = nullptr, *crc_bit = nullptr;
-    int32_t *qpp_off = nullptr, *crc_off = nullptr, *crcb_off = nullptr;
+    uint32_t *qpp_wm = nullptr, *qpp_ts = nullptr, *qinv_ts = nullptr, *crc_bit = nullptr,
+             *qinv_wm = nullptr;
+    int32_t *qpp_off = nullptr, *crcb_off = nullptr;
     crn_tables tab{};
     int grid = 0;
 };
