@@ -386,23 +386,39 @@ __device__ __forceinline__ void load16(const int16_t *__restrict__ src, u32 w[HW
     }
 }
 
+/* Shared load at the packed gather address of constituent c (c = 0: low 16 bits,
+ * c = 1: high 16 bits); the halves are split with IMAD-pipe arithmetic so the
+ * ALU pipe, the kernel's bottleneck, is not used. */
+__device__ __forceinline__ u32 lds_q(u32 qq, int c) {
+    const u32 hi = __umulhi(qq, 0x10000u);
+    const u32 a = c ? hi : qq - hi * 0x10000u;
+    u32 v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
 /* One half-iteration of constituent c (rows a5-a8).  Le -> Y (c = 0, natural
  * order) or Z (c = 1, interleaved order). */
 template <bool SCALE>
-__device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, int it, const u32 (&q)[HW],
-                                           const u32 *la, bool zero_la) {
+__device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, int it, const u32 (&qq)[HW],
+                                           bool zero_la) {
     uint2 *ch = reinterpret_cast<uint2 *>(f.sm + S_CH) + f.tid;
     const u32 *lp = f.sm + S_LP + c * SUMK + f.k0 * TS + f.t;
     /* row a4 fused into phase 1: this thread's 16 (Lu+Lp, Lu-Lp) pairs are formed
      * step by step from the TMEM static sums, the parity plane and the a-priori
      * LLRs gathered at its QPP indices, used at once and kept in smem for phase 2 */
     u32 av[HW], pv[HW], sn[HW];
-#pragma unroll
-    for (int s = 0; s < HW; s++) {
-        av[s] = zero_la ? 0u : la[q[s]];
-        pv[s] = lp[s * TS];
-    }
     tm_load16_wait(f.ts + c * HW, sn);
+    /* the 32 shared loads are issued LA steps ahead of their use, in processing
+     * order (volatile asm keeps that order against the TMEM stores), so the
+     * warps do not all queue 32 loads at the phase start */
+    constexpr int LA = 2;
+    const u32 lp_s = smem_addr(lp);
+    auto ld = [&](int s) {
+        if (zero_la) av[s] = 0u;
+        else av[s] = lds_q(qq[s], c);
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pv[s]) : "r"(lp_s + 4 * s * TS));
+    };
     u32 *nii = f.sm + S_NII;
     u32 *X = f.sm + S_X;
     u32 *le = f.sm + (c ? S_Z : S_Y) + f.t;
@@ -421,7 +437,10 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
             for (int s = 0; s < NS; s++) m[s] = nii[nii1_ix(c, 0, s, f.t - 1)];
         }
 #pragma unroll
+        for (int s = 0; s < LA; s++) ld(s);
+#pragma unroll
         for (int s = 0; s < HW; s++) {          /* store alpha_s, advance to alpha_{s+1} */
+            if (s + LA < HW) ld(s + LA);
             const u32 d = vadd(sn[s], av[s]);                /* Lu - Lp */
             const u32 x = vadd(vadd(d, pv[s]), pv[s]);       /* Lu + Lp */
             ch[s * BLOCK] = make_uint2(x, d);
@@ -443,7 +462,10 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
             for (int s = 0; s < NS; s++) m[s] = nii[nii1_ix(c, 1, s, f.t + 1)];
         }
 #pragma unroll
+        for (int s = HW - 1; s >= HW - LA; s--) ld(s);
+#pragma unroll
         for (int s = HW - 1; s >= 0; s--) {     /* store beta_{17+s}, advance to beta_{16+s} */
+            if (s - LA >= 0) ld(s - LA);
             const u32 d = vadd(sn[s], av[s]);
             const u32 x = vadd(vadd(d, pv[s]), pv[s]);
             ch[s * BLOCK] = make_uint2(x, d);
@@ -535,6 +557,8 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
      * the shared planes, Ls-Lp1 (natural) and Ls[Pi]-Lp2 (interleaved) into
      * TMEM; the thread's QPP word indices stay in registers for the task */
     u32 q1[HW], q2[HW];     /* pM + position of Pi^-1(jW+k) (DEC1 gather) / Pi(jW+k) (DEC2 gather) */
+    u32 qq[HW];             /* for the task: shared byte addresses of the DEC1 gather (Z, low half) and
+                               the DEC2 gather (Y, high half); both < 64 KiB */
     {
         const int p = f.p, j = f.j;
         const int clo = sh.cb[2 * p], chi = sh.cb[2 * p + 1];
@@ -622,6 +646,11 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
 #pragma unroll
         for (int s = 0; s < HW; s++)          /* interleaved systematic Ls[Pi(jW+k)] */
             sn[s] = __vsub2(tmp[q2[s]], sm[S_LP + SUMK + (f.k0 + s) * TS + f.t]);
+        {
+            const u32 base = smem_addr(sm);
+#pragma unroll
+            for (int s = 0; s < HW; s++) qq[s] = (base + 4 * (S_Z + q1[s])) | ((base + 4 * (S_Y + q2[s])) << 16);
+        }
         tm_store16(f.ts + HW, sn);
         tm_wait_st();
         __syncthreads();
@@ -631,13 +660,13 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
     for (int it = 1; it <= max_iters; it++) {
         /* DEC1: La1[n] = Le2[Pi^-1(n)] gathered from Z (zero in iteration 1) */
         prof_mark(P_CHUNK);
-        siso_split<SCALE>(f, tail_thr, 0, it, q1, sm + S_Z, it == 1);
+        siso_split<SCALE>(f, tail_thr, 0, it, qq, it == 1);
         prof_mark(P_PH2);
         __syncthreads();
         prof_mark(P_BAR2);
         /* DEC2: La2[i] = Le1[Pi(i)] gathered from Y */
         prof_mark(P_CHUNK);
-        siso_split<SCALE>(f, tail_thr, 1, it, q2, sm + S_Y, false);
+        siso_split<SCALE>(f, tail_thr, 1, it, qq, false);
         prof_mark(P_PH2);
         __syncthreads();
         prof_mark(P_BAR2);
@@ -651,7 +680,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             tm_load16_wait(f.ts, sn);
 #pragma unroll
             for (int s = 0; s < HW; s++) {
-                const u32 la1n = sm[S_Z + q1[s]];                    /* La1_next[n] = Le2[Pi^-1(n)] */
+                const u32 la1n = lds_q(qq[s], 0);                    /* La1_next[n] = Le2[Pi^-1(n)] */
                 const u32 ls = vadd(sn[s], sm[S_LP + (f.k0 + s) * TS + f.t]);
                 const u32 lapp = vadd(vadd(ls, sm[S_Y + (f.k0 + s) * TS + f.t]), la1n);
                 const u32 ge = __vcmpges2(lapp, 0u);
@@ -697,7 +726,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                     if (ext_out) {
 #pragma unroll
                         for (int s = 0; s < HW; s++) {
-                            const u32 x = sm[S_Z + q1[s]];
+                            const u32 x = lds_q(qq[s], 0);
                             ext_out[d.ext_off + j * W + f.k0 + s] = (int16_t)(l ? (x >> 16) : (x & 0xFFFFu));
                         }
                     }
