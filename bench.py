@@ -1,9 +1,11 @@
 #!/usr/bin/env python
 """Benchmark of the hot path: batched LTE turbo decoding on B200 (libcrn).
 
-A step = one decode of this rank's shard of BASELINE.json config 4 (65,536
+A step = one decode of this rank's batch of BASELINE.json config 4 (65,536
 code blocks of K=6144, BPSK/AWGN at Eb/N0 = 1.0 dB, int16 LLRs, 8 fixed
-iterations; 256 cells x 256 CBs, cells sharded evenly over the ranks).
+iterations; 256 cells x 256 CBs).  Multi-GPU shards by cell with no
+data-path collective: by default every rank serves its own 256 cells (weak
+scaling, R27); --scaling strong splits cfg4's 256 cells instead.
 Prints ONE JSON line on rank 0.  See DESIGN.md "measurement".
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {crn,reference}]
@@ -38,15 +40,20 @@ def _dist():
     return ws, rank, local
 
 
-def _workload_name(iters):
-    return f"cfg4: 65536 CBs (256 cells x 256) K=6144, BPSK Eb/N0=1.0 dB, int16 LLR, {iters} fixed iterations"
+def _workload_name(iters, ws=1, scaling="weak"):
+    if scaling == "weak":
+        return (f"cfg4 per GPU: 65536 CBs (256 cells x 256 CBs) K=6144 on each of {ws} GPU(s), cells disjoint "
+                f"across ranks, BPSK Eb/N0=1.0 dB, int16 LLR, {iters} fixed iterations")
+    return (f"cfg4: 65536 CBs (256 cells x 256) K=6144 sharded by cell over {ws} GPU(s), BPSK Eb/N0=1.0 dB, "
+            f"int16 LLR, {iters} fixed iterations")
 
 
 class ClockSampler:
     """NVML SM clock + throttle reasons sampled during the timed region."""
 
-    def __init__(self, index):
+    def __init__(self, index, interval=None):
         self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.interval = interval if interval is not None else float(os.environ.get("BENCH_CLK_INTERVAL", "0.1"))
         self._stop = threading.Event()
         self._idx = index
         self._t = None
@@ -71,7 +78,7 @@ class ClockSampler:
                         self.reasons |= {k for k, v in names.items() if r & v and k != "gpu_idle"}
                     except Exception:
                         pass
-                    time.sleep(0.02)
+                    time.sleep(self.interval)
 
             self._t = threading.Thread(target=run, daemon=True)
             self._t.start()
@@ -155,8 +162,8 @@ def run_reference(args):
     cb["value"] = v
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Mbit/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(times),
-           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int16",
-           "data": "synthetic", "config": {"workload": _workload_name(args.iters) + f" -- bounded sample of "
+           "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int16",
+           "data": "synthetic", "config": {"workload": _workload_name(args.iters, 1, args.scaling) + f" -- bounded sample of "
                                                                               f"{args.ref_sample} CBs per step",
                                             "parallelism": "CPU threads (oracle)"},
            "cpu_baseline": cb, "e2e": {"value": v, "unit": "Mbit/s", "h2d_bytes_per_step": 0,
@@ -233,7 +240,10 @@ def run_crn(args):
     crn_build.build()
     dev = crn.device_info()
 
-    cells = shard.cells_for_rank(rank, ws, N_CELLS)
+    if args.scaling == "weak":      # DESIGN.md R27: every rank serves its own 256 cells (a full cfg4 batch)
+        cells = list(range(rank * N_CELLS, (rank + 1) * N_CELLS))
+    else:                           # cfg4's fixed 256 cells split over the ranks
+        cells = shard.cells_for_rank(rank, ws, N_CELLS)
     wl = wlmod.make_workload(CFG, seed=args.seed, cells=cells, device="cuda")
     b = bmod.build(wl)
     del wl.payload
@@ -332,9 +342,9 @@ def run_crn(args):
             if clocks.get("sm_mhz") else None}
     out = {
         "metric": METRIC, "value": value, "unit": "Mbit/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "int16", "data": "synthetic",
-        "config": {"workload": _workload_name(iters), "n_cb": n_cb, "cb_per_rank": b.n_cb,
+        "config": {"workload": _workload_name(iters, ws, args.scaling), "n_cb": n_cb, "cb_per_rank": b.n_cb,
                    "iters": iters, "seed": args.seed,
                    "l2": f"inputs {in_bytes / 1e9:.2f} GB per rank > L2 {L2_BYTES / 2**20:.0f} MiB: no flush needed",
                    "parallelism": f"dp{ws} (cells sharded, no data-path collective)",
@@ -367,6 +377,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="crn", choices=["crn", "reference"])
     ap.add_argument("--iters", type=int, default=8)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: each rank decodes its own full cfg4 batch (default); strong: cfg4 split over ranks")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ref-sample", type=int, default=2048,
                     help="CBs of the oracle's bounded sample (cpu_baseline / --impl reference)")
