@@ -26,7 +26,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so with plain gcc -O2 (scalar C11, no intrinsics)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-fPIC", "-shared", "-pthread",
-                               "-o", _SO, _SRC])
+                               "-o", _SO, _SRC, "-lm"])
     return _SO
 
 
@@ -61,6 +61,8 @@ def lib():
         L.oracle_decode_cb_v.argtypes = [i16p, i16p, i16p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.c_int, C.c_int, u8p, u8p, u8p, i16p, u64p]
         L.oracle_decode_cb_v.restype = C.c_int64
+        L.oracle_mi_table.argtypes = [C.c_int32]
+        L.oracle_mi_table.restype = C.c_int32
         L.oracle_ext_scale.argtypes = [C.c_int32]
         L.oracle_ext_scale.restype = C.c_int32
         L.oracle_decode_batch.argtypes = [C.c_int, i32p, i32p, i32p, i64p, i64p, i16p, i16p, i16p,
@@ -207,6 +209,13 @@ def nii_update(alpha_out, beta_out):
 
 
 VAR_MAXLOG, VAR_SCALED = 0, 1
+ET_NONE, ET_CRC, ET_MI = 0, 1, 2
+MI_EPS = 66
+
+
+def mi_table(a: int) -> int:
+    """Q16 MI of an LLR of magnitude a/8 (R29)."""
+    return int(lib().oracle_mi_table(int(a)))
 
 
 def ext_scale(x: int) -> int:

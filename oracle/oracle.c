@@ -17,6 +17,7 @@
  * operand is the literal-zero branch metric of the (u,z) = (0,0) branch.
  */
 #include "oracle.h"
+#include <math.h>
 #include <pthread.h>
 #include <stdatomic.h>
 #include <stdlib.h>
@@ -378,6 +379,19 @@ static int32_t scale34(int32_t x) {
 
 int32_t oracle_ext_scale(int32_t x) { return scale34(x); }
 
+/* MI of an LLR of magnitude a/8 (the channel quantiser's scale, R9)
+ * under the consistent-Gaussian assumption: I = 1 - Hb(p), p = 1/(1+e^(a/8)),
+ * Hb the binary entropy; in Q16, a saturated at 255 (R29). */
+int32_t oracle_mi_table(int32_t a) {
+    if (a < 0) return -1;
+    if (a > 255) a = 255;
+    const double L = a / 8.0;
+    const double p = 1.0 / (1.0 + exp(L));            /* probability of the less likely value */
+    const double q = 1.0 - p;
+    const double h = (p > 0 ? -p * log2(p) : 0.0) + (q > 0 ? -q * log2(q) : 0.0);
+    return (int32_t)floor(65536.0 * (1.0 - h) + 0.5);
+}
+
 int64_t oracle_decode_cb(const int16_t *d0, const int16_t *d1, const int16_t *d2,
                          int K, int F, int crc_kind, int max_iters, int early_term, int wmin,
                          uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
@@ -391,7 +405,7 @@ int64_t oracle_decode_cb_v(const int16_t *d0, const int16_t *d1, const int16_t *
                            uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
                            int16_t *ext, uint64_t *ops) {
     if (k_row(K) < 0 || F < 0 || F > K - 25 || max_iters < 1 || crc_kind < 0 || crc_kind > 2 ||
-        variant < 0 || variant > 1)
+        variant < 0 || variant > 1 || early_term < 0 || early_term > 2)
         return -1;
     int64_t viol = 0;
     int W = K / oracle_num_windows(K, wmin), M = K / W;
@@ -423,6 +437,7 @@ int64_t oracle_decode_cb_v(const int16_t *d0, const int16_t *d1, const int16_t *
     for (int i = 0; i < K; i++) Ls2[i] = Ls[Pi[i]];
 
     int t_used = 0, pass = 0;
+    int64_t mi_prev = 0;
     for (int it = 1; it <= max_iters; it++) {
         t_used = it;
         /* DEC1: R(b_i), R(b_i)' and the a-priori La1 -> extrinsic Le1 */
@@ -438,13 +453,19 @@ int64_t oracle_decode_cb_v(const int16_t *d0, const int16_t *d1, const int16_t *
         for (int i = 0; i < K; i++) La1n[Pi[i]] = Le2[i];
         for (int q = 0; q < 2; q++) oracle_nii_update(M, a_new[q], b_new[q], a_prev[q], b_prev[q]);
         /* hard decision on L_APP = Ls + Le1 + La1_next; tie -> 1 (R16) */
+        int64_t mi = 0;                       /* average-MI statistic of the L_APP (R29) */
         for (int n = 0; n < K; n++) {
             int32_t lapp = Ls[n] + Le1[n] + La1n[n];
             if (lapp < -32768 || lapp > 32767) viol++;
             bits[n] = (uint8_t)(n < F ? 0 : (lapp >= 0 ? 1 : 0));
+            if (n >= F) mi += oracle_mi_table(lapp < 0 ? -lapp : lapp);
         }
         pass = (crc_kind != ORACLE_CRC_NONE) && oracle_crc24(crc_kind, bits, K) == 0;
-        if (early_term && pass) break;        /* stopping rule (R3) */
+        if (early_term == ORACLE_ET_CRC && pass) break;     /* stopping rule (R3) */
+        /* the paper's rule: stop once the average mutual information of
+         * the LLRs has converged, |S_t - S_{t-1}| <= (K - F) * eps, from iteration 2 on */
+        if (early_term == ORACLE_ET_MI && it >= 2 && llabs(mi - mi_prev) <= (int64_t)(K - F) * ORACLE_MI_EPS) break;
+        mi_prev = mi;
         memcpy(La1, La1n, 4 * nK);
     }
     *crc_ok = (uint8_t)pass;

@@ -33,6 +33,12 @@ enum { ORACLE_CRC_NONE = 0, ORACLE_CRC24A = 1, ORACLE_CRC24B = 2 };
  * the scaled-extrinsic max-log-MAP of SURVEY.md §8(f) f2 (R28): each
  * SISO's extrinsic Le = clamp(L1 - L0, +-4096) is handed on as floor(3 Le / 4). */
 enum { ORACLE_VAR_MAXLOG = 0, ORACLE_VAR_SCALED = 1 };
+/* Stopping rules (early_term): none (fixed iterations), CRC (R3), or
+ * the paper's average-MI convergence (R29). */
+enum { ORACLE_ET_NONE = 0, ORACLE_ET_CRC = 1, ORACLE_ET_MI = 2 };
+#define ORACLE_MI_EPS 66   /* per-bit MI change threshold in Q16 (about 0.001) */
+/* Q16 MI of an LLR of magnitude a/8, a saturated at 255 (R29); -1 for a < 0. */
+int32_t oracle_mi_table(int32_t a);
 
 /* Number of supported interleaver sizes (188 sizes 40..6144). */
 int oracle_num_k(void);
@@ -89,8 +95,10 @@ void oracle_nii_update(int M, const int32_t *alpha_out, const int32_t *beta_out,
  *   d0,d1,d2 : the K+4 received int16 LLRs of each stream (positive => bit 1)
  *   F        : number of leading filler bits (known 0)
  *   crc_kind : ORACLE_CRC_NONE / 24A / 24B (the check used for ET and crc_ok)
- *   max_iters: I >= 1;  early_term: stop after the first full iteration whose
- *              hard decision passes the CRC
+ *   max_iters: I >= 1;  early_term: ORACLE_ET_CRC stops after the first full
+ *              iteration whose hard decision passes the CRC; ORACLE_ET_MI after the
+ *              first iteration t >= 2 whose MI statistic sum_{n>=F} mi_table(|L_APP_n|)
+ *              moved by at most (K-F)*ORACLE_MI_EPS from iteration t-1
  *   wmin     : minimum window length (32 in the product definition; K forces M = 1)
  * Outputs: bits[K] (0/1 per byte), *crc_ok, *iters_used, ext[K] (La1_next of
  * the last iteration, natural order), *ops (counted ops, accumulated).

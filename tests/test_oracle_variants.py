@@ -1,6 +1,7 @@
-"""Pins of the oracle's scaled-extrinsic max-log-MAP variant (SURVEY.md §8(f)
-f2, R28): the extrinsic each SISO hands on is floor(3 Le / 4).
-CPU only.
+"""Pins of the oracle's decoder variants, CPU only:
+the scaled-extrinsic max-log-MAP (R28: the extrinsic each SISO
+hands on is floor(3 Le / 4)) and the paper's average-MI stopping rule
+(R29).  Scaled variant:
 
 * the scaling map against the definition of the floor (4 s <= 3x < 4 s + 4);
 * one iteration equals the composition of the brute-force-pinned SISO
@@ -8,6 +9,11 @@ CPU only.
 * noiseless round trips, zero-evidence failure, int16 safety, ET prefix;
 * the known behaviour of scaling max-log-MAP extrinsics (it offsets the
   max-log over-estimate): fewer block errors and iterations at the same Eb/N0.
+MI rule: its table against the definition of binary entropy (via a second
+closed form) and special values; libcrn's independent table equals it; the
+rule never stops at iteration 1, stops at 2 when the statistic is saturated
+(noiseless) or identically 0 (no evidence); an MI-stopped run is a prefix of
+the fixed-iteration run.
 """
 import numpy as np
 import pytest
@@ -90,3 +96,56 @@ def test_scaling_lowers_bler_and_iterations(orc):
                              max_iters=8, early_term=True, nthreads=4, variant=v, want_ext=False)
         res.append((1 - r["crc_ok"].mean(), r["iters"].mean()))
     assert res[1][0] < res[0][0] and res[1][1] < res[0][1], res
+
+
+# ---------------------------------------------------------------- MI stopping rule (R29)
+def test_mi_table_pins(orc):
+    """Q16 MI of a consistent LLR of magnitude a/8: I(0) = 0 exactly (a fair coin
+    carries no information), nondecreasing, saturating at 1, and equal (to one
+    Q16 unit) to the identity I(L) = 1 - log2(1 + e^L) + (L / ln 2) e^L / (1 + e^L),
+    a different closed form of 1 - Hb(1 / (1 + e^L))."""
+    import math
+    t = np.array([orc.mi_table(a) for a in range(256)])
+    assert t[0] == 0 and t[255] == 65536 and np.all(np.diff(t) >= 0)
+    assert orc.mi_table(1000) == t[255] and orc.mi_table(-1) == -1
+    for a in range(256):
+        L = a / 8.0
+        alt = 1.0 - math.log2(1.0 + math.exp(L)) + (L / math.log(2.0)) * math.exp(L) / (1.0 + math.exp(L))
+        assert abs(t[a] - 65536.0 * alt) <= 1.0, a
+    # I(L) for L = 1 (a = 8): 1 - Hb(0.268941...) = 0.16007...
+    assert abs(t[8] / 65536.0 - 0.16007) < 1e-4
+
+
+def test_mi_table_product_equals_oracle(orc):
+    """libcrn computes the same table independently (crn_mi_table, host side)."""
+    from paper_1905_01141_b200 import crn
+    assert np.array_equal(crn.mi_table(), np.array([orc.mi_table(a) for a in range(256)], np.int32))
+
+
+def test_mi_stop_special_cases(orc):
+    rng = np.random.default_rng(7)
+    for K in (40, 1056):
+        c = orc.crc_attach(orc.CRC24B, rng.integers(0, 2, K - 24, dtype=np.uint8))
+        r = orc.decode_cb(*_noiseless(orc, c, 4096), max_iters=8, early_term=orc.ET_MI)
+        assert r["iters"] == 2 and r["crc_ok"] == 1 and np.array_equal(r["bits"], c)   # saturated from t=1
+        z = [np.zeros(K + 4, np.int16)] * 3
+        r = orc.decode_cb(*z, max_iters=8, early_term=orc.ET_MI)
+        assert r["iters"] == 2 and r["crc_ok"] == 0          # the MI stays 0: converged, CB lost
+        r = orc.decode_cb(*z, max_iters=1, early_term=orc.ET_MI)
+        assert r["iters"] == 1
+
+
+def test_mi_stop_is_prefix_of_fixed(orc):
+    wl = wlmod.make_workload(5, seed=6)
+    cbs, ll = oracle_llrs(wl)
+    lo, _ = offsets([cb["K"] for cb in cbs])
+    its = []
+    for cb, o in list(zip(cbs, lo))[:60]:
+        K = cb["K"]
+        x = [t[o:o + K + 4].numpy() for t in ll]
+        r = orc.decode_cb(*x, F=cb["F"], crc_kind=cb["crc"], max_iters=8, early_term=orc.ET_MI)
+        f = orc.decode_cb(*x, F=cb["F"], crc_kind=cb["crc"], max_iters=r["iters"])
+        assert np.array_equal(r["bits"], f["bits"]) and np.array_equal(r["ext"], f["ext"])
+        assert r["crc_ok"] == f["crc_ok"] and r["iters"] >= 2
+        its.append(r["iters"])
+    assert min(its) < 8                                       # it does stop early somewhere
