@@ -43,6 +43,16 @@ enum { CRN_EXT_SCALED = 2 };               /* flag bit 1: scaled-extrinsic varia
  * a-priori inputs, L_APP and ext_out all use the scaled value (R28). */
 enum { CRN_VARIANT_MAXLOG = 0, CRN_VARIANT_SCALED = 1 };
 enum { CRN_MAX_ITERS = 32, CRN_KMIN = 40, CRN_KMAX = 6144 };
+/* Stopping rules (the early_term argument of every decode entry point):
+ * CRN_ET_NONE runs max_iters iterations; CRN_ET_CRC stops a CB after the first
+ * full iteration whose hard decision passes its CRC (R3, R18);
+ * CRN_ET_MI is the paper's rule ("the average mutual information
+ * of LLR, if it converges the decoding process may terminate earlier"): after
+ * each full iteration t the CB's statistic S_t = sum over non-filler n of
+ * crn_mi_table[min(|L_APP(n)|, 255)] is formed, and the CB stops at the first
+ * t >= 2 with |S_t - S_{t-1}| <= (K - F) * 66 (a per-bit MI change of about
+ * 0.001 in Q16; R29). */
+enum { CRN_ET_NONE = 0, CRN_ET_CRC = 1, CRN_ET_MI = 2 };
 
 /* Per-CB descriptor (the paper's CCDU at CB granularity).
  *   K        interleaver size, one of the 188 LTE sizes 40..6144
@@ -79,8 +89,8 @@ int crn_decode_batch(const int16_t *llr_sys, const int16_t *llr_p1, const int16_
 /* General form.  desc: n_cb descriptors in HOST memory (copied during the
  * call), or in DEVICE memory if flags & CRN_DESC_ON_DEVICE (then they are
  * validated on the device; an invalid one yields crc_ok = 0, iters_used = 0).
- * max_iters in [1,32]; early_term != 0 stops a CB after the first full
- * iteration whose hard decision passes its CRC (R3, R18).
+ * max_iters in [1,32]; early_term one of CRN_ET_NONE / CRN_ET_CRC / CRN_ET_MI
+ * (above; CRN_EINVAL otherwise).
  * Outputs (device memory): out_bits (required), crc_ok[n_cb] (required),
  * iters_used[n_cb] (may be NULL; full iterations executed, R17), ext_out
  * (may be NULL; int16 La1_next of the last iteration in natural order, R15).
@@ -250,6 +260,11 @@ uint32_t crn_crc24b(const uint8_t *bits, int64_t nbits);
 const char *crn_strerror(int code);
 /* Text of the last CUDA failure seen by this thread inside libcrn ("" if none). */
 const char *crn_last_error(void);
+
+/* The MI stopping rule's table (host computation, no device needed): out[a] =
+ * round(65536 * (1 - Hb(1 / (1 + e^(a/8))))) for a = 0..255, the mutual
+ * information of a consistent LLR of magnitude a/8 (R29). */
+int crn_mi_table(int32_t *out);
 
 /* ------------------------------------------------------------------ device facts / microbench */
 

@@ -21,6 +21,7 @@ CRC_NONE, CRC24A, CRC24B = 0, 1, 2
 DESC_ON_DEVICE = 1
 EXT_SCALED = 2
 VARIANT_MAXLOG, VARIANT_SCALED = 0, 1
+ET_NONE, ET_CRC, ET_MI = 0, 1, 2
 
 DESC_DTYPE = np.dtype([("K", "<i4"), ("F", "<i4"), ("crc_kind", "<i4"), ("reserved", "<i4"),
                        ("llr_off", "<i8"), ("bit_off", "<i8"), ("ext_off", "<i8")])
@@ -77,6 +78,7 @@ _SIGS = {
     "crn_strerror": (C.c_char_p, [C.c_int]),
     "crn_last_error": (C.c_char_p, []),
     "crn_device_info": (C.c_int, [i32p, i32p, i32p, i32p]),
+    "crn_mi_table": (C.c_int, [i32p]),
     "crn_decode_kernel_info": (C.c_int, [i32p, i32p, i32p, i32p]),
     "crn_ubench_int16x2": (C.c_int, [C.c_int32, i64p, P(C.c_float), i64p]),
 }
@@ -308,6 +310,12 @@ def crc24b(bits) -> int:
 
 def strerror(code: int) -> str:
     return lib().crn_strerror(code).decode()
+
+
+def mi_table() -> np.ndarray:
+    out = np.zeros(256, np.int32)
+    _chk(lib().crn_mi_table(_np(out, C.c_int32)), "crn_mi_table")
+    return out
 
 
 def device_info() -> dict:

@@ -71,7 +71,7 @@ constexpr int S_WORDS = S_TAIL + MAXP * 16;
 static_assert(S_CH % 2 == 0, "chunk array must be 8-byte aligned");
 constexpr int SMEM_WORDS = S_WORDS;
 static_assert(SMEM_WORDS == CRN_SMEM_WORDS, "split-window sizing (crn_internal.h) must see the same shared memory");
-static_assert(SMEM_WORDS * 4 + 6400 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
+static_assert(SMEM_WORDS * 4 + 8704 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
 
 /* ---- optional phase profiler (build with -DCRN_PHASE_PROF; never in the product
  * build): lane 0 of warp 0 (a head warp) and of warp 6 (a tail warp) attribute
@@ -262,8 +262,18 @@ __device__ __forceinline__ u32 clamp_pack(int16_t lo, int16_t hi) {
 /* fast path (shared memory, single-buffered): [c][alpha(0)/beta(1)][s][WMAX] */
 __device__ __forceinline__ int nii1_ix(int c, int ab, int s, int t) { return ((c * 2 + ab) * NS + s) * WMAX + t; }
 
+/* Q16 MI contribution of the two L_APP halves of a word (fillers excluded by the
+ * caller's masks): table[min(|L|, 255)] per half (R29). */
+__device__ __forceinline__ int mi_pair(const int *tab, u32 lapp, bool use_lo, bool use_hi) {
+    const int lo = (int)(int16_t)(lapp & 0xFFFFu), hi = (int)(int16_t)(lapp >> 16);
+    const int alo = min(lo < 0 ? -lo : lo, 255), ahi = min(hi < 0 ? -hi : hi, 255);
+    return (use_lo ? tab[alo] : 0) + (use_hi ? tab[ahi] : 0);
+}
+
 struct TaskSh {
     int *cb, *F, *kind;
+    int *mi, *mip;              /* per CB: average-MI statistic of this / the previous iteration (R29) */
+    const int *mitab;           /* Q16 MI of |L_APP| = 0..255 (the tables' mi_tab, staged in smem) */
     uint8_t *done, *fin;
     u32 *crc;
     int *left;
@@ -271,12 +281,16 @@ struct TaskSh {
 
 /* Row a9 bookkeeping after the CRC reduction: completion / early termination
  * per CB, CRC flag and iteration count.  Returns after the barrier. */
-__device__ __forceinline__ void decide(TaskSh sh, int NP, int it, int max_iters, int et, uint8_t *crc_ok,
+__device__ __forceinline__ void decide(TaskSh sh, int NP, int it, int max_iters, int et, int K, uint8_t *crc_ok,
                                        uint8_t *iters_used) {
     for (int e = threadIdx.x; e < 2 * NP; e += BLOCK) {
         if (sh.done[e]) continue;
         const bool pass = sh.kind[e] != CRN_CRC_NONE && sh.crc[e] == 0;
-        if ((et && pass) || it == max_iters) {
+        /* stopping rules: CRC (R3) or the paper's MI convergence (R29) */
+        const int dmi = sh.mi[e] - sh.mip[e];
+        const bool mi_conv = et == CRN_ET_MI && it >= 2 && (dmi < 0 ? -dmi : dmi) <= (K - sh.F[e]) * CRN_MI_EPS;
+        sh.mip[e] = sh.mi[e];
+        if ((et == CRN_ET_CRC && pass) || mi_conv || it == max_iters) {
             sh.fin[e] = 1;
             sh.done[e] = 1;
             crc_ok[sh.cb[e]] = pass;
@@ -294,7 +308,7 @@ __device__ __forceinline__ int finish_iteration(TaskSh sh, int NP) {
         *sh.left = left;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < 2 * NP; e += BLOCK) { sh.fin[e] = 0; sh.crc[e] = 0; }
+    for (int e = threadIdx.x; e < 2 * NP; e += BLOCK) { sh.fin[e] = 0; sh.crc[e] = 0; sh.mi[e] = 0; }
     const int left = *sh.left;
     __syncthreads();
     return left;
@@ -676,8 +690,10 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
          * thread and CB lane, merged per window; windowed CRC */
         {
             u32 wlo = 0, whi = 0;
+            int mlo = 0, mhi = 0;             /* MI statistic of this thread's steps (R29) */
             u32 sn[HW];
             tm_load16_wait(f.ts, sn);
+            const int n00 = f.j * W + f.k0, Fl = sh.F[2 * f.p], Fh = sh.F[2 * f.p + 1];
 #pragma unroll
             for (int s = 0; s < HW; s++) {
                 const u32 la1n = lds_q(qq[s], 0);                    /* La1_next[n] = Le2[Pi^-1(n)] */
@@ -686,11 +702,19 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                 const u32 ge = __vcmpges2(lapp, 0u);
                 wlo |= (ge & 1u) << s;
                 whi |= ((ge >> 16) & 1u) << s;
+                if (et == CRN_ET_MI) {
+                    mlo += mi_pair(sh.mitab, lapp, n00 + s >= Fl, false);
+                    mhi += mi_pair(sh.mitab, lapp, false, n00 + s >= Fh);
+                }
             }
             u32 *hb = sm + S_X;               /* [half][lo/hi][window] */
             if (active) {
                 hb[((tail_thr ? 2 : 0) + 0) * TS + f.t] = wlo;
                 hb[((tail_thr ? 2 : 0) + 1) * TS + f.t] = whi;
+                if (et == CRN_ET_MI) {
+                    atomicAdd(&sh.mi[2 * f.p], mlo);
+                    atomicAdd(&sh.mi[2 * f.p + 1], mhi);
+                }
             }
             __syncthreads();
             if (active && !tail_thr) {
@@ -715,7 +739,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                 }
             }
             __syncthreads();
-            decide(sh, NP, it, max_iters, et, crc_ok, iters_used);
+            decide(sh, NP, it, max_iters, et, tk.K, crc_ok, iters_used);
             if (active) {
                 const int p = f.p, j = f.j;
 #pragma unroll
@@ -985,6 +1009,7 @@ __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_des
         for (int e = tid; e < 2 * NP * nw; e += BLOCK) bits[e] = 0;
         __syncthreads();
         u32 blo = 0, bhi = 0;
+        int mlo = 0, mhi = 0;                   /* MI statistic (R29) */
         if (working) {                          /* TMEM loads are warp-collective: every lane of a working warp */
 #pragma unroll 1
             for (int s = 0; s < hw; s++) {
@@ -994,7 +1019,15 @@ __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_des
                 const u32 ge = __vcmpges2(lapp, 0u);
                 blo |= (n < Flo ? 0u : (ge & 1u)) << s;
                 bhi |= (n < Fhi ? 0u : ((ge >> 16) & 1u)) << s;
+                if (et == CRN_ET_MI) {
+                    mlo += mi_pair(sh.mitab, lapp, n >= Flo, false);
+                    mhi += mi_pair(sh.mitab, lapp, false, n >= Fhi);
+                }
             }
+        }
+        if (active && et == CRN_ET_MI) {
+            atomicAdd(&sh.mi[2 * p], mlo);
+            atomicAdd(&sh.mi[2 * p + 1], mhi);
         }
         if (active) {
             const int n0 = j * W + k0, w0 = n0 >> 5, off = n0 & 31;
@@ -1014,7 +1047,7 @@ __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_des
             }
         }
         __syncthreads();
-        decide(sh, NP, it, max_iters, et, crc_ok, iters_used);
+        decide(sh, NP, it, max_iters, et, K, crc_ok, iters_used);
         for (int e = tid; e < 2 * NP * nw; e += BLOCK) {
             const int pl = e / nw, w = e - pl * nw;
             if (sh.fin[pl]) out_bits[desc[sh.cb[pl]].bit_off + w] = bits[e];
@@ -1092,10 +1125,12 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     __shared__ u32 s_crc[2 * MAXP];
     __shared__ int s_cb[2 * MAXP], s_F[2 * MAXP], s_kind[2 * MAXP];
     __shared__ uint8_t s_done[2 * MAXP], s_fin[2 * MAXP];
+    __shared__ int s_mi[2 * MAXP], s_mip[2 * MAXP], s_mitab[256];
 
     int *counter = (int *)ws;
     const int tid = threadIdx.x;
-    const TaskSh sh{s_cb, s_F, s_kind, s_done, s_fin, s_crc, &s_left};
+    const TaskSh sh{s_cb, s_F, s_kind, s_mi, s_mip, s_mitab, s_done, s_fin, s_crc, &s_left};
+    for (int i = tid; i < 256; i += BLOCK) s_mitab[i] = tab.mi_tab[i];
 
     /* TMEM: the whole 512 columns (one CTA per SM: the shared-memory footprint guarantees it) */
     if ((tid >> 5) == 0) {
@@ -1125,6 +1160,8 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             s_done[e] = cb < 0;
             s_fin[e] = 0;
             s_crc[e] = 0;
+            s_mi[e] = 0;
+            s_mip[e] = 0;
         }
         __syncthreads();                        /* next slots consumed */
         if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid);

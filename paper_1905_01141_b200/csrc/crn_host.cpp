@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -134,6 +135,21 @@ extern "C" int64_t crn_counted_ops(const int32_t *K, int32_t n_cb, const uint8_t
     return s;
 }
 
+/* ------------------------------------------------------------------ MI stopping rule */
+extern "C" int crn_mi_table(int32_t *out) {
+    /* I(L) = 1 - Hb(p), p = 1/(1 + e^L), L = a/8 (the channel quantiser's LLR scale), in
+     * Q16 rounded to nearest; the MI of a consistent Gaussian LLR of magnitude L
+     * ("average mutual information of LLR", R29) */
+    if (!out) return CRN_EINVAL;
+    for (int a = 0; a < 256; a++) {
+        const double L = a / 8.0;
+        const double p = 1.0 / (1.0 + std::exp(L)), q = 1.0 - p;
+        const double h = (p > 0 ? -p * std::log2(p) : 0.0) + (q > 0 ? -q * std::log2(q) : 0.0);
+        out[a] = (int32_t)std::floor(65536.0 * (1.0 - h) + 0.5);
+    }
+    return CRN_OK;
+}
+
 /* ------------------------------------------------------------------ device context */
 static bool check_device(int *dev) {
     if (cudaGetDevice(dev) != cudaSuccess) return false;
@@ -210,7 +226,8 @@ static int build_tables(int dev, DevTables **out) {
         cudaMalloc(&t.qinv_wm, qiw.size() * 4) != cudaSuccess ||
         cudaMalloc(&t.qpp_off, CRN_NUM_K * 4) != cudaSuccess ||
         cudaMalloc(&t.crc_bit, cb.size() * 4) != cudaSuccess ||
-        cudaMalloc(&t.crcb_off, CRN_NUM_K * 4) != cudaSuccess) {
+        cudaMalloc(&t.crcb_off, CRN_NUM_K * 4) != cudaSuccess ||
+        cudaMalloc(&t.mi_tab, 256 * 4) != cudaSuccess) {
         cudaGetLastError();
         return CRN_ENOMEM;
     }
@@ -221,10 +238,13 @@ static int build_tables(int dev, DevTables **out) {
     cudaMemcpy(t.qpp_off, qoff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.crc_bit, cb.data(), cb.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.crcb_off, cboff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
+    int32_t mt[256];
+    crn_mi_table(mt);
+    cudaMemcpy(t.mi_tab, mt, sizeof(mt), cudaMemcpyHostToDevice);
     if (cudaError_t e = cudaGetLastError()) return crn_cuda_fail(e, "table upload", CRN_ECUDA);
     t.tab.qpp_wm = t.qpp_wm; t.tab.qpp_ts = t.qpp_ts; t.tab.qinv_ts = t.qinv_ts;
     t.tab.qpp_off = t.qpp_off;
-    t.tab.crc_bit = t.crc_bit; t.tab.crcb_off = t.crcb_off;
+    t.tab.crc_bit = t.crc_bit; t.tab.crcb_off = t.crcb_off; t.tab.mi_tab = t.mi_tab;
     t.tab.qinv_wm = t.qinv_wm;
     t.grid = crn_decode_grid(dev);
     if (t.grid <= 0) {
@@ -396,7 +416,7 @@ extern "C" int crn_plan_decode(void *plan, const int16_t *l0, const int16_t *l1,
                                int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it,
                                int16_t *ext, void *stream) {
     Plan *P = (Plan *)plan;
-    if (!P || max_iters < 1 || max_iters > CRN_MAX_ITERS) return CRN_EINVAL;
+    if (!P || max_iters < 1 || max_iters > CRN_MAX_ITERS || et < 0 || et > CRN_ET_MI) return CRN_EINVAL;
     if (P->n_cb && (!l0 || !l1 || !l2 || !bits || !ok)) return CRN_EINVAL;
     int dev;
     DevTables *t;
@@ -430,7 +450,8 @@ extern "C" int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb, const 
                                    const int16_t *l1, const int16_t *l2, int32_t max_iters,
                                    int32_t et, int32_t flags, uint32_t *bits, uint8_t *ok,
                                    uint8_t *it, int16_t *ext, void *ws, size_t ws_bytes, void *stream) {
-    if (n_cb < 0 || (flags & ~(CRN_DESC_ON_DEVICE | CRN_EXT_SCALED)) || max_iters < 1 || max_iters > CRN_MAX_ITERS)
+    if (n_cb < 0 || (flags & ~(CRN_DESC_ON_DEVICE | CRN_EXT_SCALED)) || max_iters < 1 || max_iters > CRN_MAX_ITERS ||
+        et < 0 || et > CRN_ET_MI)
         return CRN_EINVAL;
     if (n_cb == 0) return CRN_OK;
     if (!desc || !l0 || !l1 || !l2 || !bits || !ok) return CRN_EINVAL;

@@ -7,6 +7,7 @@
 #include "../../include/crn.h"
 
 #define CRN_NSTATE 8
+#define CRN_MI_EPS 66      /* MI stopping rule: per-bit change threshold in Q16 (R29) */
 /* Decode work unit: one CTA task = n_pairs pairs of CBs with the same K; the
  * two CBs of a pair share every int16x2 register (lo half / hi half), so all
  * trellis arithmetic is pair-SIMD and the 8-state butterfly is a register
@@ -63,6 +64,7 @@ typedef struct {
     const uint32_t *qinv_wm;  /* same index, inverse permutation in the qpp_wm format: (m % W) << 16 | m / W */
     const uint32_t *crc_bit;  /* per K at crcb_off[kidx]: [kind(0=A,1=B)*K + i*M + j] = x^(K-1-n+24) mod g, n = jW+i:
                                  the CRC register contribution of a 1 at bit n (register = XOR over the set bits) */
+    const int32_t *mi_tab;    /* [256] Q16 MI of an LLR of magnitude a/8 (crn_mi_table, R29) */
     const int32_t *qpp_off;
     const int32_t *crcb_off;
 } crn_tables;

@@ -156,7 +156,8 @@ extern "C" int crn_plan_decode_host(void *plan, const int16_t *h0, const int16_t
                                     int32_t max_iters, int32_t et, uint32_t *h_bits, uint8_t *h_ok,
                                     uint8_t *h_it, int32_t n_chunks, void *stream) {
     Plan *P = (Plan *)plan;
-    if (!P || max_iters < 1 || max_iters > CRN_MAX_ITERS || n_chunks < 0 || n_chunks > 64) return CRN_EINVAL;
+    if (!P || max_iters < 1 || max_iters > CRN_MAX_ITERS || n_chunks < 0 || n_chunks > 64 || et < 0 || et > CRN_ET_MI)
+        return CRN_EINVAL;
     if (P->n_cb == 0) return CRN_OK;
     if (!h0 || !h1 || !h2 || !h_bits || !h_ok) return CRN_EINVAL;
     int dev;
@@ -245,7 +246,7 @@ Layout layout(int n_cb, int n_tasks, int n_pairs, int64_t n_llr, int64_t n_words
 extern "C" int crn_stream_run(const crn_tti_group *g, int32_t n_tti, int32_t n_groups, double period_us,
                               int32_t max_iters, int32_t et, crn_tti_timing *timing) {
     if (!g || !timing || n_tti < 1 || n_groups < 1 || n_groups > 64 || period_us < 0 || max_iters < 1 ||
-        max_iters > CRN_MAX_ITERS)
+        max_iters > CRN_MAX_ITERS || et < 0 || et > CRN_ET_MI)
         return CRN_EINVAL;
     int dev;
     DevTables *t;

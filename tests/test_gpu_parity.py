@@ -413,3 +413,17 @@ def test_outputs_write_only_their_ranges(orc):
     assert np.all(words[wmask] == SENT)
     assert np.all(g["ext"][emask] == 0x7B7B)
     assert np.all(ok.cpu().numpy()[b.n_cb:] == 0xA5) and np.all(it.cpu().numpy()[b.n_cb:] == 0xA5)
+
+
+@pytest.mark.parametrize("cfg,scale", [(5, 1.0), (3, 0.1), (1, 1.0)])
+def test_mi_stopping_rule_parity(orc, cfg, scale):
+    """The paper's MI stopping rule (CRN_ET_MI, R29) on
+    both kernel paths: bits, extrinsics, iteration counts and CRC flags equal the
+    oracle's; the plain and scaled variants both."""
+    b = _full(cfg, scale)
+    idx = np.arange(b.n_cb)
+    for flags, var in ((0, orc.VAR_MAXLOG), (crn.EXT_SCALED, orc.VAR_SCALED)):
+        g = run_gpu(b, 8, crn.ET_MI, flags=flags)
+        r = run_oracle(b, idx, 8, orc.ET_MI, variant=var)
+        assert_parity(b, g, r, idx)
+        assert np.all(g["iters"] >= 2)
