@@ -61,6 +61,10 @@ def lib():
         L.oracle_decode_cb_v.argtypes = [i16p, i16p, i16p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.c_int, C.c_int, u8p, u8p, u8p, i16p, u64p]
         L.oracle_decode_cb_v.restype = C.c_int64
+        L.oracle_rm_perm.argtypes = [C.c_int]
+        L.oracle_rm_params.argtypes = [C.c_int, C.c_int, P(C.c_int), P(C.c_int), P(C.c_int), P(C.c_int)]
+        L.oracle_rate_match.argtypes = [u8p, u8p, u8p, C.c_int, C.c_int, C.c_int, u8p]
+        L.oracle_rate_dematch.argtypes = [i16p, C.c_int, C.c_int, C.c_int, C.c_int, i16p, i16p, i16p]
         L.oracle_mi_table.argtypes = [C.c_int32]
         L.oracle_mi_table.restype = C.c_int32
         L.oracle_ext_scale.argtypes = [C.c_int32]
@@ -211,6 +215,37 @@ def nii_update(alpha_out, beta_out):
 VAR_MAXLOG, VAR_SCALED = 0, 1
 ET_NONE, ET_CRC, ET_MI = 0, 1, 2
 MI_EPS = 66
+
+
+def rm_perm(c: int) -> int:
+    """Sub-block interleaver inter-column permutation P(c) (36.212 5.1.4.1.1)."""
+    return int(lib().oracle_rm_perm(int(c)))
+
+
+def rm_params(K: int, rv: int = 0) -> dict:
+    R, ND, Kpi, k0 = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    if lib().oracle_rm_params(K, rv, C.byref(R), C.byref(ND), C.byref(Kpi), C.byref(k0)):
+        raise ValueError("bad K / rv")
+    return dict(R=R.value, ND=ND.value, Kpi=Kpi.value, k0=k0.value, Ncb=3 * Kpi.value)
+
+
+def rate_match(d, E: int, rv: int = 0) -> np.ndarray:
+    """d = (d0, d1, d2) coded bits (K+4 each) -> E selected bits."""
+    d0, d1, d2 = (np.ascontiguousarray(x, np.uint8) for x in d)
+    e = np.zeros(E, np.uint8)
+    if lib().oracle_rate_match(_p(d0, C.c_uint8), _p(d1, C.c_uint8), _p(d2, C.c_uint8), d0.size - 4, E, rv,
+                               _p(e, C.c_uint8)):
+        raise ValueError("bad arguments")
+    return e
+
+
+def rate_dematch(e, K: int, rv: int = 0, h=None):
+    """E soft values -> (h0, h1, h2) soft buffers (K+4 each); h: previous buffers (HARQ) or None."""
+    e = np.ascontiguousarray(e, np.int16)
+    hs = [np.zeros(K + 4, np.int16) for _ in range(3)] if h is None else [np.array(x, np.int16) for x in h]
+    if lib().oracle_rate_dematch(_p(e, C.c_int16), K, e.size, rv, int(h is not None), *(_p(x, C.c_int16) for x in hs)):
+        raise ValueError("bad arguments")
+    return tuple(hs)
 
 
 def mi_table(a: int) -> int:

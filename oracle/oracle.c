@@ -533,3 +533,74 @@ int64_t oracle_decode_batch_v(int n_cb, const int32_t *K, const int32_t *F, cons
     if (ops) *ops += atomic_load(&b.ops);
     return atomic_load(&b.viol);
 }
+
+/* ---------------------------------------------------------------- rate matching (row f4)
+ * TS 36.212 5.1.4.1 for turbo-coded channels (R30): the received data
+ * R(x_i) the paper de-multiplexes are the E rate-matched soft
+ * values of a CB.  Sub-block interleaver with 32 columns and the inter-column
+ * permutation P; bit collection w = v0 | interlace(v1, v2); bit selection from
+ * k0 = R (2 ceil(Ncb / 8R) rv + 2) skipping <NULL>, wrapping modulo Ncb = 3 Kpi
+ * (full circular buffer).  De-matching adds every received value to the soft
+ * buffer position it was read from (repetition accumulates, punctured positions
+ * stay 0) and, for HARQ, onto the previous buffer content, saturating once. */
+static const int RM_P[32] = {0, 16, 8, 24, 4, 20, 12, 28, 2, 18, 10, 26, 6, 22, 14, 30,
+                             1, 17, 9, 25, 5, 21, 13, 29, 3, 19, 11, 27, 7, 23, 15, 31};
+
+int oracle_rm_perm(int c) { return (c >= 0 && c < 32) ? RM_P[c] : -1; }
+
+int oracle_rm_params(int K, int rv, int *R, int *ND, int *Kpi, int *k0) {
+    if (k_row(K) < 0 || rv < 0 || rv > 3) return -1;
+    const int D = K + 4, r = (D + 31) / 32, kpi = 32 * r, ncb = 3 * kpi;
+    *R = r; *ND = kpi - D; *Kpi = kpi;
+    *k0 = r * (2 * ((ncb + 8 * r - 1) / (8 * r)) * rv + 2);
+    return 0;
+}
+
+/* w position p -> d index of its stream (*s), or -1 for <NULL> */
+static int rm_wpos(int K, int p, int *s) {
+    const int D = K + 4, R = (D + 31) / 32, kpi = 32 * R, ND = kpi - D;
+    int y;
+    if (p < kpi) {                                  /* v0: column-wise read of the permuted matrix */
+        *s = 0;
+        y = (p % R) * 32 + RM_P[p / R];
+    } else {
+        const int q = p - kpi, k = q / 2;
+        if ((q & 1) == 0) { *s = 1; y = (k % R) * 32 + RM_P[k / R]; }
+        else { *s = 2; y = (RM_P[k / R] + 32 * (k % R) + 1) % kpi; }
+    }
+    return y < ND ? -1 : y - ND;
+}
+
+int oracle_rate_match(const uint8_t *d0, const uint8_t *d1, const uint8_t *d2, int K, int E, int rv, uint8_t *e) {
+    int R, ND, kpi, k0;
+    if (E < 1 || oracle_rm_params(K, rv, &R, &ND, &kpi, &k0)) return -1;
+    const uint8_t *d[3] = {d0, d1, d2};
+    const int ncb = 3 * kpi;
+    for (int k = 0, j = 0; k < E; j++) {
+        int s;
+        const int n = rm_wpos(K, (k0 + j) % ncb, &s);
+        if (n >= 0) e[k++] = d[s][n];
+    }
+    return 0;
+}
+
+int oracle_rate_dematch(const int16_t *e, int K, int E, int rv, int combine, int16_t *h0, int16_t *h1,
+                        int16_t *h2) {
+    int R, ND, kpi, k0;
+    if (E < 1 || oracle_rm_params(K, rv, &R, &ND, &kpi, &k0)) return -1;
+    const int D = K + 4, ncb = 3 * kpi;
+    int32_t *acc = (int32_t *)calloc(3 * (size_t)D, sizeof(int32_t));
+    for (int k = 0, j = 0; k < E; j++) {
+        int s;
+        const int n = rm_wpos(K, (k0 + j) % ncb, &s);
+        if (n >= 0) acc[(size_t)s * D + n] += e[k++];
+    }
+    int16_t *h[3] = {h0, h1, h2};
+    for (int s = 0; s < 3; s++)
+        for (int n = 0; n < D; n++) {
+            int32_t v = acc[(size_t)s * D + n] + (combine ? h[s][n] : 0);
+            h[s][n] = (int16_t)(v < -32768 ? -32768 : (v > 32767 ? 32767 : v));
+        }
+    free(acc);
+    return 0;
+}

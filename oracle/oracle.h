@@ -137,6 +137,20 @@ int64_t oracle_decode_batch_v(int n_cb, const int32_t *K, const int32_t *F, cons
                               uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
                               int16_t *ext, uint64_t *ops);
 
+/* Rate matching for turbo-coded channels, TS 36.212 5.1.4.1 (row f4, DESIGN.md
+ * R30): full circular buffer Ncb = 3*Kpi, Kpi = 32*ceil((K+4)/32).
+ *   oracle_rm_perm(c): the sub-block inter-column permutation P(c), c in [0,32)
+ *   oracle_rm_params: R rows, ND dummy bits, Kpi, and k0 for redundancy version rv
+ *   oracle_rate_match: d0/d1/d2 coded bits (K+4 each) -> e[E] selected bits
+ *   oracle_rate_dematch: e[E] soft values -> soft buffers h0/h1/h2 (K+4 each):
+ *     h = sat16((combine ? h : 0) + sum of the values read from each position).
+ * All return 0, or -1 for an unsupported K, rv outside [0,3] or E < 1. */
+int oracle_rm_perm(int c);
+int oracle_rm_params(int K, int rv, int *R, int *ND, int *Kpi, int *k0);
+int oracle_rate_match(const uint8_t *d0, const uint8_t *d1, const uint8_t *d2, int K, int E, int rv, uint8_t *e);
+int oracle_rate_dematch(const int16_t *e, int K, int E, int rv, int combine, int16_t *h0, int16_t *h1,
+                        int16_t *h2);
+
 #ifdef __cplusplus
 }
 #endif
