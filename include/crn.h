@@ -205,6 +205,37 @@ int64_t crn_counted_ops(const int32_t *K_host, int32_t n_cb, const uint8_t *iter
 int crn_encode_batch(const crn_cb_desc *desc, int32_t n_cb, const uint8_t *info, int32_t attach_crc,
                      uint8_t *d0, uint8_t *d1, uint8_t *d2, void *cuda_stream);
 
+/* ------------------------------------------------------------------ rate matching */
+
+/* One CB's rate-matching parameters (TS 36.212 5.1.4.1, R30):
+ *   K       interleaver size (the 188 LTE sizes); the CB has 3 (K+4) coded bits
+ *   E       rate-matched length (>= 1; E > 3(K+4) repeats, E < 3(K+4) punctures)
+ *   rv      redundancy version 0..3 (start k0 = R (24 rv + 2) of the circular buffer)
+ *   e_off   element offset of the CB's E values in e
+ *   llr_off element offset of the CB's K+4 values in each of the three streams */
+typedef struct {
+    int32_t K, E, rv, reserved;
+    int64_t e_off, llr_off;
+} crn_rm_desc;
+
+/* De-matching on the DEVICE (the input side of the decoder):
+ * for every CB, each of the E received int16 soft values e[e_off + k] is added
+ * to the coded-bit position it was selected from (repetitions accumulate,
+ * punctured positions receive nothing); the int32 sums are written to
+ * h_sys / h_p1 / h_p2 [llr_off .. llr_off + K+4) saturated to int16 -- onto the
+ * previous content (HARQ soft combining) if combine != 0, else replacing it.
+ * The three output streams are exactly the decoder's llr_sys / llr_p1 /
+ * llr_p2 inputs (dense or any layout).  desc: HOST array (copied); e, h_*:
+ * DEVICE memory.  Asynchronous on cuda_stream.  CRN_EINVAL for a bad K, rv, E,
+ * negative offsets.  Results do not depend on order (exact integer sums). */
+int crn_rate_dematch_batch(const crn_rm_desc *desc, int32_t n_cb, const int16_t *e, int32_t combine,
+                           int16_t *h_sys, int16_t *h_p1, int16_t *h_p2, void *cuda_stream);
+/* Rate matching on the DEVICE (DL direction): CB i's coded
+ * bits d0/d1/d2 [llr_off .. +K+4) (one bit per byte, as crn_encode_batch writes
+ * them) -> its E selected bits e[e_off ..) (one bit per byte). */
+int crn_rate_match_batch(const crn_rm_desc *desc, int32_t n_cb, const uint8_t *d0, const uint8_t *d1,
+                         const uint8_t *d2, uint8_t *e, void *cuda_stream);
+
 /* ------------------------------------------------------------------ host helpers */
 
 /* TB of tbs_bits payload bits -> 36.212 5.1.2 code-block segmentation (B = tbs+24). */

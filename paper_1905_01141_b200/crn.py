@@ -68,6 +68,8 @@ _SIGS = {
     "crn_encode_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp]),
     "crn_tb_build_cbs": (C.c_int, [u8p, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_int64, u8p, vp,
                                    i32p]),
+    "crn_rate_dematch_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp]),
+    "crn_rate_match_batch": (C.c_int, [vp, C.c_int32, vp, vp, vp, vp, vp]),
     "crn_tb_verdict_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp, vp]),
     "crn_tb_reassemble": (C.c_int, [u32p, vp, u8p, C.c_int32, C.c_int64, u8p]),
     "crn_segment_tb": (C.c_int, [C.c_int64, P(Seg)]),
@@ -254,6 +256,26 @@ def tb_build_cbs(tb_bits, base_bit: int = 0, base_llr: int = 0, base_word: int =
                                 _np(out, C.c_uint8), desc.ctypes.data, C.byref(n)), "crn_tb_build_cbs")
     desc = desc[:n.value].copy()
     return out[:int(desc["K"].sum())].copy(), desc
+
+
+RM_DTYPE = np.dtype([("K", "<i4"), ("E", "<i4"), ("rv", "<i4"), ("reserved", "<i4"), ("e_off", "<i8"),
+                     ("llr_off", "<i8")])
+
+
+def rate_dematch_batch(desc, e, combine: bool, h0, h1, h2, stream=None) -> None:
+    """crn_rate_dematch_batch: desc (RM_DTYPE) host array; e, h* CUDA tensors."""
+    _cuda_dev(e, h0, h1, h2)
+    desc = np.ascontiguousarray(desc, RM_DTYPE)
+    _chk(lib().crn_rate_dematch_batch(desc.ctypes.data, desc.size, _ptr(e), int(combine), _ptr(h0), _ptr(h1),
+                                      _ptr(h2), _stream(stream)), "crn_rate_dematch_batch")
+
+
+def rate_match_batch(desc, d0, d1, d2, e, stream=None) -> None:
+    """crn_rate_match_batch: desc (RM_DTYPE) host array; d*, e CUDA uint8 tensors."""
+    _cuda_dev(d0, d1, d2, e)
+    desc = np.ascontiguousarray(desc, RM_DTYPE)
+    _chk(lib().crn_rate_match_batch(desc.ctypes.data, desc.size, _ptr(d0), _ptr(d1), _ptr(d2), _ptr(e),
+                                    _stream(stream)), "crn_rate_match_batch")
 
 
 TB_DTYPE = np.dtype([("cb0", "<i4"), ("n_cb", "<i4"), ("tbs", "<i8"), ("word_off", "<i8")])

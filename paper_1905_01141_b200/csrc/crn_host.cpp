@@ -619,3 +619,50 @@ extern "C" int crn_tb_verdict_batch(const crn_tb_desc *tb, int32_t n_tb, const c
     if (cudaError_t e = cudaGetLastError()) return crn_cuda_fail(e, "crn_tb_verdict_batch", CRN_ECUDA);
     return rc;
 }
+
+/* ------------------------------------------------------------------ rate matching (row f4) */
+static int rm_upload(const crn_rm_desc *desc, int32_t n_cb, cudaStream_t st, void **dd) {
+    for (int i = 0; i < n_cb; i++) {
+        const crn_rm_desc &d = desc[i];
+        if (crn_k_index(d.K) < 0 || d.E < 1 || d.rv < 0 || d.rv > 3 || d.e_off < 0 || d.llr_off < 0)
+            return CRN_EINVAL;
+    }
+    const size_t b = sizeof(crn_rm_desc) * (size_t)n_cb;
+    if (cudaMallocAsync(dd, b, st) != cudaSuccess) { cudaGetLastError(); return CRN_ENOMEM; }
+    cudaMemcpyAsync(*dd, desc, b, cudaMemcpyHostToDevice, st);
+    return CRN_OK;
+}
+
+extern "C" int crn_rate_dematch_batch(const crn_rm_desc *desc, int32_t n_cb, const int16_t *e, int32_t combine,
+                                      int16_t *h0, int16_t *h1, int16_t *h2, void *stream) {
+    if (n_cb < 0) return CRN_EINVAL;
+    if (n_cb == 0) return CRN_OK;
+    if (!desc || !e || !h0 || !h1 || !h2) return CRN_EINVAL;
+    int dev;
+    DevTables *t;
+    int rc = crn_get_ctx(&dev, &t);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    void *dd = nullptr;
+    if ((rc = rm_upload(desc, n_cb, st, &dd))) return rc;
+    rc = crn_launch_dematch((const crn_rm_desc *)dd, n_cb, e, combine, h0, h1, h2, (void *)st);
+    cudaFreeAsync(dd, st);
+    return rc;
+}
+
+extern "C" int crn_rate_match_batch(const crn_rm_desc *desc, int32_t n_cb, const uint8_t *d0, const uint8_t *d1,
+                                    const uint8_t *d2, uint8_t *e, void *stream) {
+    if (n_cb < 0) return CRN_EINVAL;
+    if (n_cb == 0) return CRN_OK;
+    if (!desc || !d0 || !d1 || !d2 || !e) return CRN_EINVAL;
+    int dev;
+    DevTables *t;
+    int rc = crn_get_ctx(&dev, &t);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    void *dd = nullptr;
+    if ((rc = rm_upload(desc, n_cb, st, &dd))) return rc;
+    rc = crn_launch_match((const crn_rm_desc *)dd, n_cb, d0, d1, d2, e, (void *)st);
+    cudaFreeAsync(dd, st);
+    return rc;
+}

@@ -87,6 +87,11 @@ int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const uint8_t *in
 /* crn_tb.cu */
 int crn_launch_tb(const crn_tb_desc *d_tbs, int32_t n_tb, const crn_cb_desc *d_desc, const uint32_t *cb_words,
                   const uint8_t *crc_ok, uint8_t *tb_ok, uint32_t *tb_words, void *stream);
+/* crn_ratematch.cu */
+int crn_launch_dematch(const crn_rm_desc *d_desc, int32_t n_cb, const int16_t *e, int32_t combine, int16_t *h0,
+                       int16_t *h1, int16_t *h2, void *stream);
+int crn_launch_match(const crn_rm_desc *d_desc, int32_t n_cb, const uint8_t *d0, const uint8_t *d1,
+                     const uint8_t *d2, uint8_t *e, void *stream);
 /* crn_ubench.cu */
 int crn_launch_ubench(int32_t op, int64_t *lane_instr, float *ms, int64_t *cycles_per_block);
 /* crn_host.cpp */

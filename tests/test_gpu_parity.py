@@ -427,3 +427,82 @@ def test_mi_stopping_rule_parity(orc, cfg, scale):
         r = run_oracle(b, idx, 8, orc.ET_MI, variant=var)
         assert_parity(b, g, r, idx)
         assert np.all(g["iters"] >= 2)
+
+
+def _rm_case(rng, n, ks):
+    K = rng.choice(ks, n)
+    N = 3 * (K + 4)
+    E = np.maximum(1, (N * rng.choice([0.31, 0.5, 1.0, 1.7, 2.6], n)).astype(np.int64))
+    rv = rng.integers(0, 4, n)
+    d = np.zeros(n, crn.RM_DTYPE)
+    d["K"], d["E"], d["rv"] = K, E, rv
+    d["e_off"] = np.concatenate([[0], np.cumsum(E)[:-1]]) + 3 * np.arange(n)          # gaps between CBs
+    d["llr_off"] = np.concatenate([[0], np.cumsum(K + 4)[:-1]]) + 5 * np.arange(n)
+    return d
+
+
+def test_rate_dematch_and_match_parity(orc):
+    """Row f4: device rate de-matching (with and without HARQ combining) and rate
+    matching equal the oracle's for mixed K (both kernel geometries), E from
+    heavy puncturing to repetition and every redundancy version."""
+    rng = np.random.default_rng(21)
+    ks = np.array([40, 48, 104, 248, 1008, 1056, 2112, 6144])
+    d = _rm_case(rng, 40, ks)
+    n_e = int((d["e_off"] + d["E"]).max())
+    n_l = int((d["llr_off"] + d["K"] + 4).max())
+    e = rng.integers(-3000, 3001, n_e).astype(np.int16)
+    h_prev = [rng.integers(-30000, 30001, n_l).astype(np.int16) for _ in range(3)]
+    for combine in (False, True):
+        hg = [torch.from_numpy(x.copy()).cuda() for x in h_prev]
+        crn.rate_dematch_batch(d, torch.from_numpy(e).cuda(), combine, *hg)
+        torch.cuda.synchronize()
+        hg = [x.cpu().numpy() for x in hg]
+        for i in range(d.size):
+            K, lo, eo, E = int(d["K"][i]), int(d["llr_off"][i]), int(d["e_off"][i]), int(d["E"][i])
+            prev = [x[lo:lo + K + 4] for x in h_prev] if combine else None
+            ho = orc.rate_dematch(e[eo:eo + E], K, int(d["rv"][i]), h=prev)
+            for s in range(3):
+                assert np.array_equal(hg[s][lo:lo + K + 4], ho[s]), (combine, i, s)
+    bits = [rng.integers(0, 2, n_l, dtype=np.uint8) for _ in range(3)]
+    eg = torch.zeros(n_e, dtype=torch.uint8, device="cuda")
+    crn.rate_match_batch(d, *(torch.from_numpy(x).cuda() for x in bits), eg)
+    torch.cuda.synchronize()
+    eg = eg.cpu().numpy()
+    for i in range(d.size):
+        K, lo, eo, E = int(d["K"][i]), int(d["llr_off"][i]), int(d["e_off"][i]), int(d["E"][i])
+        ref = orc.rate_match([x[lo:lo + K + 4] for x in bits], E, int(d["rv"][i]))
+        assert np.array_equal(eg[eo:eo + E], ref), i
+
+
+def test_rate_matched_chain_decodes_like_oracle(orc):
+    """GPU encode -> GPU rate match -> noisy int16 soft values -> GPU de-match ->
+    GPU decode, against the oracle de-matching + decoding of the same soft values."""
+    b = _full(5, 0.5)
+    rng = np.random.default_rng(5)
+    K = b.desc["K"].astype(np.int64)
+    d = np.zeros(b.n_cb, crn.RM_DTYPE)
+    d["K"] = K
+    d["E"] = (3 * (K + 4) * 0.75).astype(np.int64)                    # rate about 0.45
+    d["rv"] = 0
+    d["e_off"] = np.concatenate([[0], np.cumsum(d["E"])[:-1]])
+    d["llr_off"] = b.desc["llr_off"]
+    n_e = int(d["E"].sum())
+    eb = torch.zeros(n_e, dtype=torch.uint8, device="cuda")
+    crn.rate_match_batch(d, *b.coded, eb)
+    torch.cuda.synchronize()
+    x = (2 * eb.cpu().numpy().astype(np.int32) - 1) * 40 + rng.normal(0, 25, n_e).round().astype(np.int32)
+    soft = np.clip(x, -32768, 32767).astype(np.int16)
+    hg = [torch.zeros_like(t) for t in b.llr]
+    crn.rate_dematch_batch(d, torch.from_numpy(soft).cuda(), False, *hg)
+    g = run_gpu(b, 8, True, l=hg)
+    hh = [t.cpu().numpy() for t in hg]
+    for i in range(b.n_cb):
+        k, lo, eo, E = int(K[i]), int(d["llr_off"][i]), int(d["e_off"][i]), int(d["E"][i])
+        ho = orc.rate_dematch(soft[eo:eo + E], k, 0)
+        for s in range(3):
+            assert np.array_equal(hh[s][lo:lo + k + 4], ho[s])
+    b2 = type("B", (), {})()
+    b2.llr, b2.desc = tuple(torch.from_numpy(x) for x in hh), b.desc
+    r = run_oracle(b2, np.arange(b.n_cb), 8, True)
+    assert_parity(b, g, r, np.arange(b.n_cb))
+    assert g["crc_ok"].mean() > 0.5
