@@ -209,11 +209,12 @@ def run_latency(args, seed=0):
     tim = crn.stream_run(groups, args.lat_ttis, n_groups, 1000.0, 8, True)
     skip = min(10, args.lat_ttis // 10)
     lat, dev = tim["latency_us"][skip:], tim["device_us"][skip:]
+
     its = np.concatenate([g["it"].numpy()[:g["n_cb"]] for grp in distinct for g in grp])
     sum_k = [sum(g["sum_k"] for g in grp) for grp in distinct]
     return {"workload": "cfg5: 1 ms TTIs of 200 CBs (20 cells x 10), K ~ U(188 sizes), QPSK Eb/N0 ~ U[0.5,3] dB "
-                        "per CB, CRC24B ET max 8 iterations, 4 cell groups = 4 CUDA streams, host buffers in/out "
-                        "(crn_stream_run)",
+                        "per CB, CRC24B ET max 8 iterations, 4 cell groups = 4 CUDA streams each with its own "
+                        "upload / decode launch / download, host buffers in/out (crn_stream_run)",
             "n_tti": args.lat_ttis, "distinct_ttis": args.lat_distinct, "period_us": 1000.0,
             "measured_ttis": int(lat.size), "p50_us": float(np.percentile(lat, 50)),
             "p99_us": float(np.percentile(lat, 99)), "max_us": float(lat.max()), "mean_us": float(lat.mean()),

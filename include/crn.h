@@ -186,6 +186,14 @@ typedef struct {
  * (CRN_EINVAL as crn_decode_batch_ex, or n_llr / n_words too small). */
 int crn_stream_run(const crn_tti_group *groups, int32_t n_tti, int32_t n_groups, double period_us,
                    int32_t max_iters, int32_t early_term, crn_tti_timing *timing);
+/* Same with flags: CRN_STREAM_MERGED keeps one CUDA stream per cell group for
+ * the uploads and downloads but decodes each TTI with ONE launch over all
+ * groups' CBs (on an internal decode stream that waits for every group's
+ * upload; each group's download waits for the decode): the groups' persistent
+ * kernels no longer split the SMs between them.  Other flag bits: CRN_EINVAL. */
+enum { CRN_STREAM_MERGED = 1 };
+int crn_stream_run_ex(const crn_tti_group *groups, int32_t n_tti, int32_t n_groups, double period_us,
+                      int32_t max_iters, int32_t early_term, int32_t flags, crn_tti_timing *timing);
 
 /* Counted operations of one decode (the roofline numerator, DESIGN.md "op
  * count"): sum over CBs and executed iterations of 2 x (129 K + 90).  For a

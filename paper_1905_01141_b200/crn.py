@@ -63,6 +63,7 @@ _SIGS = {
     "crn_plan_decode_host": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, C.c_int32, vp]),
     "crn_plan_chunks": (C.c_int, [vp]),
     "crn_stream_run": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int32, vp]),
+    "crn_stream_run_ex": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_int32, vp]),
     "crn_plan_destroy": (None, [vp]),
     "crn_counted_ops": (C.c_int64, [i32p, C.c_int32, u8p, C.c_int32]),
     "crn_encode_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp]),
@@ -206,7 +207,11 @@ class Plan:
             pass
 
 
-def stream_run(groups, n_tti: int, n_groups: int, period_us: float, max_iters: int, early_term: bool):
+STREAM_MERGED = 1
+
+
+def stream_run(groups, n_tti: int, n_groups: int, period_us: float, max_iters: int, early_term: bool,
+               flags: int = 0):
     """crn_stream_run.  groups: list (length n_tti * n_groups, TTI-major) of dicts with
     HOST arrays desc (numpy DESC_DTYPE), l0/l1/l2 (int16 tensors, pinned), bits (int32 tensor),
     ok (uint8 tensor), it (uint8 tensor or None).  Returns a numpy structured array of timings."""
@@ -222,8 +227,8 @@ def stream_run(groups, n_tti: int, n_groups: int, period_us: float, max_iters: i
                           _ptr(g["l2"]), g["l0"].numel(), _ptr(g["bits"]), g["bits"].numel(), _ptr(g["ok"]),
                           _ptr(g.get("it")))
     tim = (TtiTiming * n_tti)()
-    _chk(lib().crn_stream_run(arr, n_tti, n_groups, period_us, max_iters, int(early_term), tim),
-         "crn_stream_run")
+    _chk(lib().crn_stream_run_ex(arr, n_tti, n_groups, period_us, max_iters, int(early_term), flags, tim),
+         "crn_stream_run_ex")
     out = np.zeros(n_tti, [(n, "f8") for n, _ in TtiTiming._fields_])
     for i in range(n_tti):
         for n, _ in TtiTiming._fields_:

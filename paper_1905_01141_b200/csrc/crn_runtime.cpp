@@ -243,37 +243,48 @@ Layout layout(int n_cb, int n_tasks, int n_pairs, int64_t n_llr, int64_t n_words
 
 }  // namespace
 
-extern "C" int crn_stream_run(const crn_tti_group *g, int32_t n_tti, int32_t n_groups, double period_us,
-                              int32_t max_iters, int32_t et, crn_tti_timing *timing) {
+extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t n_groups, double period_us,
+                                 int32_t max_iters, int32_t et, int32_t flags, crn_tti_timing *timing) {
     if (!g || !timing || n_tti < 1 || n_groups < 1 || n_groups > 64 || period_us < 0 || max_iters < 1 ||
-        max_iters > CRN_MAX_ITERS || et < 0 || et > CRN_ET_MI)
+        max_iters > CRN_MAX_ITERS || et < 0 || et > CRN_ET_MI || (flags & ~CRN_STREAM_MERGED))
         return CRN_EINVAL;
+    const bool merged = flags & CRN_STREAM_MERGED;
     int dev;
     DevTables *t;
     int rc = crn_get_ctx(&dev, &t);
     if (rc) return rc;
     const int64_t NG = (int64_t)n_tti * n_groups;
-    /* validate every group up front (host), size the per-group device buffers */
+    /* validate every group up front (host); per group its LLR / word extent */
+    std::vector<int64_t> g_llr(NG, 0), g_words(NG, 0);
     std::vector<size_t> need(n_groups, 0), hneed(n_groups, 0);
-    for (int64_t x = 0; x < NG; x++) {
-        const crn_tti_group &q = g[x];
-        if (q.n_cb < 0 || (q.n_cb > 0 && (!q.desc || !q.llr_sys || !q.llr_p1 || !q.llr_p2 || !q.out_bits ||
-                                          !q.crc_ok)))
-            return CRN_EINVAL;
-        if ((rc = crn_validate(q.desc, q.n_cb, false))) return rc;
-        int64_t n_llr = 0, n_words = 0;
-        for (int i = 0; i < q.n_cb; i++) {
-            n_llr = std::max(n_llr, q.desc[i].llr_off + q.desc[i].K + 4);
-            n_words = std::max(n_words, q.desc[i].bit_off + (q.desc[i].K + 31) / 32);
+    size_t m_need = 0, m_hneed = 0;                 /* merged mode: one buffer set for the whole TTI */
+    for (int ti = 0; ti < n_tti; ti++) {
+        int m_cb = 0;
+        int64_t m_llr = 0, m_words = 0;
+        for (int gi = 0; gi < n_groups; gi++) {
+            const int64_t x = (int64_t)ti * n_groups + gi;
+            const crn_tti_group &q = g[x];
+            if (q.n_cb < 0 || (q.n_cb > 0 && (!q.desc || !q.llr_sys || !q.llr_p1 || !q.llr_p2 || !q.out_bits ||
+                                              !q.crc_ok)))
+                return CRN_EINVAL;
+            if ((rc = crn_validate(q.desc, q.n_cb, false))) return rc;
+            for (int i = 0; i < q.n_cb; i++) {
+                g_llr[x] = std::max(g_llr[x], q.desc[i].llr_off + q.desc[i].K + 4);
+                g_words[x] = std::max(g_words[x], q.desc[i].bit_off + (q.desc[i].K + 31) / 32);
+            }
+            if (g_llr[x] > q.n_llr || g_words[x] > q.n_words) return CRN_EINVAL;
+            const Layout L = layout(q.n_cb, q.n_cb, q.n_cb, g_llr[x], g_words[x]);   /* tasks, pairs <= CBs */
+            need[gi] = std::max(need[gi], L.tot);
+            hneed[gi] = std::max(hneed[gi], L.o_l);
+            m_cb += q.n_cb;
+            m_llr += g_llr[x];
+            m_words += g_words[x];
         }
-        if (n_llr > q.n_llr || n_words > q.n_words) return CRN_EINVAL;
-        /* upper bounds: tasks <= CBs, pairs <= CBs */
-        const Layout L = layout(q.n_cb, q.n_cb, q.n_cb, n_llr, n_words);
-        const int gi = (int)(x % n_groups);
-        need[gi] = std::max(need[gi], L.tot);
-        hneed[gi] = std::max(hneed[gi], L.o_l);
+        const Layout L = layout(m_cb, m_cb, m_cb, m_llr, m_words);
+        m_need = std::max(m_need, L.tot);
+        m_hneed = std::max(m_hneed, L.o_l);
     }
-    std::vector<GroupRes> G(n_groups);
+    std::vector<GroupRes> G(n_groups + (merged ? 1 : 0));   /* merged: G[n_groups] = the shared decode set */
     auto cleanup = [&]() {
         for (auto &r : G) {
             if (r.st) cudaStreamSynchronize(r.st);
@@ -286,26 +297,31 @@ extern "C" int crn_stream_run(const crn_tti_group *g, int32_t n_tti, int32_t n_g
             if (r.st) cudaStreamDestroy(r.st);
         }
     };
-    for (int gi = 0; gi < n_groups; gi++) {
+    for (int gi = 0; gi < (int)G.size(); gi++) {
         GroupRes &r = G[gi];
+        const bool dec = merged && gi == n_groups;
+        const size_t dn = merged ? (dec ? m_need : 0) : need[gi], hn = merged ? (dec ? m_hneed : 0) : hneed[gi];
         if (cudaStreamCreateWithFlags(&r.st, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaMalloc(&r.dmem, std::max<size_t>(need[gi], 256)) != cudaSuccess ||
-            cudaMallocHost(&r.hblob[0], std::max<size_t>(hneed[gi], 256)) != cudaSuccess ||
-            cudaMallocHost(&r.hblob[1], std::max<size_t>(hneed[gi], 256)) != cudaSuccess ||
+            (dn && cudaMalloc(&r.dmem, std::max<size_t>(dn, 256)) != cudaSuccess) ||
+            (hn && cudaMallocHost(&r.hblob[0], std::max<size_t>(hn, 256)) != cudaSuccess) ||
+            (hn && cudaMallocHost(&r.hblob[1], std::max<size_t>(hn, 256)) != cudaSuccess) ||
             cudaEventCreateWithFlags(&r.ev_blob[0], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&r.ev_blob[1], cudaEventDisableTiming) != cudaSuccess ||
-            cudaMalloc(&r.ws, crn_decode_ws_bytes(t->grid)) != cudaSuccess) {
+            ((!merged || dec) && cudaMalloc(&r.ws, crn_decode_ws_bytes(t->grid)) != cudaSuccess)) {
             cudaGetLastError();
             cleanup();
             return CRN_ENOMEM;
         }
     }
     /* per (TTI, group): timing events (start before the uploads, end after the downloads) */
-    std::vector<cudaEvent_t> ev0(NG), ev1(NG);
+    std::vector<cudaEvent_t> ev0(NG), ev1(NG), ev_in(merged ? n_groups : 0);
     for (int64_t x = 0; x < NG; x++) {
         cudaEventCreate(&ev0[x]);
         cudaEventCreate(&ev1[x]);
     }
+    for (auto &e : ev_in) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEvent_t ev_dec = nullptr;
+    if (merged) cudaEventCreateWithFlags(&ev_dec, cudaEventDisableTiming);
     std::vector<double> done_us(NG, 0.0), rel_us(n_tti, 0.0), sub_us(n_tti, 0.0);
     std::atomic<int64_t> submitted{0};
     std::atomic<bool> abort_flag{false};
@@ -327,56 +343,138 @@ extern "C" int crn_stream_run(const crn_tti_group *g, int32_t n_tti, int32_t n_g
         }
     });
 
+    std::vector<crn_cb_desc> mdesc;
+    std::vector<int64_t> lbase(n_groups), wbase(n_groups);
+    std::vector<int> cbase(n_groups);
     for (int ti = 0; ti < n_tti && rc == CRN_OK; ti++) {
         const Clock::time_point rel = t0 + std::chrono::duration_cast<Clock::duration>(
                                                std::chrono::duration<double, std::micro>(period_us * ti));
         while (Clock::now() < rel) { /* pacer: release TTI ti at t0 + ti * period */ }
         rel_us[ti] = us_since(t0, rel);
-        for (int gi = 0; gi < n_groups && rc == CRN_OK; gi++) {
-            const int64_t x = (int64_t)ti * n_groups + gi;
-            const crn_tti_group &q = g[x];
-            GroupRes &r = G[gi];
-            cudaEventRecord(ev0[x], r.st);
-            if (q.n_cb > 0) {
-                /* row a1 per TTI: bucket / pair / task the group's CBs (host) */
-                std::vector<crn_task> tasks;
-                std::vector<crn_pair> pairs;
-                std::vector<int> sel(q.n_cb);
-                for (int i = 0; i < q.n_cb; i++) sel[i] = i;
-                crn_build_tasks(q.desc, sel.data(), q.n_cb, tasks, pairs);
-                int64_t n_llr = 0, n_words = 0;
+        const int64_t x0 = (int64_t)ti * n_groups;
+        if (!merged) {
+            for (int gi = 0; gi < n_groups && rc == CRN_OK; gi++) {
+                const int64_t x = x0 + gi;
+                const crn_tti_group &q = g[x];
+                GroupRes &r = G[gi];
+                cudaEventRecord(ev0[x], r.st);
+                if (q.n_cb > 0) {
+                    /* row a1 per TTI: bucket / pair / task the group's CBs (host) */
+                    std::vector<crn_task> tasks;
+                    std::vector<crn_pair> pairs;
+                    std::vector<int> sel(q.n_cb);
+                    for (int i = 0; i < q.n_cb; i++) sel[i] = i;
+                    crn_build_tasks(q.desc, sel.data(), q.n_cb, tasks, pairs);
+                    const int64_t n_llr = g_llr[x], n_words = g_words[x];
+                    const Layout L = layout(q.n_cb, (int)tasks.size(), (int)pairs.size(), n_llr, n_words);
+                    const int b = ti & 1;
+                    cudaEventSynchronize(r.ev_blob[b]);          /* blob slot from TTI ti-2 uploaded */
+                    uint8_t *hb = (uint8_t *)r.hblob[b];
+                    memcpy(hb + L.o_desc, q.desc, sizeof(crn_cb_desc) * q.n_cb);
+                    memcpy(hb + L.o_tasks, tasks.data(), sizeof(crn_task) * tasks.size());
+                    memcpy(hb + L.o_pairs, pairs.data(), sizeof(crn_pair) * pairs.size());
+                    uint8_t *dm = (uint8_t *)r.dmem;
+                    cudaMemcpyAsync(dm, hb, L.o_l, cudaMemcpyHostToDevice, r.st);
+                    cudaEventRecord(r.ev_blob[b], r.st);
+                    const int16_t *hs[3] = {q.llr_sys, q.llr_p1, q.llr_p2};
+                    int16_t *dl[3];
+                    for (int s = 0; s < 3; s++) {
+                        dl[s] = (int16_t *)(dm + L.o_l + s * L.bl);
+                        cudaMemcpyAsync(dl[s], hs[s], sizeof(int16_t) * n_llr, cudaMemcpyHostToDevice, r.st);
+                    }
+                    uint32_t *dbits = (uint32_t *)(dm + L.o_bits);
+                    uint8_t *dok = dm + L.o_ok, *dit = dm + L.o_it;
+                    rc = crn_launch_tasks(dev, t, (const crn_cb_desc *)(dm + L.o_desc),
+                                          (const crn_task *)(dm + L.o_tasks), (int)tasks.size(),
+                                          (const crn_pair *)(dm + L.o_pairs), dl[0], dl[1], dl[2], max_iters, et, dbits,
+                                          dok, q.iters_used ? dit : nullptr, nullptr, r.ws,
+                                          crn_decode_ws_bytes(t->grid), r.st);
+                    cudaMemcpyAsync(q.out_bits, dbits, 4 * (size_t)n_words, cudaMemcpyDeviceToHost, r.st);
+                    cudaMemcpyAsync(q.crc_ok, dok, (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
+                    if (q.iters_used)
+                        cudaMemcpyAsync(q.iters_used, dit, (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
+                }
+                cudaEventRecord(ev1[x], r.st);
+                submitted.store(x + 1, std::memory_order_release);
+            }
+        } else {
+            /* merged: every group uploads its slice of one TTI-wide buffer set on its own
+             * stream; one decode launch over all groups' tasks waits for every upload;
+             * each group downloads its slice on its own stream after the decode */
+            GroupRes &dr = G[n_groups];
+            int m_cb = 0;
+            int64_t m_llr = 0, m_words = 0;
+            for (int gi = 0; gi < n_groups; gi++) {
+                cbase[gi] = m_cb;
+                lbase[gi] = m_llr;
+                wbase[gi] = m_words;
+                m_cb += g[x0 + gi].n_cb;
+                m_llr += g_llr[x0 + gi];
+                m_words += g_words[x0 + gi];
+            }
+            mdesc.resize(m_cb);
+            for (int gi = 0; gi < n_groups; gi++) {
+                const crn_tti_group &q = g[x0 + gi];
                 for (int i = 0; i < q.n_cb; i++) {
-                    n_llr = std::max(n_llr, q.desc[i].llr_off + q.desc[i].K + 4);
-                    n_words = std::max(n_words, q.desc[i].bit_off + (q.desc[i].K + 31) / 32);
+                    crn_cb_desc d = q.desc[i];
+                    d.llr_off += lbase[gi];
+                    d.bit_off += wbase[gi];
+                    mdesc[cbase[gi] + i] = d;
                 }
-                const Layout L = layout(q.n_cb, (int)tasks.size(), (int)pairs.size(), n_llr, n_words);
-                const int b = ti & 1;
-                cudaEventSynchronize(r.ev_blob[b]);              /* blob slot from TTI ti-2 uploaded */
-                uint8_t *hb = (uint8_t *)r.hblob[b];
-                memcpy(hb + L.o_desc, q.desc, sizeof(crn_cb_desc) * q.n_cb);
-                memcpy(hb + L.o_tasks, tasks.data(), sizeof(crn_task) * tasks.size());
-                memcpy(hb + L.o_pairs, pairs.data(), sizeof(crn_pair) * pairs.size());
-                uint8_t *dm = (uint8_t *)r.dmem;
-                cudaMemcpyAsync(dm, hb, L.o_l, cudaMemcpyHostToDevice, r.st);
-                cudaEventRecord(r.ev_blob[b], r.st);
+            }
+            std::vector<crn_task> tasks;
+            std::vector<crn_pair> pairs;
+            std::vector<int> sel(m_cb);
+            for (int i = 0; i < m_cb; i++) sel[i] = i;
+            crn_build_tasks(mdesc.data(), sel.data(), m_cb, tasks, pairs);
+            const Layout L = layout(m_cb, (int)tasks.size(), (int)pairs.size(), m_llr, m_words);
+            uint8_t *dm = (uint8_t *)dr.dmem;
+            int16_t *dl[3];
+            for (int s = 0; s < 3; s++) dl[s] = (int16_t *)(dm + L.o_l + s * L.bl);
+            uint32_t *dbits = (uint32_t *)(dm + L.o_bits);
+            uint8_t *dok = dm + L.o_ok, *dit = dm + L.o_it;
+            for (int gi = 0; gi < n_groups; gi++) {
+                const int64_t x = x0 + gi;
+                const crn_tti_group &q = g[x];
+                GroupRes &r = G[gi];
+                cudaEventRecord(ev0[x], r.st);
                 const int16_t *hs[3] = {q.llr_sys, q.llr_p1, q.llr_p2};
-                int16_t *dl[3];
-                for (int s = 0; s < 3; s++) {
-                    dl[s] = (int16_t *)(dm + L.o_l + s * L.bl);
-                    cudaMemcpyAsync(dl[s], hs[s], sizeof(int16_t) * n_llr, cudaMemcpyHostToDevice, r.st);
-                }
-                uint32_t *dbits = (uint32_t *)(dm + L.o_bits);
-                uint8_t *dok = dm + L.o_ok, *dit = dm + L.o_it;
+                for (int s = 0; s < 3; s++)
+                    if (g_llr[x])
+                        cudaMemcpyAsync(dl[s] + lbase[gi], hs[s], sizeof(int16_t) * g_llr[x], cudaMemcpyHostToDevice,
+                                        r.st);
+                cudaEventRecord(ev_in[gi], r.st);
+                cudaStreamWaitEvent(dr.st, ev_in[gi], 0);
+            }
+            const int b = ti & 1;
+            cudaEventSynchronize(dr.ev_blob[b]);
+            uint8_t *hb = (uint8_t *)dr.hblob[b];
+            memcpy(hb + L.o_desc, mdesc.data(), sizeof(crn_cb_desc) * m_cb);
+            memcpy(hb + L.o_tasks, tasks.data(), sizeof(crn_task) * tasks.size());
+            memcpy(hb + L.o_pairs, pairs.data(), sizeof(crn_pair) * pairs.size());
+            cudaMemcpyAsync(dm, hb, L.o_l, cudaMemcpyHostToDevice, dr.st);
+            cudaEventRecord(dr.ev_blob[b], dr.st);
+            if (m_cb > 0)
                 rc = crn_launch_tasks(dev, t, (const crn_cb_desc *)(dm + L.o_desc), (const crn_task *)(dm + L.o_tasks),
                                       (int)tasks.size(), (const crn_pair *)(dm + L.o_pairs), dl[0], dl[1], dl[2],
-                                      max_iters, et, dbits, dok, q.iters_used ? dit : nullptr, nullptr, r.ws,
-                                      crn_decode_ws_bytes(t->grid), r.st);
-                cudaMemcpyAsync(q.out_bits, dbits, 4 * (size_t)n_words, cudaMemcpyDeviceToHost, r.st);
-                cudaMemcpyAsync(q.crc_ok, dok, (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
-                if (q.iters_used) cudaMemcpyAsync(q.iters_used, dit, (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
+                                      max_iters, et, dbits, dok, dit, nullptr, dr.ws, crn_decode_ws_bytes(t->grid),
+                                      dr.st);
+            cudaEventRecord(ev_dec, dr.st);
+            for (int gi = 0; gi < n_groups; gi++) {
+                const int64_t x = x0 + gi;
+                const crn_tti_group &q = g[x];
+                GroupRes &r = G[gi];
+                cudaStreamWaitEvent(r.st, ev_dec, 0);
+                if (q.n_cb > 0) {
+                    cudaMemcpyAsync(q.out_bits, dbits + wbase[gi], 4 * (size_t)g_words[x], cudaMemcpyDeviceToHost,
+                                    r.st);
+                    cudaMemcpyAsync(q.crc_ok, dok + cbase[gi], (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
+                    if (q.iters_used)
+                        cudaMemcpyAsync(q.iters_used, dit + cbase[gi], (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
+                }
+                cudaEventRecord(ev1[x], r.st);
             }
-            cudaEventRecord(ev1[x], r.st);
-            submitted.store(x + 1, std::memory_order_release);
+            submitted.store(x0 + n_groups, std::memory_order_release);
         }
         sub_us[ti] = us_since(t0, Clock::now());
     }
@@ -410,6 +508,13 @@ extern "C" int crn_stream_run(const crn_tti_group *g, int32_t n_tti, int32_t n_g
         cudaEventDestroy(ev0[x]);
         cudaEventDestroy(ev1[x]);
     }
+    for (auto &ev : ev_in) cudaEventDestroy(ev);
+    if (ev_dec) cudaEventDestroy(ev_dec);
     cleanup();
     return rc;
+}
+
+extern "C" int crn_stream_run(const crn_tti_group *g, int32_t n_tti, int32_t n_groups, double period_us,
+                              int32_t max_iters, int32_t et, crn_tti_timing *timing) {
+    return crn_stream_run_ex(g, n_tti, n_groups, period_us, max_iters, et, 0, timing);
 }

@@ -254,9 +254,11 @@ def test_plan_decode_host_pipeline(orc, n_chunks):
     p.close()
 
 
-def test_stream_run_cfg5(orc):
-    """crn_stream_run: paced TTIs of cfg5, one stream per cell group; every CB of
-    every TTI bit-exact against the oracle; timestamps ordered."""
+@pytest.mark.parametrize("flags", [0, 1])
+def test_stream_run_cfg5(orc, flags):
+    """crn_stream_run_ex: paced TTIs of cfg5, one stream per cell group (per-group
+    decode launches, or one merged launch per TTI); every CB of every TTI
+    bit-exact against the oracle; timestamps ordered."""
     n_tti, n_groups = 3, 4
     groups, checks = [], []
     for t in range(n_tti):
@@ -277,7 +279,7 @@ def test_stream_run_cfg5(orc):
                      it=torch.zeros(max(sel.size, 1), dtype=torch.uint8).pin_memory())
             groups.append(g)
             checks.append((b, r, sel, d, g))
-    tim = crn.stream_run(groups, n_tti, n_groups, 1000.0, 8, True)
+    tim = crn.stream_run(groups, n_tti, n_groups, 1000.0, 8, True, flags=flags)
     for b, r, sel, d, g in checks:
         words = g["bits"].numpy().view(np.uint32)
         for n, i in enumerate(sel):
