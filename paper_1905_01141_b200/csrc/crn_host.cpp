@@ -621,12 +621,16 @@ extern "C" int crn_tb_verdict_batch(const crn_tb_desc *tb, int32_t n_tb, const c
 }
 
 /* ------------------------------------------------------------------ rate matching (row f4) */
-static int rm_upload(const crn_rm_desc *desc, int32_t n_cb, cudaStream_t st, void **dd) {
+static int rm_validate(const crn_rm_desc *desc, int32_t n_cb) {
     for (int i = 0; i < n_cb; i++) {
         const crn_rm_desc &d = desc[i];
         if (crn_k_index(d.K) < 0 || d.E < 1 || d.rv < 0 || d.rv > 3 || d.e_off < 0 || d.llr_off < 0)
             return CRN_EINVAL;
     }
+    return CRN_OK;
+}
+
+static int rm_upload(const crn_rm_desc *desc, int32_t n_cb, cudaStream_t st, void **dd) {
     const size_t b = sizeof(crn_rm_desc) * (size_t)n_cb;
     if (cudaMallocAsync(dd, b, st) != cudaSuccess) { cudaGetLastError(); return CRN_ENOMEM; }
     cudaMemcpyAsync(*dd, desc, b, cudaMemcpyHostToDevice, st);
@@ -637,7 +641,7 @@ extern "C" int crn_rate_dematch_batch(const crn_rm_desc *desc, int32_t n_cb, con
                                       int16_t *h0, int16_t *h1, int16_t *h2, void *stream) {
     if (n_cb < 0) return CRN_EINVAL;
     if (n_cb == 0) return CRN_OK;
-    if (!desc || !e || !h0 || !h1 || !h2) return CRN_EINVAL;
+    if (!desc || !e || !h0 || !h1 || !h2 || rm_validate(desc, n_cb)) return CRN_EINVAL;
     int dev;
     DevTables *t;
     int rc = crn_get_ctx(&dev, &t);
@@ -654,7 +658,7 @@ extern "C" int crn_rate_match_batch(const crn_rm_desc *desc, int32_t n_cb, const
                                     const uint8_t *d2, uint8_t *e, void *stream) {
     if (n_cb < 0) return CRN_EINVAL;
     if (n_cb == 0) return CRN_OK;
-    if (!desc || !d0 || !d1 || !d2 || !e) return CRN_EINVAL;
+    if (!desc || !d0 || !d1 || !d2 || !e || rm_validate(desc, n_cb)) return CRN_EINVAL;
     int dev;
     DevTables *t;
     int rc = crn_get_ctx(&dev, &t);

@@ -138,3 +138,30 @@ def test_tb_verdict_batch_validation():
     assert call(tbs, d2) == crn.CRN_EINVAL                         # filler mismatch
     d2 = desc.copy(); d2["crc_kind"][1] = crn.CRC24A
     assert call(tbs, d2) == crn.CRN_EINVAL
+
+
+def test_new_entry_points_validate_on_host():
+    """Argument checks of the runtime, variant and rate-matching entry points run
+    before any device access (CRN_EINVAL here, CRN_ENODEV only for valid calls)."""
+    import ctypes as C
+    L = crn.lib()
+    fake = C.c_void_p(16)
+    rm = np.zeros(1, crn.RM_DTYPE)
+    rm["K"], rm["E"], rm["rv"] = 1056, 3000, 0
+    ok = L.crn_rate_dematch_batch(rm.ctypes.data, 1, fake, 0, fake, fake, fake, None)
+    assert ok in (crn.CRN_ENODEV, crn.CRN_OK)
+    for field, bad in (("K", 1057), ("rv", 4), ("E", 0), ("e_off", -1)):
+        b = rm.copy()
+        b[field] = bad
+        assert L.crn_rate_dematch_batch(b.ctypes.data, 1, fake, 0, fake, fake, fake, None) == crn.CRN_EINVAL
+        assert L.crn_rate_match_batch(b.ctypes.data, 1, fake, fake, fake, fake, None) == crn.CRN_EINVAL
+    d = np.zeros(1, crn.DESC_DTYPE)
+    d["K"], d["crc_kind"] = 1056, crn.CRC24B
+    assert L.crn_decode_batch_ex(d.ctypes.data, 1, fake, fake, fake, 8, 3, 0, fake, fake, None, None, None, 0,
+                                 None) == crn.CRN_EINVAL                    # unknown stopping rule
+    assert L.crn_decode_batch_ex(d.ctypes.data, 1, fake, fake, fake, 8, 1, 4, fake, fake, None, None, None, 0,
+                                 None) == crn.CRN_EINVAL                    # unknown flag bit
+    tim = (crn.TtiTiming * 1)()
+    grp = (crn.TtiGroup * 1)()
+    assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 2, tim) == crn.CRN_EINVAL   # unknown stream flag
+    assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 5, 0, tim) == crn.CRN_EINVAL   # unknown stopping rule
