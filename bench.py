@@ -172,6 +172,70 @@ def run_reference(args):
     return 0
 
 
+def run_pool(args, seed=0):
+    """BASELINE cfg3: one TTI of a C-RAN pool -- 100 cells x 10 UEs, TBS ~ U{1000..75376},
+    36.212 segmentation (fillers, CRC24A/B), QPSK Eb/N0 ~ U[0.5, 3] dB per UE, CRC ET at
+    max 8 iterations.  Device-resident decode of the whole TTI (one launch) + device TB
+    verdicts, and the same TTI end to end from pinned host buffers (crn_plan_decode_host)."""
+    from paper_1905_01141_b200 import batch as bmod
+    from paper_1905_01141_b200 import crn
+    from paper_1905_01141_b200 import workload as wlmod
+    t_gen = time.perf_counter()
+    b = bmod.build(wlmod.make_workload(3, seed=seed, device="cuda"))
+    t_gen = time.perf_counter() - t_gen
+    plan = crn.Plan(b.desc)
+    bits, ok, it, _ = bmod.outputs(b, want_ext=False)
+    tbs = np.zeros(b.wl.n_tb, crn.TB_DTYPE)
+    w = 0
+    for t in range(b.wl.n_tb):
+        idx = np.flatnonzero(b.cb_tb == t)
+        tbs[t] = (idx[0], idx.size, int(b.wl.tbs[t]), w)
+        w += (int(b.wl.tbs[t]) + 31) // 32
+    tb_ok = torch.zeros(tbs.size, dtype=torch.uint8, device="cuda")
+    tb_words = torch.zeros(max(w, 1), dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        plan.decode(*b.llr, 8, True, bits, ok, it, stream=st)
+    torch.cuda.synchronize()
+    dec, ver = [], []
+    for _ in range(10):
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(st)
+        plan.decode(*b.llr, 8, True, bits, ok, it, stream=st)
+        e1.record(st)
+        crn.tb_verdict_batch(tbs, b.desc, bits, ok, tb_ok, tb_words, stream=st)
+        e2.record(st)
+        torch.cuda.synchronize()
+        dec.append(e0.elapsed_time(e1))
+        ver.append(e1.elapsed_time(e2))
+    hl = [x.cpu().pin_memory() for x in b.llr]
+    hb = torch.zeros(bits.numel(), dtype=torch.int32).pin_memory()
+    hok = torch.zeros(ok.numel(), dtype=torch.uint8).pin_memory()
+    for _ in range(2):
+        plan.decode_host(*hl, 8, True, hb, hok, None, stream=st)
+    torch.cuda.synchronize()
+    e2e = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        plan.decode_host(*hl, 8, True, hb, hok, None, stream=st)
+        st.synchronize()
+        e2e.append(1e3 * (time.perf_counter() - t0))
+    its = it[:b.n_cb].cpu().numpy()
+    d_ms = statistics.median(dec)
+    return {"workload": "cfg3: 100 cells x 10 UEs, TBS ~ U{1000..75376}, 36.212 segmentation, QPSK Eb/N0 ~ "
+                        "U[0.5,3] dB per UE, CRC ET max 8 iterations, one TTI",
+            "n_tb": int(b.wl.n_tb), "n_cb": b.n_cb, "sum_K": int(b.K.sum()), "info_bits": b.info_bits(),
+            "decode_ms": d_ms, "tb_verdict_ms": statistics.median(ver),
+            "decoded_mbps": b.info_bits() / (d_ms * 1e-3) / 1e6,
+            "e2e_ms": statistics.median(e2e), "e2e_path": "pinned host LLRs -> crn_plan_decode_host -> bits + crc_ok "
+                                                          "in pinned host memory (host clock, stream synced)",
+            "tb_loss_rate": float(1.0 - tb_ok.float().mean().item()),
+            "cb_crc_fail_rate": float(1.0 - ok[:b.n_cb].float().mean().item()),
+            "mean_iters": float(its.mean()),
+            "iters_hist": [int(x) for x in np.bincount(its, minlength=9)[1:9]],
+            "gen_s": round(t_gen, 1)}
+
+
 def run_latency(args, seed=0):
     """BASELINE cfg5: paced 1 ms TTIs of 200 CBs (20 cells x 10 CBs, K uniform over
     the 188 sizes, Eb/N0 ~ U[0.5, 3] dB per CB, CRC ET at max 8 iterations), 4 cell
@@ -360,6 +424,11 @@ def run_crn(args):
             out["latency"] = run_latency(args, seed=args.seed)
         except Exception as e:           # the throughput number stands without it
             out["latency"] = {"error": repr(e)}
+    if not args.no_pool and ws == 1:
+        try:
+            out["pool_tti"] = run_pool(args, seed=args.seed)
+        except Exception as e:
+            out["pool_tti"] = {"error": repr(e)}
     if not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline(_cpu_sample(args.ref_sample, args.seed), iters)
@@ -386,6 +455,7 @@ def main():
     ap.add_argument("--lat-ttis", type=int, default=1000)
     ap.add_argument("--lat-distinct", type=int, default=100)
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--no-pool", action="store_true", help="skip the cfg3 one-TTI pool measurement")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

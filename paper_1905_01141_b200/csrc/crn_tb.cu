@@ -43,6 +43,15 @@ __device__ __forceinline__ uint32_t xpow(int64_t e) {                  /* x^e mo
     return r;
 }
 
+/* n <= 32 bits of a CB starting at its bit k (LSB-first packed words), as the low bits */
+__device__ __forceinline__ uint32_t cb_bits(const uint32_t *__restrict__ w, int64_t k, int n) {
+    const int64_t wi = k >> 5;
+    const int sh = (int)(k & 31);
+    uint32_t v = __ldg(w + wi) >> sh;
+    if (sh && sh + n > 32) v |= __ldg(w + wi + 1) << (32 - sh);
+    return n >= 32 ? v : (v & ((1u << n) - 1u));
+}
+
 __global__ void __launch_bounds__(TB_THREADS)
 tb_kernel(const crn_tb_desc *__restrict__ tbs, const crn_cb_desc *__restrict__ desc,
           const uint32_t *__restrict__ cb_words, const uint8_t *__restrict__ crc_ok, uint8_t *__restrict__ tb_ok,
@@ -77,14 +86,15 @@ tb_kernel(const crn_tb_desc *__restrict__ tbs, const crn_cb_desc *__restrict__ d
     uint32_t reg = 0;
     int r = 0;
     for (int64_t w = w0; w < w1; w++) {
-        uint32_t word = 0;
         const int64_t p0 = 32 * w, p1 = p0 + 32 < N ? p0 + 32 : N;
-        for (int64_t p = p0; p < p1; p++) {
-            while (p >= s_start[r + 1]) r++;
-            const int64_t k = s_F[r] + (p - s_start[r]);
-            const uint32_t bit = (cb_words[s_woff[r] + (k >> 5)] >> (k & 31)) & 1u;
-            word |= bit << (p - p0);
-            const uint32_t fb = ((reg >> 23) ^ bit) & 1u;
+        /* the word's bits come from at most two CB segments: funnel-shift them out */
+        while (p0 >= s_start[r + 1]) r++;
+        const int n1 = (int)((s_start[r + 1] < p1 ? s_start[r + 1] : p1) - p0);
+        uint32_t word = cb_bits(cb_words + s_woff[r], s_F[r] + (p0 - s_start[r]), n1);
+        if (p0 + n1 < p1) word |= cb_bits(cb_words + s_woff[r + 1], s_F[r + 1], (int)(p1 - p0 - n1)) << n1;
+        const int nb = (int)(p1 - p0);
+        for (int i = 0; i < nb; i++) {               /* CRC24A register, stream (MSB-first) order */
+            const uint32_t fb = ((reg >> 23) ^ (word >> i)) & 1u;
             reg = ((reg << 1) & 0xFFFFFFu) ^ (fb ? POLY_A : 0u);
         }
         if (tb_words) {                              /* payload words only (the CRC24A tail is not output) */

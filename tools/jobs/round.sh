@@ -6,9 +6,9 @@ timeout 300 python __graft_entry__.py smoke > gpurun_out/${TAG}_smoke.log 2>&1; 
 timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_rc.txt
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/${TAG}_rc.txt
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${TAG}_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/${TAG}_rc.txt
-B="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-latency"
+B="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-latency --no-pool"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "timed/" --csv \
     --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_ncu_launches.log 2>&1; echo "ncu1 rc=$?" >> gpurun_out/${TAG}_rc.txt
-B1="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-latency"
+B1="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-latency --no-pool"
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:decode_kernel -s 3 -c 1 \
     -o gpurun_out/${TAG} $B1 > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu2 rc=$?" >> gpurun_out/${TAG}_rc.txt
