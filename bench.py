@@ -135,6 +135,12 @@ def cpu_baseline(sample, iters=8):
     of the same workload (decode only; inputs prepared beforehand)."""
     import oracle
     cores = len(os.sched_getaffinity(0))
+    cpu_model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu_model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
     t0 = time.perf_counter()
     r = oracle.decode_batch(*sample["args"], max_iters=iters, early_term=False, nthreads=cores, want_ext=False)
     dt = time.perf_counter() - t0
@@ -143,7 +149,7 @@ def cpu_baseline(sample, iters=8):
     return {"value": bits / dt / 1e6, "unit": "Mbit/s", "cores": cores, "kind": "oracle",
             "sample": f"{sample['n']} CBs of cfg4 (cells {c[0]}-{c[-1]}), {iters} fixed iterations, "
                       f"{dt:.2f} s wall x {cores} threads = {dt * cores:.1f} CPU-s (gcc -O2 scalar C)",
-            "ops": int(r["ops"]), "seconds": dt}
+            "ops": int(r["ops"]), "seconds": dt, "cpu_model": cpu_model}
 
 
 def run_reference(args):
@@ -234,6 +240,46 @@ def run_pool(args, seed=0):
             "mean_iters": float(its.mean()),
             "iters_hist": [int(x) for x in np.bincount(its, minlength=9)[1:9]],
             "gen_s": round(t_gen, 1)}
+
+
+def run_small_configs(seed=0):
+    """BASELINE cfg1 (32 x K=1056, 6 fixed iterations) and cfg2 (one 20 MHz subframe:
+    TB of 75,376 bits -> 13 x K=5824, CRC ET max 8) as single device launches:
+    batch / subframe latency (device, inputs resident), plus cfg2's TB verdict."""
+    from paper_1905_01141_b200 import batch as bmod
+    from paper_1905_01141_b200 import crn
+    from paper_1905_01141_b200 import workload as wlmod
+    out = {}
+    st = torch.cuda.current_stream()
+    for cfg in (1, 2):
+        wl = wlmod.make_workload(cfg, seed=seed, device="cuda")
+        b = bmod.build(wl)
+        plan = crn.Plan(b.desc)
+        bits, ok, it, _ = bmod.outputs(b, want_ext=False)
+        for _ in range(5):
+            plan.decode(*b.llr, wl.max_iters, wl.early_term, bits, ok, it, stream=st)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(50):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            plan.decode(*b.llr, wl.max_iters, wl.early_term, bits, ok, it, stream=st)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ts.append(1e3 * e0.elapsed_time(e1))
+        r = {"n_cb": b.n_cb, "K": sorted(set(int(k) for k in b.K)), "iters": wl.max_iters,
+             "early_term": bool(wl.early_term), "device_us_p50": float(np.percentile(ts, 50)),
+             "device_us_p99": float(np.percentile(ts, 99)), "crc_ok": int(ok[:b.n_cb].sum()),
+             "iters_used": [int(x) for x in it[:b.n_cb].cpu()]}
+        if cfg == 2:
+            tbs = np.zeros(1, crn.TB_DTYPE)
+            tbs[0] = (0, b.n_cb, int(wl.tbs[0]), 0)
+            tb_ok = torch.zeros(1, dtype=torch.uint8, device="cuda")
+            crn.tb_verdict_batch(tbs, b.desc, bits, ok, tb_ok)
+            r["tb_ok"] = int(tb_ok.item())
+            r["eb_n0_db"] = float(wl.tb_ebn0_db[0])
+        out[f"cfg{cfg}"] = r
+    return out
 
 
 def run_latency(args, seed=0):
@@ -424,6 +470,11 @@ def run_crn(args):
             out["latency"] = run_latency(args, seed=args.seed)
         except Exception as e:           # the throughput number stands without it
             out["latency"] = {"error": repr(e)}
+    if not args.no_pool and ws == 1:
+        try:
+            out["small_configs"] = run_small_configs(seed=args.seed)
+        except Exception as e:
+            out["small_configs"] = {"error": repr(e)}
     if not args.no_pool and ws == 1:
         try:
             out["pool_tti"] = run_pool(args, seed=args.seed)
