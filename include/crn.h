@@ -37,6 +37,7 @@ enum { CRN_OK = 0, CRN_EINVAL = -1, CRN_ECUDA = -2, CRN_ENOMEM = -3, CRN_ENODEV 
 enum { CRN_CRC_NONE = 0, CRN_CRC24A = 1, CRN_CRC24B = 2 };
 enum { CRN_DESC_ON_DEVICE = 1 };           /* flag bit 0 of crn_decode_batch_ex */
 enum { CRN_EXT_SCALED = 2 };               /* flag bit 1: scaled-extrinsic variant (below) */
+enum { CRN_PURGE = 4 };                    /* flag bit 2: purge waiting CBs of failed TBs (below) */
 /* Decoder variants: CRN_VARIANT_MAXLOG is the definition
  * every entry point computes by default (R2); CRN_VARIANT_SCALED
  * hands on floor(3 Le / 4) instead of each SISO's extrinsic Le, so the
@@ -61,7 +62,9 @@ enum { CRN_ET_NONE = 0, CRN_ET_CRC = 1, CRN_ET_MI = 2 };
  *            CRN_CRC_NONE (never passes; runs max iterations)          (R7)
  *   llr_off  element offset of the CB's K+4 LLRs in each of llr_sys/p1/p2
  *   bit_off  uint32-WORD offset of the CB's ceil(K/32) packed output words
- *   ext_off  element offset of the CB's K extrinsic outputs in ext_out      */
+ *   ext_off  element offset of the CB's K extrinsic outputs in ext_out
+ *   reserved the CB's TB id (0, 1, ...; -1 = none) when purging (CRN_PURGE /
+ *            crn_plan_set_purge), otherwise ignored                       */
 typedef struct {
     int32_t K, F, crc_kind, reserved;
     int64_t llr_off, bit_off, ext_off;
@@ -124,6 +127,20 @@ int crn_plan_decode(void *plan, const int16_t *llr_sys, const int16_t *llr_p1,
 /* Decoder variant of later crn_plan_decode / crn_plan_decode_host calls of this
  * plan (CRN_VARIANT_*; default CRN_VARIANT_MAXLOG).  CRN_EINVAL otherwise. */
 int crn_plan_set_variant(void *plan, int32_t variant);
+/* TB purge ("In case of decoding failure, the
+ * scheduler purges all CCDUs belonging to the same UE (TB)" -- Algorithm 2
+ * "purge waiting CCDU of the same TB"): with on = 1, a CB whose decoding fails
+ * (crc_ok = 0 at its stop) marks its TB (descriptor field reserved) lost, and
+ * a CB of a lost TB that has not started decoding yet is not decoded at all:
+ * crc_ok = 0, iters_used = 0, its out_bits / ext_out left untouched; CBs that
+ * do get decoded have exactly the outputs they have without purging, and
+ * every TB verdict is unchanged (a TB with a failed CB is lost either way).
+ * Which CBs get purged depends on timing.  CRN_EINVAL if a reserved field is
+ * < -1.  Applies to crn_plan_decode (crn_decode_batch_ex: flag CRN_PURGE). */
+int crn_plan_set_purge(void *plan, int32_t on);
+/* At most max_ctas persistent CTAs for this plan's decodes (0 = one per SM):
+ * shares the GPU with other work; with 1 the tasks run strictly in order. */
+int crn_plan_set_grid(void *plan, int32_t max_ctas);
 /* Number of decode-kernel launches one crn_plan_decode performs (for gpu_launches). */
 int crn_plan_launches(void *plan);
 void crn_plan_destroy(void *plan);

@@ -20,6 +20,7 @@ CRN_OK, CRN_EINVAL, CRN_ECUDA, CRN_ENOMEM, CRN_ENODEV = 0, -1, -2, -3, -4
 CRC_NONE, CRC24A, CRC24B = 0, 1, 2
 DESC_ON_DEVICE = 1
 EXT_SCALED = 2
+PURGE = 4
 VARIANT_MAXLOG, VARIANT_SCALED = 0, 1
 ET_NONE, ET_CRC, ET_MI = 0, 1, 2
 
@@ -60,6 +61,8 @@ _SIGS = {
     "crn_plan_decode": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp]),
     "crn_plan_launches": (C.c_int, [vp]),
     "crn_plan_set_variant": (C.c_int, [vp, C.c_int32]),
+    "crn_plan_set_purge": (C.c_int, [vp, C.c_int32]),
+    "crn_plan_set_grid": (C.c_int, [vp, C.c_int32]),
     "crn_plan_decode_host": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, C.c_int32, vp]),
     "crn_plan_chunks": (C.c_int, [vp]),
     "crn_stream_run": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int32, vp]),
@@ -94,6 +97,8 @@ def lib():
             raise CrnError(f"{SO} is not built: run paper_1905_01141_b200.build.build() (no CPU fallback)")
         L = C.CDLL(SO)
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("CRN_LIB") and not hasattr(L, name):
+                continue                    # A/B experiments may load an older build
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
@@ -186,6 +191,12 @@ class Plan:
 
     def set_variant(self, variant: int) -> None:
         _chk(lib().crn_plan_set_variant(self.h, variant), "crn_plan_set_variant")
+
+    def set_purge(self, on: bool) -> None:
+        _chk(lib().crn_plan_set_purge(self.h, int(on)), "crn_plan_set_purge")
+
+    def set_grid(self, max_ctas: int) -> None:
+        _chk(lib().crn_plan_set_grid(self.h, max_ctas), "crn_plan_set_grid")
 
     @property
     def chunks(self) -> int:

@@ -71,7 +71,7 @@ constexpr int S_WORDS = S_TAIL + MAXP * 16;
 static_assert(S_CH % 2 == 0, "chunk array must be 8-byte aligned");
 constexpr int SMEM_WORDS = S_WORDS;
 static_assert(SMEM_WORDS == CRN_SMEM_WORDS, "split-window sizing (crn_internal.h) must see the same shared memory");
-static_assert(SMEM_WORDS * 4 + 8704 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
+static_assert(SMEM_WORDS * 4 + 9728 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
 
 /* ---- optional phase profiler (build with -DCRN_PHASE_PROF; never in the product
  * build): lane 0 of warp 0 (a head warp) and of warp 6 (a tail warp) attribute
@@ -281,8 +281,16 @@ struct TaskSh {
 
 /* Row a9 bookkeeping after the CRC reduction: completion / early termination
  * per CB, CRC flag and iteration count.  Returns after the barrier. */
+/* TB purge state (crn_plan_set_purge): per CB of the task its TB id, per TB a
+ * "lost" flag in global memory. */
+struct Purge {
+    const int *tb;
+    uint8_t *dead;
+};
+
+template <bool PURGE>
 __device__ __forceinline__ void decide(TaskSh sh, int NP, int it, int max_iters, int et, int K, uint8_t *crc_ok,
-                                       uint8_t *iters_used) {
+                                       uint8_t *iters_used, Purge pg) {
     for (int e = threadIdx.x; e < 2 * NP; e += BLOCK) {
         if (sh.done[e]) continue;
         const bool pass = sh.kind[e] != CRN_CRC_NONE && sh.crc[e] == 0;
@@ -294,6 +302,8 @@ __device__ __forceinline__ void decide(TaskSh sh, int NP, int it, int max_iters,
             sh.fin[e] = 1;
             sh.done[e] = 1;
             crc_ok[sh.cb[e]] = pass;
+            if (PURGE && !pass && pg.tb[e] >= 0)              /* decoding failure: its TB is lost */
+                *(volatile uint8_t *)&pg.dead[pg.tb[e]] = 1;
             if (iters_used) iters_used[sh.cb[e]] = (uint8_t)it;
         }
     }
@@ -540,13 +550,13 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
     }
 }
 
-template <bool SCALE>
+template <bool SCALE, bool PURGE>
 __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
                                               const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
                                               const int16_t *__restrict__ l2, int max_iters, int et,
                                               uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok,
                                               uint8_t *__restrict__ iters_used, int16_t *__restrict__ ext_out,
-                                              const crn_tables &tab, u32 *sm, u32 tmem, TaskSh sh) {
+                                              const crn_tables &tab, u32 *sm, u32 tmem, TaskSh sh, Purge pg) {
     constexpr int W = 32;
     const int M = tk.M, NP = tk.n_pairs, T = NP * M;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -739,7 +749,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                 }
             }
             __syncthreads();
-            decide(sh, NP, it, max_iters, et, tk.K, crc_ok, iters_used);
+            decide<PURGE>(sh, NP, it, max_iters, et, tk.K, crc_ok, iters_used, pg);
             if (active) {
                 const int p = f.p, j = f.j;
 #pragma unroll
@@ -898,13 +908,13 @@ __device__ __forceinline__ void siso_gsplit(const GSplit &g, bool tail_thr, int 
     }
 }
 
-template <bool SCALE>
+template <bool SCALE, bool PURGE>
 __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
                                             const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
                                             const int16_t *__restrict__ l2, int max_iters, int et,
                                             uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok,
                                             uint8_t *__restrict__ iters_used, int16_t *__restrict__ ext_out,
-                                            const crn_tables &tab, u32 *sm, u32 tmem, TaskSh sh) {
+                                            const crn_tables &tab, u32 *sm, u32 tmem, TaskSh sh, Purge pg) {
     const int tid = threadIdx.x, warp = tid >> 5;
     GSplit g;
     g.W = tk.W;
@@ -1047,7 +1057,7 @@ __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_des
             }
         }
         __syncthreads();
-        decide(sh, NP, it, max_iters, et, K, crc_ok, iters_used);
+        decide<PURGE>(sh, NP, it, max_iters, et, K, crc_ok, iters_used, pg);
         for (int e = tid; e < 2 * NP * nw; e += BLOCK) {
             const int pl = e / nw, w = e - pl * nw;
             if (sh.fin[pl]) out_bits[desc[sh.cb[pl]].bit_off + w] = bits[e];
@@ -1074,7 +1084,7 @@ __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_des
 struct NextSh {
     int *task;
     crn_task *tk;
-    int *cb, *F, *kind;
+    int *cb, *F, *kind, *tb;
 };
 
 __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks, const crn_task *__restrict__ tasks,
@@ -1094,11 +1104,13 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
         if (cb < 0) {
             nx.F[e] = 0;
             nx.kind[e] = 0;
+            if (nx.tb) nx.tb[e] = -1;
             continue;
         }
         const crn_cb_desc &d = desc[cb];
         nx.F[e] = d.F;
         nx.kind[e] = d.crc_kind;
+        if (nx.tb) nx.tb[e] = d.reserved;
         const int64_t off = d.llr_off;
         const uint32_t bytes = 2u * (uint32_t)(t.K + 4);
 #pragma unroll
@@ -1111,16 +1123,21 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
     }
 }
 
+/* PURGE: the TB-purge instantiation (crn_plan_set_purge); the default one has no
+ * purge code at all, so the hot loops are compiled exactly as without it. */
+template <bool PURGE>
 __global__ void __launch_bounds__(BLOCK, 1)
 decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__ tasks, int n_tasks,
               const crn_pair *__restrict__ pairs, const int16_t *__restrict__ l0,
               const int16_t *__restrict__ l1, const int16_t *__restrict__ l2, int max_iters, int et,
               uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok, uint8_t *__restrict__ iters_used,
-              int16_t *__restrict__ ext_out, crn_tables tab, uint8_t *ws, int variant) {
+              int16_t *__restrict__ ext_out, crn_tables tab, uint8_t *ws, int variant, uint8_t *tb_dead_arg) {
+    uint8_t *const tb_dead = PURGE ? tb_dead_arg : nullptr;
     extern __shared__ __align__(16) u32 smem[];
     __shared__ int s_ntask, s_left;
     __shared__ crn_task s_ntk;
-    __shared__ int s_ncb[2 * MAXP], s_nF[2 * MAXP], s_nkind[2 * MAXP];
+    __shared__ int s_ncb[2 * MAXP], s_nF[2 * MAXP], s_nkind[2 * MAXP], s_ntb[2 * MAXP];
+    __shared__ int s_tb[2 * MAXP];
     __shared__ u32 s_tmem;
     __shared__ u32 s_crc[2 * MAXP];
     __shared__ int s_cb[2 * MAXP], s_F[2 * MAXP], s_kind[2 * MAXP];
@@ -1130,6 +1147,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     int *counter = (int *)ws;
     const int tid = threadIdx.x;
     const TaskSh sh{s_cb, s_F, s_kind, s_mi, s_mip, s_mitab, s_done, s_fin, s_crc, &s_left};
+    const Purge pg{s_tb, tb_dead};
     for (int i = tid; i < 256; i += BLOCK) s_mitab[i] = tab.mi_tab[i];
 
     /* TMEM: the whole 512 columns (one CTA per SM: the shared-memory footprint guarantees it) */
@@ -1144,7 +1162,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
 
     /* Tasks are claimed one ahead (claim_next): task t+1's metadata and LLRs
      * move on-chip / into L2 while task t decodes. */
-    const NextSh nx{&s_ntask, &s_ntk, s_ncb, s_nF, s_nkind};
+    const NextSh nx{&s_ntask, &s_ntk, s_ncb, s_nF, s_nkind, PURGE ? s_ntb : nullptr};
     prof_init();
     if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid);
     for (;;) {
@@ -1162,24 +1180,41 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             s_crc[e] = 0;
             s_mi[e] = 0;
             s_mip[e] = 0;
+            if (PURGE) s_tb[e] = s_ntb[e];
+            /* purge ("purge waiting CCDU of the same TB"): a waiting CB
+             * whose TB already lost a CB is not decoded: crc_ok = 0, iters_used = 0 */
+            if (PURGE && cb >= 0 && s_ntb[e] >= 0 && *(volatile uint8_t *)&tb_dead[s_ntb[e]]) {
+                s_done[e] = 1;
+                crc_ok[cb] = 0;
+                if (iters_used) iters_used[cb] = 0;
+            }
         }
         __syncthreads();                        /* next slots consumed */
         if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid);
+        if (PURGE) {                            /* a fully purged task is skipped */
+            if (tid == 0) {
+                int left = 0;
+                for (int e = 0; e < 2 * tk.n_pairs; e++) left += !s_done[e];
+                s_left = left;
+            }
+            __syncthreads();
+            if (s_left == 0) continue;
+        }
         prof_mark(P_FETCH);
         if (tk.W == 32) {
             if (variant == CRN_VARIANT_SCALED)
-                run_task_fast<true>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab, smem,
-                                    tmem, sh);
+                run_task_fast<true, PURGE>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab, smem,
+                                    tmem, sh, pg);
             else
-                run_task_fast<false>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
-                                     smem, tmem, sh);
+                run_task_fast<false, PURGE>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
+                                     smem, tmem, sh, pg);
         } else {
             if (variant == CRN_VARIANT_SCALED)
-                run_task_split<true>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
-                                     smem, tmem, sh);
+                run_task_split<true, PURGE>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
+                                     smem, tmem, sh, pg);
             else
-                run_task_split<false>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
-                                      smem, tmem, sh);
+                run_task_split<false, PURGE>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
+                                      smem, tmem, sh, pg);
         }
     }
     prof_flush();
@@ -1200,21 +1235,27 @@ extern "C" int crn_decode_grid(int device) {
      * query, -300 - occupancy (must be exactly 1: the CTA owns all TMEM columns) */
     static int configured = -1;
     if (configured != device) {
-        const cudaError_t e = cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes());
+        cudaError_t e = cudaFuncSetAttribute(decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem_bytes());
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes());
         if (e != cudaSuccess) return -100 - (int)e;
         configured = device;
     }
     int sms = 0, occ = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel, BLOCK, smem_bytes());
+    int occ2 = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<false>, BLOCK, smem_bytes());
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, decode_kernel<true>, BLOCK, smem_bytes());
     if (e != cudaSuccess) return -200 - (int)e;
-    if (occ != 1) return -300 - occ;
+    if (occ != 1 || occ2 != 1) return -300 - occ;
     return sms;
 }
 
 extern "C" int crn_decode_kernel_info(int32_t *static_smem, int32_t *dyn_smem, int32_t *max_dyn, int32_t *regs) {
     cudaFuncAttributes a;
-    if (cudaFuncGetAttributes(&a, decode_kernel) != cudaSuccess) return CRN_ECUDA;
+    if (cudaFuncGetAttributes(&a, decode_kernel<false>) != cudaSuccess) return CRN_ECUDA;
     *static_smem = (int32_t)a.sharedSizeBytes;
     *dyn_smem = (int32_t)smem_bytes();
     *max_dyn = a.maxDynamicSharedSizeBytes;
@@ -1226,12 +1267,16 @@ extern "C" int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_ta
                                  const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,
                                  int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it,
                                  int16_t *ext, const crn_tables *tab, void *ws, void *stream, int32_t grid,
-                                 int32_t variant) {
+                                 int32_t variant, uint8_t *tb_dead) {
     cudaStream_t st = (cudaStream_t)stream;
     if (cudaMemsetAsync(ws, 0, WS_HEAD, st) != cudaSuccess) return CRN_ECUDA;
     const int g = grid < n_tasks ? grid : n_tasks;
-    decode_kernel<<<g, BLOCK, smem_bytes(), st>>>(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits,
-                                                  ok, it, ext, *tab, (uint8_t *)ws, variant);
+    if (tb_dead)
+        decode_kernel<true><<<g, BLOCK, smem_bytes(), st>>>(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et,
+                                                            bits, ok, it, ext, *tab, (uint8_t *)ws, variant, tb_dead);
+    else
+        decode_kernel<false><<<g, BLOCK, smem_bytes(), st>>>(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters,
+                                                             et, bits, ok, it, ext, *tab, (uint8_t *)ws, variant, nullptr);
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
 }
 

@@ -377,7 +377,7 @@ static int plan_build(const crn_cb_desc *desc, int n, bool want_ext, cudaStream_
 int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn_task *d_tasks, int n_tasks,
                      const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,
                      int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
-                     void *ws, size_t ws_bytes, cudaStream_t st, int variant) {
+                     void *ws, size_t ws_bytes, cudaStream_t st, int variant, uint8_t *tb_dead, int grid_cap) {
     if (n_tasks == 0) return CRN_OK;
     if (!ws) {
         int rc = crn_get_ws(dev, (void *)st, crn_decode_ws_bytes(t->grid), &ws);
@@ -386,15 +386,25 @@ int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn
         return CRN_EINVAL;
     }
     return crn_launch_decode(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits, ok, it, ext,
-                             &t->tab, ws, (void *)st, t->grid, variant);
+                             &t->tab, ws, (void *)st, grid_cap > 0 && grid_cap < t->grid ? grid_cap : t->grid,
+                             variant, tb_dead);
 }
 
 static int launch(Plan *P, DevTables *t, const int16_t *l0, const int16_t *l1, const int16_t *l2,
                   int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
                   void *ws, size_t ws_bytes, cudaStream_t st) {
     if (P->n_cb == 0) return CRN_OK;
+    uint8_t *dead = nullptr;
+    if (P->purge && P->n_tb > 0) {
+        if (!P->d_tb_dead && cudaMalloc(&P->d_tb_dead, (size_t)P->n_tb) != cudaSuccess) {
+            cudaGetLastError();
+            return CRN_ENOMEM;
+        }
+        dead = P->d_tb_dead;
+        if (cudaMemsetAsync(dead, 0, (size_t)P->n_tb, st) != cudaSuccess) return CRN_ECUDA;
+    }
     return crn_launch_tasks(P->dev, t, P->d_desc, P->d_tasks, P->n_tasks, P->d_pairs, l0, l1, l2, max_iters, et,
-                            bits, ok, it, ext, ws, ws_bytes, st, P->variant);
+                            bits, ok, it, ext, ws, ws_bytes, st, P->variant, dead, P->grid_cap);
 }
 
 extern "C" int crn_plan_create(const crn_cb_desc *desc, int32_t n_cb, void **plan) {
@@ -433,6 +443,28 @@ extern "C" int crn_plan_set_variant(void *plan, int32_t variant) {
     return CRN_OK;
 }
 
+extern "C" int crn_plan_set_purge(void *plan, int32_t on) {
+    Plan *P = (Plan *)plan;
+    if (!P || on < 0 || on > 1) return CRN_EINVAL;
+    if (on) {                                   /* TB ids: reserved >= -1, n_tb = max + 1 */
+        int n_tb = 0;
+        for (const crn_cb_desc &d : P->h_desc) {
+            if (d.reserved < -1) return CRN_EINVAL;
+            n_tb = std::max(n_tb, d.reserved + 1);
+        }
+        P->n_tb = n_tb;
+    }
+    P->purge = on;
+    return CRN_OK;
+}
+
+extern "C" int crn_plan_set_grid(void *plan, int32_t max_ctas) {
+    Plan *P = (Plan *)plan;
+    if (!P || max_ctas < 0) return CRN_EINVAL;
+    P->grid_cap = max_ctas;
+    return CRN_OK;
+}
+
 extern "C" int crn_plan_launches(void *plan) {
     Plan *P = (Plan *)plan;
     return (P && P->n_cb) ? 1 : 0;
@@ -442,6 +474,7 @@ extern "C" void crn_plan_destroy(void *plan) {
     Plan *P = (Plan *)plan;
     if (!P) return;
     if (P->pipe) crn_pipe_destroy(P->pipe);
+    if (P->d_tb_dead) cudaFree(P->d_tb_dead);
     if (P->mem) cudaFree(P->mem);
     delete P;
 }
@@ -450,7 +483,8 @@ extern "C" int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb, const 
                                    const int16_t *l1, const int16_t *l2, int32_t max_iters,
                                    int32_t et, int32_t flags, uint32_t *bits, uint8_t *ok,
                                    uint8_t *it, int16_t *ext, void *ws, size_t ws_bytes, void *stream) {
-    if (n_cb < 0 || (flags & ~(CRN_DESC_ON_DEVICE | CRN_EXT_SCALED)) || max_iters < 1 || max_iters > CRN_MAX_ITERS ||
+    if (n_cb < 0 || (flags & ~(CRN_DESC_ON_DEVICE | CRN_EXT_SCALED | CRN_PURGE)) || max_iters < 1 ||
+        max_iters > CRN_MAX_ITERS ||
         et < 0 || et > CRN_ET_MI)
         return CRN_EINVAL;
     if (n_cb == 0) return CRN_OK;
@@ -479,7 +513,26 @@ extern "C" int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb, const 
         if (P.mem) cudaFreeAsync(P.mem, st);
         return rc;
     }
-    rc = launch(&P, t, l0, l1, l2, max_iters, et, bits, ok, it, ext, ws, ws_bytes, st);
+    uint8_t *dead = nullptr;
+    if (flags & CRN_PURGE) {
+        int n_tb = 0;
+        for (int i = 0; i < n_cb; i++) {
+            if (hdesc[i].reserved < -1) { cudaFreeAsync(P.mem, st); return CRN_EINVAL; }
+            n_tb = std::max(n_tb, hdesc[i].reserved + 1);
+        }
+        if (n_tb > 0) {
+            if (cudaMallocAsync((void **)&dead, (size_t)n_tb, st) != cudaSuccess) {
+                cudaGetLastError();
+                cudaFreeAsync(P.mem, st);
+                return CRN_ENOMEM;
+            }
+            cudaMemsetAsync(dead, 0, (size_t)n_tb, st);
+        }
+    }
+    rc = P.n_cb ? crn_launch_tasks(P.dev, t, P.d_desc, P.d_tasks, P.n_tasks, P.d_pairs, l0, l1, l2, max_iters, et,
+                                   bits, ok, it, ext, ws, ws_bytes, st, P.variant, dead)
+                : CRN_OK;
+    if (dead) cudaFreeAsync(dead, st);
     cudaFreeAsync(P.mem, st);
     return rc;
 }

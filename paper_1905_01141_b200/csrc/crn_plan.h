@@ -27,6 +27,10 @@ struct Plan {
     void *mem = nullptr;          /* one allocation holding the three arrays */
     std::vector<crn_cb_desc> h_desc;   /* host copy (kept for the host-buffer pipeline) */
     int variant = CRN_VARIANT_MAXLOG;  /* decoder variant (crn_plan_set_variant) */
+    int purge = 0;                     /* TB purge (crn_plan_set_purge) */
+    int grid_cap = 0;                  /* persistent-grid limit (crn_plan_set_grid), 0 = one CTA per SM */
+    int n_tb = 0;                      /* TB ids in the descriptors' reserved field: 0..n_tb-1 */
+    uint8_t *d_tb_dead = nullptr;      /* per TB: a CB of it failed (purge) */
     HostPipe *pipe = nullptr;
 };
 
@@ -44,7 +48,8 @@ void crn_build_tasks(const crn_cb_desc *d, const int *idx, int n_idx, std::vecto
 int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn_task *d_tasks, int n_tasks,
                      const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,
                      int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
-                     void *ws, size_t ws_bytes, cudaStream_t st, int variant = CRN_VARIANT_MAXLOG);
+                     void *ws, size_t ws_bytes, cudaStream_t st, int variant = CRN_VARIANT_MAXLOG,
+                     uint8_t *tb_dead = nullptr, int grid_cap = 0);
 /* Records the CUDA error behind a CRN_ECUDA / CRN_ENOMEM for crn_last_error(). */
 int crn_cuda_fail(cudaError_t e, const char *where, int code);
 /* Frees the host pipeline of a plan (crn_runtime.cpp). */

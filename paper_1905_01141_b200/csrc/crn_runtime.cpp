@@ -188,7 +188,7 @@ extern "C" int crn_plan_decode_host(void *plan, const int16_t *h0, const int16_t
         cudaStreamWaitEvent(st, p->ev_in[c], 0);
         rc = crn_launch_tasks(dev, t, P->d_desc, p->d_tasks + k.task0, k.n_tasks, p->d_pairs, p->d_l[0], p->d_l[1],
                               p->d_l[2], max_iters, et, p->d_bits, p->d_ok, h_it ? p->d_it : nullptr, nullptr,
-                              nullptr, 0, st, P->variant);
+                              nullptr, 0, st, P->variant, nullptr, P->grid_cap);
         if (rc) return rc;
         cudaEventRecord(p->ev_comp[c], st);
         cudaStreamWaitEvent(p->s_out, p->ev_comp[c], 0);

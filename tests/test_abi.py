@@ -159,7 +159,7 @@ def test_new_entry_points_validate_on_host():
     d["K"], d["crc_kind"] = 1056, crn.CRC24B
     assert L.crn_decode_batch_ex(d.ctypes.data, 1, fake, fake, fake, 8, 3, 0, fake, fake, None, None, None, 0,
                                  None) == crn.CRN_EINVAL                    # unknown stopping rule
-    assert L.crn_decode_batch_ex(d.ctypes.data, 1, fake, fake, fake, 8, 1, 4, fake, fake, None, None, None, 0,
+    assert L.crn_decode_batch_ex(d.ctypes.data, 1, fake, fake, fake, 8, 1, 8, fake, fake, None, None, None, 0,
                                  None) == crn.CRN_EINVAL                    # unknown flag bit
     tim = (crn.TtiTiming * 1)()
     grp = (crn.TtiGroup * 1)()

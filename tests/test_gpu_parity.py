@@ -508,3 +508,49 @@ def test_rate_matched_chain_decodes_like_oracle(orc):
     r = run_oracle(b2, np.arange(b.n_cb), 8, True)
     assert_parity(b, g, r, np.arange(b.n_cb))
     assert g["crc_ok"].mean() > 0.5
+
+
+def test_tb_purge_of_waiting_cbs(orc):
+    """The paper's purge (crn_plan_set_purge): with the TB id in
+    each descriptor, a CB that has not started when a sibling fails is not
+    decoded (crc_ok = 0, iters_used = 0); every decoded CB equals the oracle and
+    the no-purge run, purged CBs belong to TBs with a failed decoded CB, and the
+    TB verdicts do not change.  A one-CTA grid makes the order strict, so purges
+    must happen; the full grid is checked for consistency only."""
+    b = _full(3, 0.3)
+    for i in range(0, b.n_cb, 4):                          # kill a quarter of the CBs: they fail at max
+        o, K = int(b.desc["llr_off"][i]), int(b.desc["K"][i])
+        for x in b.llr:
+            x[o:o + K + 4] = 0
+    desc = b.desc.copy()
+    desc["reserved"] = b.cb_tb
+    idx = np.arange(b.n_cb)
+    r = run_oracle(b, idx, 8, True)
+    tbs, nw = _tb_table(b)
+    verdicts = []
+    for grid in (0, 1):
+        for purge in (False, True):
+            p = crn.Plan(desc)
+            p.set_grid(grid)
+            p.set_purge(purge)
+            bits, ok, it, ext = bmod.outputs(b)
+            p.decode(*b.llr, 8, True, bits, ok, it, ext)
+            tb_ok = torch.zeros(tbs.size, dtype=torch.uint8, device="cuda")
+            crn.tb_verdict_batch(tbs, b.desc, bits, ok, tb_ok)
+            torch.cuda.synchronize()
+            g = dict(words=bits.cpu().numpy().view(np.uint32), crc_ok=ok.cpu().numpy()[:b.n_cb],
+                     iters=it.cpu().numpy()[:b.n_cb], ext=ext.cpu().numpy())
+            verdicts.append(tb_ok.cpu().numpy())
+            dec = np.flatnonzero(g["iters"] > 0)
+            purged = np.flatnonzero(g["iters"] == 0)
+            assert_parity(b, g, r if dec.size == b.n_cb else run_oracle(b, dec, 8, True), dec)
+            if not purge:
+                assert purged.size == 0
+            else:
+                failed_tb = set(b.cb_tb[dec[g["crc_ok"][dec] == 0]])
+                assert all(b.cb_tb[i] in failed_tb for i in purged)
+                assert np.all(g["crc_ok"][purged] == 0)
+                if grid == 1:
+                    assert purged.size > 0
+            p.close()
+    assert all(np.array_equal(v, verdicts[0]) for v in verdicts)
