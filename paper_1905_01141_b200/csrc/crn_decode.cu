@@ -436,7 +436,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
     /* the 32 shared loads are issued LA steps ahead of their use, in processing
      * order (volatile asm keeps that order against the TMEM stores), so the
      * warps do not all queue 32 loads at the phase start */
-    constexpr int LA = 2;
+    constexpr int LA = 1;
     const u32 lp_s = smem_addr(lp);
     auto ld = [&](int s) {
         if (zero_la) av[s] = 0u;
