@@ -306,19 +306,27 @@ def run_latency(args, seed=0):
             d["bit_off"] = np.concatenate([[0], np.cumsum((K + 31) // 32)[:-1]]) if K.size else K
             src = torch.from_numpy(np.concatenate([np.arange(int(o), int(o) + int(k) + 4)
                                                    for o, k in zip(b.desc["llr_off"][sel], K)])).cuda()
-            hl = [x[src].cpu().pin_memory() for x in b.llr]
+            buf = torch.stack([x[src] for x in b.llr]).cpu().pin_memory()   # streams contiguous: one upload
+            hl = [buf[0], buf[1], buf[2]]
             nw = max(int(((K + 31) // 32).sum()), 1)
+            nc = max(sel.size, 1)
+            ob = torch.zeros(4 * nw + 2 * nc, dtype=torch.uint8).pin_memory()   # bits | crc_ok | iters: one download
             grp.append(dict(desc=d, l0=hl[0], l1=hl[1], l2=hl[2],
-                            bits=torch.zeros(nw, dtype=torch.int32).pin_memory(),
-                            ok=torch.zeros(max(sel.size, 1), dtype=torch.uint8).pin_memory(),
-                            it=torch.zeros(max(sel.size, 1), dtype=torch.uint8).pin_memory(),
+                            bits=ob[:4 * nw].view(torch.int32), ok=ob[4 * nw:4 * nw + nc],
+                            it=ob[4 * nw + nc:4 * nw + 2 * nc],
                             sum_k=int(K.sum()), n_cb=int(sel.size), info=int((d["K"] - d["F"] - 24).sum())))
         distinct.append(grp)
     t_gen = time.perf_counter() - t_gen
     groups = [g for t in range(args.lat_ttis) for g in distinct[t % args.lat_distinct]]
-    tim = crn.stream_run(groups, args.lat_ttis, n_groups, 1000.0, 8, True)
+    zflag = crn.STREAM_ZEROCOPY if os.environ.get("CRN_LAT_ZEROCOPY") == "1" else 0
+    tim = crn.stream_run(groups, args.lat_ttis, n_groups, 1000.0, 8, True, flags=zflag)
     skip = min(10, args.lat_ttis // 10)
     lat, dev = tim["latency_us"][skip:], tim["device_us"][skip:]
+    sub = (tim["submitted_us"] - tim["release_us"])[skip:]
+    n_st = min(args.lat_ttis, 200)                  # a shorter run with the stage events on (they cost time)
+    tim_s = crn.stream_run(groups[:n_st * n_groups], n_st, n_groups, 1000.0, 8, True, flags=crn.STREAM_STAGES | zflag)
+    stages = {k: float(np.percentile(tim_s[k][skip:], 50))
+              for k in ("upload_us", "decode_start_us", "decode_end_us", "device_us", "latency_us")}
 
     its = np.concatenate([g["it"].numpy()[:g["n_cb"]] for grp in distinct for g in grp])
     sum_k = [sum(g["sum_k"] for g in grp) for grp in distinct]
@@ -329,6 +337,8 @@ def run_latency(args, seed=0):
             "measured_ttis": int(lat.size), "p50_us": float(np.percentile(lat, 50)),
             "p99_us": float(np.percentile(lat, 99)), "max_us": float(lat.max()), "mean_us": float(lat.mean()),
             "device_p50_us": float(np.percentile(dev, 50)), "device_p99_us": float(np.percentile(dev, 99)),
+            "host_submit_p50_us": float(np.percentile(sub, 50)),
+            "stages_p50_us": stages,
             "deadline_us": 2000.0, "deadline_misses": int((lat > 2000.0).sum()),
             "mean_iters": float(its.mean()), "mean_sum_k_per_tti": float(np.mean(sum_k)),
             "gen_s": round(t_gen, 1),

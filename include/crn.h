@@ -187,9 +187,14 @@ typedef struct {
  * release (the pacer's release instant), submitted (all groups enqueued),
  * complete (the last group's downloads observed done by the completion
  * thread), latency = complete - release, device = span of the TTI's GPU work
- * (first upload start .. last download end, CUDA events). */
+ * (first upload start .. last download end, CUDA events).  The stage split of
+ * the device span (the paper's captor KPIs: pre-processing,
+ * channel coding, post-processing), CUDA events relative to the TTI's first
+ * upload start: upload_us = when the last group's inputs are on the device,
+ * decode_start_us / decode_end_us = first decode launch start / last end. */
 typedef struct {
     double release_us, submitted_us, complete_us, latency_us, device_us;
+    double upload_us, decode_start_us, decode_end_us;
 } crn_tti_timing;
 
 /* Paced streaming decode (Algorithm 2 as a GPU executor;
@@ -207,8 +212,18 @@ int crn_stream_run(const crn_tti_group *groups, int32_t n_tti, int32_t n_groups,
  * the uploads and downloads but decodes each TTI with ONE launch over all
  * groups' CBs (on an internal decode stream that waits for every group's
  * upload; each group's download waits for the decode): the groups' persistent
- * kernels no longer split the SMs between them.  Other flag bits: CRN_EINVAL. */
-enum { CRN_STREAM_MERGED = 1 };
+ * kernels no longer split the SMs between them.  CRN_STREAM_STAGES records
+ * the stage split of crn_tti_timing (three more events per group and TTI;
+ * otherwise those fields are -1; always recorded in merged mode).  Other flag
+ * bits: CRN_EINVAL.  When a group's out_bits, crc_ok and iters_used are one
+ * host block (crc_ok right after the n_words words, iters_used right after
+ * crc_ok) they come back in a single copy; likewise llr_sys/p1/p2 laid out
+ * back to back go up in one copy.  CRN_STREAM_ZEROCOPY (not with MERGED):
+ * the decode kernel reads each group's descriptors, tasks and LLRs straight
+ * from pinned host memory and writes its bits / crc_ok / iters_used straight
+ * into the host buffers (over PCIe, no copy stage; one launch per group and
+ * TTI); every host buffer must be pinned (CRN_EINVAL otherwise). */
+enum { CRN_STREAM_MERGED = 1, CRN_STREAM_STAGES = 2, CRN_STREAM_ZEROCOPY = 4 };
 int crn_stream_run_ex(const crn_tti_group *groups, int32_t n_tti, int32_t n_groups, double period_us,
                       int32_t max_iters, int32_t early_term, int32_t flags, crn_tti_timing *timing);
 

@@ -41,7 +41,7 @@ class TtiGroup(C.Structure):
 
 class TtiTiming(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("release_us", "submitted_us", "complete_us", "latency_us",
-                                          "device_us")]
+                                          "device_us", "upload_us", "decode_start_us", "decode_end_us")]
 
 
 class CrnError(RuntimeError):
@@ -219,6 +219,8 @@ class Plan:
 
 
 STREAM_MERGED = 1
+STREAM_STAGES = 2
+STREAM_ZEROCOPY = 4
 
 
 def stream_run(groups, n_tti: int, n_groups: int, period_us: float, max_iters: int, early_term: bool,

@@ -1267,9 +1267,9 @@ extern "C" int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_ta
                                  const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,
                                  int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it,
                                  int16_t *ext, const crn_tables *tab, void *ws, void *stream, int32_t grid,
-                                 int32_t variant, uint8_t *tb_dead) {
+                                 int32_t variant, uint8_t *tb_dead, int32_t ws_zeroed) {
     cudaStream_t st = (cudaStream_t)stream;
-    if (cudaMemsetAsync(ws, 0, WS_HEAD, st) != cudaSuccess) return CRN_ECUDA;
+    if (!ws_zeroed && cudaMemsetAsync(ws, 0, WS_HEAD, st) != cudaSuccess) return CRN_ECUDA;
     const int g = grid < n_tasks ? grid : n_tasks;
     if (tb_dead)
         decode_kernel<true><<<g, BLOCK, smem_bytes(), st>>>(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et,

@@ -377,7 +377,8 @@ static int plan_build(const crn_cb_desc *desc, int n, bool want_ext, cudaStream_
 int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn_task *d_tasks, int n_tasks,
                      const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,
                      int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
-                     void *ws, size_t ws_bytes, cudaStream_t st, int variant, uint8_t *tb_dead, int grid_cap) {
+                     void *ws, size_t ws_bytes, cudaStream_t st, int variant, uint8_t *tb_dead, int grid_cap,
+                     bool ws_zeroed) {
     if (n_tasks == 0) return CRN_OK;
     if (!ws) {
         int rc = crn_get_ws(dev, (void *)st, crn_decode_ws_bytes(t->grid), &ws);
@@ -387,7 +388,7 @@ int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn
     }
     return crn_launch_decode(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits, ok, it, ext,
                              &t->tab, ws, (void *)st, grid_cap > 0 && grid_cap < t->grid ? grid_cap : t->grid,
-                             variant, tb_dead);
+                             variant, tb_dead, ws_zeroed ? 1 : 0);
 }
 
 static int launch(Plan *P, DevTables *t, const int16_t *l0, const int16_t *l1, const int16_t *l2,

@@ -78,7 +78,7 @@ int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_tasks, int32_
                       const int16_t *l2, int32_t max_iters, int32_t early_term,
                       uint32_t *out_bits, uint8_t *crc_ok, uint8_t *iters_used, int16_t *ext_out,
                       const crn_tables *tab, void *ws, void *stream, int32_t grid, int32_t variant,
-                      uint8_t *tb_dead);
+                      uint8_t *tb_dead, int32_t ws_zeroed);
 size_t crn_decode_ws_bytes(int32_t grid);
 int crn_decode_grid(int device);
 /* crn_encode.cu */

@@ -49,7 +49,8 @@ int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn
                      const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,
                      int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
                      void *ws, size_t ws_bytes, cudaStream_t st, int variant = CRN_VARIANT_MAXLOG,
-                     uint8_t *tb_dead = nullptr, int grid_cap = 0);
+                     uint8_t *tb_dead = nullptr, int grid_cap = 0,
+                     bool ws_zeroed = false);   /* the task counter in ws is already 0 (uploaded with a blob) */
 /* Records the CUDA error behind a CRN_ECUDA / CRN_ENOMEM for crn_last_error(). */
 int crn_cuda_fail(cudaError_t e, const char *where, int code);
 /* Frees the host pipeline of a plan (crn_runtime.cpp). */

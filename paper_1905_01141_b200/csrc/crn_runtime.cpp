@@ -215,6 +215,7 @@ namespace {
 
 struct GroupRes {
     cudaStream_t st = nullptr;
+    int *ctr = nullptr;            /* zero copy: one zeroed task counter per TTI (no per-TTI memset) */
     void *dmem = nullptr;          /* device: plan blob + LLRs + outputs */
     size_t dbytes = 0;
     void *hblob[2] = {nullptr, nullptr};  /* pinned host plan blobs, double-buffered by TTI parity */
@@ -227,16 +228,19 @@ struct Layout {
     size_t o_desc, o_tasks, o_pairs, o_l, bl, o_bits, o_ok, o_it, tot;
 };
 
+/* [task counter (zeroed in the host blob, used as the decode workspace) | desc |
+ * tasks | pairs] = the uploaded blob; then the three LLR streams; then bits, crc_ok
+ * and iters_used back to back (one download when the host buffers are too). */
 Layout layout(int n_cb, int n_tasks, int n_pairs, int64_t n_llr, int64_t n_words) {
     Layout L;
-    L.o_desc = 0;
-    L.o_tasks = align256(sizeof(crn_cb_desc) * n_cb);
+    L.o_desc = 256;
+    L.o_tasks = L.o_desc + align256(sizeof(crn_cb_desc) * n_cb);
     L.o_pairs = L.o_tasks + align256(sizeof(crn_task) * n_tasks);
     L.o_l = L.o_pairs + align256(sizeof(crn_pair) * n_pairs);
     L.bl = align256(sizeof(int16_t) * n_llr);
     L.o_bits = L.o_l + 3 * L.bl;
-    L.o_ok = L.o_bits + align256(4 * n_words);
-    L.o_it = L.o_ok + align256(n_cb);
+    L.o_ok = L.o_bits + 4 * n_words;
+    L.o_it = L.o_ok + n_cb;
     L.tot = L.o_it + align256(n_cb);
     return L;
 }
@@ -246,9 +250,12 @@ Layout layout(int n_cb, int n_tasks, int n_pairs, int64_t n_llr, int64_t n_words
 extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t n_groups, double period_us,
                                  int32_t max_iters, int32_t et, int32_t flags, crn_tti_timing *timing) {
     if (!g || !timing || n_tti < 1 || n_groups < 1 || n_groups > 64 || period_us < 0 || max_iters < 1 ||
-        max_iters > CRN_MAX_ITERS || et < 0 || et > CRN_ET_MI || (flags & ~CRN_STREAM_MERGED))
+        max_iters > CRN_MAX_ITERS || et < 0 || et > CRN_ET_MI ||
+        (flags & ~(CRN_STREAM_MERGED | CRN_STREAM_STAGES | CRN_STREAM_ZEROCOPY)) ||
+        ((flags & CRN_STREAM_MERGED) && (flags & CRN_STREAM_ZEROCOPY)))
         return CRN_EINVAL;
-    const bool merged = flags & CRN_STREAM_MERGED;
+    const bool merged = flags & CRN_STREAM_MERGED, stages = merged || (flags & CRN_STREAM_STAGES);
+    const bool zc = flags & CRN_STREAM_ZEROCOPY;
     int dev;
     DevTables *t;
     int rc = crn_get_ctx(&dev, &t);
@@ -273,6 +280,17 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
                 g_words[x] = std::max(g_words[x], q.desc[i].bit_off + (q.desc[i].K + 31) / 32);
             }
             if (g_llr[x] > q.n_llr || g_words[x] > q.n_words) return CRN_EINVAL;
+            if (zc && q.n_cb > 0) {                     /* the kernel reads / writes these directly */
+                const void *ptrs[6] = {q.llr_sys, q.llr_p1, q.llr_p2, q.out_bits, q.crc_ok, q.iters_used};
+                for (const void *pp : ptrs) {
+                    if (!pp) continue;
+                    cudaPointerAttributes at;
+                    if (cudaPointerGetAttributes(&at, pp) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+                        cudaGetLastError();
+                        return CRN_EINVAL;
+                    }
+                }
+            }
             const Layout L = layout(q.n_cb, q.n_cb, q.n_cb, g_llr[x], g_words[x]);   /* tasks, pairs <= CBs */
             need[gi] = std::max(need[gi], L.tot);
             hneed[gi] = std::max(hneed[gi], L.o_l);
@@ -294,6 +312,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             }
             if (r.dmem) cudaFree(r.dmem);
             if (r.ws) cudaFree(r.ws);
+            if (r.ctr) cudaFree(r.ctr);
             if (r.st) cudaStreamDestroy(r.st);
         }
     };
@@ -307,7 +326,9 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             (hn && cudaMallocHost(&r.hblob[1], std::max<size_t>(hn, 256)) != cudaSuccess) ||
             cudaEventCreateWithFlags(&r.ev_blob[0], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&r.ev_blob[1], cudaEventDisableTiming) != cudaSuccess ||
-            ((!merged || dec) && cudaMalloc(&r.ws, crn_decode_ws_bytes(t->grid)) != cudaSuccess)) {
+            ((!merged || dec) && cudaMalloc(&r.ws, crn_decode_ws_bytes(t->grid)) != cudaSuccess) ||
+            (zc && (cudaMalloc(&r.ctr, sizeof(int) * 64 * (size_t)n_tti) != cudaSuccess ||
+                    cudaMemset(r.ctr, 0, sizeof(int) * 64 * (size_t)n_tti) != cudaSuccess))) {
             cudaGetLastError();
             cleanup();
             return CRN_ENOMEM;
@@ -315,22 +336,29 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
     }
     /* per (TTI, group): timing events (start before the uploads, end after the downloads) */
     std::vector<cudaEvent_t> ev0(NG), ev1(NG), ev_in(merged ? n_groups : 0);
+    std::vector<cudaEvent_t> evu(NG), evk0(NG), evk1(NG);   /* stage split: upload done, decode start / end */
     for (int64_t x = 0; x < NG; x++) {
         cudaEventCreate(&ev0[x]);
         cudaEventCreate(&ev1[x]);
+        cudaEventCreate(&evu[x]);
+        cudaEventCreate(&evk0[x]);
+        cudaEventCreate(&evk1[x]);
     }
     for (auto &e : ev_in) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     cudaEvent_t ev_dec = nullptr;
     if (merged) cudaEventCreateWithFlags(&ev_dec, cudaEventDisableTiming);
-    std::vector<double> done_us(NG, 0.0), rel_us(n_tti, 0.0), sub_us(n_tti, 0.0);
-    std::atomic<int64_t> submitted{0};
+    std::vector<double> done_us(NG, 0.0), rel_us(n_tti, 0.0), sub_us(n_tti, 0.0), gsub_us(NG, 0.0);
+    std::vector<std::atomic<int>> submitted(n_groups);       /* per group: TTIs enqueued so far */
+    for (auto &a : submitted) a.store(0);
     std::atomic<bool> abort_flag{false};
     const Clock::time_point t0 = Clock::now() + std::chrono::milliseconds(2);
+    for (int ti = 0; ti < n_tti; ti++) rel_us[ti] = period_us * ti;
 
     /* completion thread (the "captor"): time-stamps each (TTI, group) when its end event fires */
     std::thread watcher([&]() {
         for (int64_t x = 0; x < NG; x++) {
-            while (submitted.load(std::memory_order_acquire) <= x) {
+            const int ti = (int)(x / n_groups), gi = (int)(x % n_groups);
+            while (submitted[gi].load(std::memory_order_acquire) <= ti) {
                 if (abort_flag.load()) return;
                 std::this_thread::yield();
             }
@@ -343,61 +371,127 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
         }
     });
 
+    auto release = [&](int ti) {                /* pacer: TTI ti is released at t0 + ti * period */
+        const Clock::time_point rel = t0 + std::chrono::duration_cast<Clock::duration>(
+                                               std::chrono::duration<double, std::micro>(period_us * ti));
+        while (Clock::now() < rel) {
+        }
+    };
+    /* one cell group's share of one TTI on its own stream: row a1 on the host
+     * (bucket / pair / task its CBs), then upload -> decode -> download */
+    auto submit_group = [&](int ti, int gi) -> int {
+        const int64_t x = (int64_t)ti * n_groups + gi;
+        const crn_tti_group &q = g[x];
+        GroupRes &r = G[gi];
+        int src = CRN_OK;
+        cudaEventRecord(ev0[x], r.st);
+        if (q.n_cb > 0) {
+            std::vector<crn_task> tasks;
+            std::vector<crn_pair> pairs;
+            std::vector<int> sel(q.n_cb);
+            for (int i = 0; i < q.n_cb; i++) sel[i] = i;
+            crn_build_tasks(q.desc, sel.data(), q.n_cb, tasks, pairs);
+            const int64_t n_llr = g_llr[x], n_words = g_words[x];
+            const Layout L = layout(q.n_cb, (int)tasks.size(), (int)pairs.size(), n_llr, n_words);
+            const int b = ti & 1;
+            if (ti >= 2) {                              /* blob slot b was last uploaded by TTI ti-2 */
+                const cudaEvent_t prev = ev1[x - 2 * (int64_t)n_groups];
+                while (cudaEventQuery(prev) == cudaErrorNotReady) {
+                }
+            }
+            uint8_t *hb = (uint8_t *)r.hblob[b];
+            memset(hb, 0, L.o_desc);                    /* the decode's task counter */
+            memcpy(hb + L.o_desc, q.desc, sizeof(crn_cb_desc) * q.n_cb);
+            memcpy(hb + L.o_tasks, tasks.data(), sizeof(crn_task) * tasks.size());
+            memcpy(hb + L.o_pairs, pairs.data(), sizeof(crn_pair) * pairs.size());
+            if (zc) {
+                /* zero copy: the kernel reads the pinned blob and LLRs and writes the
+                 * results over PCIe itself -- one launch per group and TTI, no copy stage */
+                if (stages) {
+                    cudaEventRecord(evu[x], r.st);
+                    cudaEventRecord(evk0[x], r.st);
+                }
+                src = crn_launch_tasks(dev, t, (const crn_cb_desc *)(hb + L.o_desc), (const crn_task *)(hb + L.o_tasks),
+                                       (int)tasks.size(), (const crn_pair *)(hb + L.o_pairs), q.llr_sys, q.llr_p1,
+                                       q.llr_p2, max_iters, et, q.out_bits, q.crc_ok, q.iters_used, nullptr,
+                                       r.ctr + 64 * (size_t)ti, crn_decode_ws_bytes(t->grid), r.st, CRN_VARIANT_MAXLOG,
+                                       nullptr, 0, true);
+                if (stages) cudaEventRecord(evk1[x], r.st);
+                cudaEventRecord(ev1[x], r.st);
+                gsub_us[x] = us_since(t0, Clock::now());
+                submitted[gi].store(ti + 1, std::memory_order_release);
+                return src;
+            }
+            uint8_t *dm = (uint8_t *)r.dmem;
+            cudaMemcpyAsync(dm, hb, L.o_l, cudaMemcpyHostToDevice, r.st);
+            const int16_t *hs[3] = {q.llr_sys, q.llr_p1, q.llr_p2};
+            int16_t *dl[3];
+            for (int s = 0; s < 3; s++) dl[s] = (int16_t *)(dm + L.o_l + s * L.bl);
+            if (q.llr_p1 == q.llr_sys + n_llr && q.llr_p2 == q.llr_p1 + n_llr && L.bl == sizeof(int16_t) * n_llr)
+                cudaMemcpyAsync(dl[0], hs[0], 3 * sizeof(int16_t) * n_llr, cudaMemcpyHostToDevice, r.st);
+            else                                            /* the three streams: one copy if contiguous */
+                for (int s = 0; s < 3; s++)
+                    cudaMemcpyAsync(dl[s], hs[s], sizeof(int16_t) * n_llr, cudaMemcpyHostToDevice, r.st);
+            uint32_t *dbits = (uint32_t *)(dm + L.o_bits);
+            uint8_t *dok = dm + L.o_ok, *dit = dm + L.o_it;
+            if (stages) {
+                cudaEventRecord(evu[x], r.st);
+                cudaEventRecord(evk0[x], r.st);
+            }
+            src = crn_launch_tasks(dev, t, (const crn_cb_desc *)(dm + L.o_desc), (const crn_task *)(dm + L.o_tasks),
+                                   (int)tasks.size(), (const crn_pair *)(dm + L.o_pairs), dl[0], dl[1], dl[2],
+                                   max_iters, et, dbits, dok, q.iters_used ? dit : nullptr, nullptr, dm,
+                                   crn_decode_ws_bytes(t->grid), r.st, CRN_VARIANT_MAXLOG, nullptr, 0, true);
+            if (stages) cudaEventRecord(evk1[x], r.st);
+            const bool packed = (const uint8_t *)q.crc_ok == (const uint8_t *)(q.out_bits + n_words) &&
+                                (!q.iters_used || q.iters_used == q.crc_ok + q.n_cb);
+            if (packed)                                     /* bits | crc_ok | iters_used in one download */
+                cudaMemcpyAsync(q.out_bits, dbits, 4 * (size_t)n_words + (size_t)q.n_cb * (q.iters_used ? 2 : 1),
+                                cudaMemcpyDeviceToHost, r.st);
+            else {
+                cudaMemcpyAsync(q.out_bits, dbits, 4 * (size_t)n_words, cudaMemcpyDeviceToHost, r.st);
+                cudaMemcpyAsync(q.crc_ok, dok, (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
+                if (q.iters_used)
+                    cudaMemcpyAsync(q.iters_used, dit, (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
+            }
+        } else if (stages) {
+            cudaEventRecord(evu[x], r.st);
+            cudaEventRecord(evk0[x], r.st);
+            cudaEventRecord(evk1[x], r.st);
+        }
+        cudaEventRecord(ev1[x], r.st);
+        gsub_us[x] = us_since(t0, Clock::now());
+        submitted[gi].store(ti + 1, std::memory_order_release);
+        return src;
+    };
+    if (!merged) {
+        /* one host thread per cell group (the paper's dedicated channel-coding
+         * threads): each waits for the release of
+         * TTI ti itself and enqueues its group, so the groups submit in parallel */
+        std::vector<std::thread> workers;
+        std::vector<int> grc(n_groups, CRN_OK);
+        for (int gi = 0; gi < n_groups; gi++)
+            workers.emplace_back([&, gi]() {
+                cudaSetDevice(dev);
+                for (int ti = 0; ti < n_tti && !abort_flag.load(); ti++) {
+                    release(ti);
+                    if ((grc[gi] = submit_group(ti, gi)) != CRN_OK) abort_flag.store(true);
+                }
+            });
+        for (auto &w : workers) w.join();
+        for (int gi = 0; gi < n_groups; gi++)
+            if (grc[gi] != CRN_OK && rc == CRN_OK) rc = grc[gi];
+        for (int ti = 0; ti < n_tti; ti++)
+            for (int gi = 0; gi < n_groups; gi++)
+                sub_us[ti] = std::max(sub_us[ti], gsub_us[(int64_t)ti * n_groups + gi]);
+    }
     std::vector<crn_cb_desc> mdesc;
     std::vector<int64_t> lbase(n_groups), wbase(n_groups);
     std::vector<int> cbase(n_groups);
-    for (int ti = 0; ti < n_tti && rc == CRN_OK; ti++) {
-        const Clock::time_point rel = t0 + std::chrono::duration_cast<Clock::duration>(
-                                               std::chrono::duration<double, std::micro>(period_us * ti));
-        while (Clock::now() < rel) { /* pacer: release TTI ti at t0 + ti * period */ }
-        rel_us[ti] = us_since(t0, rel);
+    for (int ti = 0; merged && ti < n_tti && rc == CRN_OK; ti++) {
+        release(ti);
         const int64_t x0 = (int64_t)ti * n_groups;
-        if (!merged) {
-            for (int gi = 0; gi < n_groups && rc == CRN_OK; gi++) {
-                const int64_t x = x0 + gi;
-                const crn_tti_group &q = g[x];
-                GroupRes &r = G[gi];
-                cudaEventRecord(ev0[x], r.st);
-                if (q.n_cb > 0) {
-                    /* row a1 per TTI: bucket / pair / task the group's CBs (host) */
-                    std::vector<crn_task> tasks;
-                    std::vector<crn_pair> pairs;
-                    std::vector<int> sel(q.n_cb);
-                    for (int i = 0; i < q.n_cb; i++) sel[i] = i;
-                    crn_build_tasks(q.desc, sel.data(), q.n_cb, tasks, pairs);
-                    const int64_t n_llr = g_llr[x], n_words = g_words[x];
-                    const Layout L = layout(q.n_cb, (int)tasks.size(), (int)pairs.size(), n_llr, n_words);
-                    const int b = ti & 1;
-                    cudaEventSynchronize(r.ev_blob[b]);          /* blob slot from TTI ti-2 uploaded */
-                    uint8_t *hb = (uint8_t *)r.hblob[b];
-                    memcpy(hb + L.o_desc, q.desc, sizeof(crn_cb_desc) * q.n_cb);
-                    memcpy(hb + L.o_tasks, tasks.data(), sizeof(crn_task) * tasks.size());
-                    memcpy(hb + L.o_pairs, pairs.data(), sizeof(crn_pair) * pairs.size());
-                    uint8_t *dm = (uint8_t *)r.dmem;
-                    cudaMemcpyAsync(dm, hb, L.o_l, cudaMemcpyHostToDevice, r.st);
-                    cudaEventRecord(r.ev_blob[b], r.st);
-                    const int16_t *hs[3] = {q.llr_sys, q.llr_p1, q.llr_p2};
-                    int16_t *dl[3];
-                    for (int s = 0; s < 3; s++) {
-                        dl[s] = (int16_t *)(dm + L.o_l + s * L.bl);
-                        cudaMemcpyAsync(dl[s], hs[s], sizeof(int16_t) * n_llr, cudaMemcpyHostToDevice, r.st);
-                    }
-                    uint32_t *dbits = (uint32_t *)(dm + L.o_bits);
-                    uint8_t *dok = dm + L.o_ok, *dit = dm + L.o_it;
-                    rc = crn_launch_tasks(dev, t, (const crn_cb_desc *)(dm + L.o_desc),
-                                          (const crn_task *)(dm + L.o_tasks), (int)tasks.size(),
-                                          (const crn_pair *)(dm + L.o_pairs), dl[0], dl[1], dl[2], max_iters, et, dbits,
-                                          dok, q.iters_used ? dit : nullptr, nullptr, r.ws,
-                                          crn_decode_ws_bytes(t->grid), r.st);
-                    cudaMemcpyAsync(q.out_bits, dbits, 4 * (size_t)n_words, cudaMemcpyDeviceToHost, r.st);
-                    cudaMemcpyAsync(q.crc_ok, dok, (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
-                    if (q.iters_used)
-                        cudaMemcpyAsync(q.iters_used, dit, (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
-                }
-                cudaEventRecord(ev1[x], r.st);
-                submitted.store(x + 1, std::memory_order_release);
-            }
-        } else {
+        {
             /* merged: every group uploads its slice of one TTI-wide buffer set on its own
              * stream; one decode launch over all groups' tasks waits for every upload;
              * each group downloads its slice on its own stream after the decode */
@@ -444,6 +538,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
                         cudaMemcpyAsync(dl[s] + lbase[gi], hs[s], sizeof(int16_t) * g_llr[x], cudaMemcpyHostToDevice,
                                         r.st);
                 cudaEventRecord(ev_in[gi], r.st);
+                cudaEventRecord(evu[x], r.st);
                 cudaStreamWaitEvent(dr.st, ev_in[gi], 0);
             }
             const int b = ti & 1;
@@ -454,12 +549,18 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             memcpy(hb + L.o_pairs, pairs.data(), sizeof(crn_pair) * pairs.size());
             cudaMemcpyAsync(dm, hb, L.o_l, cudaMemcpyHostToDevice, dr.st);
             cudaEventRecord(dr.ev_blob[b], dr.st);
+            cudaEventRecord(evk0[x0], dr.st);
             if (m_cb > 0)
                 rc = crn_launch_tasks(dev, t, (const crn_cb_desc *)(dm + L.o_desc), (const crn_task *)(dm + L.o_tasks),
                                       (int)tasks.size(), (const crn_pair *)(dm + L.o_pairs), dl[0], dl[1], dl[2],
                                       max_iters, et, dbits, dok, dit, nullptr, dr.ws, crn_decode_ws_bytes(t->grid),
                                       dr.st);
             cudaEventRecord(ev_dec, dr.st);
+            cudaEventRecord(evk1[x0], dr.st);
+            for (int gi = 1; gi < n_groups; gi++) {          /* one decode for all groups */
+                cudaEventRecord(evk0[x0 + gi], dr.st);
+                cudaEventRecord(evk1[x0 + gi], dr.st);
+            }
             for (int gi = 0; gi < n_groups; gi++) {
                 const int64_t x = x0 + gi;
                 const crn_tti_group &q = g[x];
@@ -474,7 +575,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
                 }
                 cudaEventRecord(ev1[x], r.st);
             }
-            submitted.store(x0 + n_groups, std::memory_order_release);
+            for (int gi = 0; gi < n_groups; gi++) submitted[gi].store(ti + 1, std::memory_order_release);
         }
         sub_us[ti] = us_since(t0, Clock::now());
     }
@@ -487,7 +588,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
     if (rc == CRN_OK) {
         for (int ti = 0; ti < n_tti; ti++) {
             crn_tti_timing &o = timing[ti];
-            o.release_us = rel_us[ti];
+            o.release_us = rel_us[ti];                  /* the pacer's release instant (t0 + ti * period) */
             o.submitted_us = sub_us[ti];
             o.complete_us = 0;
             float smin = 0, emax = 0;
@@ -502,11 +603,28 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             }
             o.latency_us = o.complete_us - o.release_us;
             o.device_us = 1e3 * (double)(emax - smin);
+            float up = 0, k0 = 1e30f, k1 = 0;
+            for (int gi = 0; stages && gi < n_groups; gi++) {
+                const int64_t x = (int64_t)ti * n_groups + gi;
+                float a = 0, b0 = 0, b1 = 0;
+                cudaEventElapsedTime(&a, ev0[(int64_t)ti * n_groups], evu[x]);
+                cudaEventElapsedTime(&b0, ev0[(int64_t)ti * n_groups], evk0[x]);
+                cudaEventElapsedTime(&b1, ev0[(int64_t)ti * n_groups], evk1[x]);
+                up = std::max(up, a);
+                k0 = std::min(k0, b0);
+                k1 = std::max(k1, b1);
+            }
+            o.upload_us = stages ? 1e3 * (double)(up - smin) : -1.0;
+            o.decode_start_us = stages ? 1e3 * (double)(k0 - smin) : -1.0;
+            o.decode_end_us = stages ? 1e3 * (double)(k1 - smin) : -1.0;
         }
     }
     for (int64_t x = 0; x < NG; x++) {
         cudaEventDestroy(ev0[x]);
         cudaEventDestroy(ev1[x]);
+        cudaEventDestroy(evu[x]);
+        cudaEventDestroy(evk0[x]);
+        cudaEventDestroy(evk1[x]);
     }
     for (auto &ev : ev_in) cudaEventDestroy(ev);
     if (ev_dec) cudaEventDestroy(ev_dec);

@@ -254,8 +254,8 @@ def test_plan_decode_host_pipeline(orc, n_chunks):
     p.close()
 
 
-@pytest.mark.parametrize("flags", [0, 1])
-def test_stream_run_cfg5(orc, flags):
+@pytest.mark.parametrize("flags,packed", [(0, False), (0, True), (1, False), (2, True), (4, False), (6, True)])
+def test_stream_run_cfg5(orc, flags, packed):
     """crn_stream_run_ex: paced TTIs of cfg5, one stream per cell group (per-group
     decode launches, or one merged launch per TTI); every CB of every TTI
     bit-exact against the oracle; timestamps ordered."""
@@ -273,10 +273,15 @@ def test_stream_run_cfg5(orc, flags):
             d["bit_off"] = np.concatenate([[0], np.cumsum((K + 31) // 32)[:-1]])
             hl = [torch.cat([x[int(o):int(o) + int(k) + 4] for o, k in zip(b.desc["llr_off"][sel], K)]).cpu()
                   .pin_memory() if sel.size else torch.zeros(1, dtype=torch.int16).pin_memory() for x in b.llr]
-            nw = int(((K + 31) // 32).sum())
-            g = dict(desc=d, l0=hl[0], l1=hl[1], l2=hl[2], bits=torch.zeros(max(nw, 1), dtype=torch.int32).pin_memory(),
-                     ok=torch.zeros(max(sel.size, 1), dtype=torch.uint8).pin_memory(),
-                     it=torch.zeros(max(sel.size, 1), dtype=torch.uint8).pin_memory())
+            nw, nc = max(int(((K + 31) // 32).sum()), 1), max(sel.size, 1)
+            if packed:                      # one host block: bits | crc_ok | iters_used
+                ob = torch.zeros(4 * nw + 2 * nc, dtype=torch.uint8).pin_memory()
+                bits, ok, it = ob[:4 * nw].view(torch.int32), ob[4 * nw:4 * nw + nc], ob[4 * nw + nc:]
+            else:
+                bits = torch.zeros(nw, dtype=torch.int32).pin_memory()
+                ok = torch.zeros(nc, dtype=torch.uint8).pin_memory()
+                it = torch.zeros(nc, dtype=torch.uint8).pin_memory()
+            g = dict(desc=d, l0=hl[0], l1=hl[1], l2=hl[2], bits=bits, ok=ok, it=it)
             groups.append(g)
             checks.append((b, r, sel, d, g))
     tim = crn.stream_run(groups, n_tti, n_groups, 1000.0, 8, True, flags=flags)
@@ -288,6 +293,10 @@ def test_stream_run_cfg5(orc, flags):
             assert np.array_equal(unpack(words, d, n), ob)
             assert g["ok"].numpy()[n] == r["crc_ok"][i] and g["it"].numpy()[n] == r["iters"][i]
     assert np.all(tim["latency_us"] > 0) and np.all(tim["device_us"] > 0)
+    if flags & 3:                           # stage split recorded
+        assert np.all(tim["decode_end_us"] > tim["decode_start_us"]) and np.all(tim["upload_us"] > 0)
+    else:
+        assert np.all(tim["upload_us"] == -1.0)
     assert np.all(np.diff(tim["release_us"]) > 900)
     assert np.all(tim["complete_us"] > tim["release_us"])
 
