@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "crn_internal.h"
 #include "qpp_table.h"
 
@@ -94,14 +96,18 @@ __global__ void encode_kernel(const crn_cb_desc *__restrict__ desc, int n_cb, co
 
 extern "C" int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const uint8_t *info, int32_t attach,
                                  uint8_t *d0, uint8_t *d1, uint8_t *d2, const crn_tables *, void *stream) {
-    static int done_dev = -1;
+    static std::mutex mu;
+    static uint64_t done = 0;                   /* bit d: the QPP constants are on device d */
     int dev;
-    cudaGetDevice(&dev);
-    if (done_dev != dev) {
-        if (cudaMemcpyToSymbol(c_f1, crn_qpp_f1, sizeof(crn_qpp_f1)) != cudaSuccess ||
-            cudaMemcpyToSymbol(c_f2, crn_qpp_f2, sizeof(crn_qpp_f2)) != cudaSuccess)
-            return CRN_ECUDA;
-        done_dev = dev;
+    if (cudaGetDevice(&dev) != cudaSuccess) return CRN_ECUDA;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev >= 64 || !((done >> dev) & 1u)) {
+            if (cudaMemcpyToSymbol(c_f1, crn_qpp_f1, sizeof(crn_qpp_f1)) != cudaSuccess ||
+                cudaMemcpyToSymbol(c_f2, crn_qpp_f2, sizeof(crn_qpp_f2)) != cudaSuccess)
+                return CRN_ECUDA;
+            if (dev < 64) done |= 1ull << dev;
+        }
     }
     encode_kernel<<<(n_cb + 127) / 128, 128, 0, (cudaStream_t)stream>>>(d_desc, n_cb, info, attach, d0, d1, d2);
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;

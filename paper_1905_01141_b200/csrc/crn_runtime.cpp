@@ -355,7 +355,9 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
     for (int ti = 0; ti < n_tti; ti++) rel_us[ti] = period_us * ti;
 
     /* completion thread (the "captor"): time-stamps each (TTI, group) when its end event fires */
-    std::thread watcher([&]() {
+    std::thread watcher;
+    try {
+    watcher = std::thread([&]() {
         for (int64_t x = 0; x < NG; x++) {
             const int ti = (int)(x / n_groups), gi = (int)(x % n_groups);
             while (submitted[gi].load(std::memory_order_acquire) <= ti) {
@@ -370,6 +372,19 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             done_us[x] = us_since(t0, Clock::now());
         }
     });
+    } catch (const std::exception &) {           /* no thread: give everything back */
+        for (int64_t x = 0; x < NG; x++) {
+            cudaEventDestroy(ev0[x]);
+            cudaEventDestroy(ev1[x]);
+            cudaEventDestroy(evu[x]);
+            cudaEventDestroy(evk0[x]);
+            cudaEventDestroy(evk1[x]);
+        }
+        for (auto &ev : ev_in) cudaEventDestroy(ev);
+        if (ev_dec) cudaEventDestroy(ev_dec);
+        cleanup();
+        return CRN_ENOMEM;
+    }
 
     auto release = [&](int ti) {                /* pacer: TTI ti is released at t0 + ti * period */
         const Clock::time_point rel = t0 + std::chrono::duration_cast<Clock::duration>(
@@ -470,14 +485,19 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
          * TTI ti itself and enqueues its group, so the groups submit in parallel */
         std::vector<std::thread> workers;
         std::vector<int> grc(n_groups, CRN_OK);
-        for (int gi = 0; gi < n_groups; gi++)
-            workers.emplace_back([&, gi]() {
-                cudaSetDevice(dev);
-                for (int ti = 0; ti < n_tti && !abort_flag.load(); ti++) {
-                    release(ti);
-                    if ((grc[gi] = submit_group(ti, gi)) != CRN_OK) abort_flag.store(true);
-                }
-            });
+        try {
+            for (int gi = 0; gi < n_groups; gi++)
+                workers.emplace_back([&, gi]() {
+                    cudaSetDevice(dev);
+                    for (int ti = 0; ti < n_tti && !abort_flag.load(); ti++) {
+                        release(ti);
+                        if ((grc[gi] = submit_group(ti, gi)) != CRN_OK) abort_flag.store(true);
+                    }
+                });
+        } catch (const std::exception &) {       /* could not start every group thread */
+            abort_flag.store(true);
+            rc = CRN_ENOMEM;
+        }
         for (auto &w : workers) w.join();
         for (int gi = 0; gi < n_groups; gi++)
             if (grc[gi] != CRN_OK && rc == CRN_OK) rc = grc[gi];

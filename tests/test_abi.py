@@ -163,5 +163,6 @@ def test_new_entry_points_validate_on_host():
                                  None) == crn.CRN_EINVAL                    # unknown flag bit
     tim = (crn.TtiTiming * 1)()
     grp = (crn.TtiGroup * 1)()
-    assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 2, tim) == crn.CRN_EINVAL   # unknown stream flag
+    assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 8, tim) == crn.CRN_EINVAL   # unknown stream flag
+    assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 5, tim) == crn.CRN_EINVAL   # merged + zero copy
     assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 5, 0, tim) == crn.CRN_EINVAL   # unknown stopping rule
