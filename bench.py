@@ -242,6 +242,45 @@ def run_pool(args, seed=0):
             "gen_s": round(t_gen, 1)}
 
 
+def run_dl_encode(b, reps=5):
+    """The paper's other channel-coding workload (Fig. 6): DL
+    encoding of the same cfg4 batch on the device -- CRC24B attach + rate-1/3
+    turbo encoding (crn_encode_batch) and rate matching to E = 3(K+4) at rv 0
+    (crn_rate_match_batch) -- as encoded info Mbit/s."""
+    from paper_1905_01141_b200 import crn
+    st = torch.cuda.current_stream()
+    d = b.desc
+    coded = tuple(torch.empty_like(x) for x in b.coded)
+    rm = np.zeros(d.size, crn.RM_DTYPE)
+    rm["K"], rm["E"], rm["rv"] = d["K"], 3 * (d["K"] + 4), 0
+    rm["e_off"] = d["llr_off"] * 3
+    rm["llr_off"] = d["llr_off"]
+    e = torch.empty(int((rm["e_off"] + rm["E"]).max()), dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        crn.encode_batch(d, b.info, True, *coded, stream=st)
+        crn.rate_match_batch(rm, *coded, e, stream=st)
+    torch.cuda.synchronize()
+    enc, rmt = [], []
+    for _ in range(reps):
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(st)
+        crn.encode_batch(d, b.info, True, *coded, stream=st)
+        e1.record(st)
+        crn.rate_match_batch(rm, *coded, e, stream=st)
+        e2.record(st)
+        torch.cuda.synchronize()
+        enc.append(e0.elapsed_time(e1))
+        rmt.append(e1.elapsed_time(e2))
+    same = all(torch.equal(x, y) for x, y in zip(coded, b.coded))
+    bits = b.info_bits()
+    return {"workload": f"{b.n_cb} CBs of K=6144 (the cfg4 batch): CRC24B attach + turbo encode, then rate "
+                        "matching to E = 3(K+4), rv 0",
+            "encode_ms": statistics.median(enc), "rate_match_ms": statistics.median(rmt),
+            "encode_mbps": bits / (statistics.median(enc) * 1e-3) / 1e6,
+            "encode_and_rm_mbps": bits / ((statistics.median(enc) + statistics.median(rmt)) * 1e-3) / 1e6,
+            "matches_batch_encoding": bool(same)}
+
+
 def run_small_configs(seed=0):
     """BASELINE cfg1 (32 x K=1056, 6 fixed iterations) and cfg2 (one 20 MHz subframe:
     TB of 75,376 bits -> 13 x K=5824, CRC ET max 8) as single device launches:
@@ -480,6 +519,11 @@ def run_crn(args):
             out["latency"] = run_latency(args, seed=args.seed)
         except Exception as e:           # the throughput number stands without it
             out["latency"] = {"error": repr(e)}
+    if not args.no_pool and ws == 1:
+        try:
+            out["dl_encode"] = run_dl_encode(b)
+        except Exception as e:
+            out["dl_encode"] = {"error": repr(e)}
     if not args.no_pool and ws == 1:
         try:
             out["small_configs"] = run_small_configs(seed=args.seed)

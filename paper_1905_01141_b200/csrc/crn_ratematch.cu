@@ -132,9 +132,14 @@ match_kernel(const crn_rm_desc *__restrict__ desc, const uint8_t *__restrict__ d
     for (int k = threadIdx.x; k < d.E; k += RM_THREADS) {
         int j = base + k % g.nn;                                      /* j-th non-dummy position overall */
         if (j >= g.nn) j -= g.nn;
-        /* smallest p with p - nulls_below(p) == j and p not a dummy: p = j + #dummies <= p */
-        int p = j, c = 0;
-        while (c < n_null && nul[c] <= p) { c++; p = j + c; }
+        /* the j-th non-dummy position is p = j + c, c = #dummies before it: the number of
+         * dummies i with nul[i] - i <= j (nul[i] - i is nondecreasing) -- binary search */
+        int lo = 0, hi = n_null;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (nul[mid] - mid <= j) lo = mid + 1; else hi = mid;
+        }
+        const int p = j + lo;
         int s, n, y;
         if (p < g.Kpi) { s = 0; y = (p % g.R) * 32 + bitrev5(p / g.R); }
         else {
