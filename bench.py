@@ -392,11 +392,21 @@ def run_crn(args):
     from paper_1905_01141_b200 import workload as wlmod
 
     ws, rank, local = _dist()
+    # --dist-backend gloo + CRN_BENCH_SHARE_GPU=1: every rank on cuda:0, for a functional
+    # check of the N > 1 code path on a one-GPU box (the ranks never wait on each other's
+    # kernels; the timings of such a run are not measurements and the line says so)
+    share = os.environ.get("CRN_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
+    red_dev = "cuda" if args.dist_backend == "nccl" else "cpu"
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     crn_build.build()
     dev = crn.device_info()
 
@@ -446,7 +456,7 @@ def run_crn(args):
     # outputs of the last step: counters (one NCCL reduction, DESIGN.md multi-GPU)
     n_ok_local = int(ok[:b.n_cb].to(torch.int64).sum().item())
     c, tmax = shard.reduce_counters([b.n_cb, n_ok_local, b.info_bits(), int(b.K.sum()),
-                                     crn.counted_ops(b.K, iters)], ms_total, dist, device="cuda")
+                                     crn.counted_ops(b.K, iters)], ms_total, dist, device=red_dev)
     n_cb, n_ok, info_bits, sum_k, ops = (c[k] for k in shard.COUNTERS)
     ms_step = tmax / args.steps
     value = info_bits / (ms_step * 1e-3) / 1e6
@@ -473,7 +483,7 @@ def run_crn(args):
             e2e_step()
         e1.record(stream)
         barrier()
-        te = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device="cuda")
+        te = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device=red_dev)
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         n_ok_host = int(hok[:b.n_cb].to(torch.int64).sum())
@@ -514,6 +524,8 @@ def run_crn(args):
         "e2e": e2e, "kernel_ms_mean": mean_launch_ms, "kernel_ms": launch_ms,
         "sum_k_mbps": sum_k / (ms_step * 1e-3) / 1e6,
     }
+    if share and ws > 1:
+        out["functional_check_only"] = f"{ws} ranks shared one GPU over {args.dist_backend}: not a measurement"
     if not args.no_latency and ws == 1:
         try:
             out["latency"] = run_latency(args, seed=args.seed)
@@ -534,7 +546,7 @@ def run_crn(args):
             out["pool_tti"] = run_pool(args, seed=args.seed)
         except Exception as e:
             out["pool_tti"] = {"error": repr(e)}
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and ws == 1:          # rank 0 at N = 1 only
         try:
             out["cpu_baseline"] = cpu_baseline(_cpu_sample(args.ref_sample, args.seed), iters)
         except Exception as e:           # the GPU number stands without it
@@ -563,6 +575,8 @@ def main():
     ap.add_argument("--no-pool", action="store_true", help="skip the cfg3 one-TTI pool measurement")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only for the functional N > 1 check with CRN_BENCH_SHARE_GPU=1")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

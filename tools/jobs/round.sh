@@ -12,3 +12,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --n
 B1="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-latency --no-pool"
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:decode_kernel -s 3 -c 1 \
     -o gpurun_out/${TAG} $B1 > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu2 rc=$?" >> gpurun_out/${TAG}_rc.txt
+bash tools/jobs/multirank.sh ${TAG}_mr
