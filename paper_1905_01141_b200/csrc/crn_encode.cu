@@ -1,10 +1,28 @@
 /* crn_encode.cu -- rate-1/3 LTE turbo encoder on the device (the paper's
  * downlink "encoding function"; NEXT row f3 of DESIGN.md).
- * One warp per code block: optional CRC24A/B attach over the first K-24 bits
- * (fillers counted as 0; per-lane CRC registers combined by a GF(2) multiply),
- * RSC 1 over c, RSC 2 over c'_i = c_{Pi(i)} with Pi advanced by the QPP
- * forward recurrence, each split into 32 chunks by linearity (below), 12 tail
- * bits column-wise (R11).  Also builds bench.py's synthetic uplink inputs. */
+ * A warp per code block, bit-packed in shared memory: optional CRC24A/B attach
+ * over the first K-24 bits (fillers counted as 0), RSC 1 over c, RSC 2 over
+ * c'_i = c_{Pi(i)}, 12 tail bits column-wise (R11), one bit per output byte.
+ * Also builds bench.py's synthetic uplink inputs.
+ *
+ * Work per CB is a few instructions per bit:
+ *   input    K bytes (one bit each) -> packed words: 8-byte loads, 8 bits per
+ *            load by a multiply (or a ballot per 32 bytes when unaligned);
+ *   CRC      byte-table CRC over word-aligned lane chunks, the 32 lane
+ *            registers combined as crc(A||B) = crc(A) x^|B| + crc(B) with
+ *            x^(32 m) mod g from a per-CTA table;
+ *   c'       c_{Pi(i)} gathered bit by bit with the QPP forward recurrence
+ *            Pi(i+1) = Pi(i) + g(i), g(i+1) = g(i) + 2 f2 (mod K), two
+ *            add-and-fold steps per bit;
+ *   RSC      the code is linear over GF(2): with state s = 4 r1 + 2 r2 + r3 one
+ *            step is s' = A s + 4u, A of order 7 (1 + D^2 + D^3 is primitive).
+ *            Each lane runs its chunk a byte at a time through a (state, input
+ *            byte) -> (next state, 8 parity bits) table, first from state 0 to
+ *            learn the chunk's input-driven end state f, then -- after a 32-step
+ *            scan s_{l+1} = A^{L_l} s_l + f_l gives every chunk's true start
+ *            state -- again, emitting parity;
+ *   output   4 bits -> 4 bytes by a multiply, 32-bit coalesced stores.
+ * A persistent grid; each CTA builds its tables once. */
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -16,6 +34,11 @@
 namespace {
 __constant__ int16_t c_f1[CRN_NUM_K], c_f2[CRN_NUM_K];
 
+constexpr int ENC_WARPS = 8;
+constexpr int ENC_THREADS = 32 * ENC_WARPS;
+constexpr int ENC_WORDS = 6144 / 32;                 /* packed words of the largest CB */
+constexpr uint32_t POLY_A = 0x864CFBu, POLY_B = 0x800063u;
+
 /* index of K in the ascending size table (closed form of SPEC.md:217's set) */
 __device__ __forceinline__ int crn_k_index_dev(int K) {
     if (K <= 512) return (K - 40) / 8;
@@ -23,17 +46,6 @@ __device__ __forceinline__ int crn_k_index_dev(int K) {
     if (K <= 2048) return 92 + (K - 1056) / 32;
     return 124 + (K - 2112) / 64;
 }
-
-/* ---- warp-per-CB encoder.  The RSC code is linear over GF(2): with state
- * s = 4 r1 + 2 r2 + r3, one step is s' = A s + 4u and z = c.s + u, and A has
- * order 7 (feedback 1 + D^2 + D^3 is primitive), so A^L = A^(L mod 7).  Each
- * lane encodes a contiguous chunk of the CB twice: from state 0 to learn the
- * chunk's input-driven end state f, then -- after a 32-step scan of
- * s_{l+1} = A^{L_l} s_l + f_l gives every chunk's true start state -- again,
- * emitting its parity bits.  Bits are staged per warp in shared memory (the
- * second encoder gathers c_{Pi(i)} there) and written out coalesced. */
-constexpr int ENC_WARPS = 4;
-constexpr int ENC_STAGE = 6144 + 2 * 6148;      /* per warp: c, then parity bytes of both encoders */
 
 __device__ __forceinline__ int rsc_A(int s) {       /* zero-input step */
     const int r1 = (s >> 2) & 1, r2 = (s >> 1) & 1, r3 = s & 1;
@@ -45,126 +57,250 @@ __device__ __forceinline__ int rsc_Apow(int s, int L) {
     return s;
 }
 
-__device__ __forceinline__ uint32_t mulmod24(uint32_t a, uint32_t b, uint32_t poly) {
+__device__ __forceinline__ uint32_t crc_step_bit(uint32_t reg, uint32_t poly) {   /* reg x mod g */
+    return ((reg << 1) & 0xFFFFFFu) ^ ((reg & 0x800000u) ? poly : 0u);
+}
+
+__device__ __forceinline__ uint32_t mulmod24(uint32_t a, uint32_t b, uint32_t poly) {   /* a b mod g */
     uint32_t acc = 0;
     for (int k = 23; k >= 0; k--) {
-        acc = ((acc << 1) & 0xFFFFFFu) ^ ((acc & 0x800000u) ? poly : 0u);
+        acc = crc_step_bit(acc, poly);
         if ((b >> k) & 1u) acc ^= a;
     }
     return acc;
 }
 
-__device__ __forceinline__ uint32_t xpow24(int64_t e, uint32_t poly) {
-    uint32_t r = 1, base = 2;
-    while (e > 0) {
-        if (e & 1) r = mulmod24(r, base, poly);
-        base = mulmod24(base, base, poly);
-        e >>= 1;
+struct EncShared {
+    uint16_t rsc[8 * 256];                /* (state, input byte) -> parity byte | next state << 8 */
+    uint32_t crc_tab[2][256];             /* byte-at-a-time CRC24A / CRC24B (MSB-first) */
+    uint32_t xp[2][ENC_WORDS + 1];        /* x^(32 m) mod g_A / g_B */
+    struct Warp {
+        uint32_t c[ENC_WORDS + 2];        /* c, packed LSB-first */
+        uint32_t ci[ENC_WORDS];           /* c' = c_{Pi(i)} */
+        uint32_t z1[ENC_WORDS], z2[ENC_WORDS];
+    } w[ENC_WARPS];
+};
+
+__device__ void build_tables(EncShared &S) {
+    for (int e = threadIdx.x; e < 8 * 256; e += ENC_THREADS) {
+        int s = e >> 8;
+        const int b = e & 255;
+        uint32_t z = 0;
+        for (int k = 0; k < 8; k++) {
+            const int u = (b >> k) & 1, r1 = (s >> 2) & 1, r2 = (s >> 1) & 1, r3 = s & 1;
+            const int a = u ^ r2 ^ r3;
+            z |= (uint32_t)(a ^ r1 ^ r3) << k;
+            s = (a << 2) | (r1 << 1) | r2;
+        }
+        S.rsc[e] = (uint16_t)(z | (uint32_t)s << 8);
     }
-    return r;
+    for (int e = threadIdx.x; e < 2 * 256; e += ENC_THREADS) {
+        const uint32_t poly = (e >> 8) ? POLY_B : POLY_A;
+        uint32_t reg = (uint32_t)(e & 255) << 16;
+        for (int k = 0; k < 8; k++) reg = crc_step_bit(reg, poly);
+        S.crc_tab[e >> 8][e & 255] = reg;
+    }
+    for (int e = threadIdx.x; e < 2 * (ENC_WORDS + 1); e += ENC_THREADS) {
+        const int p = e / (ENC_WORDS + 1), m = e % (ENC_WORDS + 1);
+        const uint32_t poly = p ? POLY_B : POLY_A;
+        uint32_t r = 1, base = 1;                                  /* x^0; base -> x^32 mod g */
+        for (int k = 0; k < 32; k++) base = crc_step_bit(base, poly);
+        for (int q = m; q > 0; q >>= 1) {                          /* square-and-multiply */
+            if (q & 1) r = mulmod24(r, base, poly);
+            base = mulmod24(base, base, poly);
+        }
+        S.xp[p][m] = r;
+    }
+    __syncthreads();
 }
 
-/* one RSC encoder over the warp's staged input: pass 1 (zero start), scan, pass 2 */
-template <bool INTERLEAVED>
-__device__ __forceinline__ int rsc_warp(const uint8_t *c, uint8_t *z_out, int K, int lane, int64_t f1, int64_t f2) {
-    const int per = (K + 31) / 32, c0 = min(K, lane * per), c1 = min(K, c0 + per), L = c1 - c0;
-    const int64_t f2x2 = (2 * f2) % K;
-    auto input = [&](int k, int64_t &pi, int64_t &g) -> int {
-        if (!INTERLEAVED) return c[k];
-        const int v = c[pi];
-        pi += g;
-        if (pi >= K) pi -= K;
-        g += f2x2;                                    /* 2 f2 mod K: 2 f2 itself may exceed K */
-        if (g >= K) g -= K;
-        return v;
-    };
-    auto pi0 = [&](int64_t &pi, int64_t &g) {       /* Pi(c0) and the recurrence increment g(c0) */
-        const int64_t k = c0;
-        pi = (f1 * k + f2 * ((k * k) % K)) % K;
-        g = (f1 + f2 * ((2 * k + 1) % K)) % K;
-    };
-    int64_t pi = 0, g = 0;
-    if (INTERLEAVED) pi0(pi, g);
-    int s = 0;
-    for (int k = c0; k < c1; k++) {
-        const int u = input(k, pi, g), r2 = (s >> 1) & 1, r3 = s & 1;
-        s = (((u ^ r2 ^ r3) & 1) << 2) | (((s >> 2) & 1) << 1) | r2;
+/* K bits (one per byte at src) -> packed words c[0 .. ceil(K/32)), zero beyond K */
+__device__ __forceinline__ void load_bits(const uint8_t *src, int K, uint32_t *c, int lane) {
+    const int nw = (K + 31) >> 5;
+    if ((reinterpret_cast<uintptr_t>(src) & 7u) == 0) {             /* K = 0 mod 8: K/8 whole 8-byte units */
+        const uint2 *s8 = reinterpret_cast<const uint2 *>(src);
+        uint8_t *cb = reinterpret_cast<uint8_t *>(c);
+        const int nu = K >> 3;
+        constexpr int U = 8;
+        for (int u0 = lane; u0 < nu; u0 += 32 * U) {
+            uint2 v[U];
+#pragma unroll
+            for (int j = 0; j < U; j++)
+                if (u0 + 32 * j < nu) v[j] = __ldg(s8 + u0 + 32 * j);
+#pragma unroll
+            for (int j = 0; j < U; j++)
+                if (u0 + 32 * j < nu) {
+                    const uint32_t lo = ((v[j].x & 0x01010101u) * 0x01020408u) >> 24;
+                    const uint32_t hi = ((v[j].y & 0x01010101u) * 0x01020408u) >> 24;
+                    cb[u0 + 32 * j] = (uint8_t)(lo | hi << 4);
+                }
+        }
+        /* (the last word's bytes past K are masked by the caller) */
+    } else {
+        for (int t = 0; t < nw; t++) {
+            const int n = 32 * t + lane;
+            const uint32_t w = __ballot_sync(0xFFFFFFFFu, n < K && (__ldg(src + n) & 1u));
+            if (lane == 0) c[t] = w;
+        }
     }
-    /* start state of every chunk: s_{l+1} = A^{L_l} s_l + f_l (lane 0 -> 31) */
-    int start = 0, run = 0;
-    for (int l = 0; l < 32; l++) {
-        const int fl = __shfl_sync(0xFFFFFFFFu, s, l), Ll = __shfl_sync(0xFFFFFFFFu, L, l);
-        if (l == lane) start = run;
-        run = rsc_Apow(run, Ll) ^ fl;
-    }
-    if (INTERLEAVED) pi0(pi, g);
-    s = start;
-    for (int k = c0; k < c1; k++) {
-        const int u = input(k, pi, g), r1 = (s >> 2) & 1, r2 = (s >> 1) & 1, r3 = s & 1;
-        const int a = u ^ r2 ^ r3;
-        z_out[k] = (uint8_t)(a ^ r1 ^ r3);
-        s = (a << 2) | (r1 << 1) | r2;
-    }
-    return run;                                       /* the state after all K inputs */
+    __syncwarp();
 }
 
-__global__ void __launch_bounds__(32 * ENC_WARPS)
-encode_kernel(const crn_cb_desc *__restrict__ desc, int n_cb, const uint8_t *__restrict__ info,
-              int attach, uint8_t *d0, uint8_t *d1, uint8_t *d2) {
-    extern __shared__ uint8_t enc_sm[];
+__global__ void __launch_bounds__(ENC_THREADS)
+encode_kernel(const crn_cb_desc *__restrict__ desc, int n_cb, const uint8_t *__restrict__ info, int attach,
+              uint8_t *d0, uint8_t *d1, uint8_t *d2) {
+    extern __shared__ __align__(16) uint8_t enc_raw[];
+    EncShared &S = *reinterpret_cast<EncShared *>(enc_raw);
+    build_tables(S);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cb = blockIdx.x * ENC_WARPS + warp;
-    if (cb >= n_cb) return;                           /* whole warps */
-    const crn_cb_desc d = desc[cb];
-    const int K = d.K, F = d.F, L = attach ? 24 : 0;
-    uint8_t *c = enc_sm + (size_t)warp * ENC_STAGE, *z1 = c + 6144, *z2 = z1 + 6148;
-    const uint8_t *src = info + d.ext_off;
-    for (int n = lane; n < K - L; n += 32) c[n] = n < F ? 0 : (src[n] & 1u);
-    __syncwarp();
-    if (attach) {                                     /* CRC of bits [0, K-24): chunk registers combined */
-        const uint32_t poly = d.crc_kind == CRN_CRC24A ? 0x864CFBu : 0x800063u;
-        const int N = K - 24, per = (N + 31) / 32, b0 = min(N, lane * per), b1 = min(N, b0 + per);
-        uint32_t reg = 0;
-        for (int n = b0; n < b1; n++) {
-            const uint32_t fb = ((reg >> 23) ^ c[n]) & 1u;
-            reg = ((reg << 1) & 0xFFFFFFu) ^ (fb ? poly : 0u);
+    EncShared::Warp &W = S.w[warp];
+    for (int cb = blockIdx.x * ENC_WARPS + warp; cb < n_cb; cb += gridDim.x * ENC_WARPS) {
+        const crn_cb_desc d = desc[cb];
+        const int K = d.K, F = d.F, nw = (K + 31) >> 5;
+        load_bits(info + d.ext_off, K, W.c, lane);
+        /* fillers read as 0; with attach the last 24 bits are recomputed */
+        const int N = attach ? K - 24 : K;
+        for (int t = lane; t < nw; t += 32) {
+            uint32_t w = W.c[t];
+            const int b0 = 32 * t;
+            if (b0 < F) w &= F - b0 >= 32 ? 0u : ~0u << (F - b0);
+            if (b0 + 32 > N) w &= N - b0 <= 0 ? 0u : ~0u >> (32 - (N - b0));
+            W.c[t] = w;
         }
-        uint32_t part = b0 < b1 ? mulmod24(reg, xpow24(N - b1, poly), poly) : 0u;
-        for (int o = 16; o > 0; o >>= 1) part ^= __shfl_xor_sync(0xFFFFFFFFu, part, o);
-        if (lane < 24) c[N + lane] = (uint8_t)((part >> (23 - lane)) & 1u);
+        if (lane == 0) W.c[nw] = 0;
         __syncwarp();
-    }
-    const int ki = crn_k_index_dev(K);
-    const int64_t f1 = c_f1[ki], f2 = c_f2[ki];
-    const int s1 = rsc_warp<false>(c, z1, K, lane, f1, f2);
-    const int s2 = rsc_warp<true>(c, z2, K, lane, f1, f2);
-    __syncwarp();
-    uint8_t *o0 = d0 + d.llr_off, *o1 = d1 + d.llr_off, *o2 = d2 + d.llr_off;
-    for (int n = lane; n < K; n += 32) {
-        o0[n] = c[n];
-        o1[n] = z1[n];
-        o2[n] = z2[n];
-    }
-    if (lane == 0) {                                  /* termination: u = r2^r3, x = u, z = r1^r3 (R11) */
-        uint8_t t[12];
-        int s = s1;
-        for (int k = 0; k < 3; k++) {
-            const int r1 = (s >> 2) & 1, r2 = (s >> 1) & 1, r3 = s & 1;
-            t[2 * k] = (uint8_t)(r2 ^ r3);
-            t[2 * k + 1] = (uint8_t)(r1 ^ r3);
-            s = (r1 << 1) | r2;
+        const int per = (nw + 31) >> 5;                            /* words per lane chunk */
+        const int w0 = min(nw, lane * per), w1 = min(nw, w0 + per);
+        if (attach) {
+            /* CRC register of bits [32 w0, min(32 w1, N)) from zero, a byte at a time */
+            const int p = d.crc_kind == CRN_CRC24A ? 0 : 1;
+            const uint32_t poly = p ? POLY_B : POLY_A;
+            const uint32_t *tab = S.crc_tab[p];
+            const int e1 = min(32 * w1, N);
+            uint32_t reg = 0;
+            for (int t = w0; 32 * t < e1; t++) {
+                const uint32_t rw = __brev(W.c[t]);                 /* first bit -> MSB */
+                const int nb = min(4, (e1 - 32 * t) >> 3);          /* N = 0 mod 8 */
+                for (int k = 0; k < nb; k++) {
+                    const uint32_t byte = (rw >> (24 - 8 * k)) & 0xFFu;
+                    reg = ((reg << 8) & 0xFFFFFFu) ^ tab[((reg >> 16) ^ byte) & 0xFFu];
+                }
+            }
+            /* times x^(N - e1): x^(32 m) from the table, then 0..3 zero bytes */
+            uint32_t part = 0;
+            if (32 * w0 < e1) {
+                const int ex = N - e1, m = ex >> 5;
+                part = m ? mulmod24(reg, S.xp[p][m], poly) : reg;
+                for (int k = 0; k < ((ex & 31) >> 3); k++) part = ((part << 8) & 0xFFFFFFu) ^ tab[(part >> 16) & 0xFFu];
+            }
+            for (int o = 16; o > 0; o >>= 1) part ^= __shfl_xor_sync(0xFFFFFFFFu, part, o);
+            if (lane == 0) {                                        /* bits N .. N+23, MSB of the CRC first */
+                const uint32_t bits = __brev(part << 8);            /* crc bit 23-i at position i */
+                const int t = N >> 5, sh = N & 31;
+                W.c[t] |= bits << sh;
+                if (sh) W.c[t + 1] |= bits >> (32 - sh);
+            }
+            __syncwarp();
         }
-        s = s2;
-        for (int k = 0; k < 3; k++) {
-            const int r1 = (s >> 2) & 1, r2 = (s >> 1) & 1, r3 = s & 1;
-            t[6 + 2 * k] = (uint8_t)(r2 ^ r3);
-            t[6 + 2 * k + 1] = (uint8_t)(r1 ^ r3);
-            s = (r1 << 1) | r2;
+        /* c'_i = c_{Pi(i)} for the lane's words */
+        {
+            const int ki = crn_k_index_dev(K);
+            const int f1 = c_f1[ki], f2 = c_f2[ki];
+            const int i0 = 32 * w0;
+            uint32_t pi = (uint32_t)((f1 * i0 + f2 * ((i0 * i0) % K)) % K);
+            uint32_t g = (uint32_t)((f1 + f2 * ((2 * i0 + 1) % K)) % K);
+            const uint32_t f2x2 = (uint32_t)((2 * f2) % K);
+            for (int t = w0; t < w1; t++) {
+                uint32_t acc = 0;
+                const int nbit = min(32, K - 32 * t);
+#pragma unroll 8
+                for (int k = 0; k < 32; k++) {
+                    if (k < nbit) {
+                        const uint32_t v = W.c[pi >> 5];
+                        acc = __funnelshift_r(acc, __funnelshift_r(v, v, pi), 1);   /* bit pi -> acc MSB */
+                        pi = min(pi + g, pi + g - (uint32_t)K);             /* (pi + g) mod K */
+                        g = min(g + f2x2, g + f2x2 - (uint32_t)K);
+                    } else {
+                        acc >>= 1;
+                    }
+                }
+                W.ci[t] = acc;
+            }
         }
-        for (int m = 0; m < 12; m++) {
-            uint8_t *o = (m % 3 == 0) ? o0 : (m % 3 == 1) ? o1 : o2;
-            o[K + m / 3] = t[m];
+        __syncwarp();
+        /* both RSC encoders: pass 1 from state 0 (end state), scan, pass 2 with parity */
+        const int L = max(0, min(32 * w1, K) - 32 * w0);              /* chunk bits, 0 mod 8 */
+        const int nbytes = L >> 3;
+        const uint8_t *cb1 = reinterpret_cast<const uint8_t *>(W.c) + 4 * w0;
+        const uint8_t *cb2 = reinterpret_cast<const uint8_t *>(W.ci) + 4 * w0;
+        int s1 = 0, s2 = 0;
+        for (int k = 0; k < nbytes; k++) {
+            s1 = S.rsc[(s1 << 8) | cb1[k]] >> 8;
+            s2 = S.rsc[(s2 << 8) | cb2[k]] >> 8;
         }
+        int st1 = 0, st2 = 0, run1 = 0, run2 = 0;
+        for (int l = 0; l < 32; l++) {
+            const int f1l = __shfl_sync(0xFFFFFFFFu, s1, l), f2l = __shfl_sync(0xFFFFFFFFu, s2, l);
+            const int Ll = __shfl_sync(0xFFFFFFFFu, L, l);
+            if (l == lane) { st1 = run1; st2 = run2; }
+            run1 = rsc_Apow(run1, Ll) ^ f1l;
+            run2 = rsc_Apow(run2, Ll) ^ f2l;
+        }
+        s1 = st1;
+        s2 = st2;
+        uint8_t *z1b = reinterpret_cast<uint8_t *>(W.z1) + 4 * w0, *z2b = reinterpret_cast<uint8_t *>(W.z2) + 4 * w0;
+        for (int k = 0; k < nbytes; k++) {
+            const uint32_t v1 = S.rsc[(s1 << 8) | cb1[k]], v2 = S.rsc[(s2 << 8) | cb2[k]];
+            z1b[k] = (uint8_t)v1;
+            z2b[k] = (uint8_t)v2;
+            s1 = v1 >> 8;
+            s2 = v2 >> 8;
+        }
+        __syncwarp();
+        /* write-out: bit n -> byte n of each stream, four bytes per store */
+        uint8_t *o0 = d0 + d.llr_off, *o1 = d1 + d.llr_off, *o2 = d2 + d.llr_off;
+        const bool al = ((reinterpret_cast<uintptr_t>(o0) | reinterpret_cast<uintptr_t>(o1) |
+                          reinterpret_cast<uintptr_t>(o2)) & 3u) == 0;
+        if (al) {
+            const uint8_t *n0 = reinterpret_cast<const uint8_t *>(W.c), *n1 = reinterpret_cast<const uint8_t *>(W.z1),
+                          *n2 = reinterpret_cast<const uint8_t *>(W.z2);
+            for (int q = lane; q < (K >> 2); q += 32) {              /* nibble q = bits 4q .. 4q+3 */
+                const int sh = (q & 1) * 4;
+                const uint32_t a = (n0[q >> 1] >> sh) & 0xFu, b = (n1[q >> 1] >> sh) & 0xFu,
+                               c = (n2[q >> 1] >> sh) & 0xFu;
+                reinterpret_cast<uint32_t *>(o0)[q] = (a * 0x00204081u) & 0x01010101u;
+                reinterpret_cast<uint32_t *>(o1)[q] = (b * 0x00204081u) & 0x01010101u;
+                reinterpret_cast<uint32_t *>(o2)[q] = (c * 0x00204081u) & 0x01010101u;
+            }
+        } else {
+            for (int n = lane; n < K; n += 32) {
+                o0[n] = (uint8_t)((W.c[n >> 5] >> (n & 31)) & 1u);
+                o1[n] = (uint8_t)((W.z1[n >> 5] >> (n & 31)) & 1u);
+                o2[n] = (uint8_t)((W.z2[n >> 5] >> (n & 31)) & 1u);
+            }
+        }
+        if (lane == 0) {                                  /* termination: u = r2^r3, x = u, z = r1^r3 (R11) */
+            uint8_t t[12];
+            int s = run1;
+            for (int k = 0; k < 3; k++) {
+                const int r1 = (s >> 2) & 1, r2 = (s >> 1) & 1, r3 = s & 1;
+                t[2 * k] = (uint8_t)(r2 ^ r3);
+                t[2 * k + 1] = (uint8_t)(r1 ^ r3);
+                s = (r1 << 1) | r2;
+            }
+            s = run2;
+            for (int k = 0; k < 3; k++) {
+                const int r1 = (s >> 2) & 1, r2 = (s >> 1) & 1, r3 = s & 1;
+                t[6 + 2 * k] = (uint8_t)(r2 ^ r3);
+                t[6 + 2 * k + 1] = (uint8_t)(r1 ^ r3);
+                s = (r1 << 1) | r2;
+            }
+            for (int m = 0; m < 12; m++) {
+                uint8_t *o = (m % 3 == 0) ? o0 : (m % 3 == 1) ? o1 : o2;
+                o[K + m / 3] = t[m];
+            }
+        }
+        __syncwarp();                                     /* W is rewritten by the next CB */
     }
 }
 }  // namespace
@@ -173,6 +309,7 @@ extern "C" int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const 
                                  uint8_t *d0, uint8_t *d1, uint8_t *d2, const crn_tables *, void *stream) {
     static std::mutex mu;
     static uint64_t done = 0;                   /* bit d: the QPP constants are on device d */
+    static int grid_max = 0;
     int dev;
     if (cudaGetDevice(&dev) != cudaSuccess) return CRN_ECUDA;
     {
@@ -181,17 +318,21 @@ extern "C" int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const 
             if (cudaMemcpyToSymbol(c_f1, crn_qpp_f1, sizeof(crn_qpp_f1)) != cudaSuccess ||
                 cudaMemcpyToSymbol(c_f2, crn_qpp_f2, sizeof(crn_qpp_f2)) != cudaSuccess)
                 return CRN_ECUDA;
+            if (cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(EncShared)) != cudaSuccess)
+                return CRN_ECUDA;
+            int sms = 0, per_sm = 0;
+            if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, encode_kernel, ENC_THREADS,
+                                                              sizeof(EncShared)) != cudaSuccess)
+                return CRN_ECUDA;
+            grid_max = sms * (per_sm > 0 ? per_sm : 1);
             if (dev < 64) done |= 1ull << dev;
         }
     }
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ENC_WARPS * ENC_STAGE) !=
-            cudaSuccess)
-            return CRN_ECUDA;
-        attr = true;
-    }
-    encode_kernel<<<(n_cb + ENC_WARPS - 1) / ENC_WARPS, 32 * ENC_WARPS, ENC_WARPS * ENC_STAGE, (cudaStream_t)stream>>>(
-        d_desc, n_cb, info, attach, d0, d1, d2);
+    const int need = (n_cb + ENC_WARPS - 1) / ENC_WARPS;
+    const int grid = need < grid_max ? need : grid_max;
+    encode_kernel<<<grid, ENC_THREADS, sizeof(EncShared), (cudaStream_t)stream>>>(d_desc, n_cb, info, attach, d0, d1,
+                                                                                 d2);
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
 }

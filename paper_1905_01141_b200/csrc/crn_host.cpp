@@ -30,14 +30,14 @@ static int k_at(int i) {
     return 2112 + 64 * (i - 124);               /* 2112..6144 step 64 */
 }
 
-extern "C" int crn_k_index(int32_t K) {
-    int lo = 0, hi = CRN_NUM_K - 1;
-    while (lo <= hi) {
-        int mid = (lo + hi) / 2, v = k_at(mid);
-        if (v == K) return mid;
-        if (v < K) lo = mid + 1; else hi = mid - 1;
-    }
-    return -1;
+extern "C" int crn_k_index(int32_t K) {            /* closed-form inverse of k_at; -1 if K is not a size */
+    int i;
+    if (K >= 40 && K <= 512) i = (K - 40) % 8 ? -1 : (K - 40) / 8;
+    else if (K > 512 && K <= 1024) i = (K - 528) % 16 ? -1 : 60 + (K - 528) / 16;
+    else if (K > 1024 && K <= 2048) i = (K - 1056) % 32 ? -1 : 92 + (K - 1056) / 32;
+    else if (K > 2048 && K <= 6144) i = (K - 2112) % 64 ? -1 : 124 + (K - 2112) / 64;
+    else i = -1;
+    return i >= 0 && k_at(i) == K ? i : -1;
 }
 
 extern "C" int crn_qpp_params(int32_t K, int32_t *f1, int32_t *f2) {
@@ -556,6 +556,74 @@ extern "C" int crn_decode_batch(const int16_t *l0, const int16_t *l1, const int1
 }
 
 /* ------------------------------------------------------------------ encode / ubench wrappers */
+/* ------------------------------------------------------------------ descriptor uploads */
+/* Stream-ordered upload of a host descriptor array for the one-shot batch calls
+ * (encode, rate matching, TB verdicts): a memcpy into a pinned staging buffer
+ * kept per (host thread, device) and an asynchronous DMA from it, so the call
+ * does not wait on a pageable copy (which waits for the stream).  Four staging
+ * buffers rotate; one is reused once its previous copy has completed (event).
+ * *d_out is stream-ordered device memory (cudaFreeAsync it on the same stream). */
+namespace {
+struct UploadStage {
+    void *pin = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+};
+constexpr int UPLOAD_RING = 4;
+struct UploadRing {
+    UploadStage slot[UPLOAD_RING];
+    int next = 0;
+};
+struct UploadStages {
+    std::map<int, UploadRing> by_dev;
+    ~UploadStages() {                        /* thread exit: best effort */
+        for (auto &kv : by_dev)
+            for (UploadStage &u : kv.second.slot) {
+                if (u.ev) cudaEventDestroy(u.ev);
+                if (u.pin) cudaFreeHost(u.pin);
+            }
+    }
+};
+thread_local UploadStages g_upload;
+}  // namespace
+
+static int crn_upload(const void *const *parts, const size_t *sizes, const size_t *offs, int n_parts, size_t total,
+                      int dev, cudaStream_t st, void **d_out) {
+    UploadRing &ring = g_upload.by_dev[dev];
+    UploadStage &u = ring.slot[ring.next];
+    ring.next = (ring.next + 1) % UPLOAD_RING;
+    if (!u.ev && cudaEventCreateWithFlags(&u.ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return CRN_ECUDA;
+    }
+    if (u.pending) cudaEventSynchronize(u.ev);        /* the previous copy out of the staging buffer */
+    u.pending = false;
+    if (u.cap < total) {
+        if (u.pin) cudaFreeHost(u.pin);
+        u.pin = nullptr;
+        u.cap = 0;
+        const size_t cap = std::max(total, (size_t)1 << 16) * 2;
+        if (cudaMallocHost(&u.pin, cap) != cudaSuccess) { cudaGetLastError(); return CRN_ENOMEM; }
+        u.cap = cap;
+    }
+    for (int i = 0; i < n_parts; i++) memcpy((uint8_t *)u.pin + offs[i], parts[i], sizes[i]);
+    if (cudaMallocAsync(d_out, total, st) != cudaSuccess) { cudaGetLastError(); return CRN_ENOMEM; }
+    if (cudaMemcpyAsync(*d_out, u.pin, total, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaEventRecord(u.ev, st) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFreeAsync(*d_out, st);
+        return CRN_ECUDA;
+    }
+    u.pending = true;
+    return CRN_OK;
+}
+
+static int crn_upload1(const void *h, size_t bytes, int dev, cudaStream_t st, void **d_out) {
+    const size_t off = 0;
+    return crn_upload(&h, &bytes, &off, 1, bytes, dev, st, d_out);
+}
+
 extern "C" int crn_encode_batch(const crn_cb_desc *desc, int32_t n_cb, const uint8_t *info, int32_t attach_crc,
                                 uint8_t *d0, uint8_t *d1, uint8_t *d2, void *stream) {
     if (n_cb < 0) return CRN_EINVAL;
@@ -571,9 +639,7 @@ extern "C" int crn_encode_batch(const crn_cb_desc *desc, int32_t n_cb, const uin
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     void *dd = nullptr;
-    size_t b = sizeof(crn_cb_desc) * (size_t)n_cb;
-    if (cudaMallocAsync(&dd, b, st) != cudaSuccess) { cudaGetLastError(); return CRN_ENOMEM; }
-    cudaMemcpyAsync(dd, desc, b, cudaMemcpyHostToDevice, st);
+    if ((rc = crn_upload1(desc, sizeof(crn_cb_desc) * (size_t)n_cb, dev, st, &dd))) return rc;
     rc = crn_launch_encode((const crn_cb_desc *)dd, n_cb, info, attach_crc, d0, d1, d2, &t->tab, (void *)st);
     cudaFreeAsync(dd, st);
     return rc;
@@ -661,12 +727,10 @@ extern "C" int crn_tb_verdict_batch(const crn_tb_desc *tb, int32_t n_tb, const c
     cudaStream_t st = (cudaStream_t)stream;
     const size_t b0 = sizeof(crn_tb_desc) * (size_t)n_tb, o1 = (b0 + 255) & ~(size_t)255;
     const size_t tot = o1 + sizeof(crn_cb_desc) * (size_t)n_cb;
-    std::vector<uint8_t> host(tot);
-    memcpy(host.data(), tb, b0);
-    memcpy(host.data() + o1, desc, sizeof(crn_cb_desc) * (size_t)n_cb);
     void *dm = nullptr;
-    if (cudaMallocAsync(&dm, tot, st) != cudaSuccess) { cudaGetLastError(); return CRN_ENOMEM; }
-    cudaMemcpyAsync(dm, host.data(), tot, cudaMemcpyHostToDevice, st);
+    const void *parts[2] = {tb, desc};
+    const size_t sizes[2] = {b0, sizeof(crn_cb_desc) * (size_t)n_cb}, offs[2] = {0, o1};
+    if ((rc = crn_upload(parts, sizes, offs, 2, tot, dev, st, &dm))) return rc;
     rc = crn_launch_tb((const crn_tb_desc *)dm, n_tb, (const crn_cb_desc *)((uint8_t *)dm + o1), cb_words, crc_ok,
                        tb_ok, tb_words, (void *)st);
     cudaFreeAsync(dm, st);
@@ -684,11 +748,8 @@ static int rm_validate(const crn_rm_desc *desc, int32_t n_cb) {
     return CRN_OK;
 }
 
-static int rm_upload(const crn_rm_desc *desc, int32_t n_cb, cudaStream_t st, void **dd) {
-    const size_t b = sizeof(crn_rm_desc) * (size_t)n_cb;
-    if (cudaMallocAsync(dd, b, st) != cudaSuccess) { cudaGetLastError(); return CRN_ENOMEM; }
-    cudaMemcpyAsync(*dd, desc, b, cudaMemcpyHostToDevice, st);
-    return CRN_OK;
+static int rm_upload(const crn_rm_desc *desc, int32_t n_cb, int dev, cudaStream_t st, void **dd) {
+    return crn_upload1(desc, sizeof(crn_rm_desc) * (size_t)n_cb, dev, st, dd);
 }
 
 extern "C" int crn_rate_dematch_batch(const crn_rm_desc *desc, int32_t n_cb, const int16_t *e, int32_t combine,
@@ -702,7 +763,7 @@ extern "C" int crn_rate_dematch_batch(const crn_rm_desc *desc, int32_t n_cb, con
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     void *dd = nullptr;
-    if ((rc = rm_upload(desc, n_cb, st, &dd))) return rc;
+    if ((rc = rm_upload(desc, n_cb, dev, st, &dd))) return rc;
     rc = crn_launch_dematch((const crn_rm_desc *)dd, n_cb, e, combine, h0, h1, h2, (void *)st);
     cudaFreeAsync(dd, st);
     return rc;
@@ -719,7 +780,7 @@ extern "C" int crn_rate_match_batch(const crn_rm_desc *desc, int32_t n_cb, const
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     void *dd = nullptr;
-    if ((rc = rm_upload(desc, n_cb, st, &dd))) return rc;
+    if ((rc = rm_upload(desc, n_cb, dev, st, &dd))) return rc;
     rc = crn_launch_match((const crn_rm_desc *)dd, n_cb, d0, d1, d2, e, (void *)st);
     cudaFreeAsync(dd, st);
     return rc;

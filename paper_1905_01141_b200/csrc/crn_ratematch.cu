@@ -6,19 +6,16 @@
  * Geometry per CB: D = K + 4 bits per stream, R = ceil(D/32) rows, Kpi = 32 R,
  * ND = Kpi - D dummy bits, circular buffer w of Ncb = 3 Kpi positions (v0, then
  * v1/v2 interlaced), k0 = R (2 ceil(Ncb / 8R) rv + 2).  The dummy positions are
- * few (<= 97: the first row of each sub-block, plus one wrapped position of
- * v2), so each CTA lists them in shared memory and both directions become
- * gathers:
- *   de-matching: for every output (stream s, bit n) find its w position p by
- *     inverting the sub-block interleaver (the column permutation is the 5-bit
- *     bit reversal, its own inverse), its rank r among non-dummy positions
- *     counted circularly from k0, and sum the received values e[r + m 3D],
- *     m >= 0 (repetition); punctured positions get nothing.  The sum is exact
- *     int32 and is saturated once (onto the previous HARQ buffer when
- *     combining), so the result does not depend on any order.
- *   matching: for every output e[k] find the (k mod 3D)-th non-dummy position
- *     after k0 and copy its coded bit.
- * One CTA per CB, a thread per output element.
+ * few (<= 97) and sit only at row 0 of a column (plus one wrapped position
+ * of v2), so the rank of a position -- its index among non-dummy positions
+ * counted circularly from k0 -- is closed-form from a 64-entry table
+ * (build_ranks).  One CTA per CB; the CB's E values (or 3D bits) are staged in
+ * shared memory in rank order, so both global sides are coalesced:
+ *   de-matching: stage[r] = sum over m >= 0 of e[r + m 3D] (repetition; exact
+ *     int32; 0 for punctured ranks r >= E), then every output (stream s, bit
+ *     n) reads stage[rank(s, n)], saturated once (onto the previous HARQ
+ *     buffer when combining), so the result does not depend on any order.
+ *   matching: stage[rank(s, n)] = d_s[n], then e[k] = stage[k mod 3D].
  */
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -27,8 +24,7 @@
 
 namespace {
 
-constexpr int RM_THREADS = 256;
-constexpr int MAX_NULL = 128;
+constexpr int RM_THREADS = 512;
 
 __device__ __forceinline__ int bitrev5(int c) { return (int)(__brev((unsigned)c) >> 27); }
 
@@ -48,121 +44,327 @@ __device__ __forceinline__ Geo geo(int K, int rv) {
     return g;
 }
 
-/* Sorted w positions of the dummy bits, written by warp 0; returns the count. */
-__device__ int list_nulls(const Geo &g, int *nul, int *s_n) {
-    if (threadIdx.x == 0) {
-        int n = 0;
-        /* v0: row 0 of column c holds y = P(c), a dummy if P(c) < ND */
-        for (int c = 0; c < 32; c++)
-            if (bitrev5(c) < g.ND) nul[n++] = c * g.R;
-        const int n0 = n;
-        /* v1 (even w offsets after Kpi) repeats v0's pattern; v2 (odd offsets):
-         * y = (P(c) + 32 row + 1) mod Kpi, a dummy at row 0 if P(c) + 1 < ND and at
-         * the wrap k = Kpi - 1 (y = 0) if ND > 0; merge the two in w order */
-        int i1 = 0;
-        for (int c = 0; c < 32; c++) {
-            const int k = c * g.R;
-            const bool d2 = bitrev5(c) + 1 < g.ND;
-            while (i1 < n0 && nul[i1] < k) { nul[n++] = g.Kpi + 2 * nul[i1]; i1++; }
-            if (i1 < n0 && nul[i1] == k) { nul[n++] = g.Kpi + 2 * k; i1++; }
-            if (d2) nul[n++] = g.Kpi + 2 * k + 1;
+/* Dummy positions lie only at row 0 of a column (v0: w = cR if P(c) < ND; v1:
+ * Kpi + 2cR under the same condition; v2: Kpi + 2cR + 1 if P(c) + 1 < ND) plus,
+ * when ND > 0, the last position of w (v2's wrapped y = 0).  So for any
+ * NON-dummy position p in column c the number of dummies below p is a function
+ * of (region, c) alone -- every row-0 dummy of columns <= c in its region and of
+ * the regions before it (a row-0 dummy of the same column lies below p, or p is
+ * itself that dummy or precedes only dummies: a2 implies a0).  Warp 0 builds
+ * the 64 counts nb[region][c] and base = k0 - (dummies below k0), so a CB
+ * position's rank counted circularly from k0 is p - nb - base (mod 3D); it keeps
+ * the rank of row 0 of each of the 96 columns and the row-0 dummy masks. */
+struct RankTab {
+    int r0[96];           /* rank of row 0 of column (s, c), index 32 s + c, in [0, 3D) */
+    uint32_t dmask[3];    /* bit c of dmask[s]: row 0 of column (s, c) is a dummy */
+};
+
+__device__ void build_ranks(const Geo &g, RankTab *t) {
+    if (threadIdx.x < 32) {
+        const int c = threadIdx.x, P = bitrev5(c);
+        const int a0 = P < g.ND, a2 = P + 1 < g.ND;
+        int s0 = a0, s12 = a0 + a2;                                   /* inclusive scans over c */
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u0 = __shfl_up_sync(0xFFFFFFFFu, s0, o), u12 = __shfl_up_sync(0xFFFFFFFFu, s12, o);
+            if (c >= o) { s0 += u0; s12 += u12; }
         }
-        while (i1 < n0) { nul[n++] = g.Kpi + 2 * nul[i1]; i1++; }
-        if (g.ND > 0) nul[n++] = g.Kpi + 2 * (g.Kpi - 1) + 1;
-        *s_n = n;
+        const int N0 = __shfl_sync(0xFFFFFFFFu, s0, 31);
+        /* dummies strictly below k0 (the wrapped last position never is) */
+        const int below = (a0 && c * g.R < g.k0) + (a0 && g.Kpi + 2 * c * g.R < g.k0) +
+                          (a2 && g.Kpi + 2 * c * g.R + 1 < g.k0);
+        int tot = below;
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
+        const int base = g.k0 - tot;
+        /* rank of a non-dummy p in column c: p - nb - base; row 0's (or, for a dummy
+         * row 0, the next real position's) folded into [0, 3D): p - nb in [-1, 3D) */
+        const int nb[3] = {s0, N0 + s12, N0 + s12};
+        for (int s = 0; s < 3; s++) {
+            const int p0 = (s ? g.Kpi + (s - 1) : 0) + (s ? 2 : 1) * c * g.R;
+            int r = p0 - nb[s] - base;
+            if (r < 0) r += g.nn;
+            t->r0[32 * s + c] = r;
+        }
+        const uint32_t m0 = __ballot_sync(0xFFFFFFFFu, a0), m2 = __ballot_sync(0xFFFFFFFFu, a2);
+        if (c == 0) { t->dmask[0] = m0; t->dmask[1] = m0; t->dmask[2] = m2; }
     }
     __syncthreads();
-    return *s_n;
 }
 
-/* number of dummy positions < x */
-__device__ __forceinline__ int nulls_below(const int *nul, int n, int x) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (nul[mid] < x) lo = mid + 1; else hi = mid;
+
+/* ---- staging.  The CB's input range is brought into shared memory by one
+ * bulk copy (cp.async.bulk, completion on an mbarrier) of the 16-byte blocks
+ * that hold it -- never a byte outside those blocks, so never a page the range
+ * does not touch.  It is then re-laid out as T[s][c][row]: sub-block s's bit in
+ * column c (after the inter-column permutation) and row, column stride Rp
+ * chosen so that both walks over T are bank-conflict-free -- stream order n
+ * (y = n + ND, or y - 1 for v2, lies in column c = P(y mod 32), row y / 32: a
+ * warp's 32 consecutive y hit 32 distinct c, and c (Rp / elements-per-word) is
+ * a bijection mod 32 when that quotient is odd) and circular-buffer order (a
+ * column's rows are consecutive elements and consecutive ranks). */
+constexpr int RM_MAXR = (6144 + 4 + 31) / 32;                         /* 193 rows at most */
+
+/* (volatile: computed once and kept in a register, not re-derived per access) */
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    uint32_t a;
+    asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(p));
+    return a;
+}
+
+__device__ __forceinline__ void bar_init(uint64_t *bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void bar_expect(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bar_wait0(uint64_t *bar) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(smem_addr(bar)) : "memory");
+}
+
+/* shared-memory accesses by 32-bit shared address (keeps the compiler from
+ * re-deriving a generic window address at every access) */
+__device__ __forceinline__ uint32_t ld_s8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_s16(uint32_t a) {
+    int32_t v;
+    asm volatile("ld.shared.s16 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void st_s8(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_s8_if(uint32_t a, uint32_t v, bool p) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u8 [%0], %1; }" ::"r"(a), "r"(v),
+                 "r"((uint32_t)p) : "memory");
+}
+__device__ __forceinline__ void st_s16_if(uint32_t a, int32_t v, bool p) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u16 [%0], %1; }" ::"r"(a), "r"(v),
+                 "r"((uint32_t)p) : "memory");
+}
+
+struct Blocks {           /* the 16-byte blocks holding [src, src + len) */
+    const uint8_t *a0;
+    uint32_t bytes;
+    int lead;
+};
+
+__device__ __forceinline__ Blocks blocks_of(const void *src, int64_t len) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src), a0 = a & ~(uintptr_t)15;
+    const uintptr_t a1 = (a + (uintptr_t)len + 15) & ~(uintptr_t)15;
+    return Blocks{reinterpret_cast<const uint8_t *>(a0), (uint32_t)(a1 - a0), (int)(a - a0)};
+}
+
+__device__ __forceinline__ void bulk_load(void *dst, const Blocks &b, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(b.a0), "r"(b.bytes), "r"(smem_addr(bar)) : "memory");
+}
+
+/* smallest Rp >= R with Rp / q odd (q = elements per 32-bit word) */
+__device__ __forceinline__ int pad_rows(int R, int q) {
+    int Rp = (R + q - 1) / q * q;
+    if (((Rp / q) & 1) == 0) Rp += q;
+    return Rp;
+}
+
+__device__ __forceinline__ int t_index(const Geo &g, int Rp, int s, int n) {
+    int y = n + g.ND;
+    if (s == 2) y = y == 0 ? g.Kpi - 1 : y - 1;                    /* y = (P(col) + 32 row + 1) mod Kpi */
+    return (s * 32 + bitrev5(y & 31)) * Rp + (y >> 5);
+}
+
+/* Calls f(T index, rank, in_range, real) for the circular-buffer positions, a
+ * warp per column, lanes over rows: the rank grows by 1 (v0) or 2 (v1/v2) per
+ * row, the T index by 1.  Rows run to 32 ceil(R / 32) so the loop is
+ * warp-uniform: in_range = row < R, real = in_range and not a dummy (a dummy's
+ * or an out-of-range row's "rank" is some rank in [0, 3D) of a real position). */
+template <class F>
+__device__ __forceinline__ void for_each_position(const Geo &g, const RankTab &t, int Rp, F &&f) {
+    const int lane = threadIdx.x & 31;
+    const int nrow32 = (g.R + 31) >> 5;
+    for (int col = threadIdx.x >> 5; col < 96; col += RM_THREADS / 32) {
+        const int s = col >> 5, c = col & 31;
+        const int mul = s ? 2 : 1, inc = 32 * mul;
+        int r = t.r0[col] + mul * lane;                              /* mul lane <= 62 < 3D */
+        if (r >= g.nn) r -= g.nn;
+        const int skip0 = ((t.dmask[s] >> c) & 1u) ? 0 : -1;                        /* dummy rows */
+        const int skip1 = (col == 95 && g.ND > 0) ? g.R - 1 : -1;                   /* the wrapped dummy */
+        int ix = col * Rp + lane;
+#pragma unroll
+        for (int i = 0; i < (RM_MAXR + 31) / 32; i++) {
+            if (i < nrow32) {
+                const int row = lane + 32 * i;
+                const bool in_range = row < g.R;
+                f(ix, r, in_range, in_range && row != skip0 && row != skip1);
+            }
+            ix += 32;
+            r += inc;
+            if (r >= g.nn) r -= g.nn;
+        }
     }
-    return lo;
 }
 
-/* w position of bit n of stream s (inverse sub-block interleaving) */
-__device__ __forceinline__ int w_of(const Geo &g, int s, int n) {
-    const int y = n + g.ND;
-    if (s < 2) {
-        const int k = bitrev5(y & 31) * g.R + (y >> 5);
-        return s == 0 ? k : g.Kpi + 2 * k;
-    }
-    const int y1 = (y - 1 + g.Kpi) % g.Kpi;      /* y = (P(col) + 32 row + 1) mod Kpi */
-    const int k = bitrev5(y1 & 31) * g.R + (y1 >> 5);
-    return g.Kpi + 2 * k + 1;
-}
+constexpr int DM_RAW = (2 * 3 * (6144 + 4) + 32 + 15) / 16 * 16;      /* E <= 3D int16 + two partial blocks */
+constexpr int DM_T16 = 96 * 194 * 2;                                  /* pad_rows(193, 2) = 194 */
+constexpr int DM_SMEM = DM_RAW + DM_T16;                              /* 74,160 B: 3 CTAs per SM */
+static_assert(96 * (RM_MAXR | 1) * 4 <= DM_SMEM, "int32 T (repetition) fits the same space");
+constexpr int MT_RAW = (6144 + 4 + 32 + 15) / 16 * 16;                /* one stream + two partial blocks */
+constexpr int MT_T8 = 96 * 196 + 256;                                /* pad_rows(193, 4) = 196, + over-read slack */
+constexpr int MT_SMEM = 3 * MT_RAW + MT_T8;                           /* 37,648 B; Q (3D bytes) reuses the raw area */
+static_assert(3 * MT_RAW >= 3 * (6144 + 4), "Q fits the raw area");
 
+/* De-matching.  E <= 3D (no repetition): e is bulk-copied, re-laid out into
+ * int16 T in circular-buffer order (rank r's value e[r], 0 if punctured, r >=
+ * E), then the three streams are written in stream order, saturated once (onto
+ * the previous HARQ buffer when combining).  E > 3D: T holds the exact int32
+ * sums of e[r + m 3D] over m, read from global memory.  Order-independent. */
 __global__ void __launch_bounds__(RM_THREADS)
 dematch_kernel(const crn_rm_desc *__restrict__ desc, const int16_t *__restrict__ e, int combine,
                int16_t *__restrict__ h0, int16_t *__restrict__ h1, int16_t *__restrict__ h2) {
-    __shared__ int nul[MAX_NULL];
-    __shared__ int s_n;
+    extern __shared__ __align__(16) uint8_t dm_sm[];
+    __shared__ RankTab tab;
+    __shared__ __align__(8) uint64_t bar;
     const crn_rm_desc d = desc[blockIdx.x];
     const Geo g = geo(d.K, d.rv);
-    const int n_null = list_nulls(g, nul, &s_n);
-    const int base = g.k0 - nulls_below(nul, n_null, g.k0);      /* non-dummy positions before k0 */
     const int16_t *ec = e + d.e_off;
-    for (int x = threadIdx.x; x < 3 * g.D; x += RM_THREADS) {
-        const int s = x / g.D, n = x - s * g.D;
-        const int p = w_of(g, s, n);
-        int r = p - nulls_below(nul, n_null, p) - base;              /* rank counted from k0 */
-        if (r < 0) r += g.nn;
-        int32_t acc = 0;
-        for (int k = r; k < d.E; k += g.nn) acc += ec[k];
-        int16_t *h = (s == 0 ? h0 : s == 1 ? h1 : h2) + d.llr_off + n;
-        if (combine) acc += *h;
-        *h = (int16_t)(acc < -32768 ? -32768 : (acc > 32767 ? 32767 : acc));
+    const int E = d.E, nn = g.nn;
+    const bool rep = E > nn;
+    const Blocks blk = blocks_of(ec, 2 * (int64_t)E);
+    if (!rep && threadIdx.x == 0) {
+        bar_init(&bar);
+        bar_expect(&bar, blk.bytes);
+        bulk_load(dm_sm, blk, &bar);
+    }
+    build_ranks(g, &tab);                                             /* ends with __syncthreads */
+    int16_t *T16 = reinterpret_cast<int16_t *>(dm_sm + DM_RAW);
+    int32_t *T32 = reinterpret_cast<int32_t *>(dm_sm);
+    const int Rp = rep ? (g.R | 1) : pad_rows(g.R, 2);
+    if (!rep) {
+        bar_wait0(&bar);
+        const uint32_t raw = smem_addr(dm_sm) + blk.lead, t16 = smem_addr(T16);
+        for_each_position(g, tab, Rp, [&](int ix, int r, bool in_range, bool) {
+            const int32_t v = ld_s16(raw + 2 * min(r, E - 1));
+            st_s16_if(t16 + 2 * ix, r < E ? v : 0, in_range);
+        });
+    } else {
+        for_each_position(g, tab, Rp, [&](int ix, int r, bool in_range, bool) {
+            if (!in_range) return;
+            int32_t v = 0;
+            for (int k = r; k < E; k += nn) v += __ldg(ec + k);
+            T32[ix] = v;
+        });
+    }
+    __syncthreads();
+    /* stream order: a thread's n advances by 2 x RM_THREADS = 1024, i.e. 32 rows of
+     * the same column, so its T index advances by 32 */
+    const int half = g.D >> 1;                                        /* D = K + 4 is even */
+#pragma unroll 1
+    for (int s = 0; s < 3; s++) {
+        int16_t *h = (s == 0 ? h0 : s == 1 ? h1 : h2) + d.llr_off;
+        int i = threadIdx.x;
+        if (i >= half) continue;
+        int ia = t_index(g, Rp, s, 2 * i), ib = t_index(g, Rp, s, 2 * i + 1);
+        if (!rep && !combine && (reinterpret_cast<uintptr_t>(h) & 3u) == 0) {
+            uint32_t *hw = reinterpret_cast<uint32_t *>(h);
+            const uint32_t t16 = smem_addr(T16);
+            for (; i < half; i += RM_THREADS, ia += 32, ib += 32)
+                hw[i] = (uint32_t)(uint16_t)ld_s16(t16 + 2 * ia) | ((uint32_t)ld_s16(t16 + 2 * ib) << 16);
+        } else {
+            for (; i < half; i += RM_THREADS, ia += 32, ib += 32) {
+                int32_t va = rep ? T32[ia] : (int32_t)T16[ia], vb = rep ? T32[ib] : (int32_t)T16[ib];
+                if (combine) { va += h[2 * i]; vb += h[2 * i + 1]; }
+                h[2 * i] = (int16_t)max(-32768, min(32767, va));
+                h[2 * i + 1] = (int16_t)max(-32768, min(32767, vb));
+            }
+        }
     }
 }
 
+/* Matching: the three coded streams are bulk-copied, re-laid out into byte T in
+ * stream order, and each circular-buffer position's bit is written to e[r + m
+ * 3D] for every m with r + m 3D < E (punctured ranks: none). */
 __global__ void __launch_bounds__(RM_THREADS)
 match_kernel(const crn_rm_desc *__restrict__ desc, const uint8_t *__restrict__ d0, const uint8_t *__restrict__ d1,
              const uint8_t *__restrict__ d2, uint8_t *__restrict__ e) {
-    __shared__ int nul[MAX_NULL];
-    __shared__ int s_n;
+    extern __shared__ __align__(16) uint8_t mt_sm[];
+    __shared__ RankTab tab;
+    __shared__ __align__(8) uint64_t bar;
     const crn_rm_desc d = desc[blockIdx.x];
     const Geo g = geo(d.K, d.rv);
-    const int n_null = list_nulls(g, nul, &s_n);
-    const int base = g.k0 - nulls_below(nul, n_null, g.k0);
-    for (int k = threadIdx.x; k < d.E; k += RM_THREADS) {
-        int j = base + k % g.nn;                                      /* j-th non-dummy position overall */
-        if (j >= g.nn) j -= g.nn;
-        /* the j-th non-dummy position is p = j + c, c = #dummies before it: the number of
-         * dummies i with nul[i] - i <= j (nul[i] - i is nondecreasing) -- binary search */
-        int lo = 0, hi = n_null;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (nul[mid] - mid <= j) lo = mid + 1; else hi = mid;
+    const Blocks b0 = blocks_of(d0 + d.llr_off, g.D), b1 = blocks_of(d1 + d.llr_off, g.D),
+                 b2 = blocks_of(d2 + d.llr_off, g.D);
+    if (threadIdx.x == 0) {
+        bar_init(&bar);
+        bar_expect(&bar, b0.bytes + b1.bytes + b2.bytes);
+        bulk_load(mt_sm, b0, &bar);
+        bulk_load(mt_sm + MT_RAW, b1, &bar);
+        bulk_load(mt_sm + 2 * MT_RAW, b2, &bar);
+    }
+    build_ranks(g, &tab);                                             /* ends with __syncthreads */
+    uint8_t *T8 = mt_sm + 3 * MT_RAW;
+    const int Rp = pad_rows(g.R, 4);
+    bar_wait0(&bar);
+    /* stream order: a thread's n advances by RM_THREADS = 512 = 16 rows */
+#pragma unroll 1
+    for (int s = 0; s < 3; s++) {
+        const uint32_t raw = smem_addr(mt_sm) + s * MT_RAW + (s == 0 ? b0.lead : s == 1 ? b1.lead : b2.lead);
+        int n = threadIdx.x;
+        if (n >= g.D) continue;
+        for (uint32_t ta = smem_addr(T8) + t_index(g, Rp, s, n); n < g.D; n += RM_THREADS, ta += 16)
+            st_s8(ta, ld_s8(raw + n));
+    }
+    __syncthreads();
+    /* circular-buffer order: Q[r] = bit of rank r (Q reuses the raw area) */
+    uint8_t *Q = mt_sm;
+    const uint32_t qa = smem_addr(Q), t8 = smem_addr(T8);
+    for_each_position(g, tab, Rp, [&](int ix, int r, bool, bool real) { st_s8_if(qa + r, ld_s8(t8 + ix), real); });
+    __syncthreads();
+    /* e[k] = Q[k mod 3D]: whole words when e is word-aligned (3D = 0 mod 4) */
+    uint8_t *ec = e + d.e_off;
+    const int E = d.E, nn = g.nn;
+    if ((reinterpret_cast<uintptr_t>(ec) & 3u) == 0) {
+        const uint32_t *qw = reinterpret_cast<const uint32_t *>(Q);
+        uint32_t *ew = reinterpret_cast<uint32_t *>(ec);
+        const int nw = E >> 2, nnw = nn >> 2;
+        int w = threadIdx.x, j = w % nnw;
+        const int jinc = RM_THREADS % nnw;
+        for (; w < nw; w += RM_THREADS) {
+            ew[w] = qw[j];
+            j += jinc;
+            if (j >= nnw) j -= nnw;
         }
-        const int p = j + lo;
-        int s, n, y;
-        if (p < g.Kpi) { s = 0; y = (p % g.R) * 32 + bitrev5(p / g.R); }
-        else {
-            const int q = p - g.Kpi, kk = q >> 1;
-            if ((q & 1) == 0) { s = 1; y = (kk % g.R) * 32 + bitrev5(kk / g.R); }
-            else { s = 2; y = (bitrev5(kk / g.R) + 32 * (kk % g.R) + 1) % g.Kpi; }
-        }
-        n = y - g.ND;
-        const uint8_t *src = s == 0 ? d0 : s == 1 ? d1 : d2;
-        e[d.e_off + k] = src[d.llr_off + n];
+        for (int k = 4 * nw + threadIdx.x; k < E; k += RM_THREADS) ec[k] = Q[k % nn];
+    } else {
+        for (int k = threadIdx.x; k < E; k += RM_THREADS) ec[k] = Q[k % nn];
     }
 }
 
+template <class K>
+int rm_smem_attr(K kernel, int bytes) {                  /* once per process (one device per process) */
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess
+               ? CRN_OK : CRN_ECUDA;
+}
 }  // namespace
 
 extern "C" int crn_launch_dematch(const crn_rm_desc *d_desc, int32_t n_cb, const int16_t *e, int32_t combine,
                                   int16_t *h0, int16_t *h1, int16_t *h2, void *stream) {
-    dematch_kernel<<<n_cb, RM_THREADS, 0, (cudaStream_t)stream>>>(d_desc, e, combine, h0, h1, h2);
+    static const int attr = rm_smem_attr(dematch_kernel, DM_SMEM);
+    if (attr) return attr;
+    dematch_kernel<<<n_cb, RM_THREADS, DM_SMEM, (cudaStream_t)stream>>>(d_desc, e, combine, h0, h1, h2);
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
 }
 
 extern "C" int crn_launch_match(const crn_rm_desc *d_desc, int32_t n_cb, const uint8_t *d0, const uint8_t *d1,
                                 const uint8_t *d2, uint8_t *e, void *stream) {
-    match_kernel<<<n_cb, RM_THREADS, 0, (cudaStream_t)stream>>>(d_desc, d0, d1, d2, e);
+    static const int attr = rm_smem_attr(match_kernel, MT_SMEM);
+    if (attr) return attr;
+    match_kernel<<<n_cb, RM_THREADS, MT_SMEM, (cudaStream_t)stream>>>(d_desc, d0, d1, d2, e);
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
 }

@@ -457,8 +457,8 @@ def test_rate_dematch_and_match_parity(orc):
     matching equal the oracle's for mixed K (both kernel geometries), E from
     heavy puncturing to repetition and every redundancy version."""
     rng = np.random.default_rng(21)
-    ks = np.array([40, 48, 104, 248, 1008, 1056, 2112, 6144])
-    d = _rm_case(rng, 40, ks)
+    ks = np.array([40, 48, 56, 104, 112, 120, 248, 512, 1008, 528, 1056, 2112, 4096, 6144])   # ND in {4, 12, 20, 28}
+    d = _rm_case(rng, 80, ks)
     n_e = int((d["e_off"] + d["E"]).max())
     n_l = int((d["llr_off"] + d["K"] + 4).max())
     e = rng.integers(-3000, 3001, n_e).astype(np.int16)
