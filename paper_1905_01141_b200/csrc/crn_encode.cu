@@ -52,11 +52,6 @@ __device__ __forceinline__ int rsc_A(int s) {       /* zero-input step */
     return ((r2 ^ r3) << 2) | (r1 << 1) | r2;
 }
 
-__device__ __forceinline__ int rsc_Apow(int s, int L) {
-    for (int i = L % 7; i > 0; i--) s = rsc_A(s);
-    return s;
-}
-
 __device__ __forceinline__ uint32_t crc_step_bit(uint32_t reg, uint32_t poly) {   /* reg x mod g */
     return ((reg << 1) & 0xFFFFFFu) ^ ((reg & 0x800000u) ? poly : 0u);
 }
@@ -74,6 +69,7 @@ struct EncShared {
     uint16_t rsc[8 * 256];                /* (state, input byte) -> parity byte | next state << 8 */
     uint32_t crc_tab[2][256];             /* byte-at-a-time CRC24A / CRC24B (MSB-first) */
     uint32_t xp[2][ENC_WORDS + 1];        /* x^(32 m) mod g_A / g_B */
+    uint8_t apow[8 * 8];                  /* A^e s, index 8 e + s, e in [0, 7) */
     struct Warp {
         uint32_t c[ENC_WORDS + 2];        /* c, packed LSB-first */
         uint32_t ci[ENC_WORDS];           /* c' = c_{Pi(i)} */
@@ -93,6 +89,11 @@ __device__ void build_tables(EncShared &S) {
             s = (a << 2) | (r1 << 1) | r2;
         }
         S.rsc[e] = (uint16_t)(z | (uint32_t)s << 8);
+    }
+    if (threadIdx.x < 56) {
+        int s = threadIdx.x & 7;
+        for (int k = threadIdx.x >> 3; k > 0; k--) s = rsc_A(s);
+        S.apow[threadIdx.x] = (uint8_t)s;
     }
     for (int e = threadIdx.x; e < 2 * 256; e += ENC_THREADS) {
         const uint32_t poly = (e >> 8) ? POLY_B : POLY_A;
@@ -212,17 +213,19 @@ encode_kernel(const crn_cb_desc *__restrict__ desc, int n_cb, const uint8_t *__r
             const uint32_t f2x2 = (uint32_t)((2 * f2) % K);
             for (int t = w0; t < w1; t++) {
                 uint32_t acc = 0;
-                const int nbit = min(32, K - 32 * t);
-#pragma unroll 8
-                for (int k = 0; k < 32; k++) {
-                    if (k < nbit) {
-                        const uint32_t v = W.c[pi >> 5];
-                        acc = __funnelshift_r(acc, __funnelshift_r(v, v, pi), 1);   /* bit pi -> acc MSB */
-                        pi = min(pi + g, pi + g - (uint32_t)K);             /* (pi + g) mod K */
-                        g = min(g + f2x2, g + f2x2 - (uint32_t)K);
-                    } else {
-                        acc >>= 1;
-                    }
+                const int nbit = min(32, K - 32 * t);                /* 32, or 8/16/24 in the last word */
+                auto step = [&]() {
+                    const uint32_t v = W.c[pi >> 5];
+                    acc = __funnelshift_r(acc, __funnelshift_r(v, v, pi), 1);   /* bit pi -> acc MSB */
+                    pi = min(pi + g, pi + g - (uint32_t)K);                     /* (pi + g) mod K */
+                    g = min(g + f2x2, g + f2x2 - (uint32_t)K);
+                };
+                if (nbit == 32) {
+#pragma unroll
+                    for (int k = 0; k < 32; k++) step();
+                } else {
+                    for (int k = 0; k < nbit; k++) step();
+                    acc >>= 32 - nbit;
                 }
                 W.ci[t] = acc;
             }
@@ -238,14 +241,24 @@ encode_kernel(const crn_cb_desc *__restrict__ desc, int n_cb, const uint8_t *__r
             s1 = S.rsc[(s1 << 8) | cb1[k]] >> 8;
             s2 = S.rsc[(s2 << 8) | cb2[k]] >> 8;
         }
-        int st1 = 0, st2 = 0, run1 = 0, run2 = 0;
-        for (int l = 0; l < 32; l++) {
-            const int f1l = __shfl_sync(0xFFFFFFFFu, s1, l), f2l = __shfl_sync(0xFFFFFFFFu, s2, l);
-            const int Ll = __shfl_sync(0xFFFFFFFFu, L, l);
-            if (l == lane) { st1 = run1; st2 = run2; }
-            run1 = rsc_Apow(run1, Ll) ^ f1l;
-            run2 = rsc_Apow(run2, Ll) ^ f2l;
+        /* chunk l maps its start state s to A^{L_l} s + f_l: an affine map over GF(2)^3
+         * whose linear part is a power of A (order 7), so maps compose as
+         * (e2, b2) o (e1, b1) = (e1 + e2 mod 7, A^{e2} b1 + b2).  Inclusive scan over
+         * the lanes; lane l starts from lane l-1's b (the map of chunks < l applied
+         * to state 0), the CB ends in lane 31's. */
+        int e = L % 7, b1 = s1, b2 = s2;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int pe = __shfl_up_sync(0xFFFFFFFFu, e, o), pb1 = __shfl_up_sync(0xFFFFFFFFu, b1, o),
+                      pb2 = __shfl_up_sync(0xFFFFFFFFu, b2, o);
+            if (lane >= o) {
+                b1 ^= S.apow[8 * e + pb1];
+                b2 ^= S.apow[8 * e + pb2];
+                e = e + pe >= 7 ? e + pe - 7 : e + pe;
+            }
         }
+        const int u1 = __shfl_up_sync(0xFFFFFFFFu, b1, 1), u2 = __shfl_up_sync(0xFFFFFFFFu, b2, 1);
+        const int st1 = lane ? u1 : 0, st2 = lane ? u2 : 0;
+        const int run1 = __shfl_sync(0xFFFFFFFFu, b1, 31), run2 = __shfl_sync(0xFFFFFFFFu, b2, 31);
         s1 = st1;
         s2 = st2;
         uint8_t *z1b = reinterpret_cast<uint8_t *>(W.z1) + 4 * w0, *z2b = reinterpret_cast<uint8_t *>(W.z2) + 4 * w0;
@@ -262,15 +275,28 @@ encode_kernel(const crn_cb_desc *__restrict__ desc, int n_cb, const uint8_t *__r
         const bool al = ((reinterpret_cast<uintptr_t>(o0) | reinterpret_cast<uintptr_t>(o1) |
                           reinterpret_cast<uintptr_t>(o2)) & 3u) == 0;
         if (al) {
+            /* packed byte q = bits 8q .. 8q+7 -> output bytes 8q .. 8q+7 (two words, or one
+             * 8-byte store when the streams are 8-byte aligned) */
             const uint8_t *n0 = reinterpret_cast<const uint8_t *>(W.c), *n1 = reinterpret_cast<const uint8_t *>(W.z1),
                           *n2 = reinterpret_cast<const uint8_t *>(W.z2);
-            for (int q = lane; q < (K >> 2); q += 32) {              /* nibble q = bits 4q .. 4q+3 */
-                const int sh = (q & 1) * 4;
-                const uint32_t a = (n0[q >> 1] >> sh) & 0xFu, b = (n1[q >> 1] >> sh) & 0xFu,
-                               c = (n2[q >> 1] >> sh) & 0xFu;
-                reinterpret_cast<uint32_t *>(o0)[q] = (a * 0x00204081u) & 0x01010101u;
-                reinterpret_cast<uint32_t *>(o1)[q] = (b * 0x00204081u) & 0x01010101u;
-                reinterpret_cast<uint32_t *>(o2)[q] = (c * 0x00204081u) & 0x01010101u;
+            const bool al8 = ((reinterpret_cast<uintptr_t>(o0) | reinterpret_cast<uintptr_t>(o1) |
+                               reinterpret_cast<uintptr_t>(o2)) & 7u) == 0;
+            auto expand = [](uint32_t b) {
+                return make_uint2(((b & 0xFu) * 0x00204081u) & 0x01010101u, ((b >> 4) * 0x00204081u) & 0x01010101u);
+            };
+            for (int q = lane; q < (K >> 3); q += 32) {
+                const uint2 a = expand(n0[q]), b = expand(n1[q]), c = expand(n2[q]);
+                if (al8) {
+                    reinterpret_cast<uint2 *>(o0)[q] = a;
+                    reinterpret_cast<uint2 *>(o1)[q] = b;
+                    reinterpret_cast<uint2 *>(o2)[q] = c;
+                } else {
+                    uint32_t *p0 = reinterpret_cast<uint32_t *>(o0) + 2 * q, *p1 = reinterpret_cast<uint32_t *>(o1) + 2 * q,
+                             *p2 = reinterpret_cast<uint32_t *>(o2) + 2 * q;
+                    p0[0] = a.x; p0[1] = a.y;
+                    p1[0] = b.x; p1[1] = b.y;
+                    p2[0] = c.x; p2[1] = c.y;
+                }
             }
         } else {
             for (int n = lane; n < K; n += 32) {
