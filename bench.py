@@ -518,6 +518,42 @@ def run_crn(args):
                        "packed bits + crc_ok in pinned host memory"}
         del host
 
+        # int8 ingest (row f4, crn_plan_set_llr_format, R31): the same CBs with
+        # their int16 LLRs (scale 8: |L| is almost always < 128 at cfg4's 1 dB) saturated
+        # to int8 and read back with shift 0 -- half the bytes over PCIe; a (slightly)
+        # different input, so reported beside e2e with the clipped fraction
+        sh = 0
+        clipped = sum(int((x.abs() > 127).sum()) for x in b.llr) / (3 * b.n_llr)
+        q8 = [torch.clamp(x, -128, 127).to(torch.int8) for x in b.llr]
+        host8 = [x.cpu().pin_memory() for x in q8]
+        del q8
+        plan8 = crn.Plan(b.desc)
+        plan8.set_llr_format(8, sh)
+        hok8 = torch.empty(ok.numel(), dtype=ok.dtype).pin_memory()
+
+        def e2e8_step():
+            plan8.decode_host(host8[0], host8[1], host8[2], iters, False, hb, hok8, None, stream=stream)
+
+        for _ in range(max(1, args.warmup)):
+            e2e8_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ne):
+            e2e8_step()
+        e1.record(stream)
+        barrier()
+        t8 = torch.tensor([e0.elapsed_time(e1) / ne], dtype=torch.float64, device=red_dev)
+        if dist:
+            dist.all_reduce(t8, op=dist.ReduceOp.MAX)
+        e2e["int8_ingest"] = {
+            "value": info_bits / (t8.item() * 1e-3) / 1e6, "unit": "Mbit/s", "ms_per_step": t8.item(),
+            "h2d_bytes_per_step": in_bytes // 2 * ws, "d2h_bytes_per_step": (b.n_words * 4 + b.n_cb) * ws,
+            "llr_format": f"int8, read as x * 2^{sh}", "crc_ok_host": int(hok8[:b.n_cb].to(torch.int64).sum()),
+            "clipped_fraction": clipped,
+            "note": "same CBs, int16 LLRs saturated to int8 (the int16 e2e above decodes the unsaturated input)"}
+        del host8, plan8
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()

@@ -141,6 +141,17 @@ int crn_plan_set_purge(void *plan, int32_t on);
 /* At most max_ctas persistent CTAs for this plan's decodes (0 = one per SM):
  * shares the GPU with other work; with 1 the tasks run strictly in order. */
 int crn_plan_set_grid(void *plan, int32_t max_ctas);
+/* LLR input format of later crn_plan_decode / crn_plan_decode_host calls of
+ * this plan (SURVEY.md §8(f) row f4 "int8 LLR ingest": half the host->device
+ * and HBM bytes).  bits = 16, shift = 0: int16 LLRs (the default).  bits = 8,
+ * shift in [0, 8]: the three LLR arrays hold int8 values x at the same element
+ * offsets (desc.llr_off) -- pass them cast to const int16_t * -- and each is
+ * read as the int16 LLR x * 2^shift, after which decoding is exactly that of
+ * the int16 input (clamp to +-4096, filler override, R31).
+ * crn_stream_run stays int16.  CRN_EINVAL for any other (bits, shift). */
+int crn_plan_set_llr_format(void *plan, int32_t bits, int32_t shift);
+/* Bytes per LLR element of the plan's current format (2 or 1). */
+int crn_plan_llr_bytes(void *plan);
 /* Number of decode-kernel launches one crn_plan_decode performs (for gpu_launches). */
 int crn_plan_launches(void *plan);
 void crn_plan_destroy(void *plan);

@@ -63,6 +63,8 @@ _SIGS = {
     "crn_plan_set_variant": (C.c_int, [vp, C.c_int32]),
     "crn_plan_set_purge": (C.c_int, [vp, C.c_int32]),
     "crn_plan_set_grid": (C.c_int, [vp, C.c_int32]),
+    "crn_plan_set_llr_format": (C.c_int, [vp, C.c_int32, C.c_int32]),
+    "crn_plan_llr_bytes": (C.c_int, [vp]),
     "crn_plan_decode_host": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, C.c_int32, vp]),
     "crn_plan_chunks": (C.c_int, [vp]),
     "crn_stream_run": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int32, vp]),
@@ -175,6 +177,7 @@ class Plan:
     def decode(self, l0, l1, l2, max_iters: int, early_term: bool, out_bits, crc_ok, iters_used=None,
                ext_out=None, stream=None) -> None:
         _cuda_dev(l0, l1, l2, out_bits, crc_ok, iters_used, ext_out)
+        self._check_llr(l0, l1, l2)
         _chk(lib().crn_plan_decode(self.h, _ptr(l0), _ptr(l1), _ptr(l2), max_iters, int(early_term),
                                    _ptr(out_bits), _ptr(crc_ok), _ptr(iters_used), _ptr(ext_out),
                                    _stream(stream)), "crn_plan_decode")
@@ -185,6 +188,7 @@ class Plan:
         for t in (h0, h1, h2, h_bits, h_ok, h_iters):
             if t is not None and t.is_cuda:
                 raise CrnError("crn_plan_decode_host takes host buffers")
+        self._check_llr(h0, h1, h2)
         _chk(lib().crn_plan_decode_host(self.h, _ptr(h0), _ptr(h1), _ptr(h2), max_iters, int(early_term),
                                         _ptr(h_bits), _ptr(h_ok), _ptr(h_iters), n_chunks, _stream(stream)),
              "crn_plan_decode_host")
@@ -197,6 +201,22 @@ class Plan:
 
     def set_grid(self, max_ctas: int) -> None:
         _chk(lib().crn_plan_set_grid(self.h, max_ctas), "crn_plan_set_grid")
+
+    def set_llr_format(self, bits: int, shift: int = 0) -> None:
+        """crn_plan_set_llr_format: 16 (int16 LLRs) or 8 (int8 LLRs read as x * 2^shift);
+        the LLR tensors of later decode / decode_host calls must then be int8."""
+        _chk(lib().crn_plan_set_llr_format(self.h, bits, shift), "crn_plan_set_llr_format")
+
+    @property
+    def llr_bytes(self) -> int:
+        return int(lib().crn_plan_llr_bytes(self.h))
+
+    def _check_llr(self, *ts):
+        import torch
+        want = torch.int8 if self.llr_bytes == 1 else torch.int16
+        for t in ts:
+            if t.dtype != want:
+                raise CrnError(f"LLR tensors must be {want} for this plan's LLR format, got {t.dtype}")
 
     @property
     def chunks(self) -> int:

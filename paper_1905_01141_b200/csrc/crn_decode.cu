@@ -392,21 +392,58 @@ __device__ __forceinline__ void tm_load16_wait(u32 ta, u32 v[HW]) {
                  : "memory");
 }
 
-/* 16 consecutive int16 LLRs of one stream: 8-byte vector loads when aligned.
- * Returned as 8 words of (element 2i, element 2i+1). */
-__device__ __forceinline__ void load16(const int16_t *__restrict__ src, u32 w[HW / 2]) {
-    if ((reinterpret_cast<uintptr_t>(src) & 7) == 0) {
-        const uint2 *v = reinterpret_cast<const uint2 *>(src);
+/* LLR element idx of a stream: int16, or with sh8 >= 0 (int8 ingest, row f4,
+ * crn_plan_set_llr_format) the int8 value x read as the int16 x * 2^sh8. */
+template <bool LLR8>
+__device__ __forceinline__ int16_t ld_llr(const int16_t *__restrict__ base, int64_t idx, int sh8) {
+    if (!LLR8) return __ldg(base + idx);
+    return (int16_t)((int)__ldg(reinterpret_cast<const int8_t *>(base) + idx) << sh8);
+}
+
+/* int8 bytes (b0, b1) selected by sel (0x9180: bytes 0, 1; 0xB3A2: bytes 2, 3) ->
+ * the int16x2 word (b0 2^sh8, b1 2^sh8): prmt sign-replicates into the high bytes */
+__device__ __forceinline__ u32 widen8(u32 x, int sh8, bool hi) {
+    u32 r;
+    if (hi) asm("prmt.b32 %0, %1, 0, 0xB3A2;" : "=r"(r) : "r"(x));
+    else asm("prmt.b32 %0, %1, 0, 0x9180;" : "=r"(r) : "r"(x));
+    return ((r & 0xFFFF0000u) << sh8) | ((r << sh8) & 0xFFFFu);
+}
+
+/* 16 consecutive LLRs of one stream from element idx: 8-byte (int16) or 4-byte
+ * (int8) vector loads when aligned.  Returned as 8 words of (element 2i, 2i+1). */
+template <bool LLR8>
+__device__ __forceinline__ void load16(const int16_t *__restrict__ base, int64_t idx, int sh8, u32 w[HW / 2]) {
+    if (!LLR8) {
+        const int16_t *src = base + idx;
+        if ((reinterpret_cast<uintptr_t>(src) & 7) == 0) {
+            const uint2 *v = reinterpret_cast<const uint2 *>(src);
 #pragma unroll
-        for (int k = 0; k < HW / 4; k++) {
-            const uint2 x = __ldg(v + k);
-            w[2 * k] = x.x;
-            w[2 * k + 1] = x.y;
+            for (int k = 0; k < HW / 4; k++) {
+                const uint2 x = __ldg(v + k);
+                w[2 * k] = x.x;
+                w[2 * k + 1] = x.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < HW / 2; k++)
+                w[k] = (u32)(uint16_t)__ldg(src + 2 * k) | ((u32)(uint16_t)__ldg(src + 2 * k + 1) << 16);
         }
     } else {
+        const int8_t *src = reinterpret_cast<const int8_t *>(base) + idx;
+        if ((reinterpret_cast<uintptr_t>(src) & 3) == 0) {
+            const u32 *v = reinterpret_cast<const u32 *>(src);
 #pragma unroll
-        for (int k = 0; k < HW / 2; k++)
-            w[k] = (u32)(uint16_t)__ldg(src + 2 * k) | ((u32)(uint16_t)__ldg(src + 2 * k + 1) << 16);
+            for (int k = 0; k < HW / 4; k++) {
+                const u32 x = __ldg(v + k);
+                w[2 * k] = widen8(x, sh8, false);
+                w[2 * k + 1] = widen8(x, sh8, true);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < HW / 2; k++)
+                w[k] = (u32)(uint16_t)(int16_t)((int)__ldg(src + 2 * k) << sh8) |
+                       ((u32)(uint16_t)(int16_t)((int)__ldg(src + 2 * k + 1) << sh8) << 16);
+        }
     }
 }
 
@@ -550,13 +587,14 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
     }
 }
 
-template <bool SCALE, bool PURGE>
+template <bool SCALE, bool PURGE, bool LLR8>
 __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
                                               const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
                                               const int16_t *__restrict__ l2, int max_iters, int et,
                                               uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok,
                                               uint8_t *__restrict__ iters_used, int16_t *__restrict__ ext_out,
-                                              const crn_tables &tab, u32 *sm, u32 tmem, TaskSh sh, Purge pg) {
+                                              const crn_tables &tab, u32 *sm, u32 tmem, TaskSh sh, Purge pg,
+                                              int sh8) {
     constexpr int W = 32;
     const int M = tk.M, NP = tk.n_pairs, T = NP * M;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -597,12 +635,12 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
 #pragma unroll
         for (int x = 0; x < 3; x++) {
             const int16_t *src = x == 0 ? l0 : x == 1 ? l1 : l2;
-            if (clo >= 0) load16(src + olo + n0, wl[x]);
+            if (clo >= 0) load16<LLR8>(src, olo + n0, sh8, wl[x]);
             else {
 #pragma unroll
                 for (int k = 0; k < HW / 2; k++) wl[x][k] = 0;
             }
-            if (chi >= 0) load16(src + ohi + n0, wh[x]);
+            if (chi >= 0) load16<LLR8>(src, ohi + n0, sh8, wh[x]);
             else {
 #pragma unroll
                 for (int k = 0; k < HW / 2; k++) wh[x][k] = 0;
@@ -620,8 +658,8 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             for (int mm = 0; mm < 12; mm++) {     /* tails: DESIGN.md R11 column order */
                 const int col = tk.K + mm / 3;
                 const int16_t *src = (mm % 3 == 0) ? l0 : (mm % 3 == 1) ? l1 : l2;
-                t0[mm] = clo >= 0 ? __ldg(src + olo + col) : (int16_t)0;
-                t1[mm] = chi >= 0 ? __ldg(src + ohi + col) : (int16_t)0;
+                t0[mm] = clo >= 0 ? ld_llr<LLR8>(src, olo + col, sh8) : (int16_t)0;
+                t1[mm] = chi >= 0 ? ld_llr<LLR8>(src, ohi + col, sh8) : (int16_t)0;
             }
         }
         u32 sn[HW];
@@ -908,13 +946,14 @@ __device__ __forceinline__ void siso_gsplit(const GSplit &g, bool tail_thr, int 
     }
 }
 
-template <bool SCALE, bool PURGE>
+template <bool SCALE, bool PURGE, bool LLR8>
 __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
                                             const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
                                             const int16_t *__restrict__ l2, int max_iters, int et,
                                             uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok,
                                             uint8_t *__restrict__ iters_used, int16_t *__restrict__ ext_out,
-                                            const crn_tables &tab, u32 *sm, u32 tmem, TaskSh sh, Purge pg) {
+                                            const crn_tables &tab, u32 *sm, u32 tmem, TaskSh sh, Purge pg,
+                                            int sh8) {
     const int tid = threadIdx.x, warp = tid >> 5;
     GSplit g;
     g.W = tk.W;
@@ -961,8 +1000,8 @@ __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_des
 #pragma unroll
             for (int x = 0; x < 3; x++) {
                 const int16_t *src = x == 0 ? l0 : x == 1 ? l1 : l2;
-                int16_t a = clo >= 0 ? __ldg(src + olo + n) : (int16_t)0;
-                int16_t b = chi >= 0 ? __ldg(src + ohi + n) : (int16_t)0;
+                int16_t a = clo >= 0 ? ld_llr<LLR8>(src, olo + n, sh8) : (int16_t)0;
+                int16_t b = chi >= 0 ? ld_llr<LLR8>(src, ohi + n, sh8) : (int16_t)0;
                 if (x < 2) {                                   /* known filler 0: Ls = Lp1 = -4096 */
                     if (n < Flo) a = -4096;
                     if (n < Fhi) b = -4096;
@@ -983,8 +1022,8 @@ __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_des
             for (int mm = 0; mm < 12; mm++) {
                 const int col = K + mm / 3;
                 const int16_t *src = (mm % 3 == 0) ? l0 : (mm % 3 == 1) ? l1 : l2;
-                tl[mm] = clamp_pack(clo >= 0 ? __ldg(src + olo + col) : (int16_t)0,
-                                    chi >= 0 ? __ldg(src + ohi + col) : (int16_t)0);
+                tl[mm] = clamp_pack(clo >= 0 ? ld_llr<LLR8>(src, olo + col, sh8) : (int16_t)0,
+                                    chi >= 0 ? ld_llr<LLR8>(src, ohi + col, sh8) : (int16_t)0);
             }
 #pragma unroll
             for (int c = 0; c < 2; c++) {
@@ -1089,7 +1128,8 @@ struct NextSh {
 
 __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks, const crn_task *__restrict__ tasks,
                                            const crn_pair *__restrict__ pairs, const crn_cb_desc *__restrict__ desc,
-                                           const int16_t *l0, const int16_t *l1, const int16_t *l2, int lane) {
+                                           const int16_t *l0, const int16_t *l1, const int16_t *l2, int lane,
+                                           int sh8) {
     int nt = 0;
     if (lane == 0) nt = atomicAdd(counter, 1);
     nt = __shfl_sync(0xFFFFFFFFu, nt, 0);
@@ -1111,11 +1151,12 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
         nx.F[e] = d.F;
         nx.kind[e] = d.crc_kind;
         if (nx.tb) nx.tb[e] = d.reserved;
-        const int64_t off = d.llr_off;
-        const uint32_t bytes = 2u * (uint32_t)(t.K + 4);
+        const int esz = sh8 < 0 ? 2 : 1;                 /* int16 or int8 LLRs */
+        const int64_t off = esz * d.llr_off;
+        const uint32_t bytes = (uint32_t)esz * (uint32_t)(t.K + 4);
 #pragma unroll
         for (int x = 0; x < 3; x++) {
-            const uintptr_t a = reinterpret_cast<uintptr_t>((x == 0 ? l0 : x == 1 ? l1 : l2) + off);
+            const uintptr_t a = reinterpret_cast<uintptr_t>(x == 0 ? l0 : x == 1 ? l1 : l2) + off;
             const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (a + bytes + 15) & ~(uintptr_t)15;
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
                          : "memory");
@@ -1125,7 +1166,7 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
 
 /* PURGE: the TB-purge instantiation (crn_plan_set_purge); the default one has no
  * purge code at all, so the hot loops are compiled exactly as without it. */
-template <bool PURGE>
+template <bool PURGE, bool LLR8>
 __global__ void __launch_bounds__(BLOCK, 1)
 decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__ tasks, int n_tasks,
               const crn_pair *__restrict__ pairs, const int16_t *__restrict__ l0,
@@ -1133,6 +1174,8 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
               uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok, uint8_t *__restrict__ iters_used,
               int16_t *__restrict__ ext_out, crn_tables tab, uint8_t *ws, int variant, uint8_t *tb_dead_arg) {
     uint8_t *const tb_dead = PURGE ? tb_dead_arg : nullptr;
+    const int sh8 = (variant >> 8) - 1;         /* LLR format: -1 int16, else int8 << sh8 (LLR8) */
+    variant &= 0xFF;
     extern __shared__ __align__(16) u32 smem[];
     __shared__ int s_ntask, s_left;
     __shared__ crn_task s_ntk;
@@ -1164,7 +1207,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
      * move on-chip / into L2 while task t decodes. */
     const NextSh nx{&s_ntask, &s_ntk, s_ncb, s_nF, s_nkind, PURGE ? s_ntb : nullptr};
     prof_init();
-    if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid);
+    if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
     for (;;) {
         __syncthreads();                        /* next slots filled */
         const int task = s_ntask;
@@ -1190,7 +1233,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             }
         }
         __syncthreads();                        /* next slots consumed */
-        if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid);
+        if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
         if (PURGE) {                            /* a fully purged task is skipped */
             if (tid == 0) {
                 int left = 0;
@@ -1203,18 +1246,18 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
         prof_mark(P_FETCH);
         if (tk.W == 32) {
             if (variant == CRN_VARIANT_SCALED)
-                run_task_fast<true, PURGE>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab, smem,
-                                    tmem, sh, pg);
+                run_task_fast<true, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab, smem,
+                                    tmem, sh, pg, sh8);
             else
-                run_task_fast<false, PURGE>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
-                                     smem, tmem, sh, pg);
+                run_task_fast<false, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
+                                     smem, tmem, sh, pg, sh8);
         } else {
             if (variant == CRN_VARIANT_SCALED)
-                run_task_split<true, PURGE>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
-                                     smem, tmem, sh, pg);
+                run_task_split<true, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
+                                     smem, tmem, sh, pg, sh8);
             else
-                run_task_split<false, PURGE>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
-                                      smem, tmem, sh, pg);
+                run_task_split<false, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
+                                      smem, tmem, sh, pg, sh8);
         }
     }
     prof_flush();
@@ -1229,33 +1272,44 @@ size_t smem_bytes() { return (size_t)SMEM_WORDS * 4; }
 
 extern "C" size_t crn_decode_ws_bytes(int32_t) { return WS_HEAD; }   /* the task counter; all decode state is on chip */
 
+/* the four instantiations: <purge?, int8 LLRs?> */
+template <class F>
+cudaError_t for_each_kernel(F &&f) {
+    cudaError_t e = f((const void *)decode_kernel<false, false>);
+    if (e == cudaSuccess) e = f((const void *)decode_kernel<true, false>);
+    if (e == cudaSuccess) e = f((const void *)decode_kernel<false, true>);
+    if (e == cudaSuccess) e = f((const void *)decode_kernel<true, true>);
+    return e;
+}
+
 extern "C" int crn_decode_grid(int device) {
     /* returns the persistent grid (one CTA per SM), or a negative code:
      * -100 - cudaError of the smem attribute, -200 - cudaError of the occupancy
      * query, -300 - occupancy (must be exactly 1: the CTA owns all TMEM columns) */
     static int configured = -1;
     if (configured != device) {
-        cudaError_t e = cudaFuncSetAttribute(decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem_bytes());
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes());
+        cudaError_t e = for_each_kernel([](const void *k) {
+            return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes());
+        });
         if (e != cudaSuccess) return -100 - (int)e;
         configured = device;
     }
-    int sms = 0, occ = 0;
+    int sms = 0, bad = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    int occ2 = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decode_kernel<false>, BLOCK, smem_bytes());
-    if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, decode_kernel<true>, BLOCK, smem_bytes());
+    cudaError_t e = for_each_kernel([&](const void *k) {
+        int occ = 0;
+        cudaError_t r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, BLOCK, smem_bytes());
+        if (r == cudaSuccess && occ != 1) bad = occ ? occ : -1;
+        return r;
+    });
     if (e != cudaSuccess) return -200 - (int)e;
-    if (occ != 1 || occ2 != 1) return -300 - occ;
+    if (bad) return -300 - (bad > 0 ? bad : 0);
     return sms;
 }
 
 extern "C" int crn_decode_kernel_info(int32_t *static_smem, int32_t *dyn_smem, int32_t *max_dyn, int32_t *regs) {
     cudaFuncAttributes a;
-    if (cudaFuncGetAttributes(&a, decode_kernel<false>) != cudaSuccess) return CRN_ECUDA;
+    if (cudaFuncGetAttributes(&a, decode_kernel<false, false>) != cudaSuccess) return CRN_ECUDA;
     *static_smem = (int32_t)a.sharedSizeBytes;
     *dyn_smem = (int32_t)smem_bytes();
     *max_dyn = a.maxDynamicSharedSizeBytes;
@@ -1271,12 +1325,19 @@ extern "C" int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_ta
     cudaStream_t st = (cudaStream_t)stream;
     if (!ws_zeroed && cudaMemsetAsync(ws, 0, WS_HEAD, st) != cudaSuccess) return CRN_ECUDA;
     const int g = grid < n_tasks ? grid : n_tasks;
-    if (tb_dead)
-        decode_kernel<true><<<g, BLOCK, smem_bytes(), st>>>(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et,
-                                                            bits, ok, it, ext, *tab, (uint8_t *)ws, variant, tb_dead);
-    else
-        decode_kernel<false><<<g, BLOCK, smem_bytes(), st>>>(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters,
-                                                             et, bits, ok, it, ext, *tab, (uint8_t *)ws, variant, nullptr);
+    const bool llr8 = (variant >> 8) != 0;      /* crn_plan_set_llr_format: int8 LLRs */
+#define CRN_LAUNCH(PG, L8)                                                                                        \
+    decode_kernel<PG, L8><<<g, BLOCK, smem_bytes(), st>>>(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, \
+                                                          et, bits, ok, it, ext, *tab, (uint8_t *)ws, variant,      \
+                                                          PG ? tb_dead : nullptr)
+    if (tb_dead) {
+        if (llr8) CRN_LAUNCH(true, true);
+        else CRN_LAUNCH(true, false);
+    } else {
+        if (llr8) CRN_LAUNCH(false, true);
+        else CRN_LAUNCH(false, false);
+    }
+#undef CRN_LAUNCH
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
 }
 

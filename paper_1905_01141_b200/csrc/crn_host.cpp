@@ -405,7 +405,7 @@ static int launch(Plan *P, DevTables *t, const int16_t *l0, const int16_t *l1, c
         if (cudaMemsetAsync(dead, 0, (size_t)P->n_tb, st) != cudaSuccess) return CRN_ECUDA;
     }
     return crn_launch_tasks(P->dev, t, P->d_desc, P->d_tasks, P->n_tasks, P->d_pairs, l0, l1, l2, max_iters, et,
-                            bits, ok, it, ext, ws, ws_bytes, st, P->variant, dead, P->grid_cap);
+                            bits, ok, it, ext, ws, ws_bytes, st, crn_plan_kernel_variant(P), dead, P->grid_cap);
 }
 
 extern "C" int crn_plan_create(const crn_cb_desc *desc, int32_t n_cb, void **plan) {
@@ -457,6 +457,21 @@ extern "C" int crn_plan_set_purge(void *plan, int32_t on) {
     }
     P->purge = on;
     return CRN_OK;
+}
+
+int crn_plan_kernel_variant(const Plan *P) { return P->variant | ((P->llr8 + 1) << 8); }
+
+extern "C" int crn_plan_set_llr_format(void *plan, int32_t bits, int32_t shift) {
+    Plan *P = (Plan *)plan;
+    if (!P) return CRN_EINVAL;
+    if (bits == 16 && shift == 0) { P->llr8 = -1; return CRN_OK; }
+    if (bits == 8 && shift >= 0 && shift <= 8) { P->llr8 = shift; return CRN_OK; }
+    return CRN_EINVAL;
+}
+
+extern "C" int crn_plan_llr_bytes(void *plan) {
+    const Plan *P = (const Plan *)plan;
+    return P ? (P->llr8 < 0 ? 2 : 1) : CRN_EINVAL;
 }
 
 extern "C" int crn_plan_set_grid(void *plan, int32_t max_ctas) {

@@ -18,6 +18,10 @@ struct DevTables {
 
 struct HostPipe;      /* crn_runtime.cpp: staging buffers + streams of crn_plan_decode_host */
 
+/* the kernel's variant word: decoder variant | (LLR format + 1) << 8 */
+struct Plan;
+int crn_plan_kernel_variant(const Plan *P);
+
 struct Plan {
     int dev = -1;
     int n_cb = 0, n_tasks = 0;
@@ -29,6 +33,7 @@ struct Plan {
     int variant = CRN_VARIANT_MAXLOG;  /* decoder variant (crn_plan_set_variant) */
     int purge = 0;                     /* TB purge (crn_plan_set_purge) */
     int grid_cap = 0;                  /* persistent-grid limit (crn_plan_set_grid), 0 = one CTA per SM */
+    int llr8 = -1;                     /* LLR format (crn_plan_set_llr_format): -1 int16, else int8 << llr8 */
     int n_tb = 0;                      /* TB ids in the descriptors' reserved field: 0..n_tb-1 */
     uint8_t *d_tb_dead = nullptr;      /* per TB: a CB of it failed (purge) */
     HostPipe *pipe = nullptr;

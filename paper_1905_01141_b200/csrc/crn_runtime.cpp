@@ -178,17 +178,19 @@ extern "C" int crn_plan_decode_host(void *plan, const int16_t *h0, const int16_t
     cudaEventRecord(p->ev_start, st);
     cudaStreamWaitEvent(p->s_in, p->ev_start, 0);
     cudaStreamWaitEvent(p->s_out, p->ev_start, 0);
-    const int16_t *hs[3] = {h0, h1, h2};
+    const uint8_t *hs[3] = {(const uint8_t *)h0, (const uint8_t *)h1, (const uint8_t *)h2};
+    const size_t esz = P->llr8 < 0 ? sizeof(int16_t) : sizeof(int8_t);    /* crn_plan_set_llr_format */
     for (int c = 0; c < p->n_chunks; c++) {
         const Chunk &k = p->ch[c];
-        const size_t nb = sizeof(int16_t) * (size_t)(k.llr1 - k.llr0);
+        const size_t nb = esz * (size_t)(k.llr1 - k.llr0);
         for (int s = 0; s < 3; s++)
-            cudaMemcpyAsync(p->d_l[s] + k.llr0, hs[s] + k.llr0, nb, cudaMemcpyHostToDevice, p->s_in);
+            cudaMemcpyAsync((uint8_t *)p->d_l[s] + esz * k.llr0, hs[s] + esz * k.llr0, nb, cudaMemcpyHostToDevice,
+                            p->s_in);
         cudaEventRecord(p->ev_in[c], p->s_in);
         cudaStreamWaitEvent(st, p->ev_in[c], 0);
         rc = crn_launch_tasks(dev, t, P->d_desc, p->d_tasks + k.task0, k.n_tasks, p->d_pairs, p->d_l[0], p->d_l[1],
                               p->d_l[2], max_iters, et, p->d_bits, p->d_ok, h_it ? p->d_it : nullptr, nullptr,
-                              nullptr, 0, st, P->variant, nullptr, P->grid_cap);
+                              nullptr, 0, st, crn_plan_kernel_variant(P), nullptr, P->grid_cap);
         if (rc) return rc;
         cudaEventRecord(p->ev_comp[c], st);
         cudaStreamWaitEvent(p->s_out, p->ev_comp[c], 0);

@@ -166,3 +166,10 @@ def test_new_entry_points_validate_on_host():
     assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 8, tim) == crn.CRN_EINVAL   # unknown stream flag
     assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 5, tim) == crn.CRN_EINVAL   # merged + zero copy
     assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 5, 0, tim) == crn.CRN_EINVAL   # unknown stopping rule
+
+
+def test_llr_format_validation(L):
+    """crn_plan_set_llr_format (row f4 int8 ingest): only a NULL-plan check is
+    reachable without a GPU (plans need a device)."""
+    assert L.crn_plan_set_llr_format(None, 8, 3) == crn.CRN_EINVAL
+    assert L.crn_plan_llr_bytes(None) == crn.CRN_EINVAL

@@ -563,3 +563,42 @@ def test_tb_purge_of_waiting_cbs(orc):
                     assert purged.size > 0
             p.close()
     assert all(np.array_equal(v, verdicts[0]) for v in verdicts)
+
+
+@pytest.mark.parametrize("cfg,scale,shift,pad", [(1, 1.0, 4, 0), (5, 1.0, 5, 1), (3, 0.1, 3, 0), (2, 1.0, 8, 3)])
+def test_int8_llr_ingest_parity(orc, cfg, scale, shift, pad):
+    """Row f4 int8 ingest (crn_plan_set_llr_format, R31): int8 LLRs x
+    decode exactly as the int16 LLRs x * 2^shift -- the GPU int8 path against the
+    oracle on the widened int16 input, every output, through the device path and
+    the host-buffer pipeline; pad shifts every offset off 4-byte alignment."""
+    import dataclasses
+    b = _full(cfg, scale)
+    I, et = b.wl.max_iters, b.wl.early_term
+    q = [torch.clamp(torch.round(x.float() / (1 << shift)), -128, 127).to(torch.int8) for x in b.llr]
+    desc = b.desc.copy()
+    if pad:
+        desc["llr_off"] += pad
+        q = [torch.cat([torch.full((pad,), 77, dtype=torch.int8, device=x.device), x]) for x in q]
+    wide = tuple(x.to(torch.int16)[pad:] * (1 << shift) for x in q)
+    b16 = dataclasses.replace(b, llr=wide)
+    plan = crn.Plan(desc)
+    plan.set_llr_format(8, shift)
+    with pytest.raises(crn.CrnError):
+        plan.decode(*b.llr, I, et, *bmod.outputs(b, want_ext=False)[:3])      # int16 tensors refused
+    bits, ok, it, _ = bmod.outputs(b, want_ext=False)
+    plan.decode(*q, I, et, bits, ok, it)
+    torch.cuda.synchronize()
+    g = dict(words=bits.cpu().numpy().view(np.uint32), crc_ok=ok.cpu().numpy()[:b.n_cb],
+             iters=it.cpu().numpy()[:b.n_cb], ext=None)
+    idx = np.arange(b.n_cb)
+    r = run_oracle(b16, idx, I, et)
+    assert_parity(b16, g, r, idx)
+    hq = [x.cpu().pin_memory() for x in q]
+    hb = torch.zeros(bits.numel(), dtype=torch.int32).pin_memory()
+    hok = torch.zeros(ok.numel(), dtype=torch.uint8).pin_memory()
+    hit = torch.zeros(it.numel(), dtype=torch.uint8).pin_memory()
+    plan.decode_host(*hq, I, et, hb, hok, hit, n_chunks=3)
+    torch.cuda.synchronize()
+    assert np.array_equal(hb.numpy().view(np.uint32)[:b.n_words], g["words"][:b.n_words])
+    assert np.array_equal(hok.numpy()[:b.n_cb], g["crc_ok"])
+    assert np.array_equal(hit.numpy()[:b.n_cb], g["iters"])
