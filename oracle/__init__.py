@@ -53,6 +53,13 @@ def lib():
         L.oracle_siso.argtypes = [i32p, i32p, i32p, i32p, C.c_int, C.c_int, i32p, i32p, i32p, i32p,
                                   i32p, u64p]
         L.oracle_siso.restype = C.c_int64
+        L.oracle_siso_v.argtypes = [i32p, i32p, i32p, i32p, C.c_int, C.c_int, i32p, i32p, i32p, i32p,
+                                    i32p, u64p, C.c_int]
+        L.oracle_siso_v.restype = C.c_int64
+        L.oracle_max_star.argtypes = [C.c_int32, C.c_int32]
+        L.oracle_max_star.restype = C.c_int32
+        L.oracle_logmap_correction.argtypes = [C.c_int32]
+        L.oracle_logmap_correction.restype = C.c_int32
         L.oracle_nii_update.argtypes = [C.c_int, i32p, i32p, i32p, i32p]
         L.oracle_nii_update.restype = None
         L.oracle_decode_cb.argtypes = [i16p, i16p, i16p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -185,7 +192,7 @@ def turbo_encode(c) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
     return d[0], d[1], d[2]
 
 
-def siso(lsys, lpar, la, tail, W: int, alpha_in=None, beta_in=None):
+def siso(lsys, lpar, la, tail, W: int, alpha_in=None, beta_in=None, variant: int = 0):
     """One constituent half-iteration.  Returns (le, alpha_out, beta_out, ops, violations)."""
     lsys, lpar, la = (np.ascontiguousarray(x, np.int32) for x in (lsys, lpar, la))
     tail = np.ascontiguousarray(tail, np.int32)
@@ -196,9 +203,9 @@ def siso(lsys, lpar, la, tail, W: int, alpha_in=None, beta_in=None):
     ao, bo = np.zeros((M, 8), np.int32), np.zeros((M, 8), np.int32)
     le = np.zeros(K, np.int32)
     ops = C.c_uint64(0)
-    v = lib().oracle_siso(_p(lsys, C.c_int32), _p(lpar, C.c_int32), _p(la, C.c_int32),
-                          _p(tail, C.c_int32), K, W, _p(ai, C.c_int32), _p(bi, C.c_int32),
-                          _p(ao, C.c_int32), _p(bo, C.c_int32), _p(le, C.c_int32), C.byref(ops))
+    v = lib().oracle_siso_v(_p(lsys, C.c_int32), _p(lpar, C.c_int32), _p(la, C.c_int32),
+                            _p(tail, C.c_int32), K, W, _p(ai, C.c_int32), _p(bi, C.c_int32),
+                            _p(ao, C.c_int32), _p(bo, C.c_int32), _p(le, C.c_int32), C.byref(ops), variant)
     return le, ao, bo, ops.value, v
 
 
@@ -212,7 +219,16 @@ def nii_update(alpha_out, beta_out):
     return ai, bi
 
 
-VAR_MAXLOG, VAR_SCALED = 0, 1
+VAR_MAXLOG, VAR_SCALED, VAR_LOGMAP = 0, 1, 2
+
+
+def max_star(a: int, b: int) -> int:
+    """Log-MAP's max*(a, b) = max(a, b) + LUT correction (R32)."""
+    return int(lib().oracle_max_star(int(a), int(b)))
+
+
+def logmap_correction(d: int) -> int:
+    return int(lib().oracle_logmap_correction(int(d)))
 ET_NONE, ET_CRC, ET_MI = 0, 1, 2
 MI_EPS = 66
 

@@ -200,7 +200,7 @@ int oracle_turbo_encode(const uint8_t *c, int K, uint8_t *d0, uint8_t *d1, uint8
 }
 
 /* ---------------------------------------------------------------- arithmetic */
-typedef struct { uint64_t ops; int64_t viol; } ctx_t;
+typedef struct { uint64_t ops; int64_t viol; int logmap; } ctx_t;
 
 static int32_t chk(ctx_t *c, int32_t v) {
     if (v < -32768 || v > 32767) c->viol++;
@@ -209,6 +209,32 @@ static int32_t chk(ctx_t *c, int32_t v) {
 static int32_t ADD(ctx_t *c, int32_t a, int32_t b) { c->ops++; return chk(c, a + b); }
 static int32_t SUB(ctx_t *c, int32_t a, int32_t b) { c->ops++; return chk(c, a - b); }
 static int32_t MAX(ctx_t *c, int32_t a, int32_t b) { c->ops++; return a > b ? a : b; }
+
+/* Log-MAP (SURVEY.md §8(f) f2 "Log-MAP with a LUT correction", R32):
+ * the Jacobian logarithm max*(a, b) = ln(e^a + e^b) = max(a, b) + ln(1 + e^-|a-b|),
+ * in the channel quantiser's units (an LLR value v means v/8 nat, R9):
+ * max*(a, b) = max(a, b) + c(|a - b|) with c(d) = 8 ln(1 + e^(-d/8)) read from an
+ * 8-entry table over buckets of 4 units, entry b = round(c(4b + 1.5)) (the value
+ * at the bucket centre), bucket min(d >> 2, 7). */
+static int32_t logmap_lut(int b) {
+    return (int32_t)floor(8.0 * log(1.0 + exp(-(4.0 * b + 1.5) / 8.0)) + 0.5);
+}
+
+int32_t oracle_logmap_correction(int32_t d) {
+    if (d < 0) return -1;
+    return logmap_lut(d >> 2 < 7 ? d >> 2 : 7);
+}
+
+int32_t oracle_max_star(int32_t a, int32_t b) {
+    int32_t d = a > b ? a - b : b - a;
+    return (a > b ? a : b) + oracle_logmap_correction(d);
+}
+
+/* The SISO's two-way selection: max in max-log-MAP, max* in Log-MAP. */
+static int32_t SEL(ctx_t *c, int32_t a, int32_t b) {
+    c->ops++;
+    return c->logmap ? chk(c, oracle_max_star(a, b)) : (a > b ? a : b);
+}
 static int32_t CLAMP(ctx_t *c, int32_t v, int32_t lim) { /* a max and a min: 2 ops */
     c->ops += 2;
     return v < -lim ? -lim : (v > lim ? lim : v);
@@ -251,7 +277,7 @@ static void alpha_step(ctx_t *c, const int32_t a[NSTATE], int32_t an[NSTATE],
             int Sn = next_state(S, u), z = parity_out(S, u);
             int32_t cand = add_gamma(c, a[S], u, z, Lu, Lp, Lup);
             if (!have[Sn]) { best[Sn] = cand; have[Sn] = 1; }
-            else best[Sn] = MAX(c, best[Sn], cand);
+            else best[Sn] = SEL(c, best[Sn], cand);
         }
     normalise(c, best);
     memcpy(an, best, sizeof(best));
@@ -264,7 +290,7 @@ static void beta_step(ctx_t *c, const int32_t bn[NSTATE], int32_t b[NSTATE],
     for (int S = 0; S < NSTATE; S++) {
         int32_t c0 = add_gamma(c, bn[next_state(S, 0)], 0, parity_out(S, 0), Lu, Lp, Lup);
         int32_t c1 = add_gamma(c, bn[next_state(S, 1)], 1, parity_out(S, 1), Lu, Lp, Lup);
-        v[S] = MAX(c, c0, c1);
+        v[S] = SEL(c, c0, c1);
     }
     normalise(c, v);
     memcpy(b, v, sizeof(v));
@@ -279,7 +305,7 @@ static int32_t lambda_le(ctx_t *c, const int32_t a[NSTATE], const int32_t bn[NST
         for (int S = 0; S < NSTATE; S++) {
             int32_t t = ADD(c, a[S], bn[next_state(S, u)]);
             if (parity_out(S, u)) t = ADD(c, t, Lp);
-            lam[u] = first ? t : MAX(c, lam[u], t);
+            lam[u] = first ? t : SEL(c, lam[u], t);          /* fold over S = 0..7 in order */
             first = 0;
         }
     }
@@ -312,7 +338,16 @@ int64_t oracle_siso(const int32_t *lsys, const int32_t *lpar, const int32_t *la,
                     const int32_t *alpha_in, const int32_t *beta_in,
                     int32_t *alpha_out, int32_t *beta_out,
                     int32_t *le, uint64_t *ops) {
-    ctx_t c = {0, 0};
+    return oracle_siso_v(lsys, lpar, la, tail, K, W, alpha_in, beta_in, alpha_out, beta_out, le, ops,
+                         ORACLE_VAR_MAXLOG);
+}
+
+int64_t oracle_siso_v(const int32_t *lsys, const int32_t *lpar, const int32_t *la,
+                      const int32_t *tail, int K, int W,
+                      const int32_t *alpha_in, const int32_t *beta_in,
+                      int32_t *alpha_out, int32_t *beta_out,
+                      int32_t *le, uint64_t *ops, int variant) {
+    ctx_t c = {0, 0, variant == ORACLE_VAR_LOGMAP};
     int M = K / W;
     int32_t *beta = (int32_t *)malloc(sizeof(int32_t) * NSTATE * (size_t)(W + 1));
     int32_t *Lu = (int32_t *)malloc(sizeof(int32_t) * (size_t)K);
@@ -405,7 +440,7 @@ int64_t oracle_decode_cb_v(const int16_t *d0, const int16_t *d1, const int16_t *
                            uint8_t *bits, uint8_t *crc_ok, uint8_t *iters_used,
                            int16_t *ext, uint64_t *ops) {
     if (k_row(K) < 0 || F < 0 || F > K - 25 || max_iters < 1 || crc_kind < 0 || crc_kind > 2 ||
-        variant < 0 || variant > 1 || early_term < 0 || early_term > 2)
+        variant < 0 || variant > 2 || early_term < 0 || early_term > 2)
         return -1;
     int64_t viol = 0;
     int W = K / oracle_num_windows(K, wmin), M = K / W;
@@ -441,12 +476,13 @@ int64_t oracle_decode_cb_v(const int16_t *d0, const int16_t *d1, const int16_t *
     for (int it = 1; it <= max_iters; it++) {
         t_used = it;
         /* DEC1: R(b_i), R(b_i)' and the a-priori La1 -> extrinsic Le1 */
-        viol += oracle_siso(Ls, Lp1, La1, tail1, K, W, a_prev[0], b_prev[0], a_new[0], b_new[0], Le1, ops);
+        viol += oracle_siso_v(Ls, Lp1, La1, tail1, K, W, a_prev[0], b_prev[0], a_new[0], b_new[0], Le1, ops, variant);
         if (variant == ORACLE_VAR_SCALED)     /* extrinsic handed on = floor(3 Le / 4) (R28) */
             for (int k = 0; k < K; k++) Le1[k] = scale34(Le1[k]);
         /* DEC2: interleaved R(b_i), R(b_i)'' and La2 = interleaved Le1 */
         for (int i = 0; i < K; i++) La2[i] = Le1[Pi[i]];
-        viol += oracle_siso(Ls2, Lp2, La2, tail2, K, W, a_prev[1], b_prev[1], a_new[1], b_new[1], Le2, ops);
+        viol += oracle_siso_v(Ls2, Lp2, La2, tail2, K, W, a_prev[1], b_prev[1], a_new[1], b_new[1], Le2, ops,
+                              variant);
         if (variant == ORACLE_VAR_SCALED)
             for (int i = 0; i < K; i++) Le2[i] = scale34(Le2[i]);
         /* de-interleave back to DEC1 */

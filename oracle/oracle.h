@@ -32,7 +32,13 @@ enum { ORACLE_CRC_NONE = 0, ORACLE_CRC24A = 1, ORACLE_CRC24B = 2 };
 /* Decoder variants: plain max-log-MAP (the product definition, R2) and
  * the scaled-extrinsic max-log-MAP of SURVEY.md §8(f) f2 (R28): each
  * SISO's extrinsic Le = clamp(L1 - L0, +-4096) is handed on as floor(3 Le / 4). */
-enum { ORACLE_VAR_MAXLOG = 0, ORACLE_VAR_SCALED = 1 };
+/* and Log-MAP (f2, R32): every two-way selection of the recursions and
+ * of Lambda is max*(a, b) = max(a, b) + c(|a - b|) (oracle_max_star). */
+enum { ORACLE_VAR_MAXLOG = 0, ORACLE_VAR_SCALED = 1, ORACLE_VAR_LOGMAP = 2 };
+/* Log-MAP correction c(d) = LUT[min(d >> 2, 7)], LUT[b] = round(8 ln(1 + e^(-(4b+1.5)/8)));
+ * -1 for d < 0.  max*(a, b) = max(a, b) + c(|a - b|). */
+int32_t oracle_logmap_correction(int32_t d);
+int32_t oracle_max_star(int32_t a, int32_t b);
 /* Stopping rules (early_term): none (fixed iterations), CRC (R3), or
  * the paper's average-MI convergence (R29). */
 enum { ORACLE_ET_NONE = 0, ORACLE_ET_CRC = 1, ORACLE_ET_MI = 2 };
@@ -85,6 +91,14 @@ int64_t oracle_siso(const int32_t *lsys, const int32_t *lpar, const int32_t *la,
                     const int32_t *alpha_in, const int32_t *beta_in,
                     int32_t *alpha_out, int32_t *beta_out,
                     int32_t *le, uint64_t *ops);
+
+/* Same with a decoder variant (ORACLE_VAR_LOGMAP: max* selections; the others
+ * are plain max-log-MAP SISOs). */
+int64_t oracle_siso_v(const int32_t *lsys, const int32_t *lpar, const int32_t *la,
+                      const int32_t *tail, int K, int W,
+                      const int32_t *alpha_in, const int32_t *beta_in,
+                      int32_t *alpha_out, int32_t *beta_out,
+                      int32_t *le, uint64_t *ops, int variant);
 
 /* NII hand-over between iterations (R13): alpha_in[j] <- alpha_out[j-1]
  * (j >= 1), beta_in[j] <- beta_out[j+1] (j <= M-2); the unused rows are zeroed. */

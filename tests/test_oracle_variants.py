@@ -149,3 +149,88 @@ def test_mi_stop_is_prefix_of_fixed(orc):
         assert r["crc_ok"] == f["crc_ok"] and r["iters"] >= 2
         its.append(r["iters"])
     assert min(its) < 8                                       # it does stop early somewhere
+
+
+# ---------------------------------------------------------------- Log-MAP (R32)
+# max*(a, b) = max(a, b) + LUT[min(|a-b| >> 2, 7)], values in 1/8 nat.  Pinned against
+# the exact Jacobian logarithm 8 ln(e^(a/8) + e^(b/8)) -- not against the table --
+# and, at SISO level, against exact MAP (log-sum-exp over every path by brute force).
+LOGMAP_EPS = 0.82     # max |LUT bucket value - 8 ln(1 + e^(-d/8))| over d >= 0 (bucket 0 at d = 3)
+
+
+def test_max_star_is_jacobian_log_within_table_error(orc):
+    a = np.arange(-200, 201, 3)
+    for x in a:
+        for y in (-211, -40, -9, -3, 0, 1, 2, 5, 13, 31, 32, 77, 200):
+            m = orc.max_star(int(x), int(y))
+            exact = 8 * np.logaddexp(x / 8, y / 8)
+            assert abs(m - exact) <= LOGMAP_EPS, (x, y, m, exact)
+            assert m == orc.max_star(int(y), int(x))                       # symmetric
+            assert orc.max_star(int(x) + 17, int(y) + 17) == m + 17       # shift-invariant
+            assert m >= max(x, y)
+    # far apart the correction vanishes: max* = max (the max-log-MAP limit)
+    assert all(orc.max_star(d, 0) == d for d in range(32, 400, 7))
+    assert orc.logmap_correction(0) == 5 and orc.logmap_correction(-1) == -1
+
+
+def _exact_map_le(lsys, lpar, la, tail):
+    """Exact APP extrinsics (float64) of one terminated constituent by enumerating paths."""
+    from tests.test_oracle_encoder_siso import rsc_paths
+    n = lsys.size
+    U, Z, TX, TZ, S = rsc_paths(n)
+    Lu = lsys + la
+    tot = (U * Lu + Z * lpar).sum(1) + TX @ tail[0::2] + TZ @ tail[1::2]
+    lse = lambda v: np.logaddexp.reduce(v / 8.0) * 8.0
+    return np.array([lse(tot[U[:, k] == 1]) - lse(tot[U[:, k] == 0]) - Lu[k] for k in range(n)])
+
+
+@pytest.mark.parametrize("n", [8, 11, 13])
+def test_logmap_siso_is_exact_map_within_bound(orc, n):
+    """Every Le of the Log-MAP SISO is within the accumulated table error of exact
+    MAP (alpha chain + beta chain + the 7-term Lambda fold, both Lambdas), and on
+    average far closer to it than max-log-MAP is (a missing or wrong-signed
+    correction fails this)."""
+    rng = np.random.default_rng(7 + n)
+    bound = 2 * (n + 7) * LOGMAP_EPS + 1
+    err_log, err_max = [], []
+    for _ in range(12):
+        lsys, lpar, la = (rng.integers(-40, 41, n) for _ in range(3))
+        tail = rng.integers(-40, 41, 6)
+        ex = _exact_map_le(lsys, lpar, la, tail)
+        le_l, _, _, _, v = orc.siso(lsys, lpar, la, tail, n, variant=orc.VAR_LOGMAP)
+        le_m = orc.siso(lsys, lpar, la, tail, n)[0]
+        assert v == 0
+        assert np.all(np.abs(le_l - ex) <= bound), np.abs(le_l - ex).max()
+        err_log.append(np.abs(le_l - ex).mean())
+        err_max.append(np.abs(le_m - ex).mean())
+    assert np.mean(err_log) < 0.4 * np.mean(err_max), (np.mean(err_log), np.mean(err_max))
+
+
+def test_logmap_zero_evidence_and_noiseless(orc):
+    """No evidence: Le = 0 everywhere by symmetry of max*; noiseless (+-800 LLRs):
+    every selection is decided by >= 32 units, so Log-MAP = max-log-MAP."""
+    for n in (9, 12):
+        z = np.zeros(n, np.int64)
+        assert np.all(orc.siso(z, z, z, np.zeros(6, np.int64), n, variant=orc.VAR_LOGMAP)[0] == 0)
+    c = np.random.default_rng(3).integers(0, 2, 40).astype(np.uint8)
+    d = [800 * (2 * x.astype(np.int16) - 1) for x in orc.turbo_encode(c)]
+    a = orc.decode_cb(*d, F=0, crc_kind=0, max_iters=3, variant=orc.VAR_LOGMAP)
+    b = orc.decode_cb(*d, F=0, crc_kind=0, max_iters=3)
+    assert np.array_equal(a["bits"], c) and np.array_equal(a["ext"], b["ext"])
+
+
+def test_logmap_lowers_bler_and_iterations(orc):
+    """Same seeded CBs as the scaled-variant pin: Log-MAP decodes at least as many
+    and stops earlier on average than max-log-MAP (its known gain)."""
+    wl = wlmod.make_workload(1, seed=5, scale=4.0)
+    wl.tb_ebn0_db[:] = 0.9
+    cbs, ll = oracle_llrs(wl)
+    K = np.array([c["K"] for c in cbs], np.int32)
+    lo, bo = offsets(K)
+    res = []
+    for v in (orc.VAR_MAXLOG, orc.VAR_LOGMAP):
+        r = orc.decode_batch(K, np.zeros_like(K), np.full_like(K, 2), lo, bo, *(x.numpy() for x in ll),
+                             max_iters=8, early_term=True, nthreads=4, variant=v, want_ext=False)
+        assert r["violations"] == 0
+        res.append((1 - r["crc_ok"].mean(), r["iters"].mean()))
+    assert res[1][0] < res[0][0] and res[1][1] < res[0][1], res
