@@ -228,6 +228,33 @@ def run_pool(args, seed=0):
         e2e.append(1e3 * (time.perf_counter() - t0))
     its = it[:b.n_cb].cpu().numpy()
     d_ms = statistics.median(dec)
+    tb_loss = float(1.0 - tb_ok.float().mean().item())
+    cb_fail = float(1.0 - ok[:b.n_cb].float().mean().item())
+    # row f2: the decoder variants / stopping rules on the same TTI (SURVEY.md §8(f) 2:
+    # "score on BLER and mean iterations"): device time, TB loss, CB failures, iterations
+    variants = {}
+    for name, var, et in (("maxlog_crc", crn.VARIANT_MAXLOG, crn.ET_CRC), ("maxlog_mi", crn.VARIANT_MAXLOG, crn.ET_MI),
+                          ("scaled_crc", crn.VARIANT_SCALED, crn.ET_CRC), ("logmap_crc", crn.VARIANT_LOGMAP, crn.ET_CRC)):
+        pv = crn.Plan(b.desc)
+        pv.set_variant(var)
+        for _ in range(2):
+            pv.decode(*b.llr, 8, et, bits, ok, it, stream=st)
+        torch.cuda.synchronize()
+        tv = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            pv.decode(*b.llr, 8, et, bits, ok, it, stream=st)
+            e1.record(st)
+            torch.cuda.synchronize()
+            tv.append(e0.elapsed_time(e1))
+        crn.tb_verdict_batch(tbs, b.desc, bits, ok, tb_ok, None, stream=st)
+        torch.cuda.synchronize()
+        variants[name] = {"decode_ms": statistics.median(tv),
+                          "tb_loss_rate": float(1.0 - tb_ok.float().mean().item()),
+                          "cb_crc_fail_rate": float(1.0 - ok[:b.n_cb].float().mean().item()),
+                          "mean_iters": float(it[:b.n_cb].float().mean().item())}
+        pv.close()
     return {"workload": "cfg3: 100 cells x 10 UEs, TBS ~ U{1000..75376}, 36.212 segmentation, QPSK Eb/N0 ~ "
                         "U[0.5,3] dB per UE, CRC ET max 8 iterations, one TTI",
             "n_tb": int(b.wl.n_tb), "n_cb": b.n_cb, "sum_K": int(b.K.sum()), "info_bits": b.info_bits(),
@@ -235,9 +262,9 @@ def run_pool(args, seed=0):
             "decoded_mbps": b.info_bits() / (d_ms * 1e-3) / 1e6,
             "e2e_ms": statistics.median(e2e), "e2e_path": "pinned host LLRs -> crn_plan_decode_host -> bits + crc_ok "
                                                           "in pinned host memory (host clock, stream synced)",
-            "tb_loss_rate": float(1.0 - tb_ok.float().mean().item()),
-            "cb_crc_fail_rate": float(1.0 - ok[:b.n_cb].float().mean().item()),
+            "tb_loss_rate": tb_loss, "cb_crc_fail_rate": cb_fail,
             "mean_iters": float(its.mean()),
+            "variants": variants,
             "iters_hist": [int(x) for x in np.bincount(its, minlength=9)[1:9]],
             "gen_s": round(t_gen, 1)}
 

@@ -41,8 +41,14 @@ enum { CRN_PURGE = 4 };                    /* flag bit 2: purge waiting CBs of f
 /* Decoder variants: CRN_VARIANT_MAXLOG is the definition
  * every entry point computes by default (R2); CRN_VARIANT_SCALED
  * hands on floor(3 Le / 4) instead of each SISO's extrinsic Le, so the
- * a-priori inputs, L_APP and ext_out all use the scaled value (R28). */
-enum { CRN_VARIANT_MAXLOG = 0, CRN_VARIANT_SCALED = 1 };
+ * a-priori inputs, L_APP and ext_out all use the scaled value (R28);
+ * CRN_VARIANT_LOGMAP replaces every two-way selection of the alpha / beta
+ * recursions and of the Lambda fold (over the 8 transitions in state order) by
+ * max*(a, b) = max(a, b) + LUT[min(|a - b| >> 2, 7)], LUT[b] = round(8 ln(1 +
+ * e^(-(4b + 1.5)/8))): Log-MAP with the Jacobian correction in the LLR
+ * quantiser's 1/8-nat units (R32; normalisation, clamps and NII as
+ * in max-log-MAP).  Selected per plan (crn_plan_set_variant). */
+enum { CRN_VARIANT_MAXLOG = 0, CRN_VARIANT_SCALED = 1, CRN_VARIANT_LOGMAP = 2 };
 enum { CRN_MAX_ITERS = 32, CRN_KMIN = 40, CRN_KMAX = 6144 };
 /* Stopping rules (the early_term argument of every decode entry point):
  * CRN_ET_NONE runs max_iters iterations; CRN_ET_CRC stops a CB after the first
@@ -125,7 +131,8 @@ int crn_plan_decode(void *plan, const int16_t *llr_sys, const int16_t *llr_p1,
                     uint32_t *out_bits, uint8_t *crc_ok, uint8_t *iters_used, int16_t *ext_out,
                     void *cuda_stream);
 /* Decoder variant of later crn_plan_decode / crn_plan_decode_host calls of this
- * plan (CRN_VARIANT_*; default CRN_VARIANT_MAXLOG).  CRN_EINVAL otherwise. */
+ * plan (CRN_VARIANT_MAXLOG / _SCALED / _LOGMAP; default CRN_VARIANT_MAXLOG).
+ * CRN_EINVAL otherwise. */
 int crn_plan_set_variant(void *plan, int32_t variant);
 /* TB purge ("In case of decoding failure, the
  * scheduler purges all CCDUs belonging to the same UE (TB)" -- Algorithm 2
@@ -152,6 +159,8 @@ int crn_plan_set_grid(void *plan, int32_t max_ctas);
 int crn_plan_set_llr_format(void *plan, int32_t bits, int32_t shift);
 /* Bytes per LLR element of the plan's current format (2 or 1). */
 int crn_plan_llr_bytes(void *plan);
+/* The Log-MAP correction table of CRN_VARIANT_LOGMAP: out[0..7] = LUT[b]. */
+int crn_logmap_lut(int32_t *out);
 /* Number of decode-kernel launches one crn_plan_decode performs (for gpu_launches). */
 int crn_plan_launches(void *plan);
 void crn_plan_destroy(void *plan);

@@ -21,7 +21,7 @@ CRC_NONE, CRC24A, CRC24B = 0, 1, 2
 DESC_ON_DEVICE = 1
 EXT_SCALED = 2
 PURGE = 4
-VARIANT_MAXLOG, VARIANT_SCALED = 0, 1
+VARIANT_MAXLOG, VARIANT_SCALED, VARIANT_LOGMAP = 0, 1, 2
 ET_NONE, ET_CRC, ET_MI = 0, 1, 2
 
 DESC_DTYPE = np.dtype([("K", "<i4"), ("F", "<i4"), ("crc_kind", "<i4"), ("reserved", "<i4"),
@@ -87,6 +87,7 @@ _SIGS = {
     "crn_last_error": (C.c_char_p, []),
     "crn_device_info": (C.c_int, [i32p, i32p, i32p, i32p]),
     "crn_mi_table": (C.c_int, [i32p]),
+    "crn_logmap_lut": (C.c_int, [i32p]),
     "crn_decode_kernel_info": (C.c_int, [i32p, i32p, i32p, i32p]),
     "crn_ubench_int16x2": (C.c_int, [C.c_int32, i64p, P(C.c_float), i64p]),
 }
@@ -370,6 +371,13 @@ def crc24b(bits) -> int:
 
 def strerror(code: int) -> str:
     return lib().crn_strerror(code).decode()
+
+
+def logmap_lut() -> np.ndarray:
+    """crn_logmap_lut: the Log-MAP correction table LUT[0..7] (R32)."""
+    out = np.zeros(8, np.int32)
+    _chk(lib().crn_logmap_lut(_np(out, C.c_int32)), "crn_logmap_lut")
+    return out
 
 
 def mi_table() -> np.ndarray:

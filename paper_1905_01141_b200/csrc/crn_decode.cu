@@ -116,6 +116,22 @@ __host__ __device__ constexpr int par(int S, int u) { return (u ^ (S >> 1) ^ (S 
 __device__ __forceinline__ u32 vadd(u32 a, u32 b) { return __vadd2(a, b); }
 __device__ __forceinline__ u32 vaddmax(u32 a, u32 b, u32 c) { return __viaddmax_s16x2(a, b, c); } /* max(a+b, c) */
 
+/* Log-MAP's max*(a, b) = max(a, b) + LUT[min(|a - b| >> 2, 7)] per int16 half
+ * (R32).  |a - b| <= 24576 on every selection (int16 safety), so the
+ * difference is exact; the bucket index of each half goes into a PRMT selector
+ * that picks the LUT byte (bytes 1 and 3 pick LUT[6] = 0), giving the
+ * int16x2 correction in one instruction. */
+__device__ __forceinline__ u32 maxs2(u32 a, u32 b, u32 lut_lo, u32 lut_hi) {
+    const u32 m = __vmaxs2(a, b), d = __vsub2(m, __vmins2(a, b));
+    const u32 q = __vmins2((d >> 2) & 0x3FFF3FFFu, 0x00070007u);
+    return __vadd2(m, __byte_perm(lut_lo, lut_hi, q | (q >> 8) | 0x6060u));
+}
+
+struct Lut {                                    /* the LUT's two PRMT source words */
+    u32 lo, hi;
+};
+__constant__ u32 c_logmap[2];                   /* crn_decode_set_logmap */
+
 /* gamma(u, z) = u*Lu + z*Lp; the (0,0) branch is never formed */
 __device__ __forceinline__ u32 gsel(int u, int z, u32 Lu, u32 Lp, u32 Lup) { return u ? (z ? Lup : Lu) : Lp; }
 
@@ -181,41 +197,61 @@ __device__ __forceinline__ void norm_ab(const u32 v[NS], u32 Lp, u32 out[NS]) {
     for (int s = 0; s < NS; s++) out[s] = vaddmax(v[s], (ALPHA ? a_isB(s) : b_isB(s)) ? lpm : nm, FLOORB);
 }
 
-/* alpha_{k+1} = N(max over predecessors of alpha_k + gamma_k)  (row a6) */
-__device__ __forceinline__ void alpha_step_d(u32 a[NS], u32 Lp, u32 Lup, u32 D) {
+/* alpha_{k+1} = N(max over predecessors of alpha_k + gamma_k)  (row a6); with
+ * LOG the selection is max* (shift-invariant, so the type-B "+ Lp" still folds
+ * into the normaliser exactly) */
+template <bool LOG = false>
+__device__ __forceinline__ void alpha_step_d(u32 a[NS], u32 Lp, u32 Lup, u32 D, Lut lut = Lut{0, 0}) {
     u32 v[NS];
 #pragma unroll
     for (int Sp = 0; Sp < NS; Sp++) {
         const int x = a_base(Sp), y = x ^ 1;    /* y carries (1,1) [A] or (1,0) [B] */
-        v[Sp] = vaddmax(a[y], a_isB(Sp) ? D : Lup, a[x]);
+        v[Sp] = LOG ? maxs2(a[x], vadd(a[y], a_isB(Sp) ? D : Lup), lut.lo, lut.hi)
+                    : vaddmax(a[y], a_isB(Sp) ? D : Lup, a[x]);
     }
     norm_ab<true>(v, Lp, a);
 }
 
 /* beta_k = N(max over successors of beta_{k+1} + gamma_k)  (row a5) */
-__device__ __forceinline__ void beta_step_d(u32 b[NS], u32 Lp, u32 Lup, u32 D) {
+template <bool LOG = false>
+__device__ __forceinline__ void beta_step_d(u32 b[NS], u32 Lp, u32 Lup, u32 D, Lut lut = Lut{0, 0}) {
     u32 v[NS];
 #pragma unroll
-    for (int S = 0; S < NS; S++) v[S] = vaddmax(b[nxt(S, 1)], b_isB(S) ? D : Lup, b[nxt(S, 0)]);
+    for (int S = 0; S < NS; S++)
+        v[S] = LOG ? maxs2(b[nxt(S, 0)], vadd(b[nxt(S, 1)], b_isB(S) ? D : Lup), lut.lo, lut.hi)
+                   : vaddmax(b[nxt(S, 1)], b_isB(S) ? D : Lup, b[nxt(S, 0)]);
     norm_ab<false>(v, Lp, b);
 }
 
 /* Row a7: Lambda_u = max over the 8 transitions with input u of alpha_k(S) +
  * z Lp + beta_{k+1}(S'), grouped by z; Le = clamp(L1 - L0, +-4096) computed as
  * min(max(L1 + ~L0, -4097) + 1, 4096).  The -1 biases of alpha and beta cancel. */
-__device__ __forceinline__ u32 lambda_le(const u32 a[NS], const u32 bn[NS], u32 Lp) {
+template <bool LOG = false>
+__device__ __forceinline__ u32 lambda_le(const u32 a[NS], const u32 bn[NS], u32 Lp, Lut lut = Lut{0, 0}) {
     u32 lam[2];
+    if constexpr (LOG) {                        /* max* folded over S = 0..7 in order (R32) */
 #pragma unroll
-    for (int u = 0; u < 2; u++) {
-        u32 m[2] = {0, 0};
-        bool first[2] = {true, true};
+        for (int u = 0; u < 2; u++) {
 #pragma unroll
-        for (int S = 0; S < NS; S++) {
-            const int z = par(S, u), Sn = nxt(S, u);
-            m[z] = first[z] ? vadd(a[S], bn[Sn]) : vaddmax(a[S], bn[Sn], m[z]);
-            first[z] = false;
+            for (int S = 0; S < NS; S++) {
+                u32 t = vadd(a[S], bn[nxt(S, u)]);
+                if (par(S, u)) t = vadd(t, Lp);
+                lam[u] = S ? maxs2(lam[u], t, lut.lo, lut.hi) : t;
+            }
         }
-        lam[u] = vaddmax(m[1], Lp, m[0]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            u32 m[2] = {0, 0};
+            bool first[2] = {true, true};
+#pragma unroll
+            for (int S = 0; S < NS; S++) {
+                const int z = par(S, u), Sn = nxt(S, u);
+                m[z] = first[z] ? vadd(a[S], bn[Sn]) : vaddmax(a[S], bn[Sn], m[z]);
+                first[z] = false;
+            }
+            lam[u] = vaddmax(m[1], Lp, m[0]);
+        }
     }
     return __viaddmin_s16x2(vaddmax(lam[1], ~lam[0], NEG4097), ONE2, CLIP_HI);
 }
@@ -230,8 +266,8 @@ __device__ __forceinline__ u32 scale34(u32 x) {
     return ((t >> 2) & 0x3FFF3FFFu) | s | (s >> 1);
 }
 
-template <bool SCALE>
-__device__ __forceinline__ u32 ext_out_map(u32 le) { return SCALE ? scale34(le) : le; }
+template <int VAR>
+__device__ __forceinline__ u32 ext_out_map(u32 le) { return VAR == CRN_VARIANT_SCALED ? scale34(le) : le; }
 
 /* beta_K from the tail: beta_{K+3} = (0, -F x7), three forced steps (R11) */
 __device__ __forceinline__ void tail_beta(const u32 *tail, u32 b[NS]) {
@@ -352,6 +388,7 @@ struct SCtx {
     u32 ta;         /* this thread's TMEM metric slots: lane quadrant + 128-column block */
     u32 ts;         /* this thread's TMEM statics: Ls-Lp1 (16 columns), Ls[Pi]-Lp2 (16) */
     int tid, t, p, j, M, pM, k0;
+    u32 lut_lo, lut_hi;     /* Log-MAP LUT words (tab.lm_lo / lm_hi) */
 };
 
 __device__ __forceinline__ void tm_store8(u32 ta, const u32 v[NS]) {
@@ -460,9 +497,11 @@ __device__ __forceinline__ u32 lds_q(u32 qq, int c) {
 
 /* One half-iteration of constituent c (rows a5-a8).  Le -> Y (c = 0, natural
  * order) or Z (c = 1, interleaved order). */
-template <bool SCALE>
+template <int VAR>
 __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, int it, const u32 (&qq)[HW],
                                            bool zero_la) {
+    constexpr bool LOGV = VAR == CRN_VARIANT_LOGMAP;
+    const Lut lut{f.lut_lo, f.lut_hi};
     uint2 *ch = reinterpret_cast<uint2 *>(f.sm + S_CH) + f.tid;
     const u32 *lp = f.sm + S_LP + c * SUMK + f.k0 * TS + f.t;
     /* row a4 fused into phase 1: this thread's 16 (Lu+Lp, Lu-Lp) pairs are formed
@@ -506,7 +545,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
             const u32 x = vadd(vadd(d, pv[s]), pv[s]);       /* Lu + Lp */
             ch[s * BLOCK] = make_uint2(x, d);
             tm_store8(f.ta + s * 8, m);
-            alpha_step_d(m, pv[s], x, d);
+            alpha_step_d<LOGV>(m, pv[s], x, d, lut);
         }
 #pragma unroll
         for (int s = 0; s < NS; s++) X[s * TS + f.t] = m[s];             /* alpha_16 -> tail thread */
@@ -531,7 +570,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
             const u32 x = vadd(vadd(d, pv[s]), pv[s]);
             ch[s * BLOCK] = make_uint2(x, d);
             tm_store8(f.ta + s * 8, m);
-            beta_step_d(m, pv[s], x, d);
+            beta_step_d<LOGV>(m, pv[s], x, d, lut);
         }
 #pragma unroll
         for (int s = 0; s < NS; s++) X[(NS + s) * TS + f.t] = m[s];      /* beta_16 -> head thread */
@@ -557,8 +596,8 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
                 const u32 p = lp[ss * TS];
                 tm_wait_ld8(cur);
                 tm_load8(f.ta + (ss > 0 ? ss - 1 : 0) * 8, nx);      /* unconditional: no branch around the load */
-                le[ss * TS] = ext_out_map<SCALE>(lambda_le(cur, b, p));   /* alpha_ss (stored) + beta_{ss+1} */
-                beta_step_d(b, p, g.x, g.y);
+                le[ss * TS] = ext_out_map<VAR>(lambda_le<LOGV>(cur, b, p, lut));   /* alpha_ss (stored) + beta_{ss+1} */
+                beta_step_d<LOGV>(b, p, g.x, g.y, lut);
             }
         }
 #pragma unroll
@@ -578,8 +617,8 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
                 const u32 p = lp[ss * TS];
                 tm_wait_ld8(cur);
                 tm_load8(f.ta + (ss < HW - 1 ? ss + 1 : ss) * 8, nx);
-                le[(HW + ss) * TS] = ext_out_map<SCALE>(lambda_le(a, cur, p));   /* alpha_{16+ss} + beta_{17+ss} (stored) */
-                alpha_step_d(a, p, g.x, g.y);
+                le[(HW + ss) * TS] = ext_out_map<VAR>(lambda_le<LOGV>(a, cur, p, lut));   /* alpha_{16+ss} + beta_{17+ss} (stored) */
+                alpha_step_d<LOGV>(a, p, g.x, g.y, lut);
             }
         }
 #pragma unroll
@@ -587,7 +626,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
     }
 }
 
-template <bool SCALE, bool PURGE, bool LLR8>
+template <int VAR, bool PURGE, bool LLR8>
 __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
                                               const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
                                               const int16_t *__restrict__ l2, int max_iters, int et,
@@ -611,6 +650,10 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
     f.j = active ? f.t - f.p * M : 0;
     f.pM = f.p * M;
     f.k0 = tail_thr ? HW : 0;
+    if (VAR == CRN_VARIANT_LOGMAP) {
+        f.lut_lo = c_logmap[0];
+        f.lut_hi = c_logmap[1];
+    }
     const u32 *qts = tab.qpp_ts + tab.qpp_off[tk.kidx];     /* natural position of Pi(jW+i)  */
     const u32 *qinv = tab.qinv_ts + tab.qpp_off[tk.kidx];   /* interleaved position of jW+i */
     const u32 *cbit = tab.crc_bit + tab.crcb_off[tk.kidx] + f.j;        /* + kind*K + i*M */
@@ -722,13 +765,13 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
     for (int it = 1; it <= max_iters; it++) {
         /* DEC1: La1[n] = Le2[Pi^-1(n)] gathered from Z (zero in iteration 1) */
         prof_mark(P_CHUNK);
-        siso_split<SCALE>(f, tail_thr, 0, it, qq, it == 1);
+        siso_split<VAR>(f, tail_thr, 0, it, qq, it == 1);
         prof_mark(P_PH2);
         __syncthreads();
         prof_mark(P_BAR2);
         /* DEC2: La2[i] = Le1[Pi(i)] gathered from Y */
         prof_mark(P_CHUNK);
-        siso_split<SCALE>(f, tail_thr, 1, it, qq, false);
+        siso_split<VAR>(f, tail_thr, 1, it, qq, false);
         prof_mark(P_PH2);
         __syncthreads();
         prof_mark(P_BAR2);
@@ -828,6 +871,7 @@ struct GSplit {
     int tid2;                  /* position in the per-thread arrays: tid for head, Tp + t for tail */
     int t, p, j, pM, k0, hw;   /* window, pair, window in CB, steps owned */
     u32 ta, ts;                /* TMEM: 8*hw_h stored-metric columns, then 2*hw_h static columns */
+    u32 lut_lo, lut_hi;        /* Log-MAP LUT words */
 };
 
 __device__ __forceinline__ void tm_store1(u32 ta, u32 v) {
@@ -841,8 +885,10 @@ __device__ __forceinline__ u32 tm_load1_wait(u32 ta) {
 }
 
 /* One half-iteration of constituent c on the split-window path (rows a4-a8). */
-template <bool SCALE>
+template <int VAR>
 __device__ __forceinline__ void siso_gsplit(const GSplit &g, bool tail_thr, int c, int it) {
+    constexpr bool LOGV = VAR == CRN_VARIANT_LOGMAP;
+    const Lut lut{g.lut_lo, g.lut_hi};
     const int Tp = g.Tp, W = g.W, hw = g.hw, t = g.t, st2 = 2 * Tp;
     const u32 *lp = g.LP + c * W * Tp + g.k0 * Tp + t;           /* this thread's steps, stride Tp */
     const u32 *Qc = g.Q + c * g.hw_h * st2 + g.tid2;              /* QPP word indices (stride 2Tp) */
@@ -873,7 +919,7 @@ __device__ __forceinline__ void siso_gsplit(const GSplit &g, bool tail_thr, int 
             const u32 d = vadd(sn, av), x = vadd(vadd(d, pv), pv);
             ch[s * st2] = make_uint2(x, d);
             tm_store8(g.ta + s * 8, m);
-            alpha_step_d(m, pv, x, d);
+            alpha_step_d<LOGV>(m, pv, x, d, lut);
         }
 #pragma unroll
         for (int s = 0; s < NS; s++) g.X[s * Tp + t] = m[s];                 /* alpha_hw -> tail thread */
@@ -896,7 +942,7 @@ __device__ __forceinline__ void siso_gsplit(const GSplit &g, bool tail_thr, int 
             const u32 d = vadd(sn, av), x = vadd(vadd(d, pv), pv);
             ch[s * st2] = make_uint2(x, d);
             tm_store8(g.ta + s * 8, m);
-            beta_step_d(m, pv, x, d);
+            beta_step_d<LOGV>(m, pv, x, d, lut);
         }
 #pragma unroll
         for (int s = 0; s < NS; s++) g.X[(NS + s) * Tp + t] = m[s];          /* beta_hw_h -> head thread */
@@ -918,8 +964,8 @@ __device__ __forceinline__ void siso_gsplit(const GSplit &g, bool tail_thr, int 
 #pragma unroll
             for (int k = 0; k < NS; k++) cur[k] = nx[k];
             tm_load8(g.ta + (s > 0 ? s - 1 : 0) * 8, nx);
-            le[s * Tp] = ext_out_map<SCALE>(lambda_le(cur, b, pv));
-            beta_step_d(b, pv, gg.x, gg.y);
+            le[s * Tp] = ext_out_map<VAR>(lambda_le<LOGV>(cur, b, pv, lut));
+            beta_step_d<LOGV>(b, pv, gg.x, gg.y, lut);
         }
         tm_wait_ld8(nx);
 #pragma unroll
@@ -937,8 +983,8 @@ __device__ __forceinline__ void siso_gsplit(const GSplit &g, bool tail_thr, int 
 #pragma unroll
             for (int k = 0; k < NS; k++) cur[k] = nx[k];
             tm_load8(g.ta + (s + 1 < hw ? s + 1 : s) * 8, nx);
-            le[s * Tp] = ext_out_map<SCALE>(lambda_le(a, cur, pv));
-            alpha_step_d(a, pv, gg.x, gg.y);
+            le[s * Tp] = ext_out_map<VAR>(lambda_le<LOGV>(a, cur, pv, lut));
+            alpha_step_d<LOGV>(a, pv, gg.x, gg.y, lut);
         }
         tm_wait_ld8(nx);
 #pragma unroll
@@ -946,7 +992,7 @@ __device__ __forceinline__ void siso_gsplit(const GSplit &g, bool tail_thr, int 
     }
 }
 
-template <bool SCALE, bool PURGE, bool LLR8>
+template <int VAR, bool PURGE, bool LLR8>
 __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
                                             const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
                                             const int16_t *__restrict__ l2, int max_iters, int et,
@@ -980,6 +1026,10 @@ __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_des
     g.pM = g.p * M;
     g.k0 = tail_thr ? g.hw_h : 0;
     g.hw = tail_thr ? W - g.hw_h : g.hw_h;
+    if (VAR == CRN_VARIANT_LOGMAP) {
+        g.lut_lo = c_logmap[0];
+        g.lut_hi = c_logmap[1];
+    }
     g.ta = tmem + ((u32)((warp & 3) * 32) << 16) + (u32)((warp >> 2) * 10 * g.hw_h);
     g.ts = g.ta + 8 * g.hw_h;
     const u32 *qw = tab.qpp_wm + tab.qpp_off[tk.kidx];      /* (row << 16) | col of Pi(jW+i) */
@@ -1045,10 +1095,10 @@ __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_des
 
     const int nw = (K + 31) >> 5;
     for (int it = 1; it <= max_iters; it++) {
-        if (working) siso_gsplit<SCALE>(g, tail_thr, 0, it);
+        if (working) siso_gsplit<VAR>(g, tail_thr, 0, it);
         else __syncthreads();                   /* the hand-over barrier inside siso_gsplit */
         __syncthreads();
-        if (working) siso_gsplit<SCALE>(g, tail_thr, 1, it);
+        if (working) siso_gsplit<VAR>(g, tail_thr, 1, it);
         else __syncthreads();
         __syncthreads();
         if (!et && it != max_iters) continue;
@@ -1164,9 +1214,10 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
     }
 }
 
-/* PURGE: the TB-purge instantiation (crn_plan_set_purge); the default one has no
- * purge code at all, so the hot loops are compiled exactly as without it. */
-template <bool PURGE, bool LLR8>
+/* One instantiation per (purge?, int8 LLRs?, Log-MAP?): the default
+ * <false, false, MAXLOG> (which also runs CRN_VARIANT_SCALED, chosen per launch)
+ * has no purge, int8 or Log-MAP code at all. */
+template <bool PURGE, bool LLR8, int VAR>
 __global__ void __launch_bounds__(BLOCK, 1)
 decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__ tasks, int n_tasks,
               const crn_pair *__restrict__ pairs, const int16_t *__restrict__ l0,
@@ -1175,7 +1226,6 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
               int16_t *__restrict__ ext_out, crn_tables tab, uint8_t *ws, int variant, uint8_t *tb_dead_arg) {
     uint8_t *const tb_dead = PURGE ? tb_dead_arg : nullptr;
     const int sh8 = (variant >> 8) - 1;         /* LLR format: -1 int16, else int8 << sh8 (LLR8) */
-    variant &= 0xFF;
     extern __shared__ __align__(16) u32 smem[];
     __shared__ int s_ntask, s_left;
     __shared__ crn_task s_ntk;
@@ -1244,21 +1294,20 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             if (s_left == 0) continue;
         }
         prof_mark(P_FETCH);
-        if (tk.W == 32) {
-            if (variant == CRN_VARIANT_SCALED)
-                run_task_fast<true, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab, smem,
-                                    tmem, sh, pg, sh8);
-            else
-                run_task_fast<false, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
-                                     smem, tmem, sh, pg, sh8);
-        } else {
-            if (variant == CRN_VARIANT_SCALED)
-                run_task_split<true, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
-                                     smem, tmem, sh, pg, sh8);
-            else
-                run_task_split<false, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, ext_out, tab,
-                                      smem, tmem, sh, pg, sh8);
-        }
+        /* VAR = LOGMAP: its own kernels; otherwise MAXLOG / SCALED chosen per launch */
+#define CRN_RUN(V)                                                                                                \
+        do {                                                                                                      \
+            if (tk.W == 32)                                                                                       \
+                run_task_fast<V, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used,  \
+                                              ext_out, tab, smem, tmem, sh, pg, sh8);                             \
+            else                                                                                                  \
+                run_task_split<V, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, \
+                                               ext_out, tab, smem, tmem, sh, pg, sh8);                            \
+        } while (0)
+        if constexpr (VAR == CRN_VARIANT_LOGMAP) CRN_RUN(CRN_VARIANT_LOGMAP);
+        else if ((variant & 0xFF) == CRN_VARIANT_SCALED) CRN_RUN(CRN_VARIANT_SCALED);
+        else CRN_RUN(CRN_VARIANT_MAXLOG);
+#undef CRN_RUN
     }
     prof_flush();
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -1270,15 +1319,24 @@ size_t smem_bytes() { return (size_t)SMEM_WORDS * 4; }
 
 }  // namespace
 
-extern "C" size_t crn_decode_ws_bytes(int32_t) { return WS_HEAD; }   /* the task counter; all decode state is on chip */
+extern "C" size_t crn_decode_ws_bytes(int32_t) { return WS_HEAD; }
+
+extern "C" int crn_decode_set_logmap(uint32_t lo, uint32_t hi) {
+    const u32 w[2] = {lo, hi};
+    return cudaMemcpyToSymbol(c_logmap, w, sizeof(w)) == cudaSuccess ? CRN_OK : CRN_ECUDA;
+}   /* the task counter; all decode state is on chip */
 
 /* the four instantiations: <purge?, int8 LLRs?> */
 template <class F>
 cudaError_t for_each_kernel(F &&f) {
-    cudaError_t e = f((const void *)decode_kernel<false, false>);
-    if (e == cudaSuccess) e = f((const void *)decode_kernel<true, false>);
-    if (e == cudaSuccess) e = f((const void *)decode_kernel<false, true>);
-    if (e == cudaSuccess) e = f((const void *)decode_kernel<true, true>);
+    const void *k[] = {
+        (const void *)decode_kernel<false, false, CRN_VARIANT_MAXLOG>, (const void *)decode_kernel<true, false, CRN_VARIANT_MAXLOG>,
+        (const void *)decode_kernel<false, true, CRN_VARIANT_MAXLOG>, (const void *)decode_kernel<true, true, CRN_VARIANT_MAXLOG>,
+        (const void *)decode_kernel<false, false, CRN_VARIANT_LOGMAP>, (const void *)decode_kernel<true, false, CRN_VARIANT_LOGMAP>,
+        (const void *)decode_kernel<false, true, CRN_VARIANT_LOGMAP>, (const void *)decode_kernel<true, true, CRN_VARIANT_LOGMAP>};
+    cudaError_t e = cudaSuccess;
+    for (const void *x : k)
+        if (e == cudaSuccess) e = f(x);
     return e;
 }
 
@@ -1309,7 +1367,7 @@ extern "C" int crn_decode_grid(int device) {
 
 extern "C" int crn_decode_kernel_info(int32_t *static_smem, int32_t *dyn_smem, int32_t *max_dyn, int32_t *regs) {
     cudaFuncAttributes a;
-    if (cudaFuncGetAttributes(&a, decode_kernel<false, false>) != cudaSuccess) return CRN_ECUDA;
+    if (cudaFuncGetAttributes(&a, decode_kernel<false, false, CRN_VARIANT_MAXLOG>) != cudaSuccess) return CRN_ECUDA;
     *static_smem = (int32_t)a.sharedSizeBytes;
     *dyn_smem = (int32_t)smem_bytes();
     *max_dyn = a.maxDynamicSharedSizeBytes;
@@ -1326,17 +1384,24 @@ extern "C" int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_ta
     if (!ws_zeroed && cudaMemsetAsync(ws, 0, WS_HEAD, st) != cudaSuccess) return CRN_ECUDA;
     const int g = grid < n_tasks ? grid : n_tasks;
     const bool llr8 = (variant >> 8) != 0;      /* crn_plan_set_llr_format: int8 LLRs */
-#define CRN_LAUNCH(PG, L8)                                                                                        \
-    decode_kernel<PG, L8><<<g, BLOCK, smem_bytes(), st>>>(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, \
-                                                          et, bits, ok, it, ext, *tab, (uint8_t *)ws, variant,      \
-                                                          PG ? tb_dead : nullptr)
+    const int var = variant & 0xFF;
+#define CRN_LAUNCH(PG, L8, V)                                                                                      \
+    decode_kernel<PG, L8, V><<<g, BLOCK, smem_bytes(), st>>>(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2,         \
+                                                             max_iters, et, bits, ok, it, ext, *tab, (uint8_t *)ws, \
+                                                             variant, PG ? tb_dead : nullptr)
+#define CRN_LAUNCH_V(PG, L8)                                                                                       \
+    do {                                                                                                           \
+        if (var == CRN_VARIANT_LOGMAP) CRN_LAUNCH(PG, L8, CRN_VARIANT_LOGMAP);                                     \
+        else CRN_LAUNCH(PG, L8, CRN_VARIANT_MAXLOG);   /* MAXLOG or SCALED, chosen inside */                       \
+    } while (0)
     if (tb_dead) {
-        if (llr8) CRN_LAUNCH(true, true);
-        else CRN_LAUNCH(true, false);
+        if (llr8) CRN_LAUNCH_V(true, true);
+        else CRN_LAUNCH_V(true, false);
     } else {
-        if (llr8) CRN_LAUNCH(false, true);
-        else CRN_LAUNCH(false, false);
+        if (llr8) CRN_LAUNCH_V(false, true);
+        else CRN_LAUNCH_V(false, false);
     }
+#undef CRN_LAUNCH_V
 #undef CRN_LAUNCH
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
 }

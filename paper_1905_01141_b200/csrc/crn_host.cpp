@@ -136,6 +136,22 @@ extern "C" int64_t crn_counted_ops(const int32_t *K, int32_t n_cb, const uint8_t
 }
 
 /* ------------------------------------------------------------------ MI stopping rule */
+/* Log-MAP correction (R32): LUT[b] = round(8 ln(1 + e^(-(4b+1.5)/8))),
+ * b = min(|a-b| >> 2, 7), packed as the eight bytes the kernel's PRMT selects
+ * from (bytes 6 and 7 are 0 and double as its zero filler). */
+extern "C" int crn_logmap_lut(int32_t *out) {
+    if (!out) return CRN_EINVAL;
+    for (int b = 0; b < 8; b++) out[b] = (int32_t)std::floor(8.0 * std::log(1.0 + std::exp(-(4.0 * b + 1.5) / 8.0)) + 0.5);
+    return CRN_OK;
+}
+
+void crn_logmap_words(uint32_t *lo, uint32_t *hi) {
+    int32_t l[8];
+    crn_logmap_lut(l);
+    *lo = (uint32_t)l[0] | (uint32_t)l[1] << 8 | (uint32_t)l[2] << 16 | (uint32_t)l[3] << 24;
+    *hi = (uint32_t)l[4] | (uint32_t)l[5] << 8 | (uint32_t)l[6] << 16 | (uint32_t)l[7] << 24;
+}
+
 extern "C" int crn_mi_table(int32_t *out) {
     /* I(L) = 1 - Hb(p), p = 1/(1 + e^L), L = a/8 (the channel quantiser's LLR scale), in
      * Q16 rounded to nearest; the MI of a consistent Gaussian LLR of magnitude L
@@ -245,6 +261,11 @@ static int build_tables(int dev, DevTables **out) {
     t.tab.qpp_wm = t.qpp_wm; t.tab.qpp_ts = t.qpp_ts; t.tab.qinv_ts = t.qinv_ts;
     t.tab.qpp_off = t.qpp_off;
     t.tab.crc_bit = t.crc_bit; t.tab.crcb_off = t.crcb_off; t.tab.mi_tab = t.mi_tab;
+    {
+        uint32_t lo, hi;
+        crn_logmap_words(&lo, &hi);
+        crn_decode_set_logmap(lo, hi);
+    }
     t.tab.qinv_wm = t.qinv_wm;
     t.grid = crn_decode_grid(dev);
     if (t.grid <= 0) {
@@ -439,7 +460,8 @@ extern "C" int crn_plan_decode(void *plan, const int16_t *l0, const int16_t *l1,
 
 extern "C" int crn_plan_set_variant(void *plan, int32_t variant) {
     Plan *P = (Plan *)plan;
-    if (!P || (variant != CRN_VARIANT_MAXLOG && variant != CRN_VARIANT_SCALED)) return CRN_EINVAL;
+    if (!P || (variant != CRN_VARIANT_MAXLOG && variant != CRN_VARIANT_SCALED && variant != CRN_VARIANT_LOGMAP))
+        return CRN_EINVAL;
     P->variant = variant;
     return CRN_OK;
 }

@@ -80,6 +80,9 @@ int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_tasks, int32_
                       const crn_tables *tab, void *ws, void *stream, int32_t grid, int32_t variant,
                       uint8_t *tb_dead, int32_t ws_zeroed);
 size_t crn_decode_ws_bytes(int32_t grid);
+/* Log-MAP correction LUT[0..7] as two byte-packed words into the decode kernel's
+ * constant bank (crn_logmap_lut, R32); once per device. */
+int crn_decode_set_logmap(uint32_t lo, uint32_t hi);
 int crn_decode_grid(int device);
 /* crn_encode.cu */
 int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const uint8_t *info,

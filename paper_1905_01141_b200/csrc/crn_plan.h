@@ -21,6 +21,8 @@ struct HostPipe;      /* crn_runtime.cpp: staging buffers + streams of crn_plan_
 /* the kernel's variant word: decoder variant | (LLR format + 1) << 8 */
 struct Plan;
 int crn_plan_kernel_variant(const Plan *P);
+/* The Log-MAP LUT as the decode kernel's two PRMT source words (crn_host.cpp). */
+void crn_logmap_words(uint32_t *lo, uint32_t *hi);
 
 struct Plan {
     int dev = -1;

@@ -173,3 +173,10 @@ def test_llr_format_validation(L):
     reachable without a GPU (plans need a device)."""
     assert L.crn_plan_set_llr_format(None, 8, 3) == crn.CRN_EINVAL
     assert L.crn_plan_llr_bytes(None) == crn.CRN_EINVAL
+
+
+def test_logmap_lut_matches_oracle(L, orc):
+    """libcrn's Log-MAP table (its own computation) equals the oracle's."""
+    lut = crn.logmap_lut()
+    assert [int(x) for x in lut] == [orc.logmap_correction(4 * b) for b in range(8)]
+    assert lut[6] == 0 and lut[7] == 0          # the kernel's PRMT zero filler (DESIGN.md R32)

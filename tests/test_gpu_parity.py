@@ -602,3 +602,28 @@ def test_int8_llr_ingest_parity(orc, cfg, scale, shift, pad):
     assert np.array_equal(hb.numpy().view(np.uint32)[:b.n_words], g["words"][:b.n_words])
     assert np.array_equal(hok.numpy()[:b.n_cb], g["crc_ok"])
     assert np.array_equal(hit.numpy()[:b.n_cb], g["iters"])
+
+
+@pytest.mark.parametrize("cfg,scale,I,et", [(1, 1.0, 6, False), (5, 1.0, 8, True), (3, 0.1, 8, True)])
+def test_logmap_variant_parity(orc, cfg, scale, I, et):
+    """Row f2: Log-MAP (CRN_VARIANT_LOGMAP, R32) is bit-exact against the
+    oracle's Log-MAP -- bits, int16 extrinsics, iteration counts, CRC flags -- on
+    both kernel paths (W = 32 and generic W), device and host-buffer plans."""
+    b = _full(cfg, scale)
+    p = crn.Plan(b.desc)
+    p.set_variant(crn.VARIANT_LOGMAP)
+    bits, ok, it, ext = bmod.outputs(b)
+    p.decode(*b.llr, I, et, bits, ok, it, ext)
+    torch.cuda.synchronize()
+    g = dict(words=bits.cpu().numpy().view(np.uint32), crc_ok=ok.cpu().numpy()[:b.n_cb],
+             iters=it.cpu().numpy()[:b.n_cb], ext=ext.cpu().numpy())
+    idx = np.arange(b.n_cb)
+    r = run_oracle(b, idx, I, et, variant=orc.VAR_LOGMAP)
+    assert_parity(b, g, r, idx)
+    hl = [x.cpu().pin_memory() for x in b.llr]
+    hb = torch.zeros(bits.numel(), dtype=torch.int32).pin_memory()
+    hok = torch.zeros(ok.numel(), dtype=torch.uint8).pin_memory()
+    p.decode_host(*hl, I, et, hb, hok, None, n_chunks=2)
+    torch.cuda.synchronize()
+    assert np.array_equal(hb.numpy().view(np.uint32)[:b.n_words], g["words"][:b.n_words])
+    assert np.array_equal(hok.numpy()[:b.n_cb], g["crc_ok"])
