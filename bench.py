@@ -230,6 +230,30 @@ def run_pool(args, seed=0):
     d_ms = statistics.median(dec)
     tb_loss = float(1.0 - tb_ok.float().mean().item())
     cb_fail = float(1.0 - ok[:b.n_cb].float().mean().item())
+    # row f1: the paper's purge on the same TTI -- a CB not yet started
+    # when a sibling of its TB has failed is not decoded (the TB is lost either way)
+    dp = b.desc.copy()
+    dp["reserved"] = b.cb_tb
+    pp = crn.Plan(dp)
+    pp.set_purge(True)
+    for _ in range(2):
+        pp.decode(*b.llr, 8, True, bits, ok, it, stream=st)
+    torch.cuda.synchronize()
+    tp, npurged = [], []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        pp.decode(*b.llr, 8, True, bits, ok, it, stream=st)
+        e1.record(st)
+        torch.cuda.synchronize()
+        tp.append(e0.elapsed_time(e1))
+        npurged.append(int((it[:b.n_cb] == 0).sum()))
+    crn.tb_verdict_batch(tbs, b.desc, bits, ok, tb_ok, None, stream=st)
+    torch.cuda.synchronize()
+    purge = {"decode_ms": statistics.median(tp), "purged_cbs": int(np.median(npurged)),
+             "tb_loss_rate": float(1.0 - tb_ok.float().mean().item()),
+             "note": "which CBs get purged depends on timing; TB verdicts equal the no-purge run's"}
+    pp.close()
     # row f2: the decoder variants / stopping rules on the same TTI (SURVEY.md §8(f) 2:
     # "score on BLER and mean iterations"): device time, TB loss, CB failures, iterations
     variants = {}
@@ -264,7 +288,7 @@ def run_pool(args, seed=0):
                                                           "in pinned host memory (host clock, stream synced)",
             "tb_loss_rate": tb_loss, "cb_crc_fail_rate": cb_fail,
             "mean_iters": float(its.mean()),
-            "variants": variants,
+            "variants": variants, "purge": purge,
             "iters_hist": [int(x) for x in np.bincount(its, minlength=9)[1:9]],
             "gen_s": round(t_gen, 1)}
 
