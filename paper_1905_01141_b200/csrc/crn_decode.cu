@@ -123,8 +123,12 @@ __device__ __forceinline__ u32 vaddmax(u32 a, u32 b, u32 c) { return __viaddmax_
  * int16x2 correction in one instruction. */
 __device__ __forceinline__ u32 maxs2(u32 a, u32 b, u32 lut_lo, u32 lut_hi) {
     const u32 m = __vmaxs2(a, b), d = __vsub2(m, __vmins2(a, b));
-    const u32 q = __vmins2((d >> 2) & 0x3FFF3FFFu, 0x00070007u);
-    return __vadd2(m, __byte_perm(lut_lo, lut_hi, q | (q >> 8) | 0x6060u));
+    /* t = min(d, 31) >> 2 per half: bucket_lo in bits 2:0, bucket_hi in 18:16 (and
+     * d_hi's low two bits in 15:14); sel = t | t >> 8 | 0x6060 puts the buckets in
+     * selector nibbles 0 and 2, and nibbles 1 and 3 select byte 6 (= 0) -- the stray
+     * d_hi bits can only set those nibbles' bit 3 (sign-replicate a 0 byte: 0) */
+    const u32 t = __vmins2(d, 0x001F001Fu) >> 2;
+    return __vadd2(m, __byte_perm(lut_lo, lut_hi, t | (t >> 8) | 0x6060u));
 }
 
 struct Lut {                                    /* the LUT's two PRMT source words */
