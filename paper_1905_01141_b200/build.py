@@ -30,16 +30,19 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return SO
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
     bdir = os.path.join(HERE, "build")
     os.makedirs(bdir, exist_ok=True)
+    cmds, objs = [], []
     for s in SOURCES:
         o = os.path.join(bdir, s + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, s), "-o", o]
         if verbose and s.endswith(".cu"):
             cmd.insert(1, "-Xptxas=-v")
-        subprocess.check_call(cmd)
+        cmds.append(cmd)
         objs.append(o)
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:   # independent units
+        list(ex.map(subprocess.check_call, cmds))
     tmp = SO + ".tmp"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs])
     os.replace(tmp, SO)
