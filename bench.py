@@ -230,6 +230,24 @@ def run_pool(args, seed=0):
     d_ms = statistics.median(dec)
     tb_loss = float(1.0 - tb_ok.float().mean().item())
     cb_fail = float(1.0 - ok[:b.n_cb].float().mean().item())
+    # the same TTI with int8 LLRs over PCIe (row f4, R31: saturated to [-128, 127], shift 0)
+    clipped = sum(int((x.abs() > 127).sum()) for x in b.llr) / (3 * b.n_llr)
+    h8 = [torch.clamp(x, -128, 127).to(torch.int8).cpu().pin_memory() for x in b.llr]
+    p8 = crn.Plan(b.desc)
+    p8.set_llr_format(8, 0)
+    for _ in range(2):
+        p8.decode_host(*h8, 8, True, hb, hok, None, stream=st)
+    torch.cuda.synchronize()
+    e2e8 = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        p8.decode_host(*h8, 8, True, hb, hok, None, stream=st)
+        st.synchronize()
+        e2e8.append(1e3 * (time.perf_counter() - t0))
+    int8 = {"e2e_ms": statistics.median(e2e8), "clipped_fraction": clipped,
+            "cb_crc_fail_rate": float(1.0 - hok[:b.n_cb].float().mean().item())}
+    p8.close()
+    del h8
     # row f1: the paper's purge on the same TTI -- a CB not yet started
     # when a sibling of its TB has failed is not decoded (the TB is lost either way)
     dp = b.desc.copy()
@@ -288,7 +306,7 @@ def run_pool(args, seed=0):
                                                           "in pinned host memory (host clock, stream synced)",
             "tb_loss_rate": tb_loss, "cb_crc_fail_rate": cb_fail,
             "mean_iters": float(its.mean()),
-            "variants": variants, "purge": purge,
+            "variants": variants, "purge": purge, "int8_ingest": int8,
             "iters_hist": [int(x) for x in np.bincount(its, minlength=9)[1:9]],
             "gen_s": round(t_gen, 1)}
 
