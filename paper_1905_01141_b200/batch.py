@@ -1,7 +1,10 @@
 """Product-side batch assembly for a synthetic workload: CB packing via libcrn
 (crn_tb_build_cbs / descriptors, row a1), device encoding via crn_encode_batch
 (the paper's encoding function), then the shared workload
-channel.  Used by bench.py and the GPU tests; never touches oracle/.
+channel (``build``, used by bench.py); or the same dense layout around CB
+contents and coded bits the caller supplies (``from_cbs``: the parity tests
+pass the oracle's, so no oracle input comes from the CUDA path).  Never
+touches oracle/.
 """
 from __future__ import annotations
 
@@ -86,3 +89,26 @@ def outputs(b: Batch, device="cuda", want_ext: bool = True):
     it = torch.zeros(max(b.n_cb, 1), dtype=torch.uint8, device=dev)
     ext = torch.zeros(max(int(b.desc["K"].sum()), 1), dtype=torch.int16, device=dev) if want_ext else None
     return bits, ok, it, ext
+
+
+def from_cbs(wl: wlmod.Workload, cbs, coded, device="cuda") -> Batch:
+    """Batch of the given CBs in the dense layout ``build`` uses (CB i's K_i bits
+    at sum K, K_i+4 coded bits / LLRs at sum (K+4), ceil(K_i/32) words at the
+    word sum).  cbs: per CB a dict with c (uint8 bits incl. CRC and fillers), K,
+    F, crc, cell, ebn0, tb; coded: per CB (d0, d1, d2) uint8 arrays of K+4."""
+    dev = torch.device(device)
+    n = len(cbs)
+    desc = np.zeros(n, crn.DESC_DTYPE)
+    K = np.array([cb["K"] for cb in cbs], np.int64)
+    desc["K"], desc["F"], desc["crc_kind"] = K, [cb["F"] for cb in cbs], [cb["crc"] for cb in cbs]
+    z = np.zeros(1, np.int64)
+    desc["ext_off"] = np.concatenate([z, np.cumsum(K)[:-1]]) if n else K
+    desc["llr_off"] = np.concatenate([z, np.cumsum(K + 4)[:-1]]) if n else K
+    desc["bit_off"] = np.concatenate([z, np.cumsum((K + 31) // 32)[:-1]]) if n else K
+    info = torch.from_numpy(np.concatenate([cb["c"] for cb in cbs]).astype(np.uint8)).to(dev)
+    cd = tuple(torch.from_numpy(np.concatenate([e[s] for e in coded]).astype(np.uint8)).to(dev) for s in range(3))
+    cell = np.array([cb["cell"] for cb in cbs], np.int32)
+    e = np.array([cb["ebn0"] for cb in cbs], np.float64)
+    l0, l1, l2 = wlmod.channel_llr(wl, cell, desc["K"], e, cd)
+    return Batch(wl=wl, desc=desc, cb_cell=cell, cb_tb=np.array([cb["tb"] for cb in cbs], np.int64), cb_ebn0=e,
+                 info=info, coded=cd, llr=(l0, l1, l2))

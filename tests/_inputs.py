@@ -42,3 +42,14 @@ def offsets(K):
     llr_off = np.concatenate([[0], np.cumsum(K + 4)[:-1]]) if K.size else np.zeros(0, np.int64)
     bit_off = np.concatenate([[0], np.cumsum(K)[:-1]]) if K.size else np.zeros(0, np.int64)
     return llr_off, bit_off
+
+
+def oracle_batch(wl, device="cuda"):
+    """A product Batch whose CB contents (segmentation, CRC, fillers) and coded
+    bits are the oracle's -- the parity tests' inputs never come from the CUDA
+    path -- on the shared workload channel."""
+    import oracle
+    from paper_1905_01141_b200 import batch as bmod
+    cbs = oracle_cbs(wl)
+    enc = [oracle.turbo_encode(cb["c"]) for cb in cbs]
+    return bmod.from_cbs(wl, cbs, enc, device)

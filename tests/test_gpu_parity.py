@@ -10,6 +10,7 @@ from paper_1905_01141_b200 import build as crn_build
 from paper_1905_01141_b200 import crn
 from paper_1905_01141_b200 import workload as wlmod
 from tests._gpu import assert_parity, run_gpu, run_oracle, unpack
+from tests._inputs import oracle_batch
 
 pytestmark = pytest.mark.gpu
 
@@ -22,13 +23,21 @@ def _lib():
 
 
 def _full(cfg, scale=1.0, seed=0):
+    """Parity inputs: the oracle's CBs and coded bits on the shared channel."""
+    wl = wlmod.make_workload(cfg, seed=seed, device="cuda", scale=scale)
+    return oracle_batch(wl)
+
+
+def _full_gpu_encoded(cfg, scale=1.0, seed=0):
+    """The product's own batch assembly (libcrn segmentation + GPU encoder), for
+    the tests of that assembly against the oracle."""
     wl = wlmod.make_workload(cfg, seed=seed, device="cuda", scale=scale)
     return bmod.build(wl)
 
 
 def test_encoder_matches_oracle(orc):
     for cfg, scale in ((1, 1.0), (2, 1.0), (3, 0.2), (5, 1.0)):
-        b = _full(cfg, scale)
+        b = _full_gpu_encoded(cfg, scale)
         info = b.info.cpu().numpy()
         coded = [x.cpu().numpy() for x in b.coded]
         for i in range(b.n_cb):
@@ -39,6 +48,26 @@ def test_encoder_matches_oracle(orc):
             e = orc.turbo_encode(c)
             for s in range(3):
                 assert np.array_equal(coded[s][d["llr_off"]:d["llr_off"] + d["K"] + 4], e[s]), (cfg, i, s)
+
+
+@pytest.mark.parametrize("cfg,scale", [(1, 1.0), (2, 1.0), (3, 0.2), (5, 1.0)])
+def test_product_batch_equals_oracle_batch(orc, cfg, scale):
+    """The product's batch assembly (libcrn segmentation / CRC / fillers, GPU
+    encoder) produces exactly the oracle's CBs, layout, coded bits and LLRs."""
+    p = _full_gpu_encoded(cfg, scale)
+    o = _full(cfg, scale)
+    for f in ("K", "F", "crc_kind", "llr_off", "bit_off", "ext_off"):
+        assert np.array_equal(p.desc[f], o.desc[f]), f
+    pi, oi = p.info.cpu().numpy(), o.info.cpu().numpy()
+    if p.wl.tb_kind == "cb":                     # the product attaches the CRC24B while encoding
+        keep = np.ones(pi.size, bool)
+        for d in p.desc:
+            keep[d["ext_off"] + d["K"] - 24:d["ext_off"] + d["K"]] = False
+        assert np.array_equal(pi[keep], oi[keep])
+    else:
+        assert np.array_equal(pi, oi)
+    for x, y in zip(p.coded + p.llr, o.coded + o.llr):
+        assert torch.equal(x, y)
 
 
 @pytest.mark.parametrize("cfg,scale", [(1, 1.0), (2, 1.0), (3, 0.2), (5, 1.0)])
