@@ -515,8 +515,10 @@ def test_rate_dematch_and_match_parity(orc):
 
 
 def test_rate_matched_chain_decodes_like_oracle(orc):
-    """GPU encode -> GPU rate match -> noisy int16 soft values -> GPU de-match ->
-    GPU decode, against the oracle de-matching + decoding of the same soft values."""
+    """Rate match -> noisy int16 soft values -> de-match -> decode: the GPU chain
+    (crn_rate_match_batch, crn_rate_dematch_batch, decode) against the oracle's
+    chain on the same soft values, which are made from the ORACLE's rate-matched
+    bits (the GPU's are checked equal to them), every stage compared."""
     b = _full(5, 0.5)
     rng = np.random.default_rng(5)
     K = b.desc["K"].astype(np.int64)
@@ -527,22 +529,28 @@ def test_rate_matched_chain_decodes_like_oracle(orc):
     d["e_off"] = np.concatenate([[0], np.cumsum(d["E"])[:-1]])
     d["llr_off"] = b.desc["llr_off"]
     n_e = int(d["E"].sum())
+    coded = [x.cpu().numpy() for x in b.coded]                        # the oracle's coded bits (_full)
+    eo_bits = np.concatenate([orc.rate_match([x[lo:lo + k + 4] for x in coded], int(E), 0)
+                              for k, lo, E in zip(K, d["llr_off"], d["E"])])
     eb = torch.zeros(n_e, dtype=torch.uint8, device="cuda")
     crn.rate_match_batch(d, *b.coded, eb)
     torch.cuda.synchronize()
-    x = (2 * eb.cpu().numpy().astype(np.int32) - 1) * 40 + rng.normal(0, 25, n_e).round().astype(np.int32)
+    assert np.array_equal(eb.cpu().numpy(), eo_bits)
+    x = (2 * eo_bits.astype(np.int32) - 1) * 40 + rng.normal(0, 25, n_e).round().astype(np.int32)
     soft = np.clip(x, -32768, 32767).astype(np.int16)
     hg = [torch.zeros_like(t) for t in b.llr]
     crn.rate_dematch_batch(d, torch.from_numpy(soft).cuda(), False, *hg)
     g = run_gpu(b, 8, True, l=hg)
     hh = [t.cpu().numpy() for t in hg]
+    ho_all = [np.zeros_like(t) for t in hh]
     for i in range(b.n_cb):
         k, lo, eo, E = int(K[i]), int(d["llr_off"][i]), int(d["e_off"][i]), int(d["E"][i])
         ho = orc.rate_dematch(soft[eo:eo + E], k, 0)
         for s in range(3):
             assert np.array_equal(hh[s][lo:lo + k + 4], ho[s])
+            ho_all[s][lo:lo + k + 4] = ho[s]
     b2 = type("B", (), {})()
-    b2.llr, b2.desc = tuple(torch.from_numpy(x) for x in hh), b.desc
+    b2.llr, b2.desc = tuple(torch.from_numpy(x) for x in ho_all), b.desc   # the oracle's de-matched streams
     r = run_oracle(b2, np.arange(b.n_cb), 8, True)
     assert_parity(b, g, r, np.arange(b.n_cb))
     assert g["crc_ok"].mean() > 0.5
