@@ -787,6 +787,19 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             u32 wlo = 0, whi = 0;
             int mlo = 0, mhi = 0;             /* MI statistic of this thread's steps (R29) */
             u32 sn[HW];
+            /* the CBs' output offsets are loaded first: their round trip overlaps
+             * the L_APP pass below instead of following the stop decision */
+            int64_t obit[2] = {0, 0}, oext[2] = {0, 0};
+            if (active) {
+#pragma unroll
+                for (int l = 0; l < 2; l++) {
+                    const int cbx = sh.cb[2 * f.p + l];
+                    if (cbx >= 0) {
+                        obit[l] = desc[cbx].bit_off;
+                        if (ext_out) oext[l] = desc[cbx].ext_off;
+                    }
+                }
+            }
             tm_load16_wait(f.ts, sn);
             const int n00 = f.j * W + f.k0, Fl = sh.F[2 * f.p], Fh = sh.F[2 * f.p + 1];
 #pragma unroll
@@ -840,13 +853,12 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
 #pragma unroll
                 for (int l = 0; l < 2; l++) {
                     if (!sh.fin[2 * p + l]) continue;
-                    const crn_cb_desc &d = desc[sh.cb[2 * p + l]];
-                    if (!tail_thr) out_bits[d.bit_off + j] = hb[l * TS + f.t];
+                    if (!tail_thr) out_bits[obit[l] + j] = hb[l * TS + f.t];
                     if (ext_out) {
 #pragma unroll
                         for (int s = 0; s < HW; s++) {
                             const u32 x = lds_q(qq[s], 0);
-                            ext_out[d.ext_off + j * W + f.k0 + s] = (int16_t)(l ? (x >> 16) : (x & 0xFFFFu));
+                            ext_out[oext[l] + j * W + f.k0 + s] = (int16_t)(l ? (x >> 16) : (x & 0xFFFFu));
                         }
                     }
                 }
