@@ -203,31 +203,55 @@ encode_kernel(const crn_cb_desc *__restrict__ desc, int n_cb, const uint8_t *__r
             }
             __syncwarp();
         }
-        /* c'_i = c_{Pi(i)} for the lane's words */
+        /* c'_i = c_{Pi(i)} for the lane's words.  With K = 0 mod 64 the two halves
+         * go together: Pi(i + K/2) = Pi(i) + K/2 mod K (f1 odd, f2 even), so one
+         * recurrence step serves bit i and bit i + K/2 */
         {
             const int ki = crn_k_index_dev(K);
             const int f1 = c_f1[ki], f2 = c_f2[ki];
-            const int i0 = 32 * w0;
+            const uint32_t f2x2 = (uint32_t)((2 * f2) % K);
+            const bool halves = (K & 63) == 0;
+            const int nwh = halves ? nw >> 1 : nw;               /* words the recurrence walks */
+            const int perh = (nwh + 31) >> 5;
+            const int h0 = min(nwh, lane * perh), h1 = min(nwh, h0 + perh);
+            const int i0 = 32 * h0;
             uint32_t pi = (uint32_t)((f1 * i0 + f2 * ((i0 * i0) % K)) % K);
             uint32_t g = (uint32_t)((f1 + f2 * ((2 * i0 + 1) % K)) % K);
-            const uint32_t f2x2 = (uint32_t)((2 * f2) % K);
-            for (int t = w0; t < w1; t++) {
-                uint32_t acc = 0;
-                const int nbit = min(32, K - 32 * t);                /* 32, or 8/16/24 in the last word */
-                auto step = [&]() {
-                    const uint32_t v = W.c[pi >> 5];
-                    acc = __funnelshift_r(acc, __funnelshift_r(v, v, pi), 1);   /* bit pi -> acc MSB */
-                    pi = min(pi + g, pi + g - (uint32_t)K);                     /* (pi + g) mod K */
-                    g = min(g + f2x2, g + f2x2 - (uint32_t)K);
-                };
-                if (nbit == 32) {
+            if (halves) {
+                const uint32_t Kh = (uint32_t)(K >> 1);
+                for (int t = h0; t < h1; t++) {
+                    uint32_t acc = 0, acc2 = 0;
 #pragma unroll
-                    for (int k = 0; k < 32; k++) step();
-                } else {
-                    for (int k = 0; k < nbit; k++) step();
-                    acc >>= 32 - nbit;
+                    for (int k = 0; k < 32; k++) {
+                        const uint32_t pj = min(pi + Kh, pi - Kh);        /* Pi(i + K/2) */
+                        const uint32_t v = W.c[pi >> 5], v2 = W.c[pj >> 5];
+                        acc = __funnelshift_r(acc, __funnelshift_r(v, v, pi), 1);
+                        acc2 = __funnelshift_r(acc2, __funnelshift_r(v2, v2, pj), 1);
+                        pi = min(pi + g, pi + g - (uint32_t)K);
+                        g = min(g + f2x2, g + f2x2 - (uint32_t)K);
+                    }
+                    W.ci[t] = acc;
+                    W.ci[t + nwh] = acc2;
                 }
-                W.ci[t] = acc;
+            } else {
+                for (int t = h0; t < h1; t++) {
+                    uint32_t acc = 0;
+                    const int nbit = min(32, K - 32 * t);                /* 32, or 8/16/24 in the last word */
+                    auto step = [&]() {
+                        const uint32_t v = W.c[pi >> 5];
+                        acc = __funnelshift_r(acc, __funnelshift_r(v, v, pi), 1);   /* bit pi -> acc MSB */
+                        pi = min(pi + g, pi + g - (uint32_t)K);                     /* (pi + g) mod K */
+                        g = min(g + f2x2, g + f2x2 - (uint32_t)K);
+                    };
+                    if (nbit == 32) {
+#pragma unroll
+                        for (int k = 0; k < 32; k++) step();
+                    } else {
+                        for (int k = 0; k < nbit; k++) step();
+                        acc >>= 32 - nbit;
+                    }
+                    W.ci[t] = acc;
+                }
             }
         }
         __syncwarp();
