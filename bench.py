@@ -417,13 +417,13 @@ def run_small_configs(seed=0):
 def run_latency(args, seed=0):
     """BASELINE cfg5: paced 1 ms TTIs of 200 CBs (20 cells x 10 CBs, K uniform over
     the 188 sizes, Eb/N0 ~ U[0.5, 3] dB per CB, CRC ET at max 8 iterations), 4 cell
-    groups -> 4 CUDA streams, through crn_stream_run (host buffers in, host
+    groups (default 2 of 10 cells) -> one CUDA stream each, through crn_stream_run (host buffers in, host
     results out).  TTI t uses cells 20t..20t+19 of cfg5; args.lat_distinct distinct
     TTIs are generated and cycled over args.lat_ttis releases."""
     from paper_1905_01141_b200 import batch as bmod
     from paper_1905_01141_b200 import crn
     from paper_1905_01141_b200 import workload as wlmod
-    n_groups, cells_per_tti = 4, 20
+    n_groups, cells_per_tti = args.lat_groups, 20
     t_gen = time.perf_counter()
     distinct = []
     for t in range(args.lat_distinct):
@@ -463,7 +463,7 @@ def run_latency(args, seed=0):
     its = np.concatenate([g["it"].numpy()[:g["n_cb"]] for grp in distinct for g in grp])
     sum_k = [sum(g["sum_k"] for g in grp) for grp in distinct]
     return {"workload": "cfg5: 1 ms TTIs of 200 CBs (20 cells x 10), K ~ U(188 sizes), QPSK Eb/N0 ~ U[0.5,3] dB "
-                        "per CB, CRC24B ET max 8 iterations, 4 cell groups = 4 CUDA streams each with its own "
+                        f"per CB, CRC24B ET max 8 iterations, {n_groups} cell groups = {n_groups} CUDA streams each with its own "
                         "upload / decode launch / download, host buffers in/out (crn_stream_run)",
             "n_tti": args.lat_ttis, "distinct_ttis": args.lat_distinct, "period_us": 1000.0,
             "measured_ttis": int(lat.size), "p50_us": float(np.percentile(lat, 50)),
@@ -701,6 +701,8 @@ def main():
     ap.add_argument("--lat-ttis", type=int, default=1000)
     ap.add_argument("--lat-distinct", type=int, default=100)
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--lat-groups", type=int, default=2, choices=[1, 2, 4, 5, 10, 20],
+                    help="cell groups (CUDA streams) of the cfg5 latency run")
     ap.add_argument("--no-pool", action="store_true", help="skip the cfg3 one-TTI pool measurement")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
