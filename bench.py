@@ -438,15 +438,19 @@ def run_latency(args, seed=0):
             d["bit_off"] = np.concatenate([[0], np.cumsum((K + 31) // 32)[:-1]]) if K.size else K
             src = torch.from_numpy(np.concatenate([np.arange(int(o), int(o) + int(k) + 4)
                                                    for o, k in zip(b.desc["llr_off"][sel], K)])).cuda()
-            buf = torch.stack([x[src] for x in b.llr]).cpu().pin_memory()   # streams contiguous: one upload
+            dbuf = torch.stack([x[src] for x in b.llr])
+            buf = dbuf.cpu().pin_memory()                                  # streams contiguous: one upload
             hl = [buf[0], buf[1], buf[2]]
+            clip8 = int((dbuf.abs() > 127).sum())
+            buf8 = torch.clamp(dbuf, -128, 127).to(torch.int8).cpu().pin_memory()   # the int8 run's inputs
             nw = max(int(((K + 31) // 32).sum()), 1)
             nc = max(sel.size, 1)
             ob = torch.zeros(4 * nw + 2 * nc, dtype=torch.uint8).pin_memory()   # bits | crc_ok | iters: one download
             grp.append(dict(desc=d, l0=hl[0], l1=hl[1], l2=hl[2],
                             bits=ob[:4 * nw].view(torch.int32), ok=ob[4 * nw:4 * nw + nc],
                             it=ob[4 * nw + nc:4 * nw + 2 * nc],
-                            sum_k=int(K.sum()), n_cb=int(sel.size), info=int((d["K"] - d["F"] - 24).sum())))
+                            sum_k=int(K.sum()), n_cb=int(sel.size), info=int((d["K"] - d["F"] - 24).sum()),
+                            l8=buf8, clip8=clip8, n_llr3=int(dbuf.numel())))
         distinct.append(grp)
     t_gen = time.perf_counter() - t_gen
     groups = [g for t in range(args.lat_ttis) for g in distinct[t % args.lat_distinct]]
@@ -462,6 +466,15 @@ def run_latency(args, seed=0):
 
     its = np.concatenate([g["it"].numpy()[:g["n_cb"]] for grp in distinct for g in grp])
     sum_k = [sum(g["sum_k"] for g in grp) for grp in distinct]
+    # the same TTIs with int8 LLRs (CRN_STREAM_LLR8, shift 0: saturated int16 LLRs) --
+    # half the upload bytes; identical inputs where nothing clips
+    groups8 = [dict(g, l0=g["l8"][0], l1=g["l8"][1], l2=g["l8"][2]) for g in groups]
+    tim8 = crn.stream_run(groups8, args.lat_ttis, n_groups, 1000.0, 8, True, flags=crn.STREAM_LLR8)
+    lat8 = tim8["latency_us"][skip:]
+    clipped = sum(g["clip8"] for grp in distinct for g in grp) / max(1, sum(g["n_llr3"] for grp in distinct for g in grp))
+    int8 = {"p50_us": float(np.percentile(lat8, 50)), "p99_us": float(np.percentile(lat8, 99)),
+            "device_p50_us": float(np.percentile(tim8["device_us"][skip:], 50)), "clipped_fraction": clipped,
+            "note": "same TTIs, int16 LLRs saturated to int8 (CRN_STREAM_LLR8): half the upload bytes"}
     return {"workload": "cfg5: 1 ms TTIs of 200 CBs (20 cells x 10), K ~ U(188 sizes), QPSK Eb/N0 ~ U[0.5,3] dB "
                         f"per CB, CRC24B ET max 8 iterations, {n_groups} cell groups = {n_groups} CUDA streams each with its own "
                         "upload / decode launch / download, host buffers in/out (crn_stream_run)",
@@ -469,7 +482,7 @@ def run_latency(args, seed=0):
             "measured_ttis": int(lat.size), "p50_us": float(np.percentile(lat, 50)),
             "p99_us": float(np.percentile(lat, 99)), "max_us": float(lat.max()), "mean_us": float(lat.mean()),
             "device_p50_us": float(np.percentile(dev, 50)), "device_p99_us": float(np.percentile(dev, 99)),
-            "host_submit_p50_us": float(np.percentile(sub, 50)),
+            "host_submit_p50_us": float(np.percentile(sub, 50)), "int8_ingest": int8,
             "stages_p50_us": stages,
             "deadline_us": 2000.0, "deadline_misses": int((lat > 2000.0).sum()),
             "mean_iters": float(its.mean()), "mean_sum_k_per_tti": float(np.mean(sum_k)),

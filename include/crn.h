@@ -242,8 +242,13 @@ int crn_stream_run(const crn_tti_group *groups, int32_t n_tti, int32_t n_groups,
  * the decode kernel reads each group's descriptors, tasks and LLRs straight
  * from pinned host memory and writes its bits / crc_ok / iters_used straight
  * into the host buffers (over PCIe, no copy stage; one launch per group and
- * TTI); every host buffer must be pinned (CRN_EINVAL otherwise). */
-enum { CRN_STREAM_MERGED = 1, CRN_STREAM_STAGES = 2, CRN_STREAM_ZEROCOPY = 4 };
+ * TTI); every host buffer must be pinned (CRN_EINVAL otherwise).
+ * CRN_STREAM_LLR8 | CRN_STREAM_LLR8_SHIFT(s), s in [0, 8] (not with MERGED or
+ * ZEROCOPY): the groups' llr_sys / p1 / p2 hold int8 LLRs (n_llr elements of 1
+ * byte), read as x * 2^s exactly as crn_plan_set_llr_format does -- half the
+ * upload bytes. */
+enum { CRN_STREAM_MERGED = 1, CRN_STREAM_STAGES = 2, CRN_STREAM_ZEROCOPY = 4, CRN_STREAM_LLR8 = 8 };
+#define CRN_STREAM_LLR8_SHIFT(s) ((s) << 8)
 int crn_stream_run_ex(const crn_tti_group *groups, int32_t n_tti, int32_t n_groups, double period_us,
                       int32_t max_iters, int32_t early_term, int32_t flags, crn_tti_timing *timing);
 

@@ -242,6 +242,11 @@ class Plan:
 STREAM_MERGED = 1
 STREAM_STAGES = 2
 STREAM_ZEROCOPY = 4
+STREAM_LLR8 = 8
+
+
+def stream_llr8_shift(s: int) -> int:
+    return s << 8
 
 
 def stream_run(groups, n_tti: int, n_groups: int, period_us: float, max_iters: int, early_term: bool,

@@ -233,14 +233,16 @@ struct Layout {
 /* [task counter (zeroed in the host blob, used as the decode workspace) | desc |
  * tasks | pairs] = the uploaded blob; then the three LLR streams; then bits, crc_ok
  * and iters_used back to back (one download when the host buffers are too). */
-Layout layout(int n_cb, int n_tasks, int n_pairs, int64_t n_llr, int64_t n_words) {
+Layout layout(int n_cb, int n_tasks, int n_pairs, int64_t n_llr, int64_t n_words, int esz = 2) {
     Layout L;
     L.o_desc = 256;
     L.o_tasks = L.o_desc + align256(sizeof(crn_cb_desc) * n_cb);
     L.o_pairs = L.o_tasks + align256(sizeof(crn_task) * n_tasks);
     L.o_l = L.o_pairs + align256(sizeof(crn_pair) * n_pairs);
-    L.bl = align256(sizeof(int16_t) * n_llr);
-    L.o_bits = L.o_l + 3 * L.bl;
+    /* int16: 256-byte aligned streams; int8 (CRN_STREAM_LLR8): back to back, so a
+     * host block [sys | p1 | p2] goes up in one copy */
+    L.bl = esz == 2 ? align256(sizeof(int16_t) * n_llr) : (size_t)n_llr;
+    L.o_bits = (L.o_l + 3 * L.bl + 255) & ~(size_t)255;
     L.o_ok = L.o_bits + 4 * n_words;
     L.o_it = L.o_ok + n_cb;
     L.tot = L.o_it + align256(n_cb);
@@ -253,9 +255,15 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
                                  int32_t max_iters, int32_t et, int32_t flags, crn_tti_timing *timing) {
     if (!g || !timing || n_tti < 1 || n_groups < 1 || n_groups > 64 || period_us < 0 || max_iters < 1 ||
         max_iters > CRN_MAX_ITERS || et < 0 || et > CRN_ET_MI ||
-        (flags & ~(CRN_STREAM_MERGED | CRN_STREAM_STAGES | CRN_STREAM_ZEROCOPY)) ||
+        (flags & ~(CRN_STREAM_MERGED | CRN_STREAM_STAGES | CRN_STREAM_ZEROCOPY | CRN_STREAM_LLR8 | (0xF << 8))) ||
         ((flags & CRN_STREAM_MERGED) && (flags & CRN_STREAM_ZEROCOPY)))
         return CRN_EINVAL;
+    const bool llr8 = flags & CRN_STREAM_LLR8;
+    const int sh8 = (flags >> 8) & 0xF;
+    if ((!llr8 && sh8) || (llr8 && (sh8 > 8 || (flags & (CRN_STREAM_MERGED | CRN_STREAM_ZEROCOPY)))))
+        return CRN_EINVAL;
+    const int esz = llr8 ? 1 : 2;
+    const int kvariant = CRN_VARIANT_MAXLOG | (llr8 ? (sh8 + 1) << 8 : 0);   /* the decode kernel's variant word */
     const bool merged = flags & CRN_STREAM_MERGED, stages = merged || (flags & CRN_STREAM_STAGES);
     const bool zc = flags & CRN_STREAM_ZEROCOPY;
     int dev;
@@ -293,7 +301,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
                     }
                 }
             }
-            const Layout L = layout(q.n_cb, q.n_cb, q.n_cb, g_llr[x], g_words[x]);   /* tasks, pairs <= CBs */
+            const Layout L = layout(q.n_cb, q.n_cb, q.n_cb, g_llr[x], g_words[x], esz);   /* tasks, pairs <= CBs */
             need[gi] = std::max(need[gi], L.tot);
             hneed[gi] = std::max(hneed[gi], L.o_l);
             m_cb += q.n_cb;
@@ -409,7 +417,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             for (int i = 0; i < q.n_cb; i++) sel[i] = i;
             crn_build_tasks(q.desc, sel.data(), q.n_cb, tasks, pairs);
             const int64_t n_llr = g_llr[x], n_words = g_words[x];
-            const Layout L = layout(q.n_cb, (int)tasks.size(), (int)pairs.size(), n_llr, n_words);
+            const Layout L = layout(q.n_cb, (int)tasks.size(), (int)pairs.size(), n_llr, n_words, esz);
             const int b = ti & 1;
             if (ti >= 2) {                              /* blob slot b was last uploaded by TTI ti-2 */
                 const cudaEvent_t prev = ev1[x - 2 * (int64_t)n_groups];
@@ -441,14 +449,14 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             }
             uint8_t *dm = (uint8_t *)r.dmem;
             cudaMemcpyAsync(dm, hb, L.o_l, cudaMemcpyHostToDevice, r.st);
-            const int16_t *hs[3] = {q.llr_sys, q.llr_p1, q.llr_p2};
+            const uint8_t *hs[3] = {(const uint8_t *)q.llr_sys, (const uint8_t *)q.llr_p1, (const uint8_t *)q.llr_p2};
             int16_t *dl[3];
             for (int s = 0; s < 3; s++) dl[s] = (int16_t *)(dm + L.o_l + s * L.bl);
-            if (q.llr_p1 == q.llr_sys + n_llr && q.llr_p2 == q.llr_p1 + n_llr && L.bl == sizeof(int16_t) * n_llr)
-                cudaMemcpyAsync(dl[0], hs[0], 3 * sizeof(int16_t) * n_llr, cudaMemcpyHostToDevice, r.st);
+            const size_t sb = (size_t)esz * (size_t)n_llr;             /* bytes per stream */
+            if (hs[1] == hs[0] + sb && hs[2] == hs[1] + sb && L.bl == sb)
+                cudaMemcpyAsync(dl[0], hs[0], 3 * sb, cudaMemcpyHostToDevice, r.st);
             else                                            /* the three streams: one copy if contiguous */
-                for (int s = 0; s < 3; s++)
-                    cudaMemcpyAsync(dl[s], hs[s], sizeof(int16_t) * n_llr, cudaMemcpyHostToDevice, r.st);
+                for (int s = 0; s < 3; s++) cudaMemcpyAsync(dl[s], hs[s], sb, cudaMemcpyHostToDevice, r.st);
             uint32_t *dbits = (uint32_t *)(dm + L.o_bits);
             uint8_t *dok = dm + L.o_ok, *dit = dm + L.o_it;
             if (stages) {
@@ -458,7 +466,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             src = crn_launch_tasks(dev, t, (const crn_cb_desc *)(dm + L.o_desc), (const crn_task *)(dm + L.o_tasks),
                                    (int)tasks.size(), (const crn_pair *)(dm + L.o_pairs), dl[0], dl[1], dl[2],
                                    max_iters, et, dbits, dok, q.iters_used ? dit : nullptr, nullptr, dm,
-                                   crn_decode_ws_bytes(t->grid), r.st, CRN_VARIANT_MAXLOG, nullptr, 0, true);
+                                   crn_decode_ws_bytes(t->grid), r.st, kvariant, nullptr, 0, true);
             if (stages) cudaEventRecord(evk1[x], r.st);
             const bool packed = (const uint8_t *)q.crc_ok == (const uint8_t *)(q.out_bits + n_words) &&
                                 (!q.iters_used || q.iters_used == q.crc_ok + q.n_cb);

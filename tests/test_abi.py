@@ -163,7 +163,11 @@ def test_new_entry_points_validate_on_host():
                                  None) == crn.CRN_EINVAL                    # unknown flag bit
     tim = (crn.TtiTiming * 1)()
     grp = (crn.TtiGroup * 1)()
-    assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 8, tim) == crn.CRN_EINVAL   # unknown stream flag
+    assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 16, tim) == crn.CRN_EINVAL  # unknown stream flag
+    assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 3 << 8, tim) == crn.CRN_EINVAL   # shift without LLR8
+    assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 8 | (9 << 8), tim) == crn.CRN_EINVAL   # shift > 8
+    assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 8 | 1, tim) == crn.CRN_EINVAL    # int8 + merged
+    assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 8 | 4, tim) == crn.CRN_EINVAL    # int8 + zero copy
     assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 1, 5, tim) == crn.CRN_EINVAL   # merged + zero copy
     assert L.crn_stream_run_ex(grp, 1, 1, 1000.0, 8, 5, 0, tim) == crn.CRN_EINVAL   # unknown stopping rule
 

@@ -283,15 +283,23 @@ def test_plan_decode_host_pipeline(orc, n_chunks):
     p.close()
 
 
-@pytest.mark.parametrize("flags,packed", [(0, False), (0, True), (1, False), (2, True), (4, False), (6, True)])
+@pytest.mark.parametrize("flags,packed", [(0, False), (0, True), (1, False), (2, True), (4, False), (6, True),
+                                          (8, True), (8 | (3 << 8), False), (10 | (5 << 8), True)])
 def test_stream_run_cfg5(orc, flags, packed):
     """crn_stream_run_ex: paced TTIs of cfg5, one stream per cell group (per-group
-    decode launches, or one merged launch per TTI); every CB of every TTI
-    bit-exact against the oracle; timestamps ordered."""
+    decode launches, or one merged launch per TTI; int16 or -- CRN_STREAM_LLR8 --
+    int8 LLRs read as x * 2^shift); every CB of every TTI bit-exact against the
+    oracle (on the widened input for int8); timestamps ordered."""
+    import dataclasses
     n_tti, n_groups = 3, 4
+    llr8, sh = bool(flags & 8), (flags >> 8) & 0xF
     groups, checks = [], []
     for t in range(n_tti):
         b = _full(5, seed=100 + t)
+        src = b.llr
+        if llr8:
+            src = tuple(torch.clamp(torch.round(x.float() / (1 << sh)), -128, 127).to(torch.int8) for x in b.llr)
+            b = dataclasses.replace(b, llr=tuple(x.to(torch.int16) * (1 << sh) for x in src))
         r = run_oracle(b, np.arange(b.n_cb), 8, True)
         cells = np.unique(b.cb_cell)
         for gi in range(n_groups):
@@ -301,7 +309,7 @@ def test_stream_run_cfg5(orc, flags, packed):
             d["llr_off"] = np.concatenate([[0], np.cumsum(K + 4)[:-1]])
             d["bit_off"] = np.concatenate([[0], np.cumsum((K + 31) // 32)[:-1]])
             hl = [torch.cat([x[int(o):int(o) + int(k) + 4] for o, k in zip(b.desc["llr_off"][sel], K)]).cpu()
-                  .pin_memory() if sel.size else torch.zeros(1, dtype=torch.int16).pin_memory() for x in b.llr]
+                  .pin_memory() if sel.size else torch.zeros(1, dtype=x.dtype).pin_memory() for x in src]
             nw, nc = max(int(((K + 31) // 32).sum()), 1), max(sel.size, 1)
             if packed:                      # one host block: bits | crc_ok | iters_used
                 ob = torch.zeros(4 * nw + 2 * nc, dtype=torch.uint8).pin_memory()
