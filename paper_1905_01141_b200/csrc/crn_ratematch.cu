@@ -18,6 +18,8 @@
  *   matching: stage[rank(s, n)] = d_s[n], then e[k] = stage[k mod 3D].
  */
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <stdint.h>
 
 #include "crn_internal.h"
@@ -346,16 +348,25 @@ match_kernel(const crn_rm_desc *__restrict__ desc, const uint8_t *__restrict__ d
     }
 }
 
+/* the kernels' dynamic shared-memory attribute, set once per device (a bit per
+ * device id; the attribute is per device context) */
 template <class K>
-int rm_smem_attr(K kernel, int bytes) {                  /* once per process (one device per process) */
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess
-               ? CRN_OK : CRN_ECUDA;
+int rm_smem_attr(K kernel, int bytes, std::atomic<uint64_t> &done) {
+    int dev;
+    if (cudaGetDevice(&dev) != cudaSuccess) return CRN_ECUDA;
+    if (dev < 64 && ((done.load() >> dev) & 1u)) return CRN_OK;
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+        return CRN_ECUDA;
+    if (dev < 64) done.fetch_or(1ull << dev);
+    return CRN_OK;
 }
+
 }  // namespace
 
 extern "C" int crn_launch_dematch(const crn_rm_desc *d_desc, int32_t n_cb, const int16_t *e, int32_t combine,
                                   int16_t *h0, int16_t *h1, int16_t *h2, void *stream) {
-    static const int attr = rm_smem_attr(dematch_kernel, DM_SMEM);
+    static std::atomic<uint64_t> done{0};
+    const int attr = rm_smem_attr(dematch_kernel, DM_SMEM, done);
     if (attr) return attr;
     dematch_kernel<<<n_cb, RM_THREADS, DM_SMEM, (cudaStream_t)stream>>>(d_desc, e, combine, h0, h1, h2);
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
@@ -363,7 +374,8 @@ extern "C" int crn_launch_dematch(const crn_rm_desc *d_desc, int32_t n_cb, const
 
 extern "C" int crn_launch_match(const crn_rm_desc *d_desc, int32_t n_cb, const uint8_t *d0, const uint8_t *d1,
                                 const uint8_t *d2, uint8_t *e, void *stream) {
-    static const int attr = rm_smem_attr(match_kernel, MT_SMEM);
+    static std::atomic<uint64_t> done{0};
+    const int attr = rm_smem_attr(match_kernel, MT_SMEM, done);
     if (attr) return attr;
     match_kernel<<<n_cb, RM_THREADS, MT_SMEM, (cudaStream_t)stream>>>(d_desc, d0, d1, d2, e);
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
