@@ -40,11 +40,12 @@ def _dist():
     return ws, rank, local
 
 
-def _workload_name(iters, ws=1, scaling="weak"):
+def _workload_name(iters, ws=1, scaling="weak", cells=N_CELLS):
+    n = 256 * cells
     if scaling == "weak":
-        return (f"cfg4 per GPU: 65536 CBs (256 cells x 256 CBs) K=6144 on each of {ws} GPU(s), cells disjoint "
+        return (f"cfg4 per GPU: {n} CBs ({cells} cells x 256 CBs) K=6144 on each of {ws} GPU(s), cells disjoint "
                 f"across ranks, BPSK Eb/N0=1.0 dB, int16 LLR, {iters} fixed iterations")
-    return (f"cfg4: 65536 CBs (256 cells x 256) K=6144 sharded by cell over {ws} GPU(s), BPSK Eb/N0=1.0 dB, "
+    return (f"cfg4: {n} CBs ({cells} cells x 256) K=6144 sharded by cell over {ws} GPU(s), BPSK Eb/N0=1.0 dB, "
             f"int16 LLR, {iters} fixed iterations")
 
 
@@ -114,20 +115,26 @@ def _traffic():
 
 def _cpu_sample(n_sample, seed=0):
     """A bounded sample of the bench workload for the oracle: the first n_sample
-    CBs of cfg4 (cells 0.., 256 CBs per cell), inputs built by the oracle side."""
+    CBs of cfg4 (cells 0.., 256 CBs per cell), inputs built by the oracle side
+    (oracle CRC + encoder, the shared workload channel).  Generated on the GPU
+    when there is one, so the sample is byte-identical to the first n_sample
+    CBs of the batch the GPU arm times (the generators are per device type)."""
     from paper_1905_01141_b200 import workload as wlmod
     from tests._inputs import oracle_llrs, offsets
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
     per_cell = 256
-    cells = list(range((n_sample + per_cell - 1) // per_cell))
-    wl = wlmod.make_workload(CFG, seed=seed, cells=cells, device="cpu")
+    assert n_sample % per_cell == 0, "whole cells: a cell's channel noise is drawn for all its CBs at once"
+    cells = list(range(n_sample // per_cell))
+    wl = wlmod.make_workload(CFG, seed=seed, cells=cells, device=dev)
     wl.payload = wl.payload[:n_sample]
     wl.tbs, wl.tb_K, wl.tb_cell, wl.tb_ebn0_db = (wl.tbs[:n_sample], wl.tb_K[:n_sample],
                                                   wl.tb_cell[:n_sample], wl.tb_ebn0_db[:n_sample])
-    cbs, ll = oracle_llrs(wl)
+    cbs, ll = oracle_llrs(wl, device=dev)
     K = np.array([c["K"] for c in cbs], np.int32)
     lo, bo = offsets(K)
-    return dict(K=K, args=(K, np.zeros_like(K), np.full_like(K, 2), lo, bo, *(x.numpy() for x in ll)),
-                cells=cells, n=n_sample)
+    from paper_1905_01141_b200 import shard
+    return dict(K=K, args=(K, np.zeros_like(K), np.full_like(K, 2), lo, bo, *(x.cpu().numpy() for x in ll)),
+                cells=cells, n=n_sample, llr_sha=shard.sha256_tensors(ll), bo=bo)
 
 
 def cpu_baseline(sample, iters=8):
@@ -146,10 +153,67 @@ def cpu_baseline(sample, iters=8):
     dt = time.perf_counter() - t0
     bits = int((sample["K"] - 24).sum())
     c = sample["cells"]
+    r["bo"] = sample["bo"]
     return {"value": bits / dt / 1e6, "unit": "Mbit/s", "cores": cores, "kind": "oracle",
             "sample": f"{sample['n']} CBs of cfg4 (cells {c[0]}-{c[-1]}), {iters} fixed iterations, "
                       f"{dt:.2f} s wall x {cores} threads = {dt * cores:.1f} CPU-s (gcc -O2 scalar C)",
-            "ops": int(r["ops"]), "seconds": dt, "cpu_model": cpu_model}
+            "ops": int(r["ops"]), "seconds": dt, "cpu_model": cpu_model}, r
+
+
+# ---- self-check of the measured runs against the oracle (the cpu_baseline leg) ----
+# Each measured section records what it decoded: how to regenerate its inputs
+# on the oracle side, the SHA-256 of the product-built LLRs it fed the GPU and
+# the GPU's outputs.  The cpu_baseline leg then rebuilds the inputs with the
+# oracle's own CRC / segmentation / encoder, checks they are byte-identical,
+# decodes them with the oracle and counts CBs whose bits, crc_ok or iteration
+# count differ (bit-exactness on every config).
+_CHECKS = []
+
+
+def _record_check(name, cfg, seed, cells, b, words, ok, it, max_iters, et, idx=None, scale=1.0):
+    from paper_1905_01141_b200 import shard
+    _CHECKS.append(dict(name=name, cfg=cfg, seed=seed, cells=None if cells is None else list(cells), scale=scale,
+                        desc=b.desc.copy(), idx=np.arange(b.n_cb) if idx is None else np.asarray(idx),
+                        llr_sha=shard.sha256_tensors(b.llr),
+                        g=dict(words=np.array(words, copy=True).view(np.uint32), crc_ok=np.array(ok, copy=True),
+                               iters=None if it is None else np.array(it, copy=True)),
+                        max_iters=max_iters, et=et))
+
+
+def oracle_self_check(headline=None):
+    """-> {section: {checked, mismatches, inputs_identical}} for every recorded
+    measured run, plus the headline sample (oracle results already at hand)."""
+    import oracle
+    from paper_1905_01141_b200 import shard
+    from paper_1905_01141_b200 import workload as wlmod
+    from tests._gpu import count_mismatches
+    from tests._inputs import oracle_batch
+    out = {}
+    if headline is not None:
+        out["headline"] = headline
+    cores = len(os.sched_getaffinity(0))
+    for c in _CHECKS:
+        t0 = time.perf_counter()
+        wl = wlmod.make_workload(c["cfg"], seed=c["seed"], cells=c["cells"], device="cuda", scale=c["scale"])
+        ob = oracle_batch(wl)
+        same = shard.sha256_tensors(ob.llr) == c["llr_sha"] and np.array_equal(ob.desc, c["desc"])
+        idx = c["idx"]
+        d = ob.desc[idx]
+        K = d["K"].astype(np.int32)
+        lo = np.concatenate([[0], np.cumsum(K + 4)[:-1]]).astype(np.int64)
+        bo = np.concatenate([[0], np.cumsum(K)[:-1]]).astype(np.int64)
+        host = [x.cpu().numpy() for x in ob.llr]
+        ll = [np.concatenate([h[o:o + k + 4] for o, k in zip(d["llr_off"], K)]) for h in host]
+        r = oracle.decode_batch(K, d["F"], d["crc_kind"], lo, bo, *ll, max_iters=c["max_iters"], early_term=c["et"],
+                                nthreads=cores, want_ext=False)
+        r["bo"] = bo
+        mm = count_mismatches(c["desc"], c["g"], r, idx)
+        out[c["name"]] = {"checked": int(idx.size), "mismatches": mm, "inputs_identical": bool(same),
+                          "oracle_s": round(time.perf_counter() - t0, 1)}
+    out["total"] = {"checked": sum(v["checked"] for v in out.values()),
+                    "mismatches": sum(v["mismatches"] for v in out.values()),
+                    "inputs_identical": all(v["inputs_identical"] for v in out.values())}
+    return out
 
 
 def run_reference(args):
@@ -161,7 +225,7 @@ def run_reference(args):
         cpu_baseline(sample, args.iters)
     vals, times = [], []
     for _ in range(args.steps):
-        cb = cpu_baseline(sample, args.iters)
+        cb, _r = cpu_baseline(sample, args.iters)
         times.append(cb["seconds"])
         vals.append(cb["value"])
     v = statistics.median(vals)
@@ -178,16 +242,20 @@ def run_reference(args):
     return 0
 
 
-def run_pool(args, seed=0):
+def run_pool(args, seed=0, ws=1, rank=0, dist=None, red_dev="cpu", dev=None):
     """BASELINE cfg3: one TTI of a C-RAN pool -- 100 cells x 10 UEs, TBS ~ U{1000..75376},
     36.212 segmentation (fillers, CRC24A/B), QPSK Eb/N0 ~ U[0.5, 3] dB per UE, CRC ET at
     max 8 iterations.  Device-resident decode of the whole TTI (one launch) + device TB
-    verdicts, and the same TTI end to end from pinned host buffers (crn_plan_decode_host)."""
+    verdicts, and the same TTI end to end from pinned host buffers (crn_plan_decode_host).
+    With N ranks the 100 cells are split by cell (13/13/.../12 at N = 8, SURVEY.md §8(e));
+    the TTI's decode time is the max over ranks."""
     from paper_1905_01141_b200 import batch as bmod
     from paper_1905_01141_b200 import crn
+    from paper_1905_01141_b200 import shard
     from paper_1905_01141_b200 import workload as wlmod
     t_gen = time.perf_counter()
-    b = bmod.build(wlmod.make_workload(3, seed=seed, device="cuda"))
+    cells = shard.cells_for_rank(rank, ws, 100)
+    b = bmod.build(wlmod.make_workload(3, seed=seed, cells=cells, device="cuda"))
     t_gen = time.perf_counter() - t_gen
     plan = crn.Plan(b.desc)
     bits, ok, it, _ = bmod.outputs(b, want_ext=False)
@@ -205,6 +273,9 @@ def run_pool(args, seed=0):
     torch.cuda.synchronize()
     dec, ver = [], []
     for _ in range(10):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(st)
         plan.decode(*b.llr, 8, True, bits, ok, it, stream=st)
@@ -214,6 +285,36 @@ def run_pool(args, seed=0):
         torch.cuda.synchronize()
         dec.append(e0.elapsed_time(e1))
         ver.append(e1.elapsed_time(e2))
+    its = it[:b.n_cb].cpu().numpy()
+    ok_h = ok[:b.n_cb].cpu().numpy()
+    d_ms_local = statistics.median(dec)
+    ops_local = crn.counted_ops(b.K, 8, its)
+    c, d_ms = shard.reduce_counters([b.n_cb, int(ok_h.sum()), b.info_bits(), int(b.K.sum()), ops_local], d_ms_local,
+                                    dist, device=red_dev)
+    n_tb_ok = torch.tensor([int(tb_ok.sum()), b.wl.n_tb], dtype=torch.int64, device=red_dev)
+    if dist:
+        dist.all_reduce(n_tb_ok)
+    tb_loss = float(1.0 - n_tb_ok[0].item() / n_tb_ok[1].item())
+    dev = dev or crn.device_info()
+    roof = {"bound": "alu", "unit": "Tops/s (int16)", "achieved": ops_local / (d_ms_local * 1e-3) / 1e12,
+            "peak": _peak_alu(dev["num_sms"], dev["clock_khz"] / 1e3) / 1e12,
+            "ops_basis": "counted ops from each CB's executed iterations (iters_used): sum 2 x (129 K + 90) x iters"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    kpi = crn.kpi_iterations(its, ok_h, 8)
+    core = {"workload": "cfg3: 100 cells x 10 UEs, TBS ~ U{1000..75376}, 36.212 segmentation, QPSK Eb/N0 ~ "
+                        "U[0.5,3] dB per UE, CRC ET max 8 iterations, one TTI" +
+                        (f", cells split over {ws} ranks" if ws > 1 else ""),
+            "n_tb": int(n_tb_ok[1].item()), "n_cb": c["n_cb"], "sum_K": c["sum_k"], "info_bits": c["info_bits"],
+            "decode_ms": d_ms, "decoded_mbps": c["info_bits"] / (d_ms * 1e-3) / 1e6,
+            "tb_verdict_ms": statistics.median(ver), "tb_loss_rate": tb_loss,
+            "cb_crc_fail_rate": 1.0 - c["n_crc_ok"] / c["n_cb"], "roofline": roof,
+            "kpi_iters_hist": [int(x) for x in np.bincount(kpi, minlength=10)[1:10]],
+            "kpi_note": "PAPER.md:411 convention: bucket 9 (= max + 1) counts decoding failures"}
+    if ws > 1:
+        core["decode_ms_note"] = "max over ranks of each rank's median decode time of its cell shard"
+        core["ranks_cells"] = [cells[0], cells[-1]]
+        return core
+    _record_check("pool_tti", 3, seed, None, b, bits.cpu().numpy(), ok_h, its, 8, True)
     hl = [x.cpu().pin_memory() for x in b.llr]
     hb = torch.zeros(bits.numel(), dtype=torch.int32).pin_memory()
     hok = torch.zeros(ok.numel(), dtype=torch.uint8).pin_memory()
@@ -226,10 +327,8 @@ def run_pool(args, seed=0):
         plan.decode_host(*hl, 8, True, hb, hok, None, stream=st)
         st.synchronize()
         e2e.append(1e3 * (time.perf_counter() - t0))
-    its = it[:b.n_cb].cpu().numpy()
-    d_ms = statistics.median(dec)
-    tb_loss = float(1.0 - tb_ok.float().mean().item())
-    cb_fail = float(1.0 - ok[:b.n_cb].float().mean().item())
+    e2e_same = bool(np.array_equal(hok.numpy()[:b.n_cb], ok_h) and
+                    np.array_equal(hb.numpy().view(np.uint32)[:b.n_words], bits.cpu().numpy().view(np.uint32)[:b.n_words]))
     # the same TTI with int8 LLRs over PCIe (row f4, R31: saturated to [-128, 127], shift 0)
     clipped = sum(int((x.abs() > 127).sum()) for x in b.llr) / (3 * b.n_llr)
     h8 = [torch.clamp(x, -128, 127).to(torch.int8).cpu().pin_memory() for x in b.llr]
@@ -245,7 +344,8 @@ def run_pool(args, seed=0):
         st.synchronize()
         e2e8.append(1e3 * (time.perf_counter() - t0))
     int8 = {"e2e_ms": statistics.median(e2e8), "clipped_fraction": clipped,
-            "cb_crc_fail_rate": float(1.0 - hok[:b.n_cb].float().mean().item())}
+            "cb_crc_fail_rate": float(1.0 - hok[:b.n_cb].float().mean().item()),
+            "outputs_equal_int16_run": bool(clipped == 0 and np.array_equal(hok.numpy()[:b.n_cb], ok_h))}
     p8.close()
     del h8
     # row f1: the paper's purge on the same TTI -- a CB not yet started
@@ -297,18 +397,14 @@ def run_pool(args, seed=0):
                           "cb_crc_fail_rate": float(1.0 - ok[:b.n_cb].float().mean().item()),
                           "mean_iters": float(it[:b.n_cb].float().mean().item())}
         pv.close()
-    return {"workload": "cfg3: 100 cells x 10 UEs, TBS ~ U{1000..75376}, 36.212 segmentation, QPSK Eb/N0 ~ "
-                        "U[0.5,3] dB per UE, CRC ET max 8 iterations, one TTI",
-            "n_tb": int(b.wl.n_tb), "n_cb": b.n_cb, "sum_K": int(b.K.sum()), "info_bits": b.info_bits(),
-            "decode_ms": d_ms, "tb_verdict_ms": statistics.median(ver),
-            "decoded_mbps": b.info_bits() / (d_ms * 1e-3) / 1e6,
-            "e2e_ms": statistics.median(e2e), "e2e_path": "pinned host LLRs -> crn_plan_decode_host -> bits + crc_ok "
-                                                          "in pinned host memory (host clock, stream synced)",
-            "tb_loss_rate": tb_loss, "cb_crc_fail_rate": cb_fail,
-            "mean_iters": float(its.mean()),
-            "variants": variants, "purge": purge, "int8_ingest": int8,
-            "iters_hist": [int(x) for x in np.bincount(its, minlength=9)[1:9]],
-            "gen_s": round(t_gen, 1)}
+    core.update({"e2e_ms": statistics.median(e2e), "e2e_outputs_equal_device_run": e2e_same, "e2e_path": "pinned host LLRs -> crn_plan_decode_host -> "
+                                                               "bits + crc_ok in pinned host memory (host clock, "
+                                                               "stream synced)",
+                 "mean_iters": float(its.mean()),
+                 "variants": variants, "purge": purge, "int8_ingest": int8,
+                 "iters_hist": [int(x) for x in np.bincount(its, minlength=9)[1:9]],
+                 "gen_s": round(t_gen, 1)})
+    return core
 
 
 def run_dl_encode(b, reps=5):
@@ -399,6 +495,8 @@ def run_small_configs(seed=0):
             e1.record(st)
             torch.cuda.synchronize()
             ts.append(1e3 * e0.elapsed_time(e1))
+        _record_check(f"cfg{cfg}", cfg, seed, None, b, bits.cpu().numpy(), ok[:b.n_cb].cpu().numpy(),
+                      it[:b.n_cb].cpu().numpy(), wl.max_iters, wl.early_term)
         r = {"n_cb": b.n_cb, "K": sorted(set(int(k) for k in b.K)), "iters": wl.max_iters,
              "early_term": bool(wl.early_term), "device_us_p50": float(np.percentile(ts, 50)),
              "device_us_p99": float(np.percentile(ts, 99)), "crc_ok": int(ok[:b.n_cb].sum()),
@@ -425,10 +523,12 @@ def run_latency(args, seed=0):
     from paper_1905_01141_b200 import workload as wlmod
     n_groups, cells_per_tti = args.lat_groups, 20
     t_gen = time.perf_counter()
-    distinct = []
+    distinct, batches = [], []
     for t in range(args.lat_distinct):
         wl = wlmod.make_workload(5, seed=seed, cells=range(cells_per_tti * t, cells_per_tti * (t + 1)), device="cuda")
         b = bmod.build(wl)
+        if t < args.lat_check:
+            batches.append(b)
         grp = []
         for gi in range(n_groups):
             sel = np.flatnonzero(((b.cb_cell % cells_per_tti) // (cells_per_tti // n_groups)) == gi)
@@ -446,7 +546,7 @@ def run_latency(args, seed=0):
             nw = max(int(((K + 31) // 32).sum()), 1)
             nc = max(sel.size, 1)
             ob = torch.zeros(4 * nw + 2 * nc, dtype=torch.uint8).pin_memory()   # bits | crc_ok | iters: one download
-            grp.append(dict(desc=d, l0=hl[0], l1=hl[1], l2=hl[2],
+            grp.append(dict(desc=d, l0=hl[0], l1=hl[1], l2=hl[2], sel=sel,
                             bits=ob[:4 * nw].view(torch.int32), ok=ob[4 * nw:4 * nw + nc],
                             it=ob[4 * nw + nc:4 * nw + 2 * nc],
                             sum_k=int(K.sum()), n_cb=int(sel.size), info=int((d["K"] - d["F"] - 24).sum()),
@@ -456,6 +556,7 @@ def run_latency(args, seed=0):
     groups = [g for t in range(args.lat_ttis) for g in distinct[t % args.lat_distinct]]
     zflag = crn.STREAM_ZEROCOPY if os.environ.get("CRN_LAT_ZEROCOPY") == "1" else 0
     tim = crn.stream_run(groups, args.lat_ttis, n_groups, 1000.0, 8, True, flags=zflag)
+    snap = [[(g["bits"].numpy().copy(), g["ok"].numpy().copy(), g["it"].numpy().copy()) for g in grp] for grp in distinct]
     skip = min(10, args.lat_ttis // 10)
     lat, dev = tim["latency_us"][skip:], tim["device_us"][skip:]
     sub = (tim["submitted_us"] - tim["release_us"])[skip:]
@@ -471,10 +572,32 @@ def run_latency(args, seed=0):
     groups8 = [dict(g, l0=g["l8"][0], l1=g["l8"][1], l2=g["l8"][2]) for g in groups]
     tim8 = crn.stream_run(groups8, args.lat_ttis, n_groups, 1000.0, 8, True, flags=crn.STREAM_LLR8)
     lat8 = tim8["latency_us"][skip:]
+    diff8 = sum(int(np.sum((g["ok"].numpy() != o) | (g["it"].numpy() != i))) +
+                int(not np.array_equal(g["bits"].numpy(), w))
+                for grp, sgrp in zip(distinct, snap) for g, (w, o, i) in zip(grp, sgrp))
+    # oracle self-check of the first lat_check distinct TTIs (the int16 run's outputs, back in
+    # each TTI's own layout)
+    for t in range(min(args.lat_check, len(distinct))):
+        bt = batches[t]
+        words = np.zeros(max(bt.n_words, 1), np.uint32)
+        okt = np.zeros(bt.n_cb, np.uint8)
+        itt = np.zeros(bt.n_cb, np.uint8)
+        for g, (w, o, i) in zip(distinct[t], snap[t]):
+            wv = w.view(np.uint32)
+            for m, cb in enumerate(g["sel"]):
+                k = int(bt.desc["K"][cb])
+                n = (k + 31) // 32
+                words[bt.desc["bit_off"][cb]:bt.desc["bit_off"][cb] + n] = wv[g["desc"]["bit_off"][m]:
+                                                                           g["desc"]["bit_off"][m] + n]
+            okt[g["sel"]] = o
+            itt[g["sel"]] = i
+        _record_check(f"latency_tti{t}", 5, seed, range(cells_per_tti * t, cells_per_tti * (t + 1)), bt, words, okt,
+                      itt, 8, True)
     clipped = sum(g["clip8"] for grp in distinct for g in grp) / max(1, sum(g["n_llr3"] for grp in distinct for g in grp))
     int8 = {"p50_us": float(np.percentile(lat8, 50)), "p99_us": float(np.percentile(lat8, 99)),
             "device_p50_us": float(np.percentile(tim8["device_us"][skip:], 50)), "clipped_fraction": clipped,
-            "note": "same TTIs, int16 LLRs saturated to int8 (CRN_STREAM_LLR8): half the upload bytes"}
+            "note": "same TTIs, int16 LLRs saturated to int8 (CRN_STREAM_LLR8): half the upload bytes",
+            "cbs_differing_from_int16_run": diff8}
     return {"workload": "cfg5: 1 ms TTIs of 200 CBs (20 cells x 10), K ~ U(188 sizes), QPSK Eb/N0 ~ U[0.5,3] dB "
                         f"per CB, CRC24B ET max 8 iterations, {n_groups} cell groups = {n_groups} CUDA streams each with its own "
                         "upload / decode launch / download, host buffers in/out (crn_stream_run)",
@@ -488,6 +611,48 @@ def run_latency(args, seed=0):
             "mean_iters": float(its.mean()), "mean_sum_k_per_tti": float(np.mean(sum_k)),
             "gen_s": round(t_gen, 1),
             "latency": "release (pacer) -> last group's results in pinned host memory (completion thread)"}
+
+
+def _measure(plan, llr, iters, bits, ok, steps, warmup, dist, local, stream):
+    """W untimed steps, then K timed steps bracketed by a barrier + synchronize,
+    CUDA events on the launching stream; -> (total ms, per-launch ms, clocks)."""
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(warmup):
+        plan.decode(*llr, iters, False, bits, ok, None, None, stream=stream)
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    clk = ClockSampler(local).start()
+    t_all0 = torch.cuda.Event(enable_timing=True)
+    t_all1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.nvtx.range_push("timed")
+    t_all0.record(stream)
+    for k in range(steps):
+        ev[k][0].record(stream)
+        plan.decode(*llr, iters, False, bits, ok, None, None, stream=stream)
+        ev[k][1].record(stream)
+    t_all1.record(stream)
+    barrier()
+    torch.cuda.nvtx.range_pop()
+    clocks = clk.stop()
+    return t_all0.elapsed_time(t_all1), [a.elapsed_time(z) for a, z in ev], clocks
+
+
+def _roofline(ops_per_launch, mean_launch_ms, dev, clocks):
+    mhz = dev["clock_khz"] / 1e3
+    peak = _peak_alu(dev["num_sms"], mhz)
+    achieved = ops_per_launch / (mean_launch_ms * 1e-3)
+    return {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tops/s (int16)",
+            "frac": achieved / peak, "traffic": _traffic(),
+            "peak_basis": f"{dev['num_sms']} SMs x 64 lanes/clk x 4 int16 ops/lane-instr x {mhz:.0f} MHz "
+                          f"(sm max clock); counted ops = 2 x (129 K + 90) per CB-iteration",
+            "algorithmic_ops_per_launch": ops_per_launch,
+            "frac_at_median_clock": (achieved / _peak_alu(dev["num_sms"], clocks["sm_mhz"]))
+            if clocks.get("sm_mhz") else None}
 
 
 def run_crn(args):
@@ -515,62 +680,96 @@ def run_crn(args):
             dist.init_process_group("gloo")
     crn_build.build()
     dev = crn.device_info()
+    n_cells = args.cells
+    iters = args.iters
+    stream = torch.cuda.current_stream()
 
-    if args.scaling == "weak":      # DESIGN.md R27: every rank serves its own 256 cells (a full cfg4 batch)
-        cells = list(range(rank * N_CELLS, (rank + 1) * N_CELLS))
-    else:                           # cfg4's fixed 256 cells split over the ranks
-        cells = shard.cells_for_rank(rank, ws, N_CELLS)
+    # ---- weak scaling (the headline, R27): every rank serves its own
+    # n_cells cells, a full cfg4 batch per GPU (cells disjoint across ranks)
+    cells = list(range(rank * n_cells, (rank + 1) * n_cells))
     wl = wlmod.make_workload(CFG, seed=args.seed, cells=cells, device="cuda")
     b = bmod.build(wl)
     del wl.payload
-    iters = args.iters
     plan = crn.Plan(b.desc)
     bits, ok, it, _ = bmod.outputs(b, want_ext=False)
-    stream = torch.cuda.current_stream()
     l0, l1, l2 = b.llr
     in_bytes = 3 * 2 * b.n_llr
+    ms_total, launch_ms, clocks = _measure(plan, b.llr, iters, bits, ok, args.steps, args.warmup, dist, local, stream)
 
-    def step():
-        plan.decode(l0, l1, l2, iters, False, bits, ok, None, None, stream=stream)
-
-    def barrier():
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    for _ in range(args.warmup):
-        step()
-    barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    clk = ClockSampler(local).start()
-    t_all0 = torch.cuda.Event(enable_timing=True)
-    t_all1 = torch.cuda.Event(enable_timing=True)
-    barrier()
-    torch.cuda.nvtx.range_push("timed")
-    t_all0.record(stream)
-    for k in range(args.steps):
-        ev[k][0].record(stream)
-        step()
-        ev[k][1].record(stream)
-    t_all1.record(stream)
-    barrier()
-    torch.cuda.nvtx.range_pop()
-    clocks = clk.stop()
-    ms_total = t_all0.elapsed_time(t_all1)
-    launch_ms = [a.elapsed_time(z) for a, z in ev]
-
-    # outputs of the last step: counters (one NCCL reduction, DESIGN.md multi-GPU)
+    # outputs of the last step: counters (one reduction, DESIGN.md multi-GPU), digests
     n_ok_local = int(ok[:b.n_cb].to(torch.int64).sum().item())
     c, tmax = shard.reduce_counters([b.n_cb, n_ok_local, b.info_bits(), int(b.K.sum()),
                                      crn.counted_ops(b.K, iters)], ms_total, dist, device=red_dev)
     n_cb, n_ok, info_bits, sum_k, ops = (c[k] for k in shard.COUNTERS)
     ms_step = tmax / args.steps
     value = info_bits / (ms_step * 1e-3) / 1e6
+    words_h = bits.cpu().numpy().view(np.uint32)
+    ok_h = ok[:b.n_cb].cpu().numpy()
+    weak_cells = shard.gather_digests(shard.cell_digests(b.desc, b.cb_cell, words_h, ok_h), dist)
+    my_digest = {"rank": rank, "cells": [cells[0], cells[-1]], "n_cb": b.n_cb,
+                 "inputs_sha256": shard.sha256_tensors(b.llr),
+                 "outputs_sha256": shard.sha256_tensors([bits[:b.n_words], ok[:b.n_cb]])}
+    head_out = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        n = args.ref_sample                             # the oracle sample = this batch's first n CBs
+        head_out = dict(words=words_h.copy(), crc_ok=ok_h.copy(), llr_sha=shard.sha256_tensors(
+            [x[:int(b.desc["llr_off"][n - 1]) + int(b.desc["K"][n - 1]) + 4] for x in b.llr]))
+
+    # ---- strong scaling (BASELINE cfg4 as written): cfg4's n_cells cells split over the ranks
+    strong = None
+    s_cells = shard.cells_for_rank(rank, ws, n_cells)
+    if ws == 1:
+        strong = {"same_as_weak_at_n1": True, "value": value, "ms_per_step": ms_step, "cells_sha256":
+                  shard.combined_digest(weak_cells)}
+        strong_cells = weak_cells
+    else:
+        del plan
+        wl_s = wlmod.make_workload(CFG, seed=args.seed, cells=s_cells, device="cuda")
+        bs = bmod.build(wl_s)
+        del wl_s.payload
+        plan_s = crn.Plan(bs.desc)
+        bits_s, ok_s, _, _ = bmod.outputs(bs, want_ext=False)
+        ms_s, launch_s, clocks_s = _measure(plan_s, bs.llr, iters, bits_s, ok_s, args.steps, args.warmup, dist,
+                                            local, stream)
+        cs, tmax_s = shard.reduce_counters([bs.n_cb, int(ok_s[:bs.n_cb].to(torch.int64).sum().item()),
+                                            bs.info_bits(), int(bs.K.sum()), crn.counted_ops(bs.K, iters)],
+                                           ms_s, dist, device=red_dev)
+        strong_cells = shard.gather_digests(shard.cell_digests(bs.desc, bs.cb_cell, bits_s.cpu().numpy(),
+                                                               ok_s[:bs.n_cb].cpu().numpy()), dist)
+        ms_step_s = tmax_s / args.steps
+        strong = {"value": cs["info_bits"] / (ms_step_s * 1e-3) / 1e6, "unit": "Mbit/s", "ms_per_step": ms_step_s,
+                  "n_cb": cs["n_cb"], "crc_ok": cs["n_crc_ok"], "cb_per_rank": bs.n_cb,
+                  "roofline": _roofline(crn.counted_ops(bs.K, iters), statistics.mean(launch_s), dev, clocks_s),
+                  "clocks": clocks_s, "cells_sha256": shard.combined_digest(strong_cells)}
+        del plan_s, bs, bits_s, ok_s
+        plan = crn.Plan(b.desc)
+    if strong is not None:
+        strong["workload"] = _workload_name(iters, ws, "strong", n_cells)
+    if args.digest_out and rank == 0:
+        with open(args.digest_out, "w") as f:
+            json.dump({"n_gpus": ws, "weak": weak_cells, "strong": strong_cells}, f)
+    digests = [my_digest]
+    if dist:
+        digests = [None] * ws
+        dist.all_gather_object(digests, my_digest)
+
+    # ---- cfg3 pool TTI sharded by cell over the ranks (100 cells -> 13/13/.../12 at N=8)
+    pool = None
+    if not args.no_pool:
+        try:
+            pool = run_pool(args, seed=args.seed, ws=ws, rank=rank, dist=dist, red_dev=red_dev, dev=dev)
+        except Exception as e:
+            pool = {"error": repr(e)}
 
     # ---- e2e: pinned host LLRs -> crn_plan_decode_host (chunked upload / decode /
     # download overlap inside libcrn) -> packed bits + crc_ok in pinned host memory
     e2e = None
     if not args.no_e2e:
+        def barrier():
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+
         host = [x.cpu().pin_memory() for x in b.llr]
         hb = torch.empty(bits.numel(), dtype=bits.dtype).pin_memory()
         hok = torch.empty(ok.numel(), dtype=ok.dtype).pin_memory()
@@ -593,9 +792,12 @@ def run_crn(args):
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         n_ok_host = int(hok[:b.n_cb].to(torch.int64).sum())
+        same_host = bool(np.array_equal(hb.numpy().view(np.uint32)[:b.n_words], words_h[:b.n_words]) and
+                         np.array_equal(hok.numpy()[:b.n_cb], ok_h))
         e2e = {"value": info_bits / (te.item() * 1e-3) / 1e6, "unit": "Mbit/s",
                "h2d_bytes_per_step": in_bytes * ws, "d2h_bytes_per_step": (b.n_words * 4 + b.n_cb) * ws,
                "ms_per_step": te.item(), "chunks": plan.chunks, "crc_ok_host": n_ok_host,
+               "outputs_equal_device_run": same_host,
                "path": "pinned host LLRs -> crn_plan_decode_host (chunked H2D / decode / D2H overlap) -> "
                        "packed bits + crc_ok in pinned host memory"}
         del host
@@ -633,6 +835,9 @@ def run_crn(args):
             "h2d_bytes_per_step": in_bytes // 2 * ws, "d2h_bytes_per_step": (b.n_words * 4 + b.n_cb) * ws,
             "llr_format": f"int8, read as x * 2^{sh}", "crc_ok_host": int(hok8[:b.n_cb].to(torch.int64).sum()),
             "clipped_fraction": clipped,
+            "outputs_equal_int16_run": bool(clipped == 0 and np.array_equal(hok8.numpy()[:b.n_cb], ok_h) and
+                                            np.array_equal(hb.numpy().view(np.uint32)[:b.n_words],
+                                                           words_h[:b.n_words])),
             "note": "same CBs, int16 LLRs saturated to int8 (the int16 e2e above decodes the unsaturated input)"}
         del host8, plan8
 
@@ -641,31 +846,30 @@ def run_crn(args):
             dist.destroy_process_group()
         return 0
     mean_launch_ms = statistics.mean(launch_ms)
-    local_ops = crn.counted_ops(b.K, iters)
-    mhz = dev["clock_khz"] / 1e3
-    peak = _peak_alu(dev["num_sms"], mhz)
-    achieved = local_ops / (mean_launch_ms * 1e-3)
-    roof = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tops/s (int16)",
-            "frac": achieved / peak, "traffic": _traffic(),
-            "peak_basis": f"{dev['num_sms']} SMs x 64 lanes/clk x 4 int16 ops/lane-instr x {mhz:.0f} MHz "
-                          f"(sm max clock); counted ops = 2 x (129 K + 90) per CB-iteration",
-            "algorithmic_ops_per_launch": local_ops,
-            "frac_at_median_clock": (achieved / _peak_alu(dev["num_sms"], clocks["sm_mhz"]))
-            if clocks.get("sm_mhz") else None}
+    roof = _roofline(crn.counted_ops(b.K, iters), mean_launch_ms, dev, clocks)
+    kpi = crn.kpi_iterations(np.full(b.n_cb, iters, np.uint8), ok_h, iters)
     out = {
         "metric": METRIC, "value": value, "unit": "Mbit/s", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int16", "data": "synthetic",
-        "config": {"workload": _workload_name(iters, ws, args.scaling), "n_cb": n_cb, "cb_per_rank": b.n_cb,
+        "config": {"workload": _workload_name(iters, ws, "weak", n_cells), "n_cb": n_cb, "cb_per_rank": b.n_cb,
                    "iters": iters, "seed": args.seed,
                    "l2": f"inputs {in_bytes / 1e9:.2f} GB per rank > L2 {L2_BYTES / 2**20:.0f} MiB: no flush needed",
                    "parallelism": f"dp{ws} (cells sharded, no data-path collective)",
-                   "info_bits_per_step": info_bits, "sum_K": sum_k, "crc_ok": n_ok},
+                   "info_bits_per_step": info_bits, "sum_K": sum_k, "crc_ok": n_ok,
+                   "kpi_failures": int((kpi > iters).sum())},
         "roofline": roof, "clocks": clocks, "gpu_launches": args.steps * plan.launches,
         "gpu_launches_note": "one persistent decode_kernel launch per step (+1 cudaMemsetAsync of the task counter)",
         "e2e": e2e, "kernel_ms_mean": mean_launch_ms, "kernel_ms": launch_ms,
         "sum_k_mbps": sum_k / (ms_step * 1e-3) / 1e6,
+        "strong": strong,
+        "digests": {"per_rank": digests, "weak_cells_sha256": shard.combined_digest(weak_cells),
+                    "note": "per rank: SHA-256 of its input LLRs (l0|l1|l2) and of its last step's outputs "
+                            "(out_bits|crc_ok); *_cells_sha256: one digest over every cell's outputs, equal "
+                            "for any rank count that decodes the same cells"},
     }
+    if pool is not None:
+        out["pool_tti"] = pool
     if share and ws > 1:
         out["functional_check_only"] = f"{ws} ranks shared one GPU over {args.dist_backend}: not a measurement"
     if not args.no_latency and ws == 1:
@@ -683,16 +887,24 @@ def run_crn(args):
             out["small_configs"] = run_small_configs(seed=args.seed)
         except Exception as e:
             out["small_configs"] = {"error": repr(e)}
-    if not args.no_pool and ws == 1:
-        try:
-            out["pool_tti"] = run_pool(args, seed=args.seed)
-        except Exception as e:
-            out["pool_tti"] = {"error": repr(e)}
     if not args.no_cpu_baseline and ws == 1:          # rank 0 at N = 1 only
         try:
-            out["cpu_baseline"] = cpu_baseline(_cpu_sample(args.ref_sample, args.seed), iters)
+            sample = _cpu_sample(args.ref_sample, args.seed)
+            cb, r = cpu_baseline(sample, iters)
+            out["cpu_baseline"] = cb
+            from tests._gpu import count_mismatches
+            n = args.ref_sample
+            head = {"checked": n, "inputs_identical": sample["llr_sha"] == head_out["llr_sha"],
+                    "mismatches": count_mismatches(b.desc, dict(words=head_out["words"], crc_ok=head_out["crc_ok"],
+                                                                iters=None), r, np.arange(n))}
+            out["parity"] = oracle_self_check(head)
+            out["parity"]["what"] = ("GPU outputs of the measured runs (packed bits, crc_ok, iteration counts) "
+                                     "against the oracle decoding the same inputs rebuilt by the oracle's own "
+                                     "CRC / segmentation / encoder (SHA-256 of the LLRs compared): headline = "
+                                     "the first CBs of the timed cfg4 batch")
         except Exception as e:           # the GPU number stands without it
-            out["cpu_baseline"] = {"error": repr(e)}
+            out.setdefault("cpu_baseline", {"error": repr(e)})
+            out["parity"] = {"error": repr(e)}
     print(json.dumps(out), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -707,13 +919,17 @@ def main():
     ap.add_argument("--impl", default="crn", choices=["crn", "reference"])
     ap.add_argument("--iters", type=int, default=8)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: each rank decodes its own full cfg4 batch (default); strong: cfg4 split over ranks")
+                    help="label of the reference arm's line (the GPU arm reports weak and strong in one run)")
+    ap.add_argument("--cells", type=int, default=N_CELLS,
+                    help="cells of 256 CBs per cfg4 batch (default 256 = BASELINE cfg4; smaller for tests)")
+    ap.add_argument("--digest-out", default=None, help="write the per-cell output digests (JSON) on rank 0")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ref-sample", type=int, default=2048,
                     help="CBs of the oracle's bounded sample (cpu_baseline / --impl reference)")
     ap.add_argument("--lat-ttis", type=int, default=1000)
     ap.add_argument("--lat-distinct", type=int, default=100)
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--lat-check", type=int, default=10, help="distinct latency TTIs checked against the oracle")
     ap.add_argument("--lat-groups", type=int, default=2, choices=[1, 2, 4, 5, 10, 20],
                     help="cell groups (CUDA streams) of the cfg5 latency run")
     ap.add_argument("--no-pool", action="store_true", help="skip the cfg3 one-TTI pool measurement")

@@ -177,7 +177,10 @@ void crn_plan_destroy(void *plan);
  * Asynchronous: every step is ordered after prior work on cuda_stream and
  * cuda_stream waits for the last download, so synchronising cuda_stream makes
  * the host outputs valid.  The plan owns the device staging buffers (sized
- * once, on the first call).  Errors as crn_plan_decode, CRN_EINVAL for
+ * once, on the first call).  Output contract: each chunk's words come back as
+ * one span [min bit_off, max bit_off + ceil(K/32)) of its CBs, so host words in
+ * gaps between CBs' ranges inside a span are overwritten with 0 (crn_plan_decode
+ * writes only each CB's own words).  Errors as crn_plan_decode, CRN_EINVAL for
  * n_chunks outside [0, 64]; ext_out is not offered on this path. */
 int crn_plan_decode_host(void *plan, const int16_t *h_llr_sys, const int16_t *h_llr_p1,
                          const int16_t *h_llr_p2, int32_t max_iters, int32_t early_term,
@@ -257,6 +260,15 @@ int crn_stream_run_ex(const crn_tti_group *groups, int32_t n_tti, int32_t n_grou
  * fixed-iteration batch pass iters_used = NULL and it uses max_iters. */
 int64_t crn_counted_ops(const int32_t *K_host, int32_t n_cb, const uint8_t *iters_used_host,
                         int32_t max_iters);
+
+/* The paper's iteration KPI ("Performance captor": the captor
+ * records "the number of iterations carried out by the decoder per CB", and
+ * "decoding failures are detected when a value greater than the maximum
+ * number of allowed iterations is registered"): out[i] = iters_used[i] if
+ * crc_ok[i], else max_iters + 1 (R17).  HOST arrays of n entries;
+ * CRN_EINVAL for n < 0, a NULL array or max_iters outside [1, 32]. */
+int crn_kpi_iterations(const uint8_t *iters_used, const uint8_t *crc_ok, int32_t n, int32_t max_iters,
+                       uint8_t *out);
 
 /* ------------------------------------------------------------------ encode (DL) */
 

@@ -27,27 +27,33 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, so: str | None = None, defines=()) -> str:
+    """Compile libcrn.so (or, for profiling / A-B experiments, ``so`` with extra
+    ``-D`` defines, e.g. CRN_PHASE_PROF; never the product library)."""
+    if so is None and not force and not _stale():
         return SO
     from concurrent.futures import ThreadPoolExecutor
-    bdir = os.path.join(HERE, "build")
+    target = SO if so is None else so
+    bdir = os.path.join(HERE, "build" if so is None else "build_" + os.path.basename(so).replace(".so", ""))
     os.makedirs(bdir, exist_ok=True)
     cmds, objs = [], []
     for s in SOURCES:
         o = os.path.join(bdir, s + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, s), "-o", o]
+        cmd = [NVCC, *ARCH, *FLAGS, *(f"-D{d}" for d in defines), "-c", os.path.join(CSRC, s), "-o", o]
         if verbose and s.endswith(".cu"):
             cmd.insert(1, "-Xptxas=-v")
         cmds.append(cmd)
         objs.append(o)
     with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:   # independent units
         list(ex.map(subprocess.check_call, cmds))
-    tmp = SO + ".tmp"
+    tmp = target + ".tmp"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs])
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--prof" in sys.argv:            # phase-profiler build (tools/phase_prof.py): libcrn_prof.so
+        print(build(so=os.path.join(HERE, "libcrn_prof.so"), defines=("CRN_PHASE_PROF",)))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

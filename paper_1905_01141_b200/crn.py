@@ -71,6 +71,7 @@ _SIGS = {
     "crn_stream_run_ex": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_int32, vp]),
     "crn_plan_destroy": (None, [vp]),
     "crn_counted_ops": (C.c_int64, [i32p, C.c_int32, u8p, C.c_int32]),
+    "crn_kpi_iterations": (C.c_int, [u8p, u8p, C.c_int32, C.c_int32, u8p]),
     "crn_encode_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp]),
     "crn_tb_build_cbs": (C.c_int, [u8p, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_int64, u8p, vp,
                                    i32p]),
@@ -254,14 +255,25 @@ def stream_run(groups, n_tti: int, n_groups: int, period_us: float, max_iters: i
     """crn_stream_run.  groups: list (length n_tti * n_groups, TTI-major) of dicts with
     HOST arrays desc (numpy DESC_DTYPE), l0/l1/l2 (int16 tensors, pinned), bits (int32 tensor),
     ok (uint8 tensor), it (uint8 tensor or None).  Returns a numpy structured array of timings."""
+    import torch
     arr = (TtiGroup * len(groups))()
     keep = []
+    want = torch.int8 if flags & STREAM_LLR8 else torch.int16
     for x, g in enumerate(groups):
         d = np.ascontiguousarray(g["desc"], DESC_DTYPE)
         keep.append(d)
         for k in ("l0", "l1", "l2", "bits", "ok", "it"):
             if g.get(k) is not None and g[k].is_cuda:
                 raise CrnError("crn_stream_run takes host buffers")
+        # the runtime copies n_llr elements of the flag's width from each stream
+        for k in ("l0", "l1", "l2"):
+            if g[k].dtype != want:
+                raise CrnError(f"group {x}: LLR tensors must be {want} for these flags, got {g[k].dtype}")
+        if not (g["l0"].numel() == g["l1"].numel() == g["l2"].numel()):
+            raise CrnError(f"group {x}: the three LLR streams differ in length")
+        if g["bits"].dtype != torch.int32 or g["ok"].dtype != torch.uint8 or \
+                (g.get("it") is not None and g["it"].dtype != torch.uint8):
+            raise CrnError(f"group {x}: bits must be int32, ok / it uint8")
         arr[x] = TtiGroup(d.ctypes.data if d.size else None, d.size, 0, _ptr(g["l0"]), _ptr(g["l1"]),
                           _ptr(g["l2"]), g["l0"].numel(), _ptr(g["bits"]), g["bits"].numel(), _ptr(g["ok"]),
                           _ptr(g.get("it")))
@@ -280,6 +292,18 @@ def counted_ops(K, max_iters: int, iters_used=None) -> int:
     it = None if iters_used is None else np.ascontiguousarray(iters_used, np.uint8)
     return int(lib().crn_counted_ops(_np(Kh, C.c_int32), Kh.size, None if it is None else _np(it, C.c_uint8),
                                      max_iters))
+
+
+def kpi_iterations(iters_used, crc_ok, max_iters: int) -> np.ndarray:
+    """crn_kpi_iterations: the paper's per-CB iteration KPI (failures -> max_iters + 1)."""
+    it = np.ascontiguousarray(iters_used, np.uint8)
+    ok = np.ascontiguousarray(crc_ok, np.uint8)
+    if it.size != ok.size:
+        raise CrnError("iters_used and crc_ok differ in length")
+    out = np.zeros(it.size, np.uint8)
+    _chk(lib().crn_kpi_iterations(_np(it, C.c_uint8), _np(ok, C.c_uint8), it.size, max_iters, _np(out, C.c_uint8)),
+         "crn_kpi_iterations")
+    return out
 
 
 # ------------------------------------------------------------------ encode / TB helpers

@@ -135,6 +135,13 @@ extern "C" int64_t crn_counted_ops(const int32_t *K, int32_t n_cb, const uint8_t
     return s;
 }
 
+extern "C" int crn_kpi_iterations(const uint8_t *it, const uint8_t *ok, int32_t n, int32_t max_iters, uint8_t *out) {
+    /* a failure registers a value greater than the maximum (R17) */
+    if (n < 0 || max_iters < 1 || max_iters > CRN_MAX_ITERS || (n > 0 && (!it || !ok || !out))) return CRN_EINVAL;
+    for (int i = 0; i < n; i++) out[i] = ok[i] ? it[i] : (uint8_t)(max_iters + 1);
+    return CRN_OK;
+}
+
 /* ------------------------------------------------------------------ MI stopping rule */
 /* Log-MAP correction (R32): LUT[b] = round(8 ln(1 + e^(-(4b+1.5)/8))),
  * b = min(|a-b| >> 2, 7), packed as the eight bytes the kernel's PRMT selects
@@ -286,6 +293,12 @@ int crn_get_ctx(int *dev, DevTables **t) {
 
 int crn_get_ws(int dev, void *stream, size_t bytes, void **ws) {
     std::lock_guard<std::mutex> lk(g_mu);
+    /* cudaStreamPerThread names a different stream on every host thread: key its
+     * workspace by the calling thread, so two threads' concurrently running
+     * persistent kernels never share a task counter (the legacy default stream is
+     * one stream shared by all threads, whose launches serialise: one key) */
+    static thread_local char per_thread_tag;
+    if (stream == (void *)cudaStreamPerThread) stream = (void *)&per_thread_tag;
     auto key = std::make_pair(dev, stream);
     auto it = g_ws.find(key);
     if (it != g_ws.end() && it->second.second >= bytes) { *ws = it->second.first; return CRN_OK; }

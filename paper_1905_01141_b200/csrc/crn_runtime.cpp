@@ -132,6 +132,9 @@ static int pipe_build(Plan *P, int n_chunks, HostPipe **out) {
     p->d_bits = (uint32_t *)(m + o_b);
     p->d_ok = m + o_ok;
     p->d_it = m + o_it;
+    /* output staging starts zeroed: the chunks' downloads copy whole word spans,
+     * so host words in gaps between CBs' bit_off ranges come back as 0 (crn.h) */
+    cudaMemset(p->d_bits, 0, 4 * (size_t)p->n_words);
     cudaMemcpy(p->d_tasks, tasks.data(), bt, cudaMemcpyHostToDevice);
     cudaMemcpy(p->d_pairs, pairs.data(), bp, cudaMemcpyHostToDevice);
     cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking);

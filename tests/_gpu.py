@@ -41,7 +41,66 @@ def run_oracle(b, idx, max_iters, et, variant=0):
 
 
 def assert_parity(b, g, r, idx):
+    """Element-by-element comparison of the GPU outputs g (words at desc.bit_off,
+    crc_ok / iters per CB, ext at desc.ext_off) with the oracle's r for the CBs
+    idx (r in idx order).  Equal-K groups are compared vectorised."""
     desc = b.desc
+    idx = np.asarray(idx)
+    if idx.size > 64:
+        _assert_parity_vec(desc, g, r, idx)
+        return
+    _assert_parity_loop(desc, g, r, idx)
+
+
+def _assert_parity_vec(desc, g, r, idx, chunk=1024):
+    K = desc["K"][idx].astype(np.int64)
+    okg, ito = g["crc_ok"][idx], g["iters"][idx]
+    bad = np.flatnonzero(okg != r["crc_ok"])
+    assert bad.size == 0, f"crc_ok differs at CBs {idx[bad[:8]]}"
+    bad = np.flatnonzero(ito != r["iters"])
+    assert bad.size == 0, f"iters differ at CBs {idx[bad[:8]]}: {ito[bad[:4]]} vs {r['iters'][bad[:4]]}"
+    words = g["words"].view(np.uint32)
+    for k in np.unique(K):
+        sel = np.flatnonzero(K == k)
+        nw = (int(k) + 31) // 32
+        for c0 in range(0, sel.size, chunk):
+            s = sel[c0:c0 + chunk]
+            wo = desc["bit_off"][idx[s]].astype(np.int64)
+            gw = words[wo[:, None] + np.arange(nw)]                               # [n, nw] packed LSB-first
+            gb = np.unpackbits(gw.view(np.uint8), axis=1, bitorder="little")[:, :k]
+            ob = r["bits"][r["bo"][s][:, None] + np.arange(k)]
+            bad = np.flatnonzero(np.any(gb != ob, axis=1))
+            assert bad.size == 0, f"bits differ: CB {idx[s[bad[0]]]} K={k} at {np.flatnonzero(gb[bad[0]] != ob[bad[0]])[:8]}"
+            if g.get("ext") is not None:
+                eo = desc["ext_off"][idx[s]].astype(np.int64)
+                ge = g["ext"][eo[:, None] + np.arange(k)]
+                oe = r["ext"][r["bo"][s][:, None] + np.arange(k)]
+                bad = np.flatnonzero(np.any(ge != oe, axis=1))
+                assert bad.size == 0, f"ext differs: CB {idx[s[bad[0]]]} K={k}"
+
+
+def count_mismatches(desc, g, r, idx, chunk=1024) -> int:
+    """Number of CBs in idx whose packed bits, crc_ok or iters (when g has them)
+    differ from the oracle's r (r in idx order) -- bench.py's self-check."""
+    idx = np.asarray(idx)
+    K = desc["K"][idx].astype(np.int64)
+    bad = g["crc_ok"][idx] != r["crc_ok"]
+    if g.get("iters") is not None:
+        bad |= g["iters"][idx] != r["iters"]
+    words = g["words"].view(np.uint32)
+    for k in np.unique(K):
+        sel = np.flatnonzero(K == k)
+        nw = (int(k) + 31) // 32
+        for c0 in range(0, sel.size, chunk):
+            s = sel[c0:c0 + chunk]
+            wo = desc["bit_off"][idx[s]].astype(np.int64)
+            gb = np.unpackbits(words[wo[:, None] + np.arange(nw)].view(np.uint8), axis=1, bitorder="little")[:, :k]
+            ob = r["bits"][r["bo"][s][:, None] + np.arange(k)]
+            bad[s] |= np.any(gb != ob, axis=1)
+    return int(bad.sum())
+
+
+def _assert_parity_loop(desc, g, r, idx):
     for n, i in enumerate(idx):
         K = int(desc["K"][i])
         ob = r["bits"][r["bo"][n]:r["bo"][n] + K]

@@ -1,6 +1,7 @@
 """CPU tests of the C-ABI library: it builds, loads, exports every symbol
 include/crn.h declares, its host helpers agree with the oracle, and its decode
 entry points refuse to run without a GPU (no CPU fallback)."""
+import ctypes as C
 import os
 import re
 import subprocess
@@ -184,3 +185,49 @@ def test_logmap_lut_matches_oracle(L, orc):
     lut = crn.logmap_lut()
     assert [int(x) for x in lut] == [orc.logmap_correction(4 * b) for b in range(8)]
     assert lut[6] == 0 and lut[7] == 0          # the kernel's PRMT zero filler (R32)
+
+
+def test_kpi_iterations_paper_convention():
+    """crn_kpi_iterations follows PAPER.md:411 (Performance captor): the
+    registered value is the iteration count of a successful CB and a value
+    greater than the maximum for a failure, so the loss rate read from the KPI
+    (share of values > max) equals the CRC failure rate."""
+    rng = np.random.default_rng(4)
+    for I in (1, 6, 8, 32):
+        it = rng.integers(1, I + 1, 1000).astype(np.uint8)
+        ok = (rng.random(1000) < 0.8).astype(np.uint8)
+        k = crn.kpi_iterations(it, ok, I)
+        assert np.array_equal(k[ok == 1], it[ok == 1])
+        assert np.all(k[ok == 0] == I + 1) and np.all(k <= I + 1)
+        assert int((k > I).sum()) == int((ok == 0).sum())
+    assert crn.kpi_iterations([], [], 8).size == 0
+    L = crn.lib()
+    z = np.zeros(1, np.uint8)
+    p = z.ctypes.data_as(C.POINTER(C.c_uint8))
+    assert L.crn_kpi_iterations(p, p, 1, 0, p) == crn.CRN_EINVAL
+    assert L.crn_kpi_iterations(p, p, 1, 33, p) == crn.CRN_EINVAL
+    assert L.crn_kpi_iterations(None, p, 1, 8, p) == crn.CRN_EINVAL
+    assert L.crn_kpi_iterations(p, p, -1, 8, p) == crn.CRN_EINVAL
+
+
+def test_stream_run_binding_refuses_mismatched_llr_dtypes():
+    """The binding checks the LLR dtype against CRN_STREAM_LLR8 before the C call
+    (the runtime would copy n_llr elements of the flag's width), the three
+    streams' lengths and the output dtypes."""
+    d = np.zeros(1, crn.DESC_DTYPE)
+    d["K"] = 40
+
+    def grp(dt, n=(44, 44, 44)):
+        return dict(desc=d, l0=torch.zeros(n[0], dtype=dt), l1=torch.zeros(n[1], dtype=dt),
+                    l2=torch.zeros(n[2], dtype=dt), bits=torch.zeros(2, dtype=torch.int32),
+                    ok=torch.zeros(1, dtype=torch.uint8), it=None)
+    with pytest.raises(crn.CrnError):
+        crn.stream_run([grp(torch.int8)], 1, 1, 1000.0, 8, True, flags=0)
+    with pytest.raises(crn.CrnError):
+        crn.stream_run([grp(torch.int16)], 1, 1, 1000.0, 8, True, flags=crn.STREAM_LLR8)
+    with pytest.raises(crn.CrnError):
+        crn.stream_run([grp(torch.int16, (44, 44, 40))], 1, 1, 1000.0, 8, True, flags=0)
+    g = grp(torch.int16)
+    g["bits"] = torch.zeros(2, dtype=torch.int64)
+    with pytest.raises(crn.CrnError):
+        crn.stream_run([g], 1, 1, 1000.0, 8, True, flags=0)
