@@ -301,6 +301,13 @@ def run_pool(args, seed=0, ws=1, rank=0, dist=None, red_dev="cpu", dev=None):
             "ops_basis": "counted ops from each CB's executed iterations (iters_used): sum 2 x (129 K + 90) x iters"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     kpi = crn.kpi_iterations(its, ok_h, 8)
+    # lane occupancy under early termination: a task runs until its last CB stops, so
+    # every CB lane of the task (2 per pair) is busy for the task's max iteration count
+    tof = plan.layout()
+    t_max = np.zeros(tof.max() + 1, np.int64)
+    np.maximum.at(t_max, tof, its.astype(np.int64))
+    lane_k = b.K.astype(np.int64)
+    busy = float((its * lane_k).sum()) / float((t_max[tof] * lane_k).sum())
     core = {"workload": "cfg3: 100 cells x 10 UEs, TBS ~ U{1000..75376}, 36.212 segmentation, QPSK Eb/N0 ~ "
                         "U[0.5,3] dB per UE, CRC ET max 8 iterations, one TTI" +
                         (f", cells split over {ws} ranks" if ws > 1 else ""),
@@ -308,6 +315,9 @@ def run_pool(args, seed=0, ws=1, rank=0, dist=None, red_dev="cpu", dev=None):
             "decode_ms": d_ms, "decoded_mbps": c["info_bits"] / (d_ms * 1e-3) / 1e6,
             "tb_verdict_ms": statistics.median(ver), "tb_loss_rate": tb_loss,
             "cb_crc_fail_rate": 1.0 - c["n_crc_ok"] / c["n_cb"], "roofline": roof,
+            "et_lane_utilisation": busy,
+            "et_lane_note": "sum(K x iters_used) / sum(K x the task's max iters_used): trellis steps of CBs still "
+                            "running over the steps their tasks execute (dummy partner lanes not counted)",
             "kpi_iters_hist": [int(x) for x in np.bincount(kpi, minlength=10)[1:10]],
             "kpi_note": "PAPER.md:411 convention: bucket 9 (= max + 1) counts decoding failures"}
     if ws > 1:

@@ -161,6 +161,10 @@ int crn_plan_set_llr_format(void *plan, int32_t bits, int32_t shift);
 int crn_plan_llr_bytes(void *plan);
 /* The Log-MAP correction table of CRN_VARIANT_LOGMAP: out[0..7] = LUT[b]. */
 int crn_logmap_lut(int32_t *out);
+/* Diagnostic: task_of_cb[i] = the CTA task (row a1: bucket by K, pair equal-K
+ * CBs, group pairs) CB i is decoded in, in issue order; n_cb must equal the
+ * plan's.  Returns the number of tasks, or CRN_EINVAL. */
+int crn_plan_layout(void *plan, int32_t *task_of_cb, int32_t n_cb);
 /* Number of decode-kernel launches one crn_plan_decode performs (for gpu_launches). */
 int crn_plan_launches(void *plan);
 void crn_plan_destroy(void *plan);

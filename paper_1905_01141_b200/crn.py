@@ -60,6 +60,7 @@ _SIGS = {
     "crn_plan_create": (C.c_int, [vp, C.c_int32, P(vp)]),
     "crn_plan_decode": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp]),
     "crn_plan_launches": (C.c_int, [vp]),
+    "crn_plan_layout": (C.c_int, [vp, i32p, C.c_int32]),
     "crn_plan_set_variant": (C.c_int, [vp, C.c_int32]),
     "crn_plan_set_purge": (C.c_int, [vp, C.c_int32]),
     "crn_plan_set_grid": (C.c_int, [vp, C.c_int32]),
@@ -223,6 +224,12 @@ class Plan:
     @property
     def chunks(self) -> int:
         return int(lib().crn_plan_chunks(self.h))
+
+    def layout(self) -> np.ndarray:
+        """crn_plan_layout: the task index of every CB (diagnostic)."""
+        out = np.zeros(self.desc.size, np.int32)
+        _chk(lib().crn_plan_layout(self.h, _np(out, C.c_int32), self.desc.size), "crn_plan_layout")
+        return out
 
     @property
     def launches(self) -> int:

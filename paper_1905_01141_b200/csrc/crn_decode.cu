@@ -71,7 +71,8 @@ constexpr int S_WORDS = S_TAIL + MAXP * 16;
 static_assert(S_CH % 2 == 0, "chunk array must be 8-byte aligned");
 constexpr int SMEM_WORDS = S_WORDS;
 static_assert(SMEM_WORDS == CRN_SMEM_WORDS, "split-window sizing (crn_internal.h) must see the same shared memory");
-static_assert(SMEM_WORDS * 4 + 9728 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
+static_assert(SMEM_WORDS * 4 + 9728 + 8 * CRN_CRC_NIB_WORDS <= 232448,
+              "dynamic + static shared memory over the sm_100 opt-in limit");
 
 /* ---- optional phase profiler (build with -DCRN_PHASE_PROF; never in the product
  * build): lane 0 of warp 0 (a head warp) and of warp 6 (a tail warp) attribute
@@ -311,6 +312,7 @@ __device__ __forceinline__ int mi_pair(const int *tab, u32 lapp, bool use_lo, bo
 }
 
 struct TaskSh {
+    const u32 *crcnib;          /* the window-CRC nibble tables (CRN_CRC_NIB_WORDS per CRC kind) */
     int *cb, *F, *kind;
     int *mi, *mip;              /* per CB: average-MI statistic of this / the previous iteration (R29) */
     const int *mitab;           /* Q16 MI of |L_APP| = 0..255 (the tables' mi_tab, staged in smem) */
@@ -350,19 +352,17 @@ __device__ __forceinline__ void decide(TaskSh sh, int NP, int it, int max_iters,
     __syncthreads();
 }
 
-/* Clears the per-iteration flags; returns the number of CBs still running. */
+/* Returns the number of CBs still running (one counting barrier: it also
+ * orders every use of this iteration's flags before they are cleared) and
+ * clears the per-iteration flags; the next use of the flags is separated from
+ * the clear by the next half-iteration's barriers. */
 __device__ __forceinline__ int finish_iteration(TaskSh sh, int NP) {
-    if (threadIdx.x == 0) {
-        int left = 0;
-        for (int e = 0; e < 2 * NP; e++) left += !sh.done[e];
-        *sh.left = left;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < 2 * NP; e += BLOCK) { sh.fin[e] = 0; sh.crc[e] = 0; sh.mi[e] = 0; }
-    const int left = *sh.left;
-    __syncthreads();
+    const int e = threadIdx.x;                  /* 2 NP <= 2 MAXP <= BLOCK */
+    const int left = __syncthreads_count(e < 2 * NP && !sh.done[e]);
+    if (e < 2 * NP) { sh.fin[e] = 0; sh.crc[e] = 0; sh.mi[e] = 0; }
     return left;
 }
+static_assert(2 * MAXP <= BLOCK, "one thread per CB lane in finish_iteration");
 
 /* ---- tensor memory (tcgen05) helpers.  A warp may touch only the TMEM lanes
  * of its quadrant (warp % 4); warps 4-7 use columns 128-255, warps 8-11 256-383. */
@@ -487,6 +487,16 @@ __device__ __forceinline__ void load16(const int16_t *__restrict__ base, int64_t
         }
     }
 }
+
+/* Shared load at a 32-bit shared-window byte address */
+__device__ __forceinline__ u32 lds_at(u32 a) {
+    u32 v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+/* byte offset of nibble q of x in a 16-word table: 4 * ((x >> 4q) & 15) */
+__device__ __forceinline__ u32 nib_off(u32 x, int q) { return q ? (x >> (4 * q - 2)) & 60u : (x << 2) & 60u; }
 
 /* Shared load at the packed gather address of constituent c (c = 0: low 16 bits,
  * c = 1: high 16 bits); the halves are split with IMAD-pipe arithmetic so the
@@ -660,7 +670,6 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
     }
     const u32 *qts = tab.qpp_ts + tab.qpp_off[tk.kidx];     /* natural position of Pi(jW+i)  */
     const u32 *qinv = tab.qinv_ts + tab.qpp_off[tk.kidx];   /* interleaved position of jW+i */
-    const u32 *cbit = tab.crc_bit + tab.crcb_off[tk.kidx] + f.j;        /* + kind*K + i*M */
 
     /* ---- row a2: stage own half-window of both CBs of the pair: Lp1, Lp2 into
      * the shared planes, Ls-Lp1 (natural) and Ls[Pi]-Lp2 (interleaved) into
@@ -825,25 +834,30 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                 }
             }
             __syncthreads();
-            if (active && !tail_thr) {
-                const int p = f.p, j = f.j;
-                wlo = hb[0 * TS + f.t] | (hb[2 * TS + f.t] << 16);
-                whi = hb[1 * TS + f.t] | (hb[3 * TS + f.t] << 16);
-                const int n0 = j * W, Flo = sh.F[2 * p], Fhi = sh.F[2 * p + 1];
-                if (Flo > n0) wlo &= (Flo >= n0 + 32) ? 0u : (0xFFFFFFFFu << (Flo - n0));
-                if (Fhi > n0) whi &= (Fhi >= n0 + 32) ? 0u : (0xFFFFFFFFu << (Fhi - n0));
-                hb[0 * TS + f.t] = wlo;
-                hb[1 * TS + f.t] = whi;
+            if (active) {
+                /* the window's 32 hard decisions of one CB lane: the head thread takes
+                 * the low (first) CB of the pair, the tail thread the high one */
+                const int p = f.p, j = f.j, l = tail_thr ? 1 : 0;
+                u32 w = hb[l * TS + f.t] | (hb[(2 + l) * TS + f.t] << 16);
+                const int n0 = j * W, F = sh.F[2 * p + l];
+                if (F > n0) w &= (F >= n0 + 32) ? 0u : (0xFFFFFFFFu << (F - n0));
+                hb[l * TS + f.t] = w;                 /* (its own word: head and tail touch different ones) */
+                const int kind = sh.kind[2 * p + l];
+                if (kind != CRN_CRC_NONE) {
+                    /* CRC register contribution x^(32 d) R(w) mod g, d = M-1-j = 64a + 8b + c, as
+                     * three nibble-table maps (crn_internal.h CRN_CRC_NIB_WORDS) */
+                    const u32 T = smem_addr(sh.crcnib) + (kind == CRN_CRC24A ? 0u : 4u * CRN_CRC_NIB_WORDS);
+                    const u32 d = (u32)(M - 1 - j);
+                    const u32 t1 = T + (d & 7u) * 512u, t2 = T + 4096u + ((d >> 3) & 7u) * 384u,
+                              t3 = T + 7168u + (d >> 6) * 384u;         /* byte addresses of the three maps */
+                    u32 r = 0, r2 = 0, r3 = 0;
 #pragma unroll
-                for (int l = 0; l < 2; l++) {     /* CRC register = XOR of the constants of the set bits */
-                    const int kind = sh.kind[2 * p + l];
-                    if (kind == CRN_CRC_NONE) continue;
-                    const u32 w = l ? whi : wlo;
-                    const u32 *cb = cbit + (kind == CRN_CRC24A ? 0 : tk.K);
-                    u32 acc = 0;
+                    for (int q = 0; q < 8; q++) r ^= lds_at(t1 + 64u * q + nib_off(w, q));
 #pragma unroll
-                    for (int i = 0; i < W; i++) acc ^= __ldg(cb + i * M) & (0u - ((w >> i) & 1u));
-                    atomicXor(&sh.crc[2 * p + l], acc);
+                    for (int q = 0; q < 6; q++) r2 ^= lds_at(t2 + 64u * q + nib_off(r, q));
+#pragma unroll
+                    for (int q = 0; q < 6; q++) r3 ^= lds_at(t3 + 64u * q + nib_off(r2, q));
+                    atomicXor(&sh.crc[2 * p + l], r3);
                 }
             }
             __syncthreads();
@@ -853,7 +867,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
 #pragma unroll
                 for (int l = 0; l < 2; l++) {
                     if (!sh.fin[2 * p + l]) continue;
-                    if (!tail_thr) out_bits[obit[l] + j] = hb[l * TS + f.t];
+                    if (l == (tail_thr ? 1 : 0)) out_bits[obit[l] + j] = hb[l * TS + f.t];
                     if (ext_out) {
 #pragma unroll
                         for (int s = 0; s < HW; s++) {
@@ -1252,12 +1266,14 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     __shared__ int s_cb[2 * MAXP], s_F[2 * MAXP], s_kind[2 * MAXP];
     __shared__ uint8_t s_done[2 * MAXP], s_fin[2 * MAXP];
     __shared__ int s_mi[2 * MAXP], s_mip[2 * MAXP], s_mitab[256];
+    __shared__ u32 s_crcnib[2 * CRN_CRC_NIB_WORDS];
 
     int *counter = (int *)ws;
     const int tid = threadIdx.x;
-    const TaskSh sh{s_cb, s_F, s_kind, s_mi, s_mip, s_mitab, s_done, s_fin, s_crc, &s_left};
+    const TaskSh sh{s_crcnib, s_cb, s_F, s_kind, s_mi, s_mip, s_mitab, s_done, s_fin, s_crc, &s_left};
     const Purge pg{s_tb, tb_dead};
     for (int i = tid; i < 256; i += BLOCK) s_mitab[i] = tab.mi_tab[i];
+    for (int i = tid; i < 2 * CRN_CRC_NIB_WORDS; i += BLOCK) s_crcnib[i] = tab.crc_nib[i];
 
     /* TMEM: the whole 512 columns (one CTA per SM: the shared-memory footprint guarantees it) */
     if ((tid >> 5) == 0) {

@@ -242,8 +242,30 @@ static int build_tables(int dev, DevTables **out) {
             }
         }
     }
+    /* nibble tables of the W = 32 path's window CRC (crn_internal.h CRN_CRC_NIB_WORDS) */
+    std::vector<uint32_t> nib(2 * (size_t)CRN_CRC_NIB_WORDS);
+    for (int k = 0; k < 2; k++) {
+        const uint32_t poly = k ? POLY_B : POLY_A;
+        auto mulxn = [&](uint32_t r, int n) { for (int i = 0; i < n; i++) r = mulx_mod(r, poly); return r; };
+        auto xpow = [&](int e) { return mulxn(1u, e); };            /* x^e mod g */
+        uint32_t *T = nib.data() + (size_t)k * CRN_CRC_NIB_WORDS;
+        for (int c = 0; c < 8; c++)
+            for (int q = 0; q < 8; q++)
+                for (int v = 0; v < 16; v++) {
+                    uint32_t r = 0;
+                    for (int b = 0; b < 4; b++)
+                        if ((v >> b) & 1) r ^= xpow(55 - 4 * q - b);
+                    T[c * 128 + q * 16 + v] = mulxn(r, 32 * c);
+                }
+        for (int l = 0; l < 2; l++)                                    /* TB (x^256 b), TA (x^2048 a) */
+            for (int m = 0; m < (l ? 3 : 8); m++)
+                for (int q = 0; q < 6; q++)
+                    for (int v = 0; v < 16; v++)
+                        T[(l ? 1792 : 1024) + m * 96 + q * 16 + v] = mulxn((uint32_t)v << (4 * q), (l ? 2048 : 256) * m);
+    }
     DevTables t;
-    if (cudaMalloc(&t.qpp_wm, qpp.size() * 4) != cudaSuccess ||
+    if (cudaMalloc(&t.crc_nib, nib.size() * 4) != cudaSuccess ||
+        cudaMalloc(&t.qpp_wm, qpp.size() * 4) != cudaSuccess ||
         cudaMalloc(&t.qpp_ts, qts.size() * 4) != cudaSuccess ||
         cudaMalloc(&t.qinv_ts, qin.size() * 4) != cudaSuccess ||
         cudaMalloc(&t.qinv_wm, qiw.size() * 4) != cudaSuccess ||
@@ -261,13 +283,14 @@ static int build_tables(int dev, DevTables **out) {
     cudaMemcpy(t.qpp_off, qoff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.crc_bit, cb.data(), cb.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(t.crcb_off, cboff.data(), CRN_NUM_K * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(t.crc_nib, nib.data(), nib.size() * 4, cudaMemcpyHostToDevice);
     int32_t mt[256];
     crn_mi_table(mt);
     cudaMemcpy(t.mi_tab, mt, sizeof(mt), cudaMemcpyHostToDevice);
     if (cudaError_t e = cudaGetLastError()) return crn_cuda_fail(e, "table upload", CRN_ECUDA);
     t.tab.qpp_wm = t.qpp_wm; t.tab.qpp_ts = t.qpp_ts; t.tab.qinv_ts = t.qinv_ts;
     t.tab.qpp_off = t.qpp_off;
-    t.tab.crc_bit = t.crc_bit; t.tab.crcb_off = t.crcb_off; t.tab.mi_tab = t.mi_tab;
+    t.tab.crc_bit = t.crc_bit; t.tab.crcb_off = t.crcb_off; t.tab.mi_tab = t.mi_tab; t.tab.crc_nib = t.crc_nib;
     {
         uint32_t lo, hi;
         crn_logmap_words(&lo, &hi);
@@ -514,6 +537,25 @@ extern "C" int crn_plan_set_grid(void *plan, int32_t max_ctas) {
     if (!P || max_ctas < 0) return CRN_EINVAL;
     P->grid_cap = max_ctas;
     return CRN_OK;
+}
+
+extern "C" int crn_plan_layout(void *plan, int32_t *task_of_cb, int32_t n_cb) {
+    /* diagnostic: the CTA task each CB was bucketed into (row a1), -1 if none */
+    Plan *P = (Plan *)plan;
+    if (!P || !task_of_cb || n_cb != P->n_cb) return CRN_EINVAL;
+    std::vector<crn_task> tasks;
+    std::vector<crn_pair> pairs;
+    std::vector<int> all(P->n_cb);
+    for (int i = 0; i < P->n_cb; i++) all[i] = i;
+    crn_build_tasks(P->h_desc.data(), all.data(), P->n_cb, tasks, pairs);
+    for (int i = 0; i < n_cb; i++) task_of_cb[i] = -1;
+    for (size_t t = 0; t < tasks.size(); t++)
+        for (int p = 0; p < tasks[t].n_pairs; p++) {
+            const crn_pair &q = pairs[(size_t)tasks[t].pair0 + p];
+            task_of_cb[q.lo] = (int32_t)t;
+            if (q.hi >= 0) task_of_cb[q.hi] = (int32_t)t;
+        }
+    return (int)tasks.size();
 }
 
 extern "C" int crn_plan_launches(void *plan) {

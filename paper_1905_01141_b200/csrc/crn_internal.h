@@ -53,6 +53,17 @@ static inline int crn_split_fits(int W, int M, int n_pairs) {
            crn_split_tmem_cols(W, M, n_pairs) <= CRN_TMEM_COLS;
 }
 
+/* Window CRC of the W = 32 decode path (row a9).  With K = 32 M, window j's
+ * packed hard decisions w (bit i = message bit 32 j + i, MSB-first order)
+ * contribute x^(32 d) * R(w) mod g to the CRC register, d = M - 1 - j, R(w) =
+ * sum_i w_i x^(55 - i) mod g; d = 64 a + 8 b + c (a <= 2) is applied as three
+ * fixed linear maps, each an XOR of nibble-table lookups (bank-conflict-free
+ * 16-word tables):
+ *   [0, 1024)     TRC[c][q][v] = (sum over bits k of v of x^(55 - 4q - k)) x^(32 c) mod g, q = 0..7
+ *   [1024, 1792)  TB[b][q][v]  = (v x^(4q)) x^(256 b) mod g, q = 0..5
+ *   [1792, 2080)  TA[a][q][v]  = (v x^(4q)) x^(2048 a) mod g, q = 0..5          */
+#define CRN_CRC_NIB_WORDS 2080
+
 /* Max CBs per TB accepted by crn_tb_verdict_batch (LTE needs <= 64). */
 #define CRN_TB_MAX_CB 128
 
@@ -65,6 +76,8 @@ typedef struct {
     const uint32_t *crc_bit;  /* per K at crcb_off[kidx]: [kind(0=A,1=B)*K + i*M + j] = x^(K-1-n+24) mod g, n = jW+i:
                                  the CRC register contribution of a 1 at bit n (register = XOR over the set bits) */
     const int32_t *mi_tab;    /* [256] Q16 MI of an LLR of magnitude a/8 (crn_mi_table, R29) */
+    const uint32_t *crc_nib;  /* [2][CRN_CRC_NIB_WORDS] (CRC24A, CRC24B): nibble tables of the W = 32 path's
+                                 window CRC, see CRN_CRC_NIB_WORDS */
     const int32_t *qpp_off;
     const int32_t *crcb_off;
 } crn_tables;

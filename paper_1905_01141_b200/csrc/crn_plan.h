@@ -12,6 +12,7 @@ struct DevTables {
     uint32_t *qpp_wm = nullptr, *qpp_ts = nullptr, *qinv_ts = nullptr, *crc_bit = nullptr,
              *qinv_wm = nullptr;
     int32_t *qpp_off = nullptr, *crcb_off = nullptr, *mi_tab = nullptr;
+    uint32_t *crc_nib = nullptr;
     crn_tables tab{};
     int grid = 0;
 };
