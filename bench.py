@@ -480,6 +480,69 @@ def run_dl_encode(b, reps=5):
             "matches_batch_encoding": bool(same)}
 
 
+def run_dl_encode_tb(seed=0, reps=5):
+    """Row f3 end to end on the device for BASELINE cfg3's 1,000 TBs (the paper's DL
+    encoding function, with its pre-processing, :404-406): TB
+    CRC24A + 36.212 segmentation + fillers + CB CRC24B (crn_tb_build_cbs_batch),
+    turbo encoding (crn_encode_batch) and rate matching to E = 3(K+4) at rv 0
+    (crn_rate_match_batch); ms per call through the C ABI and TB info Mbit/s."""
+    from paper_1905_01141_b200 import crn
+    from paper_1905_01141_b200 import workload as wlmod
+    st = torch.cuda.current_stream()
+    wl = wlmod.make_workload(3, seed=seed, device="cuda")
+    tbs = np.asarray(wl.tbs, np.int64)
+    pay = torch.cat(wl.payload)
+    off = np.concatenate([[0], np.cumsum(tbs)[:-1]]).astype(np.int64)
+    desc, info = crn.tb_build_cbs_batch(tbs, off, pay)
+    cb_buf = torch.empty(int(desc["K"].sum()), dtype=torch.uint8, device="cuda")
+    n_llr = int((desc["K"] + 4).sum())
+    coded = tuple(torch.empty(n_llr, dtype=torch.uint8, device="cuda") for _ in range(3))
+    rm = np.zeros(desc.size, crn.RM_DTYPE)
+    rm["K"], rm["E"], rm["rv"] = desc["K"], 3 * (desc["K"] + 4), 0
+    rm["e_off"], rm["llr_off"] = desc["llr_off"] * 3, desc["llr_off"]
+    e = torch.empty(3 * n_llr, dtype=torch.uint8, device="cuda")
+
+    def seg():
+        crn.tb_build_cbs_batch(tbs, off, pay, cb_bits=cb_buf, max_cb=desc.size, stream=st)
+
+    def enc():
+        crn.encode_batch(desc, cb_buf, False, *coded, stream=st)
+
+    def rmt():
+        crn.rate_match_batch(rm, *coded, e, stream=st)
+
+    def all3():
+        seg()
+        enc()
+        rmt()
+
+    for _ in range(2):
+        all3()
+    torch.cuda.synchronize()
+
+    def per_call(fn):
+        out = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(reps):
+                fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            out.append(e0.elapsed_time(e1) / reps)
+        return statistics.median(out)
+
+    t_seg, t_enc, t_rm, t_all = per_call(seg), per_call(enc), per_call(rmt), per_call(all3)
+    same = bool(torch.equal(cb_buf, info))
+    bits = int(tbs.sum())
+    return {"workload": f"cfg3: {tbs.size} TBs (TBS ~ U{{1000..75376}}) -> {desc.size} CBs of mixed K: TB CRC24A + "
+                        "segmentation + fillers + CB CRC24B, turbo encoding, rate matching to E = 3(K+4) rv 0",
+            "segment_ms": t_seg, "encode_ms": t_enc, "rate_match_ms": t_rm, "chain_ms": t_all,
+            "tb_info_mbps": bits / (t_all * 1e-3) / 1e6, "segment_gbs": (bits + int(desc["K"].sum())) / (t_seg * 1e-3) / 1e9,
+            "repeat_identical": same,
+            "timing": f"ms per call over {reps} back-to-back calls through the C ABI, median of 3"}
+
+
 def run_small_configs(seed=0):
     """BASELINE cfg1 (32 x K=1056, 6 fixed iterations) and cfg2 (one 20 MHz subframe:
     TB of 75,376 bits -> 13 x K=5824, CRC ET max 8) as single device launches:
@@ -892,6 +955,11 @@ def run_crn(args):
             out["dl_encode"] = run_dl_encode(b)
         except Exception as e:
             out["dl_encode"] = {"error": repr(e)}
+    if not args.no_pool and ws == 1:
+        try:
+            out["dl_encode_tb"] = run_dl_encode_tb(seed=args.seed)
+        except Exception as e:
+            out["dl_encode_tb"] = {"error": repr(e)}
     if not args.no_pool and ws == 1:
         try:
             out["small_configs"] = run_small_configs(seed=args.seed)

@@ -332,6 +332,24 @@ int crn_segment_tb(int64_t tbs_bits, crn_seg *out);
 int crn_tb_build_cbs(const uint8_t *tb_bits, int64_t tbs_bits, int32_t max_cb, int64_t base_bit,
                      int64_t base_llr, int64_t base_word, uint8_t *cb_bits, crn_cb_desc *desc,
                      int32_t *n_cb);
+/* The same for a whole batch of TBs on the DEVICE (DL direction: the "code
+ * block creation, segmentation" the paper times before its encoder,
+ * PAPER.md:270-272, :404-406).  TB t has tbs_bits[t]
+ * payload bits, one per byte, at payload[payload_off[t] ..] (DEVICE memory).
+ * The CBs of all TBs are laid out densely in TB order: desc (HOST, capacity
+ * max_cb) receives K, F, crc_kind, reserved = t (the CB's TB index, as
+ * crn_plan_set_purge expects), ext_off = sum of the preceding K (the CB's first
+ * byte in cb_bits), llr_off = sum of the preceding K+4, bit_off = sum of the
+ * preceding ceil(K/32); cb_bits (DEVICE, sum K bytes) receives every CB's
+ * complete content exactly as crn_tb_build_cbs builds it: F filler zeros in CB
+ * 0, the bits of payload || CRC24A, and each CB's CRC24B when C > 1.  *n_cb
+ * receives the CB count.  The segmentation arithmetic (O(1) per TB) runs on
+ * the host; CRC24A, the bit placement and CRC24B run in one kernel (a CTA per
+ * TB), asynchronously on cuda_stream.  CRN_EINVAL for n_tb < 0, tbs < 1, a
+ * negative offset, more than max_cb CBs in total or a TB of more than
+ * CRN_TB_MAX_CB CBs. */
+int crn_tb_build_cbs_batch(const int64_t *tbs_bits, const int64_t *payload_off, int32_t n_tb, const uint8_t *payload,
+                           int32_t max_cb, uint8_t *cb_bits, crn_cb_desc *desc, int32_t *n_cb, void *cuda_stream);
 /* TB post-processing ("a TB can be successfully decoded only when
  * all CBs have been individually decoded", :408 "combination of CBs"): given the
  * C decoded CBs of one TB (packed words as written by the decoder, HOST memory,

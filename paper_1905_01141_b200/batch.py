@@ -1,5 +1,6 @@
 """Product-side batch assembly for a synthetic workload: CB packing via libcrn
-(crn_tb_build_cbs / descriptors, row a1), device encoding via crn_encode_batch
+(crn_tb_build_cbs_batch on the device for transport blocks, descriptors, row
+a1), device encoding via crn_encode_batch
 (the paper's encoding function), then the shared workload
 channel (``build``, used by bench.py); or the same dense layout around CB
 contents and coded bits the caller supplies (``from_cbs``: the parity tests
@@ -50,6 +51,8 @@ class Batch:
 
 
 def build(wl: wlmod.Workload, device="cuda") -> Batch:
+    if wl.tb_kind == "tb":
+        return _build_tb(wl, device)
     dev = torch.device(device)
     descs, infos, cells, tbs, ebn0 = [], [], [], [], []
     bit = llr = word = 0
@@ -80,6 +83,26 @@ def build(wl: wlmod.Workload, device="cuda") -> Batch:
     l0, l1, l2 = wlmod.channel_llr(wl, cell, desc["K"], e, coded)
     return Batch(wl=wl, desc=desc, cb_cell=cell, cb_tb=np.array(tbs, np.int64), cb_ebn0=e, info=info,
                  coded=coded, llr=(l0, l1, l2))
+
+
+def _build_tb(wl: wlmod.Workload, device="cuda") -> Batch:
+    """Transport-block configs on the device: TB CRC24A, 36.212 segmentation with
+    fillers and CB CRC24B (crn_tb_build_cbs_batch), then the turbo encoder."""
+    dev = torch.device(device)
+    tbs = np.asarray(wl.tbs, np.int64)
+    pay = torch.cat([p.to(dev) for p in wl.payload]) if wl.n_tb else torch.zeros(1, dtype=torch.uint8, device=dev)
+    off = np.concatenate([[0], np.cumsum(tbs)[:-1]]).astype(np.int64) if wl.n_tb else np.zeros(0, np.int64)
+    desc, info = crn.tb_build_cbs_batch(tbs, off, pay)
+    llr = int((desc["K"] + 4).sum())
+    coded = tuple(torch.empty(max(llr, 1), dtype=torch.uint8, device=dev) for _ in range(3))
+    crn.encode_batch(desc, info, False, *coded)
+    cb_tb = desc["reserved"].astype(np.int64)
+    cell = np.asarray(wl.tb_cell, np.int32)[cb_tb]
+    e = np.asarray(wl.tb_ebn0_db, np.float64)[cb_tb]
+    coded = tuple(x[:llr] for x in coded)
+    l0, l1, l2 = wlmod.channel_llr(wl, cell, desc["K"], e, coded)
+    desc["reserved"] = 0
+    return Batch(wl=wl, desc=desc, cb_cell=cell, cb_tb=cb_tb, cb_ebn0=e, info=info, coded=coded, llr=(l0, l1, l2))
 
 
 def outputs(b: Batch, device="cuda", want_ext: bool = True):

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libcrn.so")
-SOURCES = ["crn_host.cpp", "crn_runtime.cpp", "crn_decode.cu", "crn_encode.cu", "crn_tb.cu", "crn_ratematch.cu", "crn_ubench.cu"]
+SOURCES = ["crn_host.cpp", "crn_runtime.cpp", "crn_decode.cu", "crn_encode.cu", "crn_tb.cu", "crn_ratematch.cu", "crn_tbseg.cu", "crn_ubench.cu"]
 HEADERS = ["crn_internal.h", "crn_plan.h", "qpp_table.h", os.path.join("..", "..", "include", "crn.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -27,9 +27,10 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, so: str | None = None, defines=()) -> str:
+def build(force: bool = False, verbose: bool = False, so: str | None = None, defines=(), replace=None) -> str:
     """Compile libcrn.so (or, for profiling / A-B experiments, ``so`` with extra
-    ``-D`` defines, e.g. CRN_PHASE_PROF; never the product library)."""
+    ``-D`` defines, e.g. CRN_PHASE_PROF, and ``replace`` = {source: alternative
+    file} for A/B variants; never the product library)."""
     if so is None and not force and not _stale():
         return SO
     from concurrent.futures import ThreadPoolExecutor
@@ -39,7 +40,8 @@ def build(force: bool = False, verbose: bool = False, so: str | None = None, def
     cmds, objs = [], []
     for s in SOURCES:
         o = os.path.join(bdir, s + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *(f"-D{d}" for d in defines), "-c", os.path.join(CSRC, s), "-o", o]
+        src = (replace or {}).get(s, os.path.join(CSRC, s))
+        cmd = [NVCC, *ARCH, *FLAGS, *(f"-D{d}" for d in defines), "-I", CSRC, "-c", src, "-o", o]
         if verbose and s.endswith(".cu"):
             cmd.insert(1, "-Xptxas=-v")
         cmds.append(cmd)

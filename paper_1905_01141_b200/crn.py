@@ -76,6 +76,7 @@ _SIGS = {
     "crn_encode_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp]),
     "crn_tb_build_cbs": (C.c_int, [u8p, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_int64, u8p, vp,
                                    i32p]),
+    "crn_tb_build_cbs_batch": (C.c_int, [i64p, i64p, C.c_int32, vp, C.c_int32, vp, vp, i32p, vp]),
     "crn_rate_dematch_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp]),
     "crn_rate_match_batch": (C.c_int, [vp, C.c_int32, vp, vp, vp, vp, vp]),
     "crn_tb_verdict_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp, vp]),
@@ -331,6 +332,29 @@ def tb_build_cbs(tb_bits, base_bit: int = 0, base_llr: int = 0, base_word: int =
                                 _np(out, C.c_uint8), desc.ctypes.data, C.byref(n)), "crn_tb_build_cbs")
     desc = desc[:n.value].copy()
     return out[:int(desc["K"].sum())].copy(), desc
+
+
+def tb_build_cbs_batch(tbs_bits, payload_off, payload, cb_bits=None, max_cb=None, stream=None):
+    """crn_tb_build_cbs_batch: TB payloads (one bit per byte in the CUDA uint8
+    tensor ``payload``, TB t at payload_off[t]) -> (desc [n_cb] host array, cb_bits
+    CUDA uint8 tensor of sum K bytes).  cb_bits may be preallocated (>= sum K)."""
+    import torch
+    _cuda_dev(payload, cb_bits)
+    tb = np.ascontiguousarray(tbs_bits, np.int64)
+    po = np.ascontiguousarray(payload_off, np.int64)
+    if tb.size != po.size:
+        raise CrnError("tbs_bits and payload_off differ in length")
+    if max_cb is None:
+        max_cb = int(sum(segment_tb(int(x))["C"] for x in tb)) if tb.size else 0
+    desc = np.zeros(max(max_cb, 1), DESC_DTYPE)
+    if cb_bits is None:
+        cb_bits = torch.empty(max(max_cb, 1) * 6144, dtype=torch.uint8, device=payload.device)
+    n = C.c_int32()
+    _chk(lib().crn_tb_build_cbs_batch(_np(tb, C.c_int64), _np(po, C.c_int64), tb.size, _ptr(payload), max_cb,
+                                      _ptr(cb_bits), desc.ctypes.data, C.byref(n), _stream(stream)),
+         "crn_tb_build_cbs_batch")
+    desc = desc[:n.value].copy()
+    return desc, cb_bits[:int(desc["K"].sum())]
 
 
 RM_DTYPE = np.dtype([("K", "<i4"), ("E", "<i4"), ("rv", "<i4"), ("reserved", "<i4"), ("e_off", "<i8"),

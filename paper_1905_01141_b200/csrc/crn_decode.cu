@@ -69,10 +69,14 @@ constexpr int S_CH = S_LP + 2 * SUMK;
 constexpr int S_TAIL = S_CH + HW * BLOCK * 2;   /* per pair: beta_K of DEC1 (8 words), of DEC2 (8 words) */
 constexpr int S_WORDS = S_TAIL + MAXP * 16;
 static_assert(S_CH % 2 == 0, "chunk array must be 8-byte aligned");
-constexpr int SMEM_WORDS = S_WORDS;
-static_assert(SMEM_WORDS == CRN_SMEM_WORDS, "split-window sizing (crn_internal.h) must see the same shared memory");
-static_assert(SMEM_WORDS * 4 + 9728 + 8 * CRN_CRC_NIB_WORDS <= 232448,
-              "dynamic + static shared memory over the sm_100 opt-in limit");
+static_assert(S_WORDS == CRN_SMEM_WORDS, "split-window sizing (crn_internal.h) must see the same shared memory");
+/* the window-CRC nibble tables (both CRC kinds) after both paths' layouts: the
+ * Y / Z planes stay at the start of the dynamic region, because the fast path
+ * packs two of their shared byte addresses into one register (< 64 KiB each) */
+constexpr int S_CRCNIB = S_WORDS;
+constexpr int SMEM_WORDS = S_CRCNIB + 2 * CRN_CRC_NIB_WORDS;
+constexpr int YZ_END_BYTES = 4 * (S_Z + SUMK);     /* + static shared memory: must stay < 64 KiB */
+static_assert(SMEM_WORDS * 4 + 9728 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
 
 /* ---- optional phase profiler (build with -DCRN_PHASE_PROF; never in the product
  * build): lane 0 of warp 0 (a head warp) and of warp 6 (a tail warp) attribute
@@ -1266,10 +1270,10 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     __shared__ int s_cb[2 * MAXP], s_F[2 * MAXP], s_kind[2 * MAXP];
     __shared__ uint8_t s_done[2 * MAXP], s_fin[2 * MAXP];
     __shared__ int s_mi[2 * MAXP], s_mip[2 * MAXP], s_mitab[256];
-    __shared__ u32 s_crcnib[2 * CRN_CRC_NIB_WORDS];
 
     int *counter = (int *)ws;
     const int tid = threadIdx.x;
+    u32 *s_crcnib = smem + S_CRCNIB;
     const TaskSh sh{s_crcnib, s_cb, s_F, s_kind, s_mi, s_mip, s_mitab, s_done, s_fin, s_crc, &s_left};
     const Purge pg{s_tb, tb_dead};
     for (int i = tid; i < 256; i += BLOCK) s_mitab[i] = tab.mi_tab[i];
@@ -1375,7 +1379,8 @@ cudaError_t for_each_kernel(F &&f) {
 extern "C" int crn_decode_grid(int device) {
     /* returns the persistent grid (one CTA per SM), or a negative code:
      * -100 - cudaError of the smem attribute, -200 - cudaError of the occupancy
-     * query, -300 - occupancy (must be exactly 1: the CTA owns all TMEM columns) */
+     * query, -300 - occupancy (must be exactly 1: the CTA owns all TMEM columns),
+     * -400: static shared memory pushes the Y / Z planes past 64 KiB */
     static int configured = -1;
     if (configured != device) {
         cudaError_t e = for_each_kernel([](const void *k) {
@@ -1386,7 +1391,16 @@ extern "C" int crn_decode_grid(int device) {
     }
     int sms = 0, bad = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    /* the fast path's packed gather addresses: static + Y / Z planes below 64 KiB */
     cudaError_t e = for_each_kernel([&](const void *k) {
+        cudaFuncAttributes a;
+        cudaError_t r = cudaFuncGetAttributes(&a, k);
+        if (r == cudaSuccess && a.sharedSizeBytes + YZ_END_BYTES > 65536) bad = -1;
+        return r;
+    });
+    if (e != cudaSuccess) return -200 - (int)e;
+    if (bad) return -400;
+    e = for_each_kernel([&](const void *k) {
         int occ = 0;
         cudaError_t r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, BLOCK, smem_bytes());
         if (r == cudaSuccess && occ != 1) bad = occ ? occ : -1;

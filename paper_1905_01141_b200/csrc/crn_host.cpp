@@ -774,6 +774,48 @@ extern "C" int crn_tb_build_cbs(const uint8_t *tb, int64_t tbs, int32_t max_cb, 
     return src == tbs + 24 ? CRN_OK : CRN_EINVAL;
 }
 
+extern "C" int crn_tb_build_cbs_batch(const int64_t *tbs_bits, const int64_t *payload_off, int32_t n_tb,
+                                      const uint8_t *payload, int32_t max_cb, uint8_t *cb_bits, crn_cb_desc *desc,
+                                      int32_t *n_cb, void *stream) {
+    if (n_tb < 0 || max_cb < 0 || !n_cb) return CRN_EINVAL;
+    *n_cb = 0;
+    if (n_tb == 0) return CRN_OK;
+    if (!tbs_bits || !payload_off || !payload || !cb_bits || !desc) return CRN_EINVAL;
+    std::vector<crn_tbseg> rec((size_t)n_tb);
+    int32_t n = 0;
+    int64_t bit = 0, llr = 0, word = 0, max_tbs = 0;
+    for (int t = 0; t < n_tb; t++) {
+        crn_seg g;
+        if (payload_off[t] < 0 || crn_segment_tb(tbs_bits[t], &g) != CRN_OK || g.C > CRN_TB_MAX_CB ||
+            (int64_t)n + g.C > max_cb)
+            return CRN_EINVAL;
+        crn_tbseg &r = rec[(size_t)t];
+        r.tbs = tbs_bits[t]; r.payload_off = payload_off[t]; r.cb_bit0 = bit;
+        r.C = g.C; r.Kplus = g.Kplus; r.Kminus = g.Kminus; r.Cminus = g.Cminus; r.F = g.F; r.L = g.L;
+        max_tbs = std::max(max_tbs, tbs_bits[t]);
+        for (int c = 0; c < g.C; c++) {           /* 36.212 5.1.2: the C- smaller CBs first, fillers in CB 0 */
+            crn_cb_desc &d = desc[n++];
+            d.K = c < g.Cminus ? g.Kminus : g.Kplus;
+            d.F = c == 0 ? g.F : 0;
+            d.crc_kind = g.C > 1 ? CRN_CRC24B : CRN_CRC24A;
+            d.reserved = t;
+            d.ext_off = bit; d.llr_off = llr; d.bit_off = word;
+            bit += d.K; llr += d.K + 4; word += (d.K + 31) / 32;
+        }
+    }
+    int dev;
+    DevTables *tt;
+    int rc = crn_get_ctx(&dev, &tt);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    void *dd = nullptr;
+    if ((rc = crn_upload1(rec.data(), sizeof(crn_tbseg) * rec.size(), dev, st, &dd))) return rc;
+    rc = crn_launch_tbseg((const crn_tbseg *)dd, n_tb, max_tbs, payload, cb_bits, (void *)st);
+    cudaFreeAsync(dd, st);
+    if (rc == CRN_OK) *n_cb = n;
+    return rc;
+}
+
 extern "C" int crn_tb_reassemble(const uint32_t *w, const crn_cb_desc *desc, const uint8_t *ok, int32_t n_cb,
                                  int64_t tbs, uint8_t *out) {
     if (!w || !desc || !ok || n_cb < 1) return CRN_EINVAL;

@@ -64,6 +64,12 @@ static inline int crn_split_fits(int W, int M, int n_pairs) {
  *   [1792, 2080)  TA[a][q][v]  = (v x^(4q)) x^(2048 a) mod g, q = 0..5          */
 #define CRN_CRC_NIB_WORDS 2080
 
+/* Device record of one TB for crn_tb_build_cbs_batch (crn_tbseg.cu). */
+typedef struct {
+    int64_t tbs, payload_off, cb_bit0;     /* payload bits; bit 0's byte in payload; CB 0's first byte in cb_bits */
+    int32_t C, Kplus, Kminus, Cminus, F, L;
+} crn_tbseg;
+
 /* Max CBs per TB accepted by crn_tb_verdict_batch (LTE needs <= 64). */
 #define CRN_TB_MAX_CB 128
 
@@ -109,6 +115,9 @@ int crn_launch_dematch(const crn_rm_desc *d_desc, int32_t n_cb, const int16_t *e
                        int16_t *h1, int16_t *h2, void *stream);
 int crn_launch_match(const crn_rm_desc *d_desc, int32_t n_cb, const uint8_t *d0, const uint8_t *d1,
                      const uint8_t *d2, uint8_t *e, void *stream);
+/* crn_tbseg.cu */
+int crn_launch_tbseg(const crn_tbseg *d_tbs, int32_t n_tb, int64_t max_tbs, const uint8_t *payload, uint8_t *cb_bits,
+                     void *stream);
 /* crn_ubench.cu */
 int crn_launch_ubench(int32_t op, int64_t *lane_instr, float *ms, int64_t *cycles_per_block);
 /* crn_host.cpp */

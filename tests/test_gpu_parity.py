@@ -740,3 +740,47 @@ def test_logmap_variant_parity(orc, cfg, scale, I, et):
     torch.cuda.synchronize()
     assert np.array_equal(hb.numpy().view(np.uint32)[:b.n_words], g["words"][:b.n_words])
     assert np.array_equal(hok.numpy()[:b.n_cb], g["crc_ok"])
+
+
+def test_tb_build_cbs_batch_matches_oracle(orc):
+    """Row f3 (DL conditioning on the device): crn_tb_build_cbs_batch -- TB
+    CRC24A, 36.212 segmentation, fillers, CB CRC24B -- equals the oracle's
+    segment_tb_bits for every TB: descriptors, and every CB bit.  TBS cover C = 1
+    with and without fillers, the C = 1 / C = 2 boundary (6120 / 6121), the
+    smallest K, cfg2's 13 CBs, the largest LTE TBS and 4-layer sizes (C up to
+    64), random sizes; payloads sit at odd byte offsets."""
+    rng = np.random.default_rng(31)
+    tbs = [16, 17, 40, 1000, 4000, 6119, 6120, 6121, 12000, 75376, 97896, 391656, 1, 2, 3, 5, 8]
+    tbs += list(rng.integers(1, 75377, 60)) + list(rng.integers(75377, 391657, 4))
+    pays = [rng.integers(0, 2, int(t), dtype=np.uint8) for t in tbs]
+    gaps = rng.integers(0, 7, len(tbs))
+    off, buf, o = [], [], 0
+    for p, gp in zip(pays, gaps):
+        buf.append(np.full(int(gp), 9, np.uint8))               # junk between payloads (bit 0 of 9 is 1)
+        o += int(gp)
+        off.append(o)
+        buf.append(p)
+        o += p.size
+    payload = torch.from_numpy(np.concatenate(buf)).cuda()
+    desc, cb_bits = crn.tb_build_cbs_batch(np.array(tbs, np.int64), np.array(off, np.int64), payload)
+    torch.cuda.synchronize()
+    got = cb_bits.cpu().numpy()
+    n = 0
+    bit = llr = word = 0
+    for t, p in enumerate(pays):
+        cbs, Fs, seg = orc.segment_tb_bits(p)
+        assert seg["C"] == len(cbs)
+        for r, (c, F) in enumerate(zip(cbs, Fs)):
+            d = desc[n]
+            K = c.size
+            assert (d["K"], d["F"], d["reserved"]) == (K, F, t)
+            assert d["crc_kind"] == (crn.CRC24A if seg["C"] == 1 else crn.CRC24B)
+            assert (d["ext_off"], d["llr_off"], d["bit_off"]) == (bit, llr, word)
+            assert np.array_equal(got[bit:bit + K], c), (t, r, np.flatnonzero(got[bit:bit + K] != c)[:8])
+            bit += K
+            llr += K + 4
+            word += (K + 31) // 32
+            n += 1
+    assert n == desc.size and got.size == bit
+    with pytest.raises(crn.CrnError):
+        crn.tb_build_cbs_batch(np.array([0], np.int64), np.array([0], np.int64), payload)
