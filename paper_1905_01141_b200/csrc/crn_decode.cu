@@ -74,7 +74,9 @@ static_assert(S_WORDS == CRN_SMEM_WORDS, "split-window sizing (crn_internal.h) m
  * Y / Z planes stay at the start of the dynamic region, because the fast path
  * packs two of their shared byte addresses into one register (< 64 KiB each) */
 constexpr int S_CRCNIB = S_WORDS;
-constexpr int SMEM_WORDS = S_CRCNIB + 2 * CRN_CRC_NIB_WORDS;
+constexpr int S_OFFS = S_CRCNIB + 2 * CRN_CRC_NIB_WORDS;   /* int64 [4][2 MAXP]: bit_off, ext_off (current, next) */
+static_assert(S_OFFS % 2 == 0, "8-byte aligned");
+constexpr int SMEM_WORDS = S_OFFS + 4 * 2 * MAXP * 2;
 constexpr int YZ_END_BYTES = 4 * (S_Z + SUMK);     /* + static shared memory: must stay < 64 KiB */
 static_assert(SMEM_WORDS * 4 + 9728 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
 
@@ -323,6 +325,7 @@ struct TaskSh {
     uint8_t *done, *fin;
     u32 *crc;
     int *left;
+    const int64_t *bo, *eo;     /* per CB: bit_off / ext_off of its descriptor (claimed with the task) */
 };
 
 /* Row a9 bookkeeping after the CRC reduction: completion / early termination
@@ -397,6 +400,7 @@ struct SCtx {
     u32 ts;         /* this thread's TMEM statics: Ls-Lp1 (16 columns), Ls[Pi]-Lp2 (16) */
     int tid, t, p, j, M, pM, k0;
     u32 lut_lo, lut_hi;     /* Log-MAP LUT words (tab.lm_lo / lm_hi) */
+    bool wact;              /* the warp holds at least one of the task's windows (warp-uniform) */
 };
 
 __device__ __forceinline__ void tm_store8(u32 ta, const u32 v[NS]) {
@@ -522,6 +526,11 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
     const Lut lut{f.lut_lo, f.lut_hi};
     uint2 *ch = reinterpret_cast<uint2 *>(f.sm + S_CH) + f.tid;
     const u32 *lp = f.sm + S_LP + c * SUMK + f.k0 * TS + f.t;
+    u32 *nii = f.sm + S_NII;
+    u32 *X = f.sm + S_X;
+    u32 *le = f.sm + (c ? S_Z : S_Y) + f.t;
+    /* a warp whose windows are all past the task's last one only keeps the barriers */
+    if (f.wact) {
     /* row a4 fused into phase 1: this thread's 16 (Lu+Lp, Lu-Lp) pairs are formed
      * step by step from the TMEM static sums, the parity plane and the a-priori
      * LLRs gathered at its QPP indices, used at once and kept in smem for phase 2 */
@@ -537,9 +546,6 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
         else av[s] = lds_q(qq[s], c);
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pv[s]) : "r"(lp_s + 4 * s * TS));
     };
-    u32 *nii = f.sm + S_NII;
-    u32 *X = f.sm + S_X;
-    u32 *le = f.sm + (c ? S_Z : S_Y) + f.t;
     u32 m[NS];
     if (!tail_thr) {
         /* alpha_0 of window j: known start state, zero in iteration 1, NII afterwards (R13) */
@@ -593,10 +599,12 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
 #pragma unroll
         for (int s = 0; s < NS; s++) X[(NS + s) * TS + f.t] = m[s];      /* beta_16 -> head thread */
     }
-    prof_mark(P_PH1);
     tm_wait_st();
+    }   /* f.wact */
+    prof_mark(P_PH1);
     __syncthreads();        /* hand-over; also orders this half-iteration's NII reads before its writes */
     prof_mark(P_BAR1);
+    if (!f.wact) return;
 
     u32 bufA[NS], bufB[NS];
     if (!tail_thr) {
@@ -663,6 +671,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
     f.tid = tid;
     f.t = tid - (tail_thr ? WMAX : 0);
     const bool active = f.t < T;
+    f.wact = (f.t & ~31) < T;                   /* head / tail warps are 32-window aligned */
     f.M = M;
     f.p = active ? f.t / M : 0;         /* inactive threads run on pair 0 window 0 data; outputs unused */
     f.j = active ? f.t - f.p * M : 0;
@@ -688,6 +697,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         const int64_t olo = clo >= 0 ? desc[clo].llr_off : 0, ohi = chi >= 0 ? desc[chi].llr_off : 0;
         const int n0 = j * W + f.k0;
         u32 *tmp = sm + S_CH;                 /* natural Ls, window-major, for the interleaved gather */
+        {
         /* every global load of the staging first (one round trip): the thread's 16
          * LLRs of each stream and CB, its QPP word indices and, for the last
          * window's tail thread, the 12 tail columns */
@@ -764,17 +774,19 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             q1[s] += f.pM;
             q2[s] += f.pM;
         }
+        }   /* f.wact */
         __syncthreads();
-#pragma unroll
-        for (int s = 0; s < HW; s++)          /* interleaved systematic Ls[Pi(jW+k)] */
-            sn[s] = __vsub2(tmp[q2[s]], sm[S_LP + SUMK + (f.k0 + s) * TS + f.t]);
         {
+            u32 sn[HW];
+#pragma unroll
+            for (int s = 0; s < HW; s++)          /* interleaved systematic Ls[Pi(jW+k)] */
+                sn[s] = __vsub2(tmp[q2[s]], sm[S_LP + SUMK + (f.k0 + s) * TS + f.t]);
             const u32 base = smem_addr(sm);
 #pragma unroll
             for (int s = 0; s < HW; s++) qq[s] = (base + 4 * (S_Z + q1[s])) | ((base + 4 * (S_Y + q2[s])) << 16);
+            tm_store16(f.ts + HW, sn);
+            tm_wait_st();
         }
-        tm_store16(f.ts + HW, sn);
-        tm_wait_st();
         __syncthreads();
         prof_mark(P_STAGE);
     }
@@ -800,21 +812,8 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             u32 wlo = 0, whi = 0;
             int mlo = 0, mhi = 0;             /* MI statistic of this thread's steps (R29) */
             u32 sn[HW];
-            /* the CBs' output offsets are loaded first: their round trip overlaps
-             * the L_APP pass below instead of following the stop decision */
-            int64_t obit[2] = {0, 0}, oext[2] = {0, 0};
-            if (active) {
-#pragma unroll
-                for (int l = 0; l < 2; l++) {
-                    const int cbx = sh.cb[2 * f.p + l];
-                    if (cbx >= 0) {
-                        obit[l] = desc[cbx].bit_off;
-                        if (ext_out) oext[l] = desc[cbx].ext_off;
-                    }
-                }
-            }
-            tm_load16_wait(f.ts, sn);
             const int n00 = f.j * W + f.k0, Fl = sh.F[2 * f.p], Fh = sh.F[2 * f.p + 1];
+            tm_load16_wait(f.ts, sn);
 #pragma unroll
             for (int s = 0; s < HW; s++) {
                 const u32 la1n = lds_q(qq[s], 0);                    /* La1_next[n] = Le2[Pi^-1(n)] */
@@ -865,26 +864,58 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                 }
             }
             __syncthreads();
-            decide<PURGE>(sh, NP, it, max_iters, et, tk.K, crc_ok, iters_used, pg);
+            /* stop decision (row a9; R3 / R29), taken by every thread for both CB lanes of
+             * its pair from the complete CRC register and MI sum; the head (tail) thread
+             * of window 0 is the low (high) lane's owner: it records crc_ok /
+             * iters_used and counts the lane as still running */
+            int running = 0;
             if (active) {
                 const int p = f.p, j = f.j;
 #pragma unroll
                 for (int l = 0; l < 2; l++) {
-                    if (!sh.fin[2 * p + l]) continue;
-                    if (l == (tail_thr ? 1 : 0)) out_bits[obit[l] + j] = hb[l * TS + f.t];
+                    const int e = 2 * p + l;
+                    if (sh.done[e]) continue;
+                    const bool pass = sh.kind[e] != CRN_CRC_NONE && sh.crc[e] == 0;
+                    const int dmi = sh.mi[e] - sh.mip[e];
+                    const bool mi_conv = et == CRN_ET_MI && it >= 2 && (dmi < 0 ? -dmi : dmi) <= (tk.K - sh.F[e]) * CRN_MI_EPS;
+                    const bool fin = (et == CRN_ET_CRC && pass) || mi_conv || it == max_iters;
+                    const bool owner = j == 0 && l == (tail_thr ? 1 : 0);
+                    if (!fin) {
+                        running |= owner;
+                        continue;
+                    }
+                    if (owner) {
+                        crc_ok[sh.cb[e]] = pass;
+                        if (PURGE && !pass && pg.tb[e] >= 0)      /* decoding failure: its TB is lost */
+                            *(volatile uint8_t *)&pg.dead[pg.tb[e]] = 1;
+                        if (iters_used) iters_used[sh.cb[e]] = (uint8_t)it;
+                    }
+                    if (l == (tail_thr ? 1 : 0)) out_bits[sh.bo[e] + j] = hb[l * TS + f.t];
                     if (ext_out) {
+                        const int64_t oe = sh.eo[e] + j * W + f.k0;
 #pragma unroll
                         for (int s = 0; s < HW; s++) {
                             const u32 x = lds_q(qq[s], 0);
-                            ext_out[oext[l] + j * W + f.k0 + s] = (int16_t)(l ? (x >> 16) : (x & 0xFFFFu));
+                            ext_out[oe + s] = (int16_t)(l ? (x >> 16) : (x & 0xFFFFu));
                         }
                     }
                 }
             }
+            prof_mark(P_HD);
+            /* one counting barrier: every read of this iteration's flags is before it */
+            const int left = __syncthreads_count(running);
+            if (active && f.j == 0) {
+                const int e = 2 * f.p + (tail_thr ? 1 : 0);
+                if (!sh.done[e]) {
+                    sh.done[e] = !running;
+                    sh.mip[e] = sh.mi[e];
+                }
+                sh.crc[e] = 0;
+                sh.mi[e] = 0;
+            }
+            prof_mark(P_HD);
+            if (left == 0) break;
         }
-        prof_mark(P_HD);
-        if (finish_iteration(sh, NP) == 0) break;
-        prof_mark(P_HD);
     }
 }
 
@@ -1208,6 +1239,7 @@ struct NextSh {
     int *task;
     crn_task *tk;
     int *cb, *F, *kind, *tb;
+    int64_t *bo, *eo;
 };
 
 __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks, const crn_task *__restrict__ tasks,
@@ -1228,12 +1260,16 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
         if (cb < 0) {
             nx.F[e] = 0;
             nx.kind[e] = 0;
+            nx.bo[e] = 0;
+            nx.eo[e] = 0;
             if (nx.tb) nx.tb[e] = -1;
             continue;
         }
         const crn_cb_desc &d = desc[cb];
         nx.F[e] = d.F;
         nx.kind[e] = d.crc_kind;
+        nx.bo[e] = d.bit_off;
+        nx.eo[e] = d.ext_off;
         if (nx.tb) nx.tb[e] = d.reserved;
         const int esz = sh8 < 0 ? 2 : 1;                 /* int16 or int8 LLRs */
         const int64_t off = esz * d.llr_off;
@@ -1274,7 +1310,9 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     int *counter = (int *)ws;
     const int tid = threadIdx.x;
     u32 *s_crcnib = smem + S_CRCNIB;
-    const TaskSh sh{s_crcnib, s_cb, s_F, s_kind, s_mi, s_mip, s_mitab, s_done, s_fin, s_crc, &s_left};
+    int64_t *s_bo = reinterpret_cast<int64_t *>(smem + S_OFFS), *s_eo = s_bo + 2 * MAXP, *s_nbo = s_eo + 2 * MAXP,
+            *s_neo = s_nbo + 2 * MAXP;
+    const TaskSh sh{s_crcnib, s_cb, s_F, s_kind, s_mi, s_mip, s_mitab, s_done, s_fin, s_crc, &s_left, s_bo, s_eo};
     const Purge pg{s_tb, tb_dead};
     for (int i = tid; i < 256; i += BLOCK) s_mitab[i] = tab.mi_tab[i];
     for (int i = tid; i < 2 * CRN_CRC_NIB_WORDS; i += BLOCK) s_crcnib[i] = tab.crc_nib[i];
@@ -1291,7 +1329,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
 
     /* Tasks are claimed one ahead (claim_next): task t+1's metadata and LLRs
      * move on-chip / into L2 while task t decodes. */
-    const NextSh nx{&s_ntask, &s_ntk, s_ncb, s_nF, s_nkind, PURGE ? s_ntb : nullptr};
+    const NextSh nx{&s_ntask, &s_ntk, s_ncb, s_nF, s_nkind, PURGE ? s_ntb : nullptr, s_nbo, s_neo};
     prof_init();
     if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
     for (;;) {
@@ -1304,6 +1342,8 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             s_cb[e] = cb;
             s_F[e] = s_nF[e];
             s_kind[e] = s_nkind[e];
+            s_bo[e] = s_nbo[e];
+            s_eo[e] = s_neo[e];
             s_done[e] = cb < 0;
             s_fin[e] = 0;
             s_crc[e] = 0;

@@ -99,9 +99,17 @@ extern "C" int crn_segment_tb(int64_t tbs, crn_seg *o) {
     int64_t B = tbs + 24, C, L, Bp;
     if (B <= Z) { L = 0; C = 1; Bp = B; }
     else { L = 24; C = (B + Z - L - 1) / (Z - L); Bp = B + C * L; }
-    int ip = -1;
-    for (int i = 0; i < CRN_NUM_K; i++)
-        if (C * k_at(i) >= Bp) { ip = i; break; }
+    /* K+ = the smallest table size with C K >= B': the table is every multiple of
+     * 8 / 16 / 32 / 64 in its four ranges, so round ceil(B'/C) up in its range */
+    const int64_t x = (Bp + C - 1) / C;
+    int64_t kp;
+    if (x <= 40) kp = 40;
+    else if (x <= 512) kp = (x + 7) / 8 * 8;
+    else if (x <= 1024) kp = (x + 15) / 16 * 16;
+    else if (x <= 2048) kp = (x + 31) / 32 * 32;
+    else if (x <= 6144) kp = (x + 63) / 64 * 64;
+    else return CRN_EINVAL;
+    const int ip = crn_k_index((int32_t)kp);
     if (ip < 0) return CRN_EINVAL;
     int64_t Kp = k_at(ip), Km = 0, Cm = 0;
     if (C > 1) {
@@ -368,30 +376,60 @@ int crn_validate(const crn_cb_desc *d, int n, bool want_ext) {
 /* Bucket by K (largest first: longest tasks start first), pair equal-K CBs in
  * index order, group floor(6144/K) pairs per task. */
 void crn_build_tasks(const crn_cb_desc *d, const int *sel, int n, std::vector<crn_task> &tasks,
-                     std::vector<crn_pair> &pairs) {
+                     std::vector<crn_pair> &pairs, int spread_to) {
     const size_t t0 = tasks.size();
     std::vector<int> idx(sel, sel + n);
     std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return d[a].K > d[b].K; });
+    struct Bucket {
+        int K, M, W, per, np;
+        size_t s, e;
+    };
+    std::vector<Bucket> bk;
+    int64_t n_tasks = 0;
     size_t s = 0;
     while (s < idx.size()) {
         int K = d[idx[s]].K;
         size_t e = s;
         while (e < idx.size() && d[idx[e]].K == K) e++;
-        int M, W;
-        crn_windows(K, &M, &W);
-        int per = std::max(1, std::min(CRN_TASK_SUMK / K, CRN_MAX_PAIRS));
-        if (W != 32)                        /* split-window path: shared memory and TMEM bound the task */
-            while (per > 1 && !crn_split_fits(W, M, per)) per--;
+        Bucket b;
+        b.K = K; b.s = s; b.e = e;
+        crn_windows(K, &b.M, &b.W);
+        b.per = std::max(1, std::min(CRN_TASK_SUMK / K, CRN_MAX_PAIRS));
+        if (b.W != 32)                      /* split-window path: shared memory and TMEM bound the task */
+            while (b.per > 1 && !crn_split_fits(b.W, b.M, b.per)) b.per--;
+        b.np = (int)((e - s + 1) / 2);
+        n_tasks += (b.np + b.per - 1) / b.per;
+        bk.push_back(b);
+        s = e;
+    }
+    /* a small batch (fewer tasks than CTAs) is spread over more CTAs: the bucket
+     * whose tasks hold the most windows gives up one pair per task while the
+     * batch still fits in spread_to tasks -- fewer windows per SM mean fewer
+     * busy warps sharing its ALU pipe, so each task's dependent chain runs faster */
+    while (spread_to > 0 && n_tasks < spread_to) {
+        int best = -1;
+        for (int i = 0; i < (int)bk.size(); i++)
+            if (bk[i].per > 1 && bk[i].np > 1 && (best < 0 || bk[i].per * bk[i].M > bk[best].per * bk[best].M))
+                best = i;
+        if (best < 0) break;
+        Bucket &b = bk[best];
+        const int cur = (b.np + b.per - 1) / b.per;              /* one more, balanced, task */
+        const int per2 = (b.np + cur) / (cur + 1);
+        const int64_t grow = (b.np + per2 - 1) / per2 - cur;
+        if (n_tasks + grow > spread_to) break;
+        n_tasks += grow;
+        b.per = per2;
+    }
+    for (const Bucket &b : bk) {
         int32_t first_pair = (int32_t)pairs.size();
-        for (size_t i = s; i < e; i += 2) pairs.push_back({idx[i], i + 1 < e ? idx[i + 1] : -1});
+        for (size_t i = b.s; i < b.e; i += 2) pairs.push_back({idx[i], i + 1 < b.e ? idx[i + 1] : -1});
         int32_t np = (int32_t)pairs.size() - first_pair;
-        for (int32_t p = 0; p < np; p += per) {
+        for (int32_t p = 0; p < np; p += b.per) {
             crn_task t;
-            t.K = K; t.M = M; t.W = W; t.n_pairs = std::min(per, np - p);
-            t.pair0 = first_pair + p; t.kidx = crn_k_index(K);
+            t.K = b.K; t.M = b.M; t.W = b.W; t.n_pairs = std::min(b.per, np - p);
+            t.pair0 = first_pair + p; t.kidx = crn_k_index(b.K);
             tasks.push_back(t);
         }
-        s = e;
     }
     /* longest tasks first (LPT order for the persistent grid): a task's critical
      * path is the trellis steps one thread runs per half-iteration -- 16 on the
@@ -401,14 +439,16 @@ void crn_build_tasks(const crn_cb_desc *d, const int *sel, int n, std::vector<cr
                      [&](const crn_task &a, const crn_task &b) { return steps(a) > steps(b); });
 }
 
-static int plan_build(const crn_cb_desc *desc, int n, bool want_ext, cudaStream_t st, bool async, Plan *P) {
+static int plan_build(const crn_cb_desc *desc, int n, bool want_ext, cudaStream_t st, bool async, Plan *P,
+                      int spread_to) {
     int rc = crn_validate(desc, n, want_ext);
     if (rc) return rc;
     std::vector<crn_task> tasks;
     std::vector<crn_pair> pairs;
     std::vector<int> all(n);
     for (int i = 0; i < n; i++) all[i] = i;
-    crn_build_tasks(desc, all.data(), n, tasks, pairs);
+    crn_build_tasks(desc, all.data(), n, tasks, pairs, spread_to);
+    P->spread = spread_to;
     size_t b0 = sizeof(crn_cb_desc) * (size_t)n, b1 = sizeof(crn_task) * tasks.size(),
            b2 = sizeof(crn_pair) * pairs.size();
     size_t o1 = (b0 + 255) & ~(size_t)255, o2 = (o1 + b1 + 255) & ~(size_t)255, tot = o2 + b2 + 256;
@@ -473,7 +513,7 @@ extern "C" int crn_plan_create(const crn_cb_desc *desc, int32_t n_cb, void **pla
     if (rc) return rc;
     Plan *P = new Plan();
     P->dev = dev;
-    rc = plan_build(desc, n_cb, true, 0, false, P);
+    rc = plan_build(desc, n_cb, true, 0, false, P, t->grid);
     if (rc) { delete P; return rc; }
     P->h_desc.assign(desc, desc + n_cb);
     *plan = P;
@@ -547,7 +587,7 @@ extern "C" int crn_plan_layout(void *plan, int32_t *task_of_cb, int32_t n_cb) {
     std::vector<crn_pair> pairs;
     std::vector<int> all(P->n_cb);
     for (int i = 0; i < P->n_cb; i++) all[i] = i;
-    crn_build_tasks(P->h_desc.data(), all.data(), P->n_cb, tasks, pairs);
+    crn_build_tasks(P->h_desc.data(), all.data(), P->n_cb, tasks, pairs, P->spread);
     for (int i = 0; i < n_cb; i++) task_of_cb[i] = -1;
     for (size_t t = 0; t < tasks.size(); t++)
         for (int p = 0; p < tasks[t].n_pairs; p++) {
@@ -601,7 +641,7 @@ extern "C" int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb, const 
     Plan P;
     P.dev = dev;
     P.variant = (flags & CRN_EXT_SCALED) ? CRN_VARIANT_SCALED : CRN_VARIANT_MAXLOG;
-    rc = plan_build(hdesc, n_cb, ext != nullptr, st, true, &P);
+    rc = plan_build(hdesc, n_cb, ext != nullptr, st, true, &P, t->grid);
     if (rc) {
         if (P.mem) cudaFreeAsync(P.mem, st);
         return rc;

@@ -38,6 +38,7 @@ struct Plan {
     int grid_cap = 0;                  /* persistent-grid limit (crn_plan_set_grid), 0 = one CTA per SM */
     int llr8 = -1;                     /* LLR format (crn_plan_set_llr_format): -1 int16, else int8 << llr8 */
     int n_tb = 0;                      /* TB ids in the descriptors' reserved field: 0..n_tb-1 */
+    int spread = 0;                    /* the spread_to its tasks were built with (crn_build_tasks) */
     uint8_t *d_tb_dead = nullptr;      /* per TB: a CB of it failed (purge) */
     HostPipe *pipe = nullptr;
 };
@@ -49,9 +50,11 @@ int crn_get_ws(int dev, void *stream, size_t bytes, void **ws);
 /* Descriptor validation (include/crn.h CRN_EINVAL rules). */
 int crn_validate(const crn_cb_desc *d, int n, bool want_ext);
 /* Bucket by K (largest first), pair equal-K CBs, group pairs into CTA tasks.
- * Only the CBs idx[0..n_idx) take part; pair0 of the tasks indexes `pairs`. */
+ * Only the CBs idx[0..n_idx) take part; pair0 of the tasks indexes `pairs`.
+ * spread_to > 0: a batch of fewer tasks is cut into smaller tasks, up to
+ * spread_to of them (the persistent grid), so a small batch spreads over the SMs. */
 void crn_build_tasks(const crn_cb_desc *d, const int *idx, int n_idx, std::vector<crn_task> &tasks,
-                     std::vector<crn_pair> &pairs);
+                     std::vector<crn_pair> &pairs, int spread_to = 0);
 /* Launch the decode kernel over n_tasks tasks (device arrays), workspace from the cache if ws == NULL. */
 int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn_task *d_tasks, int n_tasks,
                      const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,

@@ -418,7 +418,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             std::vector<crn_pair> pairs;
             std::vector<int> sel(q.n_cb);
             for (int i = 0; i < q.n_cb; i++) sel[i] = i;
-            crn_build_tasks(q.desc, sel.data(), q.n_cb, tasks, pairs);
+            crn_build_tasks(q.desc, sel.data(), q.n_cb, tasks, pairs, t->grid);
             const int64_t n_llr = g_llr[x], n_words = g_words[x];
             const Layout L = layout(q.n_cb, (int)tasks.size(), (int)pairs.size(), n_llr, n_words, esz);
             const int b = ti & 1;
@@ -553,7 +553,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             std::vector<crn_pair> pairs;
             std::vector<int> sel(m_cb);
             for (int i = 0; i < m_cb; i++) sel[i] = i;
-            crn_build_tasks(mdesc.data(), sel.data(), m_cb, tasks, pairs);
+            crn_build_tasks(mdesc.data(), sel.data(), m_cb, tasks, pairs, t->grid);
             const Layout L = layout(m_cb, (int)tasks.size(), (int)pairs.size(), m_llr, m_words);
             uint8_t *dm = (uint8_t *)dr.dmem;
             int16_t *dl[3];

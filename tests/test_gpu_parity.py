@@ -167,6 +167,16 @@ def test_many_small_blocks_multi_pair_tasks(orc):
     _raw_parity(d, _random_llr(d, rng, 200), 4, False)
 
 
+def test_full_multi_pair_tasks_beyond_one_wave(orc):
+    """Enough small CBs that the tasks stay fully packed (96 pairs of K=64 per
+    task, more tasks than CTAs: no spreading) next to a spread small remainder,
+    with early termination."""
+    rng = np.random.default_rng(18)
+    Ks = [64] * (2 * 96 * 160) + [40] * 97 + [2112] * 3
+    d = _desc_for(list(rng.permutation(Ks)))
+    _raw_parity(d, _random_llr(d, rng, 60), 6, True)
+
+
 def test_iteration_extremes_and_et(orc):
     rng = np.random.default_rng(9)
     d = _desc_for([6144, 6144, 6144, 512, 40])
