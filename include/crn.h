@@ -165,6 +165,16 @@ int crn_logmap_lut(int32_t *out);
  * CBs, group pairs) CB i is decoded in, in issue order; n_cb must equal the
  * plan's.  Returns the number of tasks, or CRN_EINVAL. */
 int crn_plan_layout(void *plan, int32_t *task_of_cb, int32_t n_cb);
+/* Host-only diagnostic of row a1 (no device needed): buckets, pairs and tasks
+ * n_cb HOST descriptors the way a plan does (spread_to > 0: a batch that fills
+ * fewer CTAs is cut into more, smaller tasks, up to spread_to CTAs).  Per CB:
+ * task_of_cb[i] = its task in issue order.  Per task (arrays of >= n_cb + 1
+ * entries, may be NULL): task_info[4 t .. 4 t + 3] = K, n_pairs, windows
+ * (n_pairs * M), group flag (1: a four-warp group task, three per CTA).
+ * *units = the CTAs the tasks keep busy at once (whole-CTA tasks + ceil(group
+ * tasks / 3)).  Returns the number of tasks, or CRN_EINVAL (invalid descriptors). */
+int crn_task_layout(const crn_cb_desc *desc, int32_t n_cb, int32_t spread_to, int32_t *task_of_cb,
+                    int32_t *task_info, int32_t *units);
 /* Number of decode-kernel launches one crn_plan_decode performs (for gpu_launches). */
 int crn_plan_launches(void *plan);
 void crn_plan_destroy(void *plan);

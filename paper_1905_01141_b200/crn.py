@@ -60,6 +60,7 @@ _SIGS = {
     "crn_plan_create": (C.c_int, [vp, C.c_int32, P(vp)]),
     "crn_plan_decode": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp]),
     "crn_plan_launches": (C.c_int, [vp]),
+    "crn_task_layout": (C.c_int, [vp, C.c_int32, C.c_int32, i32p, i32p, i32p]),
     "crn_plan_layout": (C.c_int, [vp, i32p, C.c_int32]),
     "crn_plan_set_variant": (C.c_int, [vp, C.c_int32]),
     "crn_plan_set_purge": (C.c_int, [vp, C.c_int32]),
@@ -163,6 +164,20 @@ def decode_batch_ex(desc, n_cb: int, l0, l1, l2, max_iters: int, early_term: boo
                                    flags, _ptr(out_bits), _ptr(crc_ok), _ptr(iters_used), _ptr(ext_out),
                                    _ptr(workspace), workspace_bytes, _stream(stream)),
          "crn_decode_batch_ex")
+
+
+def task_layout(desc: np.ndarray, spread_to: int = 0):
+    """crn_task_layout (host only): (task_of_cb[n_cb], task_info[n_tasks, 4] = K, n_pairs,
+    windows, group flag, units)."""
+    desc = np.ascontiguousarray(desc, DESC_DTYPE)
+    n = desc.size
+    tof = np.zeros(max(n, 1), np.int32)
+    info = np.zeros((n + 1, 4), np.int32)
+    units = np.zeros(1, np.int32)
+    nt = lib().crn_task_layout(desc.ctypes.data if n else None, n, spread_to, _np(tof, C.c_int32),
+                               _np(info, C.c_int32), _np(units, C.c_int32))
+    _chk(nt if nt < 0 else 0, "crn_task_layout")
+    return tof[:n], info[:nt], int(units[0])
 
 
 def workspace_bytes() -> int:

@@ -377,6 +377,35 @@ __device__ __forceinline__ u32 smem_addr(const void *p) { return (u32)__cvta_gen
 
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+/* ---- thread groups (W = 32 path).  G = 1: the whole CTA runs one task of up to
+ * 192 windows (tasks with sum K <= 6144).  G = 3: the CTA runs three independent
+ * tasks of up to 64 windows (sum K <= 2048), one per group of four warps (two
+ * head, two tail warps, one per SM sub-partition), each with its own named
+ * barrier.  Group g owns window columns [64 g, 64 g + 64), pair slots
+ * [32 g, 32 g + 32) and TMEM column block g, so the shared-memory layout and the
+ * TMEM addressing are the G = 1 ones. */
+constexpr int G3 = 3;
+constexpr int GB3 = BLOCK / G3;                 /* threads per group (128) */
+constexpr int GWIN3 = WMAX / G3;                /* windows per group (64) */
+constexpr int GPB3 = MAXP / G3;                 /* pair slots per group (32) */
+static_assert(G3 == CRN_GROUPS && GWIN3 == CRN_GRP_WIN && GPB3 == CRN_GRP_PAIRS && 32 * CRN_GRP_WIN == CRN_GRP_SUMK,
+              "group geometry (crn_internal.h)");
+
+template <int G>
+__device__ __forceinline__ void gsync(int g) {
+    if constexpr (G == 1) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(BLOCK / G) : "memory");
+}
+/* barrier that also counts the group's threads with pred != 0 */
+template <int G>
+__device__ __forceinline__ int gsync_count(int g, int pred) {
+    if constexpr (G == 1) return __syncthreads_count(pred);
+    int r;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\tbar.red.popc.u32 %0, %2, %3, q;\n\t}"
+                 : "=r"(r) : "r"(pred), "r"(1 + g), "n"(BLOCK / G) : "memory");
+    return r;
+}
+
 /* ======================================================================
  * Fast path: W = 32 (every K that is a multiple of 32: all K >= 1056 and 15
  * smaller sizes).  Window t of the task is split between two threads: the
@@ -396,6 +425,7 @@ __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sy
  * ====================================================================== */
 struct SCtx {
     u32 *sm;        /* shared-memory base (fast layout) */
+    int g;          /* thread group (G = 3: four warps running their own task; G = 1: the whole CTA) */
     u32 ta;         /* this thread's TMEM metric slots: lane quadrant + 128-column block */
     u32 ts;         /* this thread's TMEM statics: Ls-Lp1 (16 columns), Ls[Pi]-Lp2 (16) */
     int tid, t, p, j, M, pM, k0;
@@ -519,7 +549,7 @@ __device__ __forceinline__ u32 lds_q(u32 qq, int c) {
 
 /* One half-iteration of constituent c (rows a5-a8).  Le -> Y (c = 0, natural
  * order) or Z (c = 1, interleaved order). */
-template <int VAR>
+template <int VAR, int G>
 __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, int it, const u32 (&qq)[HW],
                                            bool zero_la) {
     constexpr bool LOGV = VAR == CRN_VARIANT_LOGMAP;
@@ -602,7 +632,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
     tm_wait_st();
     }   /* f.wact */
     prof_mark(P_PH1);
-    __syncthreads();        /* hand-over; also orders this half-iteration's NII reads before its writes */
+    gsync<G>(f.g);          /* hand-over; also orders this half-iteration's NII reads before its writes */
     prof_mark(P_BAR1);
     if (!f.wact) return;
 
@@ -652,7 +682,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
     }
 }
 
-template <int VAR, bool PURGE, bool LLR8>
+template <int VAR, bool PURGE, bool LLR8, int G>
 __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
                                               const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
                                               const int16_t *__restrict__ l2, int max_iters, int et,
@@ -662,20 +692,25 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                                               int sh8) {
     constexpr int W = 32;
     const int M = tk.M, NP = tk.n_pairs, T = NP * M;
+    constexpr int GWIN = WMAX / G;              /* windows of the group's task */
     const int tid = threadIdx.x, warp = tid >> 5;
-    const bool tail_thr = tid >= WMAX;          /* warp-uniform: WMAX = 6 warps */
+    const int g = G == 1 ? 0 : tid / (BLOCK / G), ltid = tid - g * (BLOCK / G);
+    const bool tail_thr = ltid >= GWIN;         /* warp-uniform: GWIN = 6 or 2 warps */
+    const int tl = ltid - (tail_thr ? GWIN : 0);    /* the thread's window in its task */
     SCtx f;
     f.sm = sm;
+    f.g = g;
     f.ta = tmem + ((u32)((warp & 3) * 32) << 16) + (u32)((warp >> 2) * 128);
     f.ts = tmem + ((u32)((warp & 3) * 32) << 16) + (u32)(3 * 128 + (warp >> 2) * 2 * HW);
     f.tid = tid;
-    f.t = tid - (tail_thr ? WMAX : 0);
-    const bool active = f.t < T;
-    f.wact = (f.t & ~31) < T;                   /* head / tail warps are 32-window aligned */
+    f.t = g * GWIN + tl;                        /* its window column in the shared planes */
+    const bool active = tl < T;
+    f.wact = (tl & ~31) < T;                    /* head / tail warps are 32-window aligned */
     f.M = M;
-    f.p = active ? f.t / M : 0;         /* inactive threads run on pair 0 window 0 data; outputs unused */
-    f.j = active ? f.t - f.p * M : 0;
-    f.pM = f.p * M;
+    const int pl = active ? tl / M : 0;         /* inactive threads run on pair 0 window 0 data; outputs unused */
+    f.p = g * (MAXP / G) + pl;                  /* the pair's slot in the per-CB shared arrays */
+    f.j = active ? tl - pl * M : 0;
+    f.pM = g * GWIN + pl * M;                   /* the pair's first window column */
     f.k0 = tail_thr ? HW : 0;
     if (VAR == CRN_VARIANT_LOGMAP) {
         f.lut_lo = c_logmap[0];
@@ -696,7 +731,8 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         const int Flo = sh.F[2 * p], Fhi = sh.F[2 * p + 1];
         const int64_t olo = clo >= 0 ? desc[clo].llr_off : 0, ohi = chi >= 0 ? desc[chi].llr_off : 0;
         const int n0 = j * W + f.k0;
-        u32 *tmp = sm + S_CH;                 /* natural Ls, window-major, for the interleaved gather */
+        u32 *tmp = sm + S_Z;                  /* natural Ls, window-major, for the interleaved gather
+                                                 (the Z plane is first written in DEC2 of iteration 1) */
         {
         /* every global load of the staging first (one round trip): the thread's 16
          * LLRs of each stream and CB, its QPP word indices and, for the last
@@ -775,7 +811,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             q2[s] += f.pM;
         }
         }   /* f.wact */
-        __syncthreads();
+        gsync<G>(g);
         {
             u32 sn[HW];
 #pragma unroll
@@ -787,22 +823,22 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             tm_store16(f.ts + HW, sn);
             tm_wait_st();
         }
-        __syncthreads();
+        gsync<G>(g);
         prof_mark(P_STAGE);
     }
 
     for (int it = 1; it <= max_iters; it++) {
         /* DEC1: La1[n] = Le2[Pi^-1(n)] gathered from Z (zero in iteration 1) */
         prof_mark(P_CHUNK);
-        siso_split<VAR>(f, tail_thr, 0, it, qq, it == 1);
+        siso_split<VAR, G>(f, tail_thr, 0, it, qq, it == 1);
         prof_mark(P_PH2);
-        __syncthreads();
+        gsync<G>(g);
         prof_mark(P_BAR2);
         /* DEC2: La2[i] = Le1[Pi(i)] gathered from Y */
         prof_mark(P_CHUNK);
-        siso_split<VAR>(f, tail_thr, 1, it, qq, false);
+        siso_split<VAR, G>(f, tail_thr, 1, it, qq, false);
         prof_mark(P_PH2);
-        __syncthreads();
+        gsync<G>(g);
         prof_mark(P_BAR2);
         if (!et && it != max_iters) continue;     /* fixed mode: decide only at the end */
 
@@ -836,7 +872,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                     atomicAdd(&sh.mi[2 * f.p + 1], mhi);
                 }
             }
-            __syncthreads();
+            gsync<G>(g);
             if (active) {
                 /* the window's 32 hard decisions of one CB lane: the head thread takes
                  * the low (first) CB of the pair, the tail thread the high one */
@@ -863,7 +899,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                     atomicXor(&sh.crc[2 * p + l], r3);
                 }
             }
-            __syncthreads();
+            gsync<G>(g);
             /* stop decision (row a9; R3 / R29), taken by every thread for both CB lanes of
              * its pair from the complete CRC register and MI sum; the head (tail) thread
              * of window 0 is the low (high) lane's owner: it records crc_ok /
@@ -903,7 +939,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             }
             prof_mark(P_HD);
             /* one counting barrier: every read of this iteration's flags is before it */
-            const int left = __syncthreads_count(running);
+            const int left = gsync_count<G>(g, running);
             if (active && f.j == 0) {
                 const int e = 2 * f.p + (tail_thr ? 1 : 0);
                 if (!sh.done[e]) {
@@ -1297,8 +1333,8 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     uint8_t *const tb_dead = PURGE ? tb_dead_arg : nullptr;
     const int sh8 = (variant >> 8) - 1;         /* LLR format: -1 int16, else int8 << sh8 (LLR8) */
     extern __shared__ __align__(16) u32 smem[];
-    __shared__ int s_ntask, s_left;
-    __shared__ crn_task s_ntk;
+    __shared__ int s_ntask[G3], s_left[G3];
+    __shared__ crn_task s_ntk[G3];
     __shared__ int s_ncb[2 * MAXP], s_nF[2 * MAXP], s_nkind[2 * MAXP], s_ntb[2 * MAXP];
     __shared__ int s_tb[2 * MAXP];
     __shared__ u32 s_tmem;
@@ -1312,7 +1348,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     u32 *s_crcnib = smem + S_CRCNIB;
     int64_t *s_bo = reinterpret_cast<int64_t *>(smem + S_OFFS), *s_eo = s_bo + 2 * MAXP, *s_nbo = s_eo + 2 * MAXP,
             *s_neo = s_nbo + 2 * MAXP;
-    const TaskSh sh{s_crcnib, s_cb, s_F, s_kind, s_mi, s_mip, s_mitab, s_done, s_fin, s_crc, &s_left, s_bo, s_eo};
+    const TaskSh sh{s_crcnib, s_cb, s_F, s_kind, s_mi, s_mip, s_mitab, s_done, s_fin, s_crc, s_left, s_bo, s_eo};
     const Purge pg{s_tb, tb_dead};
     for (int i = tid; i < 256; i += BLOCK) s_mitab[i] = tab.mi_tab[i];
     for (int i = tid; i < 2 * CRN_CRC_NIB_WORDS; i += BLOCK) s_crcnib[i] = tab.crc_nib[i];
@@ -1328,15 +1364,29 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     const u32 tmem = s_tmem;
 
     /* Tasks are claimed one ahead (claim_next): task t+1's metadata and LLRs
-     * move on-chip / into L2 while task t decodes. */
-    const NextSh nx{&s_ntask, &s_ntk, s_ncb, s_nF, s_nkind, PURGE ? s_ntb : nullptr, s_nbo, s_neo};
+     * move on-chip / into L2 while task t decodes -- while the batch still has
+     * more than two tasks per task slot left; near its end a slot claims only
+     * when it is free, so no task waits behind a busy one while a slot idles.
+     * The host orders whole-CTA tasks (W = 32 with sum K <= 6144, and the split
+     * path) before group tasks (crn_task.grp); a CTA that claims a group task
+     * switches to three groups of four warps, each claiming its own tasks. */
+    const int slots = (int)gridDim.x * G3;
+    auto ahead = [&]() { return *(volatile int *)counter + slots < n_tasks; };
+    const NextSh nx{&s_ntask[0], &s_ntk[0], s_ncb, s_nF, s_nkind, PURGE ? s_ntb : nullptr, s_nbo, s_neo};
     prof_init();
     if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
+    bool pend = false;                          /* warp 0: the next task is still to be claimed */
+    bool grp_mode = false;
     for (;;) {
+        if (pend && tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
         __syncthreads();                        /* next slots filled */
-        const int task = s_ntask;
+        const int task = s_ntask[0];
         if (task >= n_tasks) break;
-        const crn_task tk = s_ntk;
+        const crn_task tk = s_ntk[0];
+        if (tk.grp) {                           /* group tasks from here on: group 0 holds this one */
+            grp_mode = true;
+            break;
+        }
         for (int e = tid; e < 2 * tk.n_pairs; e += BLOCK) {
             const int cb = s_ncb[e];
             s_cb[e] = cb;
@@ -1359,23 +1409,26 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             }
         }
         __syncthreads();                        /* next slots consumed */
-        if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
+        if (tid < 32) {
+            pend = !ahead();
+            if (!pend) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
+        }
         if (PURGE) {                            /* a fully purged task is skipped */
             if (tid == 0) {
                 int left = 0;
                 for (int e = 0; e < 2 * tk.n_pairs; e++) left += !s_done[e];
-                s_left = left;
+                s_left[0] = left;
             }
             __syncthreads();
-            if (s_left == 0) continue;
+            if (s_left[0] == 0) continue;
         }
         prof_mark(P_FETCH);
         /* VAR = LOGMAP: its own kernels; otherwise MAXLOG / SCALED chosen per launch */
 #define CRN_RUN(V)                                                                                                \
         do {                                                                                                      \
             if (tk.W == 32)                                                                                       \
-                run_task_fast<V, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used,  \
-                                              ext_out, tab, smem, tmem, sh, pg, sh8);                             \
+                run_task_fast<V, PURGE, LLR8, 1>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok,           \
+                                                 iters_used, ext_out, tab, smem, tmem, sh, pg, sh8);              \
             else                                                                                                  \
                 run_task_split<V, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, \
                                                ext_out, tab, smem, tmem, sh, pg, sh8);                            \
@@ -1384,6 +1437,65 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
         else if ((variant & 0xFF) == CRN_VARIANT_SCALED) CRN_RUN(CRN_VARIANT_SCALED);
         else CRN_RUN(CRN_VARIANT_MAXLOG);
 #undef CRN_RUN
+    }
+    if (grp_mode) {                             /* CTA-uniform */
+        const int g = tid / GB3, ltid = tid - g * GB3, eb = 2 * GPB3 * g;
+        const NextSh ng{&s_ntask[g], &s_ntk[g], s_ncb + eb, s_nF + eb, s_nkind + eb, PURGE ? s_ntb + eb : nullptr,
+                        s_nbo + eb, s_neo + eb};
+        bool gpend = g > 0;                     /* group 0 starts with the task the CTA claimed */
+        for (;;) {
+            if (gpend && ltid < 32) claim_next(ng, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, ltid, sh8);
+            gsync<G3>(g);                       /* next slots filled */
+            const int task = s_ntask[g];
+            if (task >= n_tasks) break;
+            const crn_task tk = s_ntk[g];
+            if (!tk.grp) __trap();              /* host invariant: group tasks are the batch's last */
+            for (int e = eb + ltid; e < eb + 2 * tk.n_pairs; e += GB3) {
+                const int cb = s_ncb[e];
+                s_cb[e] = cb;
+                s_F[e] = s_nF[e];
+                s_kind[e] = s_nkind[e];
+                s_bo[e] = s_nbo[e];
+                s_eo[e] = s_neo[e];
+                s_done[e] = cb < 0;
+                s_fin[e] = 0;
+                s_crc[e] = 0;
+                s_mi[e] = 0;
+                s_mip[e] = 0;
+                if (PURGE) s_tb[e] = s_ntb[e];
+                if (PURGE && cb >= 0 && s_ntb[e] >= 0 && *(volatile uint8_t *)&tb_dead[s_ntb[e]]) {
+                    s_done[e] = 1;
+                    crc_ok[cb] = 0;
+                    if (iters_used) iters_used[cb] = 0;
+                }
+            }
+            gsync<G3>(g);                       /* next slots consumed */
+            if (ltid < 32) {
+                gpend = !ahead();
+                if (!gpend) claim_next(ng, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, ltid, sh8);
+            }
+            if (PURGE) {
+                if (ltid == 0) {
+                    int left = 0;
+                    for (int e = eb; e < eb + 2 * tk.n_pairs; e++) left += !s_done[e];
+                    s_left[g] = left;
+                }
+                gsync<G3>(g);
+                if (s_left[g] == 0) continue;
+            }
+            if constexpr (VAR == CRN_VARIANT_LOGMAP)
+                run_task_fast<CRN_VARIANT_LOGMAP, PURGE, LLR8, G3>(tk, desc, l0, l1, l2, max_iters, et, out_bits,
+                                                                   crc_ok, iters_used, ext_out, tab, smem, tmem, sh,
+                                                                   pg, sh8);
+            else if ((variant & 0xFF) == CRN_VARIANT_SCALED)
+                run_task_fast<CRN_VARIANT_SCALED, PURGE, LLR8, G3>(tk, desc, l0, l1, l2, max_iters, et, out_bits,
+                                                                   crc_ok, iters_used, ext_out, tab, smem, tmem, sh,
+                                                                   pg, sh8);
+            else
+                run_task_fast<CRN_VARIANT_MAXLOG, PURGE, LLR8, G3>(tk, desc, l0, l1, l2, max_iters, et, out_bits,
+                                                                   crc_ok, iters_used, ext_out, tab, smem, tmem, sh,
+                                                                   pg, sh8);
+        }
     }
     prof_flush();
     asm volatile("tcgen05.fence::before_thread_sync;");

@@ -373,19 +373,34 @@ int crn_validate(const crn_cb_desc *d, int n, bool want_ext) {
     return CRN_OK;
 }
 
+/* Group tasks on or off (CRN_GROUPS=0 in the environment turns them off, for A/B runs). */
+static bool groups_on() {
+    static const int on = [] {
+        const char *e = getenv("CRN_GROUPS");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return on != 0;
+}
+
 /* Bucket by K (largest first: longest tasks start first), pair equal-K CBs in
- * index order, group floor(6144/K) pairs per task. */
-void crn_build_tasks(const crn_cb_desc *d, const int *sel, int n, std::vector<crn_task> &tasks,
-                     std::vector<crn_pair> &pairs, int spread_to) {
+ * index order, group floor(6144/K) pairs per whole-CTA task, or floor(2048/K)
+ * pairs per group task for W = 32 and K <= 2048 (three such tasks share a CTA,
+ * crn_internal.h CRN_GROUPS).  Whole-CTA tasks come first (LPT order), group
+ * tasks last.  Returns the CTAs the appended tasks can keep busy at once:
+ * whole-CTA tasks + ceil(group tasks / 3). */
+int crn_build_tasks(const crn_cb_desc *d, const int *sel, int n, std::vector<crn_task> &tasks,
+                    std::vector<crn_pair> &pairs, int spread_to) {
     const size_t t0 = tasks.size();
     std::vector<int> idx(sel, sel + n);
     std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return d[a].K > d[b].K; });
     struct Bucket {
-        int K, M, W, per, np;
+        int K, M, W, per, np, grp;
         size_t s, e;
+        int64_t tasks() const { return (np + per - 1) / per; }
+        int64_t thirds() const { return (grp ? 1 : CRN_GROUPS) * tasks(); }   /* CTA share x 3 */
     };
     std::vector<Bucket> bk;
-    int64_t n_tasks = 0;
+    int64_t thirds = 0;
     size_t s = 0;
     while (s < idx.size()) {
         int K = d[idx[s]].K;
@@ -394,32 +409,39 @@ void crn_build_tasks(const crn_cb_desc *d, const int *sel, int n, std::vector<cr
         Bucket b;
         b.K = K; b.s = s; b.e = e;
         crn_windows(K, &b.M, &b.W);
-        b.per = std::max(1, std::min(CRN_TASK_SUMK / K, CRN_MAX_PAIRS));
+        b.grp = b.W == 32 && K <= CRN_GRP_SUMK && groups_on();
+        b.per = b.grp ? std::max(1, std::min(CRN_GRP_SUMK / K, CRN_GRP_PAIRS))
+                      : std::max(1, std::min(CRN_TASK_SUMK / K, CRN_MAX_PAIRS));
         if (b.W != 32)                      /* split-window path: shared memory and TMEM bound the task */
             while (b.per > 1 && !crn_split_fits(b.W, b.M, b.per)) b.per--;
         b.np = (int)((e - s + 1) / 2);
-        n_tasks += (b.np + b.per - 1) / b.per;
+        thirds += b.thirds();
         bk.push_back(b);
         s = e;
     }
     /* a small batch (fewer tasks than CTAs) is spread over more CTAs: the bucket
      * whose tasks hold the most windows gives up one pair per task while the
-     * batch still fits in spread_to tasks -- fewer windows per SM mean fewer
+     * batch still fits in spread_to CTAs -- fewer windows per SM mean fewer
      * busy warps sharing its ALU pipe, so each task's dependent chain runs faster */
-    while (spread_to > 0 && n_tasks < spread_to) {
+    const int64_t cap3 = (int64_t)CRN_GROUPS * spread_to;
+    while (spread_to > 0 && thirds < cap3) {
         int best = -1;
         for (int i = 0; i < (int)bk.size(); i++)
             if (bk[i].per > 1 && bk[i].np > 1 && (best < 0 || bk[i].per * bk[i].M > bk[best].per * bk[best].M))
                 best = i;
         if (best < 0) break;
         Bucket &b = bk[best];
-        const int cur = (b.np + b.per - 1) / b.per;              /* one more, balanced, task */
-        const int per2 = (b.np + cur) / (cur + 1);
-        const int64_t grow = (b.np + per2 - 1) / per2 - cur;
-        if (n_tasks + grow > spread_to) break;
-        n_tasks += grow;
-        b.per = per2;
+        const int64_t before = b.thirds();
+        const int cur = (int)b.tasks();                           /* one more, balanced, task */
+        const int per_old = b.per;
+        /* per strictly decreases, so the loop ends (floor((np + cur) / (cur + 1)) alone can
+         * equal per, e.g. np = 16, per = 4) */
+        b.per = std::min(b.per - 1, (b.np + cur) / (cur + 1));
+        const int64_t grow = b.thirds() - before;
+        if (thirds + grow > cap3) { b.per = per_old; break; }
+        thirds += grow;
     }
+    int64_t n_big = 0, n_grp = 0;
     for (const Bucket &b : bk) {
         int32_t first_pair = (int32_t)pairs.size();
         for (size_t i = b.s; i < b.e; i += 2) pairs.push_back({idx[i], i + 1 < b.e ? idx[i + 1] : -1});
@@ -428,15 +450,21 @@ void crn_build_tasks(const crn_cb_desc *d, const int *sel, int n, std::vector<cr
             crn_task t;
             t.K = b.K; t.M = b.M; t.W = b.W; t.n_pairs = std::min(b.per, np - p);
             t.pair0 = first_pair + p; t.kidx = crn_k_index(b.K);
+            t.grp = b.grp;
             tasks.push_back(t);
+            (b.grp ? n_grp : n_big)++;
         }
     }
-    /* longest tasks first (LPT order for the persistent grid): a task's critical
-     * path is the trellis steps one thread runs per half-iteration -- 16 on the
-     * W = 32 path (split windows), W on the generic path (one thread per window) */
-    auto steps = [](const crn_task &t) { return t.W == 32 ? 16 : t.W; };
-    std::stable_sort(tasks.begin() + (std::ptrdiff_t)t0, tasks.end(),
-                     [&](const crn_task &a, const crn_task &b) { return steps(a) > steps(b); });
+    /* whole-CTA tasks first, longest first (LPT order for the persistent grid): a
+     * task's critical path is the trellis steps one thread runs per half-iteration
+     * -- 16 on the W = 32 path (split windows), ceil(W/2) on the split path; then
+     * the group tasks */
+    auto steps = [](const crn_task &t) { return t.W == 32 ? 16 : (t.W + 1) / 2; };
+    std::stable_sort(tasks.begin() + (std::ptrdiff_t)t0, tasks.end(), [&](const crn_task &a, const crn_task &b) {
+        if (a.grp != b.grp) return a.grp < b.grp;
+        return steps(a) > steps(b);
+    });
+    return (int)(n_big + (n_grp + CRN_GROUPS - 1) / CRN_GROUPS);
 }
 
 static int plan_build(const crn_cb_desc *desc, int n, bool want_ext, cudaStream_t st, bool async, Plan *P,
@@ -447,7 +475,7 @@ static int plan_build(const crn_cb_desc *desc, int n, bool want_ext, cudaStream_
     std::vector<crn_pair> pairs;
     std::vector<int> all(n);
     for (int i = 0; i < n; i++) all[i] = i;
-    crn_build_tasks(desc, all.data(), n, tasks, pairs, spread_to);
+    P->units = crn_build_tasks(desc, all.data(), n, tasks, pairs, spread_to);
     P->spread = spread_to;
     size_t b0 = sizeof(crn_cb_desc) * (size_t)n, b1 = sizeof(crn_task) * tasks.size(),
            b2 = sizeof(crn_pair) * pairs.size();
@@ -475,7 +503,7 @@ int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn
                      const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,
                      int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
                      void *ws, size_t ws_bytes, cudaStream_t st, int variant, uint8_t *tb_dead, int grid_cap,
-                     bool ws_zeroed) {
+                     bool ws_zeroed, int units) {
     if (n_tasks == 0) return CRN_OK;
     if (!ws) {
         int rc = crn_get_ws(dev, (void *)st, crn_decode_ws_bytes(t->grid), &ws);
@@ -484,7 +512,8 @@ int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn
         return CRN_EINVAL;
     }
     return crn_launch_decode(d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits, ok, it, ext,
-                             &t->tab, ws, (void *)st, grid_cap > 0 && grid_cap < t->grid ? grid_cap : t->grid,
+                             &t->tab, ws, (void *)st,
+                             std::min(grid_cap > 0 && grid_cap < t->grid ? grid_cap : t->grid, units > 0 ? units : n_tasks),
                              variant, tb_dead, ws_zeroed ? 1 : 0);
 }
 
@@ -502,7 +531,8 @@ static int launch(Plan *P, DevTables *t, const int16_t *l0, const int16_t *l1, c
         if (cudaMemsetAsync(dead, 0, (size_t)P->n_tb, st) != cudaSuccess) return CRN_ECUDA;
     }
     return crn_launch_tasks(P->dev, t, P->d_desc, P->d_tasks, P->n_tasks, P->d_pairs, l0, l1, l2, max_iters, et,
-                            bits, ok, it, ext, ws, ws_bytes, st, crn_plan_kernel_variant(P), dead, P->grid_cap);
+                            bits, ok, it, ext, ws, ws_bytes, st, crn_plan_kernel_variant(P), dead, P->grid_cap,
+                            false, P->units);
 }
 
 extern "C" int crn_plan_create(const crn_cb_desc *desc, int32_t n_cb, void **plan) {
@@ -598,6 +628,33 @@ extern "C" int crn_plan_layout(void *plan, int32_t *task_of_cb, int32_t n_cb) {
     return (int)tasks.size();
 }
 
+extern "C" int crn_task_layout(const crn_cb_desc *desc, int32_t n_cb, int32_t spread_to, int32_t *task_of_cb,
+                               int32_t *task_info, int32_t *units) {
+    if (n_cb < 0 || spread_to < 0 || (n_cb > 0 && (!desc || !task_of_cb))) return CRN_EINVAL;
+    if (crn_validate(desc, n_cb, false)) return CRN_EINVAL;
+    std::vector<crn_task> tasks;
+    std::vector<crn_pair> pairs;
+    std::vector<int> all(n_cb);
+    for (int i = 0; i < n_cb; i++) all[i] = i;
+    const int u = crn_build_tasks(desc, all.data(), n_cb, tasks, pairs, spread_to);
+    if (units) *units = u;
+    for (int i = 0; i < n_cb; i++) task_of_cb[i] = -1;
+    for (size_t t = 0; t < tasks.size(); t++) {
+        for (int p = 0; p < tasks[t].n_pairs; p++) {
+            const crn_pair &q = pairs[(size_t)tasks[t].pair0 + p];
+            task_of_cb[q.lo] = (int32_t)t;
+            if (q.hi >= 0) task_of_cb[q.hi] = (int32_t)t;
+        }
+        if (task_info) {
+            task_info[4 * t] = tasks[t].K;
+            task_info[4 * t + 1] = tasks[t].n_pairs;
+            task_info[4 * t + 2] = tasks[t].n_pairs * tasks[t].M;
+            task_info[4 * t + 3] = tasks[t].grp;
+        }
+    }
+    return (int)tasks.size();
+}
+
 extern "C" int crn_plan_launches(void *plan) {
     Plan *P = (Plan *)plan;
     return (P && P->n_cb) ? 1 : 0;
@@ -663,7 +720,7 @@ extern "C" int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb, const 
         }
     }
     rc = P.n_cb ? crn_launch_tasks(P.dev, t, P.d_desc, P.d_tasks, P.n_tasks, P.d_pairs, l0, l1, l2, max_iters, et,
-                                   bits, ok, it, ext, ws, ws_bytes, st, P.variant, dead)
+                                   bits, ok, it, ext, ws, ws_bytes, st, P.variant, dead, 0, false, P.units)
                 : CRN_OK;
     if (dead) cudaFreeAsync(dead, st);
     cudaFreeAsync(P.mem, st);

@@ -22,7 +22,16 @@ typedef struct {
     int32_t K, M, W, n_pairs;
     int32_t pair0;   /* first pair index of the task */
     int32_t kidx;    /* index of K in the size table */
+    int32_t grp;     /* 1: a group task (W = 32, n_pairs*M <= CRN_GRP_WIN), run by four warps while the
+                        CTA's other eight run two more; group tasks follow every whole-CTA task */
 } crn_task;
+
+/* Group tasks (W = 32 path, crn_decode.cu): a CTA runs three tasks of up to
+ * CRN_GRP_WIN windows (sum K <= CRN_GRP_SUMK, <= CRN_GRP_PAIRS pairs) at once. */
+#define CRN_GROUPS 3
+#define CRN_GRP_SUMK 2048
+#define CRN_GRP_WIN 64
+#define CRN_GRP_PAIRS 32
 
 typedef struct {
     int32_t lo, hi;  /* CB indices; hi = -1 for the dummy partner of an odd bucket */

@@ -28,6 +28,7 @@ void crn_logmap_words(uint32_t *lo, uint32_t *hi);
 struct Plan {
     int dev = -1;
     int n_cb = 0, n_tasks = 0;
+    int units = 0;                     /* CTAs the tasks fill (crn_build_tasks) */
     crn_cb_desc *d_desc = nullptr;
     crn_task *d_tasks = nullptr;
     crn_pair *d_pairs = nullptr;
@@ -53,15 +54,16 @@ int crn_validate(const crn_cb_desc *d, int n, bool want_ext);
  * Only the CBs idx[0..n_idx) take part; pair0 of the tasks indexes `pairs`.
  * spread_to > 0: a batch of fewer tasks is cut into smaller tasks, up to
  * spread_to of them (the persistent grid), so a small batch spreads over the SMs. */
-void crn_build_tasks(const crn_cb_desc *d, const int *idx, int n_idx, std::vector<crn_task> &tasks,
-                     std::vector<crn_pair> &pairs, int spread_to = 0);
+int crn_build_tasks(const crn_cb_desc *d, const int *idx, int n_idx, std::vector<crn_task> &tasks,
+                    std::vector<crn_pair> &pairs, int spread_to = 0);   /* returns the CTAs the tasks fill */
 /* Launch the decode kernel over n_tasks tasks (device arrays), workspace from the cache if ws == NULL. */
 int crn_launch_tasks(int dev, DevTables *t, const crn_cb_desc *d_desc, const crn_task *d_tasks, int n_tasks,
                      const crn_pair *d_pairs, const int16_t *l0, const int16_t *l1, const int16_t *l2,
                      int32_t max_iters, int32_t et, uint32_t *bits, uint8_t *ok, uint8_t *it, int16_t *ext,
                      void *ws, size_t ws_bytes, cudaStream_t st, int variant = CRN_VARIANT_MAXLOG,
                      uint8_t *tb_dead = nullptr, int grid_cap = 0,
-                     bool ws_zeroed = false);   /* the task counter in ws is already 0 (uploaded with a blob) */
+                     bool ws_zeroed = false,    /* the task counter in ws is already 0 (uploaded with a blob) */
+                     int units = 0);            /* CTAs the tasks can fill (crn_build_tasks), 0: n_tasks */
 /* Records the CUDA error behind a CRN_ECUDA / CRN_ENOMEM for crn_last_error(). */
 int crn_cuda_fail(cudaError_t e, const char *where, int code);
 /* Frees the host pipeline of a plan (crn_runtime.cpp). */

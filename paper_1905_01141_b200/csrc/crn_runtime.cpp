@@ -42,6 +42,7 @@ struct Chunk {
     int64_t llr0 = 0, llr1 = 0;           /* element range of the chunk's LLRs */
     int64_t w0 = 0, w1 = 0;               /* output word range */
     int32_t task0 = 0, n_tasks = 0;       /* slice of the pipe's task array */
+    int32_t units = 0;                    /* CTAs its tasks fill (crn_build_tasks) */
 };
 
 }  // namespace
@@ -107,7 +108,7 @@ static int pipe_build(Plan *P, int n_chunks, HostPipe **out) {
         std::vector<int> sel(cb1 - cb0);
         for (int i = cb0; i < cb1; i++) sel[i - cb0] = i;
         k.task0 = (int32_t)tasks.size();
-        crn_build_tasks(d, sel.data(), (int)sel.size(), tasks, pairs);
+        k.units = crn_build_tasks(d, sel.data(), (int)sel.size(), tasks, pairs);
         k.n_tasks = (int32_t)tasks.size() - k.task0;
         p->n_llr = std::max(p->n_llr, k.llr1);
         p->n_words = std::max(p->n_words, k.w1);
@@ -193,7 +194,7 @@ extern "C" int crn_plan_decode_host(void *plan, const int16_t *h0, const int16_t
         cudaStreamWaitEvent(st, p->ev_in[c], 0);
         rc = crn_launch_tasks(dev, t, P->d_desc, p->d_tasks + k.task0, k.n_tasks, p->d_pairs, p->d_l[0], p->d_l[1],
                               p->d_l[2], max_iters, et, p->d_bits, p->d_ok, h_it ? p->d_it : nullptr, nullptr,
-                              nullptr, 0, st, crn_plan_kernel_variant(P), nullptr, P->grid_cap);
+                              nullptr, 0, st, crn_plan_kernel_variant(P), nullptr, P->grid_cap, false, k.units);
         if (rc) return rc;
         cudaEventRecord(p->ev_comp[c], st);
         cudaStreamWaitEvent(p->s_out, p->ev_comp[c], 0);
@@ -418,7 +419,9 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             std::vector<crn_pair> pairs;
             std::vector<int> sel(q.n_cb);
             for (int i = 0; i < q.n_cb; i++) sel[i] = i;
-            crn_build_tasks(q.desc, sel.data(), q.n_cb, tasks, pairs, t->grid);
+            /* the groups' kernels run concurrently: each spreads over its share of the SMs */
+            const int units = crn_build_tasks(q.desc, sel.data(), q.n_cb, tasks, pairs,
+                                              std::max(1, t->grid / n_groups));
             const int64_t n_llr = g_llr[x], n_words = g_words[x];
             const Layout L = layout(q.n_cb, (int)tasks.size(), (int)pairs.size(), n_llr, n_words, esz);
             const int b = ti & 1;
@@ -443,7 +446,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
                                        (int)tasks.size(), (const crn_pair *)(hb + L.o_pairs), q.llr_sys, q.llr_p1,
                                        q.llr_p2, max_iters, et, q.out_bits, q.crc_ok, q.iters_used, nullptr,
                                        r.ctr + 64 * (size_t)ti, crn_decode_ws_bytes(t->grid), r.st, CRN_VARIANT_MAXLOG,
-                                       nullptr, 0, true);
+                                       nullptr, 0, true, units);
                 if (stages) cudaEventRecord(evk1[x], r.st);
                 cudaEventRecord(ev1[x], r.st);
                 gsub_us[x] = us_since(t0, Clock::now());
@@ -469,7 +472,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             src = crn_launch_tasks(dev, t, (const crn_cb_desc *)(dm + L.o_desc), (const crn_task *)(dm + L.o_tasks),
                                    (int)tasks.size(), (const crn_pair *)(dm + L.o_pairs), dl[0], dl[1], dl[2],
                                    max_iters, et, dbits, dok, q.iters_used ? dit : nullptr, nullptr, dm,
-                                   crn_decode_ws_bytes(t->grid), r.st, kvariant, nullptr, 0, true);
+                                   crn_decode_ws_bytes(t->grid), r.st, kvariant, nullptr, 0, true, units);
             if (stages) cudaEventRecord(evk1[x], r.st);
             const bool packed = (const uint8_t *)q.crc_ok == (const uint8_t *)(q.out_bits + n_words) &&
                                 (!q.iters_used || q.iters_used == q.crc_ok + q.n_cb);
@@ -553,7 +556,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             std::vector<crn_pair> pairs;
             std::vector<int> sel(m_cb);
             for (int i = 0; i < m_cb; i++) sel[i] = i;
-            crn_build_tasks(mdesc.data(), sel.data(), m_cb, tasks, pairs, t->grid);
+            const int units = crn_build_tasks(mdesc.data(), sel.data(), m_cb, tasks, pairs, t->grid);
             const Layout L = layout(m_cb, (int)tasks.size(), (int)pairs.size(), m_llr, m_words);
             uint8_t *dm = (uint8_t *)dr.dmem;
             int16_t *dl[3];
@@ -587,7 +590,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
                 rc = crn_launch_tasks(dev, t, (const crn_cb_desc *)(dm + L.o_desc), (const crn_task *)(dm + L.o_tasks),
                                       (int)tasks.size(), (const crn_pair *)(dm + L.o_pairs), dl[0], dl[1], dl[2],
                                       max_iters, et, dbits, dok, dit, nullptr, dr.ws, crn_decode_ws_bytes(t->grid),
-                                      dr.st);
+                                      dr.st, CRN_VARIANT_MAXLOG, nullptr, 0, false, units);
             cudaEventRecord(ev_dec, dr.st);
             cudaEventRecord(evk1[x0], dr.st);
             for (int gi = 1; gi < n_groups; gi++) {          /* one decode for all groups */

@@ -231,3 +231,51 @@ def test_stream_run_binding_refuses_mismatched_llr_dtypes():
     g["bits"] = torch.zeros(2, dtype=torch.int64)
     with pytest.raises(crn.CrnError):
         crn.stream_run([g], 1, 1, 1000.0, 8, True, flags=0)
+
+
+def _dense_desc(Ks):
+    K = np.asarray(Ks, np.int64)
+    d = np.zeros(K.size, crn.DESC_DTYPE)
+    d["K"] = K
+    d["crc_kind"] = crn.CRC24B
+    d["llr_off"] = np.concatenate([[0], np.cumsum(K + 4)[:-1]])
+    d["bit_off"] = np.concatenate([[0], np.cumsum((K + 31) // 32)[:-1]])
+    d["ext_off"] = np.concatenate([[0], np.cumsum(K)[:-1]])
+    return d
+
+
+@pytest.mark.timeout(120)
+def test_task_layout_invariants(L):
+    """Row a1 on the host (crn_task_layout, no GPU): every CB in exactly one task,
+    at most two CBs of one K per pair, tasks within their window / sum-K budget
+    (whole-CTA: <= 192 windows, sum K <= 6144; group tasks: W = 32, <= 64
+    windows, sum K <= 2048), group tasks after every whole-CTA task, the units
+    formula, and termination of the small-batch spreading for every batch shape
+    (np = 16, per = 4 once looped forever: floor((np + cur) / (cur + 1)) = per)."""
+    rng = np.random.default_rng(5)
+    import oracle
+    Ktab = [int(k) for k in oracle.k_table()]
+    cases = [[1056] * 32, [1056] * 33, [64] * 500, [6144] * 5, [40] * 1000, [2048] * 7 + [512] * 9,
+             list(rng.choice(Ktab, 200)), list(rng.choice(Ktab, 3000)), [1024] * 31 + [6144] * 300]
+    cases += [[int(k)] * int(n) for k, n in zip(rng.choice(Ktab, 40), rng.integers(1, 400, 40))]
+    for Ks in cases:
+        d = _dense_desc(Ks)
+        units0 = None
+        for spread in (0, 1, 7, 148, 1000):
+            tof, info, units = crn.task_layout(d, spread)
+            units0 = units if units0 is None else units0
+            nt = info.shape[0]
+            assert tof.min() >= 0 and tof.max() < nt
+            K = d["K"]
+            cnt = np.bincount(tof, minlength=nt)
+            assert np.all(cnt >= 1) and np.all(cnt <= 2 * info[:, 1])
+            for t in range(nt):                                  # one K per task
+                assert np.all(K[tof == t] == info[t, 0])
+            W32 = (info[:, 0] % 32 == 0) & (info[:, 0] >= 64)
+            grp = info[:, 3] == 1
+            assert np.all(W32[grp]) and np.all(info[grp, 2] <= 64) and np.all(info[grp, 0] * info[grp, 1] <= 2048)
+            assert np.all(info[~grp, 2] <= 192) and np.all(info[~grp, 0] * info[~grp, 1] <= 6144)
+            if grp.any():
+                assert np.all(grp[np.argmax(grp):]), "group tasks must come last"
+            assert units == int((~grp).sum()) + (int(grp.sum()) + 2) // 3
+            assert units <= max(spread, units0)                   # spreading stays within spread_to CTAs

@@ -177,6 +177,28 @@ def test_full_multi_pair_tasks_beyond_one_wave(orc):
     _raw_parity(d, _random_llr(d, rng, 60), 6, True)
 
 
+def test_group_tasks_beyond_one_wave(orc):
+    """Group tasks (W = 32, sum K <= 2048: three per CTA, one per four-warp group
+    with its own named barrier) well beyond one wave of 3 x 148 group slots,
+    behind whole-CTA tasks (K = 6144 pairs and split-path sizes), every group
+    geometry from one pair of K = 2048 (64 windows) to 32 pairs of K = 64 and a
+    lone K = 1056 (33 windows, a dummy partner lane); early termination, so the
+    groups of a CTA finish their tasks at different times."""
+    rng = np.random.default_rng(19)
+    Ks = ([64] * 640 + [96] * 300 + [512] * 257 + [1024] * 401 + [1056] * 1 + [1088] * 150 + [2048] * 333 +
+          [6144] * 61 + [1008] * 20 + [40] * 9)
+    d = _desc_for(list(rng.permutation(Ks)))
+    llr = _random_llr(d, rng, 70)
+    # every third CB leans to the all-zero codeword (CRC 0): it stops after 1-3 iterations, the rest run to 8
+    n = int((d["llr_off"] + d["K"] + 4).max())
+    lean = np.zeros(n, np.int16)
+    for o, K in zip(d["llr_off"][::3], d["K"][::3]):
+        lean[o:o + K + 4] = -60 - int(rng.integers(0, 40))
+    llr = tuple((x + torch.from_numpy(lean).cuda()).clamp(-32767, 32767) for x in llr)
+    g = _raw_parity(d, llr, 8, True)
+    assert 0 < int(g["crc_ok"].sum()) < d.size and len(set(g["iters"].tolist())) > 2
+
+
 def test_iteration_extremes_and_et(orc):
     rng = np.random.default_rng(9)
     d = _desc_for([6144, 6144, 6144, 512, 40])
