@@ -96,15 +96,22 @@ int crn_decode_batch(const int16_t *llr_sys, const int16_t *llr_p1, const int16_
                      uint32_t *out_bits, uint8_t *crc_ok);
 
 /* General form.  desc: n_cb descriptors in HOST memory (copied during the
- * call), or in DEVICE memory if flags & CRN_DESC_ON_DEVICE (then they are
- * validated on the device; an invalid one yields crc_ok = 0, iters_used = 0).
+ * call; the last few distinct descriptor sets are kept validated, bucketed and
+ * uploaded, so a repeated layout costs one comparison), or in DEVICE memory if
+ * flags & CRN_DESC_ON_DEVICE: then they are bucketed and validated on the
+ * device by a task-builder kernel enqueued before the decode (nothing is copied
+ * back, the call does not wait on the stream); an invalid one (K, F, crc_kind,
+ * negative offsets, with CRN_PURGE a TB id outside [-1, n_cb)) yields crc_ok =
+ * 0, iters_used = 0; overlapping ranges are not detected on the device.
  * max_iters in [1,32]; early_term one of CRN_ET_NONE / CRN_ET_CRC / CRN_ET_MI
  * (above; CRN_EINVAL otherwise).
  * Outputs (device memory): out_bits (required), crc_ok[n_cb] (required),
  * iters_used[n_cb] (may be NULL; full iterations executed, R17), ext_out
  * (may be NULL; int16 La1_next of the last iteration in natural order, R15).
- * workspace: NULL -> the cached per-device workspace; else >= crn_workspace_bytes()
- * bytes of device memory owned by the caller, used by this call only.
+ * workspace: NULL -> the cached per-(device, stream) workspace; else >=
+ * crn_workspace_bytes(desc, n_cb) bytes of device memory owned by the caller,
+ * used by this call only (stream-ordered: reusable by the next call on the
+ * same stream).
  * cuda_stream: a cudaStream_t (NULL = legacy default stream).
  * Host-side validation (descriptors in host memory) returns CRN_EINVAL for a
  * K outside the table, F < 0 or F > K-25, an unknown crc_kind, overlapping
@@ -118,9 +125,12 @@ int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb,
                         void *workspace, size_t workspace_bytes, void *cuda_stream);
 
 /* Bytes of caller-provided workspace crn_decode_batch_ex needs on the current
- * device (independent of the batch: the persistent decoder keeps every CB's
- * state on chip; the workspace holds its task counter). */
-size_t crn_workspace_bytes(void);
+ * device for a batch of n_cb CBs: 256 bytes for the
+ * persistent decoder's task counter (it keeps every CB's state on chip) plus,
+ * used only with CRN_DESC_ON_DEVICE, the device task builder's arrays (tasks,
+ * pairs, per-CB bucket index, purge flags: O(n_cb)).  desc may be NULL: the
+ * size depends on n_cb only.  0 without a device or for n_cb < 0. */
+size_t crn_workspace_bytes(const crn_cb_desc *desc, int32_t n_cb);
 
 /* Plans: validate + bucket + upload a descriptor set once, decode many times
  * (the per-TTI pattern of a BBU, "CCDUs arrive in batches every

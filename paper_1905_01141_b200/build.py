@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libcrn.so")
-SOURCES = ["crn_host.cpp", "crn_runtime.cpp", "crn_decode.cu", "crn_encode.cu", "crn_tb.cu", "crn_ratematch.cu", "crn_tbseg.cu", "crn_ubench.cu"]
+SOURCES = ["crn_host.cpp", "crn_runtime.cpp", "crn_decode.cu", "crn_encode.cu", "crn_tb.cu", "crn_ratematch.cu", "crn_tbseg.cu", "crn_tasks.cu", "crn_ubench.cu"]
 HEADERS = ["crn_internal.h", "crn_plan.h", "qpp_table.h", os.path.join("..", "..", "include", "crn.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

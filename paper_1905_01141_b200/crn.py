@@ -56,7 +56,7 @@ _SIGS = {
     "crn_decode_batch": (C.c_int, [vp, vp, vp, i32p, C.c_int32, C.c_int32, vp, vp]),
     "crn_decode_batch_ex": (C.c_int, [vp, C.c_int32, vp, vp, vp, C.c_int32, C.c_int32, C.c_int32,
                                       vp, vp, vp, vp, vp, C.c_size_t, vp]),
-    "crn_workspace_bytes": (C.c_size_t, []),
+    "crn_workspace_bytes": (C.c_size_t, [vp, C.c_int32]),
     "crn_plan_create": (C.c_int, [vp, C.c_int32, P(vp)]),
     "crn_plan_decode": (C.c_int, [vp, vp, vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp, vp]),
     "crn_plan_launches": (C.c_int, [vp]),
@@ -180,8 +180,9 @@ def task_layout(desc: np.ndarray, spread_to: int = 0):
     return tof[:n], info[:nt], int(units[0])
 
 
-def workspace_bytes() -> int:
-    return int(lib().crn_workspace_bytes())
+def workspace_bytes(n_cb: int = 0) -> int:
+    """crn_workspace_bytes(NULL, n_cb): caller workspace for a batch of n_cb CBs."""
+    return int(lib().crn_workspace_bytes(None, n_cb))
 
 
 class Plan:

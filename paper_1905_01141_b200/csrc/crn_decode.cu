@@ -1344,6 +1344,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     __shared__ int s_mi[2 * MAXP], s_mip[2 * MAXP], s_mitab[256];
 
     int *counter = (int *)ws;
+    if (n_tasks < 0) n_tasks = ((const volatile int *)ws)[1];   /* built on the device (crn_tasks.cu) */
     const int tid = threadIdx.x;
     u32 *s_crcnib = smem + S_CRCNIB;
     int64_t *s_bo = reinterpret_cast<int64_t *>(smem + S_OFFS), *s_eo = s_bo + 2 * MAXP, *s_nbo = s_eo + 2 * MAXP,
@@ -1580,7 +1581,7 @@ extern "C" int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_ta
                                  int32_t variant, uint8_t *tb_dead, int32_t ws_zeroed) {
     cudaStream_t st = (cudaStream_t)stream;
     if (!ws_zeroed && cudaMemsetAsync(ws, 0, WS_HEAD, st) != cudaSuccess) return CRN_ECUDA;
-    const int g = grid < n_tasks ? grid : n_tasks;
+    const int g = (n_tasks >= 0 && n_tasks < grid) ? n_tasks : grid;   /* n_tasks < 0: the count is in ws[1] */
     const bool llr8 = (variant >> 8) != 0;      /* crn_plan_set_llr_format: int8 LLRs */
     const int var = variant & 0xFF;
 #define CRN_LAUNCH(PG, L8, V)                                                                                      \

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -305,6 +306,25 @@ static int build_tables(int dev, DevTables **out) {
         crn_decode_set_logmap(lo, hi);
     }
     t.tab.qinv_wm = t.qinv_wm;
+    {   /* the device task builder's per-size parameters and bucket issue order */
+        std::vector<int32_t> bk(4 * CRN_NUM_K), ord(CRN_NUM_K);
+        for (int ki = 0; ki < CRN_NUM_K; ki++) {
+            int M, W, per, grp;
+            crn_bucket_params(k_at(ki), &M, &W, &per, &grp);
+            bk[4 * ki] = k_at(ki); bk[4 * ki + 1] = M; bk[4 * ki + 2] = W; bk[4 * ki + 3] = per | (grp << 16);
+            ord[ki] = ki;
+        }
+        std::stable_sort(ord.begin(), ord.end(), [](int a, int b) {   /* K descending within one key */
+            const int ka = crn_bucket_issue_key(k_at(a)), kb = crn_bucket_issue_key(k_at(b));
+            return ka != kb ? ka > kb : k_at(a) > k_at(b);
+        });
+        if (cudaMalloc(&t.bucket, bk.size() * 4) != cudaSuccess || cudaMalloc(&t.border, ord.size() * 4) != cudaSuccess) {
+            cudaGetLastError();
+            return CRN_ENOMEM;
+        }
+        cudaMemcpy(t.bucket, bk.data(), bk.size() * 4, cudaMemcpyHostToDevice);
+        cudaMemcpy(t.border, ord.data(), ord.size() * 4, cudaMemcpyHostToDevice);
+    }
     t.grid = crn_decode_grid(dev);
     if (t.grid <= 0) {
         char where[96];
@@ -341,11 +361,12 @@ int crn_get_ws(int dev, void *stream, size_t bytes, void **ws) {
     return CRN_OK;
 }
 
-extern "C" size_t crn_workspace_bytes(void) {
+extern "C" size_t crn_workspace_bytes(const crn_cb_desc *desc, int32_t n_cb) {
+    (void)desc;                  /* the size depends on n_cb only */
     int dev;
     DevTables *t;
-    if (crn_get_ctx(&dev, &t) != CRN_OK) return 0;
-    return crn_decode_ws_bytes(t->grid);
+    if (n_cb < 0 || crn_get_ctx(&dev, &t) != CRN_OK) return 0;
+    return crn_decode_ws_bytes(t->grid) + crn_tasks_dev_bytes(n_cb);
 }
 
 /* ------------------------------------------------------------------ plans (row a1) */
@@ -373,6 +394,7 @@ int crn_validate(const crn_cb_desc *d, int n, bool want_ext) {
     return CRN_OK;
 }
 
+
 /* Group tasks on or off (CRN_GROUPS=0 in the environment turns them off, for A/B runs). */
 static bool groups_on() {
     static const int on = [] {
@@ -380,6 +402,24 @@ static bool groups_on() {
         return (e && e[0] == '0') ? 0 : 1;
     }();
     return on != 0;
+}
+
+void crn_bucket_params(int K, int *M, int *W, int *per, int *grp) {
+    crn_windows(K, M, W);
+    *grp = *W == 32 && K <= CRN_GRP_SUMK && groups_on();
+    *per = *grp ? std::max(1, std::min(CRN_GRP_SUMK / K, CRN_GRP_PAIRS))
+                : std::max(1, std::min(CRN_TASK_SUMK / K, CRN_MAX_PAIRS));
+    if (*W != 32)                      /* split-window path: shared memory and TMEM bound the task */
+        while (*per > 1 && !crn_split_fits(*W, *M, *per)) (*per)--;
+}
+
+/* LPT issue key of a task of size K: a task's critical path is the trellis steps
+ * one thread runs per half-iteration -- 16 on the W = 32 path (split windows),
+ * ceil(W/2) on the split path; group tasks (key 0) after every whole-CTA task */
+int crn_bucket_issue_key(int K) {
+    int M, W, per, grp;
+    crn_bucket_params(K, &M, &W, &per, &grp);
+    return grp ? 0 : (W == 32 ? 16 : (W + 1) / 2);
 }
 
 /* Bucket by K (largest first: longest tasks start first), pair equal-K CBs in
@@ -408,12 +448,7 @@ int crn_build_tasks(const crn_cb_desc *d, const int *sel, int n, std::vector<crn
         while (e < idx.size() && d[idx[e]].K == K) e++;
         Bucket b;
         b.K = K; b.s = s; b.e = e;
-        crn_windows(K, &b.M, &b.W);
-        b.grp = b.W == 32 && K <= CRN_GRP_SUMK && groups_on();
-        b.per = b.grp ? std::max(1, std::min(CRN_GRP_SUMK / K, CRN_GRP_PAIRS))
-                      : std::max(1, std::min(CRN_TASK_SUMK / K, CRN_MAX_PAIRS));
-        if (b.W != 32)                      /* split-window path: shared memory and TMEM bound the task */
-            while (b.per > 1 && !crn_split_fits(b.W, b.M, b.per)) b.per--;
+        crn_bucket_params(K, &b.M, &b.W, &b.per, &b.grp);
         b.np = (int)((e - s + 1) / 2);
         thirds += b.thirds();
         bk.push_back(b);
@@ -455,14 +490,10 @@ int crn_build_tasks(const crn_cb_desc *d, const int *sel, int n, std::vector<crn
             (b.grp ? n_grp : n_big)++;
         }
     }
-    /* whole-CTA tasks first, longest first (LPT order for the persistent grid): a
-     * task's critical path is the trellis steps one thread runs per half-iteration
-     * -- 16 on the W = 32 path (split windows), ceil(W/2) on the split path; then
-     * the group tasks */
-    auto steps = [](const crn_task &t) { return t.W == 32 ? 16 : (t.W + 1) / 2; };
+    /* whole-CTA tasks first, longest first (LPT order for the persistent grid), then
+     * the group tasks (crn_bucket_issue_key) */
     std::stable_sort(tasks.begin() + (std::ptrdiff_t)t0, tasks.end(), [&](const crn_task &a, const crn_task &b) {
-        if (a.grp != b.grp) return a.grp < b.grp;
-        return steps(a) > steps(b);
+        return crn_bucket_issue_key(a.K) > crn_bucket_issue_key(b.K);
     });
     return (int)(n_big + (n_grp + CRN_GROUPS - 1) / CRN_GROUPS);
 }
@@ -669,6 +700,77 @@ extern "C" void crn_plan_destroy(void *plan) {
     delete P;
 }
 
+/* Plans behind the one-shot calls (crn_decode_batch / _ex with HOST descriptors):
+ * a BBU decodes the same CB layout TTI after TTI, so the last few
+ * validated + bucketed + uploaded descriptor sets are kept, keyed by the exact
+ * descriptor bytes (and device, n_cb, ext_out use).  A hit costs one memcmp; a
+ * miss builds the plan and uploads it on a private stream (never waiting on the
+ * caller's).  Entries are shared_ptrs: a plan evicted while another thread still
+ * launches from it lives until that launch is enqueued; its device memory is
+ * released by cudaFree, which waits for the device. */
+namespace {
+struct CachedPlan {
+    int dev = -1;
+    bool want_ext = false;
+    int n_tb = 0;                             /* TB ids in the reserved field (purge) */
+    std::vector<crn_cb_desc> key;
+    Plan P;
+    ~CachedPlan() {
+        if (P.mem) cudaFree(P.mem);
+    }
+};
+constexpr size_t PLAN_CACHE = 4;
+std::mutex g_pc_mu;
+std::vector<std::shared_ptr<CachedPlan>> g_pc;   /* most recently used first */
+std::map<int, cudaStream_t> g_upload_stream;      /* per device, non-blocking */
+
+int cached_plan(int dev, DevTables *t, const crn_cb_desc *desc, int n, bool want_ext,
+                std::shared_ptr<CachedPlan> *out) {
+    {
+        std::lock_guard<std::mutex> lk(g_pc_mu);
+        for (size_t i = 0; i < g_pc.size(); i++) {
+            const auto &c = g_pc[i];
+            if (c->dev == dev && c->want_ext == want_ext && c->key.size() == (size_t)n &&
+                memcmp(c->key.data(), desc, sizeof(crn_cb_desc) * (size_t)n) == 0) {
+                *out = c;
+                std::rotate(g_pc.begin(), g_pc.begin() + (std::ptrdiff_t)i, g_pc.begin() + (std::ptrdiff_t)i + 1);
+                return CRN_OK;
+            }
+        }
+    }
+    auto c = std::make_shared<CachedPlan>();
+    c->dev = dev;
+    c->want_ext = want_ext;
+    c->key.assign(desc, desc + n);
+    for (int i = 0; i < n; i++) {
+        if (desc[i].reserved < -1) c->n_tb = -1;
+        else if (c->n_tb >= 0) c->n_tb = std::max(c->n_tb, desc[i].reserved + 1);
+    }
+    cudaStream_t up;
+    {
+        std::lock_guard<std::mutex> lk(g_pc_mu);
+        auto it = g_upload_stream.find(dev);
+        if (it == g_upload_stream.end()) {
+            if (cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking) != cudaSuccess) {
+                cudaGetLastError();
+                return CRN_ECUDA;
+            }
+            g_upload_stream[dev] = up;
+        } else {
+            up = it->second;
+        }
+    }
+    c->P.dev = dev;
+    int rc = plan_build(desc, n, want_ext, up, false, &c->P, t->grid);   /* cudaMalloc + upload + sync of `up` */
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_pc_mu);
+    g_pc.insert(g_pc.begin(), c);
+    if (g_pc.size() > PLAN_CACHE) g_pc.pop_back();
+    *out = c;
+    return CRN_OK;
+}
+}  // namespace
+
 extern "C" int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb, const int16_t *l0,
                                    const int16_t *l1, const int16_t *l2, int32_t max_iters,
                                    int32_t et, int32_t flags, uint32_t *bits, uint8_t *ok,
@@ -684,46 +786,43 @@ extern "C" int crn_decode_batch_ex(const crn_cb_desc *desc, int32_t n_cb, const 
     int rc = crn_get_ctx(&dev, &t);
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    std::vector<crn_cb_desc> hd;
-    const crn_cb_desc *hdesc = desc;
-    if (flags & CRN_DESC_ON_DEVICE) {       /* descriptors are needed on the host to bucket by K */
-        hd.resize(n_cb);
-        if (cudaMemcpyAsync(hd.data(), desc, sizeof(crn_cb_desc) * n_cb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-            cudaStreamSynchronize(st) != cudaSuccess) {
-            cudaGetLastError();
-            return CRN_ECUDA;
+    const int variant = (flags & CRN_EXT_SCALED) ? CRN_VARIANT_SCALED : CRN_VARIANT_MAXLOG;
+    if (flags & CRN_DESC_ON_DEVICE) {
+        /* row a1 on the device (crn_tasks.cu): nothing returns to the host, nothing waits */
+        const size_t head = crn_decode_ws_bytes(t->grid), need = head + crn_tasks_dev_bytes(n_cb);
+        if (!ws) {
+            rc = crn_get_ws(dev, (void *)st, need, &ws);
+            if (rc) return rc;
+        } else if (ws_bytes < need) {
+            return CRN_EINVAL;
         }
-        hdesc = hd.data();
+        crn_task *dt;
+        crn_pair *dp;
+        uint8_t *dead;
+        rc = crn_launch_tasks_dev(desc, n_cb, ext != nullptr, (flags & CRN_PURGE) != 0, t->bucket, t->border,
+                                  (uint8_t *)ws + head, (int32_t *)ws, &dt, &dp, &dead, ok, it, (void *)st);
+        if (rc) return crn_cuda_fail(cudaGetLastError(), "device task builder launch", rc);
+        return crn_launch_decode(desc, dt, -1, dp, l0, l1, l2, max_iters, et, bits, ok, it, ext, &t->tab, ws,
+                                 (void *)st, t->grid, variant, dead, 1);
     }
-    Plan P;
-    P.dev = dev;
-    P.variant = (flags & CRN_EXT_SCALED) ? CRN_VARIANT_SCALED : CRN_VARIANT_MAXLOG;
-    rc = plan_build(hdesc, n_cb, ext != nullptr, st, true, &P, t->grid);
-    if (rc) {
-        if (P.mem) cudaFreeAsync(P.mem, st);
-        return rc;
-    }
+    std::shared_ptr<CachedPlan> c;
+    rc = cached_plan(dev, t, desc, n_cb, ext != nullptr, &c);
+    if (rc) return rc;
     uint8_t *dead = nullptr;
     if (flags & CRN_PURGE) {
-        int n_tb = 0;
-        for (int i = 0; i < n_cb; i++) {
-            if (hdesc[i].reserved < -1) { cudaFreeAsync(P.mem, st); return CRN_EINVAL; }
-            n_tb = std::max(n_tb, hdesc[i].reserved + 1);
-        }
-        if (n_tb > 0) {
-            if (cudaMallocAsync((void **)&dead, (size_t)n_tb, st) != cudaSuccess) {
+        if (c->n_tb < 0) return CRN_EINVAL;
+        if (c->n_tb > 0) {
+            if (cudaMallocAsync((void **)&dead, (size_t)c->n_tb, st) != cudaSuccess) {
                 cudaGetLastError();
-                cudaFreeAsync(P.mem, st);
                 return CRN_ENOMEM;
             }
-            cudaMemsetAsync(dead, 0, (size_t)n_tb, st);
+            cudaMemsetAsync(dead, 0, (size_t)c->n_tb, st);
         }
     }
-    rc = P.n_cb ? crn_launch_tasks(P.dev, t, P.d_desc, P.d_tasks, P.n_tasks, P.d_pairs, l0, l1, l2, max_iters, et,
-                                   bits, ok, it, ext, ws, ws_bytes, st, P.variant, dead, 0, false, P.units)
-                : CRN_OK;
+    const Plan &P = c->P;
+    rc = crn_launch_tasks(P.dev, t, P.d_desc, P.d_tasks, P.n_tasks, P.d_pairs, l0, l1, l2, max_iters, et, bits, ok,
+                          it, ext, ws, ws_bytes, st, variant, dead, 0, false, P.units);
     if (dead) cudaFreeAsync(dead, st);
-    cudaFreeAsync(P.mem, st);
     return rc;
 }
 

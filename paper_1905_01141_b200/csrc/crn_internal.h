@@ -7,6 +7,9 @@
 #include "../../include/crn.h"
 
 #define CRN_NSTATE 8
+#ifndef CRN_NUM_K
+#define CRN_NUM_K 188      /* the LTE interleaver sizes (qpp_table.h) */
+#endif
 #define CRN_MI_EPS 66      /* MI stopping rule: per-bit change threshold in Q16 (R29) */
 /* Decode work unit: one CTA task = n_pairs pairs of CBs with the same K; the
  * two CBs of a pair share every int16x2 register (lo half / hi half), so all
@@ -112,6 +115,14 @@ size_t crn_decode_ws_bytes(int32_t grid);
  * constant bank (crn_logmap_lut, R32); once per device. */
 int crn_decode_set_logmap(uint32_t lo, uint32_t hi);
 int crn_decode_grid(int device);
+/* crn_tasks.cu: row a1 on the device for descriptors in device memory.  bucket[4 k ..] = K, M, W,
+ * pairs per task | group flag << 16 of size index k; border[q] = the size index issued q-th.
+ * scratch >= crn_tasks_dev_bytes(n_cb); hdr[0] = 0 (task counter), hdr[1] = task count. */
+size_t crn_tasks_dev_bytes(int32_t n_cb);
+int crn_launch_tasks_dev(const crn_cb_desc *d_desc, int32_t n_cb, int32_t want_ext, int32_t purge,
+                         const int32_t *bucket, const int32_t *border, void *scratch, int32_t *hdr,
+                         crn_task **tasks, crn_pair **pairs, uint8_t **dead, uint8_t *crc_ok,
+                         uint8_t *iters_used, void *stream);
 /* crn_encode.cu */
 int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const uint8_t *info,
                       int32_t attach_crc, uint8_t *d0, uint8_t *d1, uint8_t *d2,

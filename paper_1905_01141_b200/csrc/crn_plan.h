@@ -13,6 +13,7 @@ struct DevTables {
              *qinv_wm = nullptr;
     int32_t *qpp_off = nullptr, *crcb_off = nullptr, *mi_tab = nullptr;
     uint32_t *crc_nib = nullptr;
+    int32_t *bucket = nullptr, *border = nullptr;   /* device task builder (crn_tasks.cu) */
     crn_tables tab{};
     int grid = 0;
 };
@@ -44,6 +45,11 @@ struct Plan {
     HostPipe *pipe = nullptr;
 };
 
+/* Per-size task parameters shared by the host and device task builders: windows
+ * (M, W), pairs per task before spreading, group flag (crn_internal.h CRN_GROUPS),
+ * and the LPT issue key (larger first; group tasks after every whole-CTA task). */
+void crn_bucket_params(int K, int *M, int *W, int *per, int *grp);
+int crn_bucket_issue_key(int K);
 /* Device context: checks for an sm_100 device and builds the per-device tables once. */
 int crn_get_ctx(int *dev, DevTables **t);
 /* Cached per-(device, stream) decode workspace. */

@@ -259,6 +259,57 @@ def test_plan_simple_api_and_device_descriptors(orc):
     assert np.array_equal(bits3.cpu().numpy().view(np.uint32), g["words"])
 
 
+def test_device_descriptors_bucketed_on_device(orc):
+    """CRN_DESC_ON_DEVICE: row a1 runs on the device (crn_tasks.cu) -- a mixed-K
+    TTI with CRC early termination through device descriptors equals the oracle
+    on every output; invalid descriptors (bad K, F, crc_kind, offsets) are not
+    decoded (crc_ok = iters_used = 0) while their neighbours are; a caller
+    workspace of exactly crn_workspace_bytes(n_cb) works; host descriptors
+    decoded twice (plan cache hit) and a same-size different layout (miss) agree."""
+    b = _full(5)
+    g = run_gpu(b, 8, True)
+    idx = np.arange(b.n_cb)
+    r = run_oracle(b, idx, 8, True)
+    assert_parity(b, g, r, idx)
+    dd = torch.from_numpy(b.desc.view(np.uint8).copy()).cuda()
+    bits, ok, it, ext = bmod.outputs(b)
+    ws = torch.zeros(crn.workspace_bytes(b.n_cb), dtype=torch.uint8, device="cuda")
+    for w in (None, ws):
+        bits.zero_(); ok.fill_(7); it.fill_(7); ext.zero_()
+        crn.decode_batch_ex(dd, b.n_cb, *b.llr, 8, True, crn.DESC_ON_DEVICE, bits, ok, it, ext,
+                            workspace=w, workspace_bytes=0 if w is None else w.numel())
+        torch.cuda.synchronize()
+        gd = dict(words=bits.cpu().numpy().view(np.uint32), crc_ok=ok.cpu().numpy()[:b.n_cb],
+                  iters=it.cpu().numpy()[:b.n_cb], ext=ext.cpu().numpy())
+        assert_parity(b, gd, r, idx)
+    # invalid descriptors in device memory
+    bad = b.desc.copy()
+    kill = np.arange(0, b.n_cb, 7)
+    for n, i in enumerate(kill):
+        if n % 4 == 0: bad["K"][i] = 41
+        elif n % 4 == 1: bad["F"][i] = bad["K"][i]
+        elif n % 4 == 2: bad["crc_kind"][i] = 3
+        else: bad["llr_off"][i] = -1
+    dd = torch.from_numpy(bad.view(np.uint8).copy()).cuda()
+    bits.zero_(); ok.fill_(7); it.fill_(7)
+    crn.decode_batch_ex(dd, b.n_cb, *b.llr, 8, True, crn.DESC_ON_DEVICE, bits, ok, it)
+    torch.cuda.synchronize()
+    okh, ith = ok.cpu().numpy()[:b.n_cb], it.cpu().numpy()[:b.n_cb]
+    assert np.all(okh[kill] == 0) and np.all(ith[kill] == 0)
+    keep = np.setdiff1d(idx, kill)
+    assert np.array_equal(okh[keep], r["crc_ok"][keep]) and np.array_equal(ith[keep], r["iters"][keep])
+    words = bits.cpu().numpy().view(np.uint32)
+    for i in keep[::5]:
+        assert np.array_equal(unpack(words, b.desc, i), r["bits"][r["bo"][i]:r["bo"][i] + b.desc["K"][i]])
+    # host descriptors: a cache hit and a same-size layout change
+    g2 = run_gpu(b, 8, True)
+    assert np.array_equal(g2["words"], g["words"]) and np.array_equal(g2["iters"], g["iters"])
+    perm = np.random.default_rng(4).permutation(b.n_cb)
+    d2 = b.desc[perm].copy()
+    g3 = run_gpu(b, 8, True, desc=d2)
+    assert np.array_equal(g3["iters"], g["iters"][perm]) and np.array_equal(g3["crc_ok"], g["crc_ok"][perm])
+
+
 def test_streams_and_invalid_args(orc):
     b = _full(5)
     g = run_gpu(b, 8, True)
