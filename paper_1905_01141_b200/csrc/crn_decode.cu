@@ -78,12 +78,13 @@ constexpr int S_OFFS = S_CRCNIB + 2 * CRN_CRC_NIB_WORDS;   /* int64 [4][2 MAXP]:
 static_assert(S_OFFS % 2 == 0, "8-byte aligned");
 constexpr int SMEM_WORDS = S_OFFS + 4 * 2 * MAXP * 2;
 constexpr int YZ_END_BYTES = 4 * (S_Z + SUMK);     /* + static shared memory: must stay < 64 KiB */
-static_assert(SMEM_WORDS * 4 + 9728 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
+static_assert(SMEM_WORDS * 4 + 10240 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
 
 /* ---- optional phase profiler (build with -DCRN_PHASE_PROF; never in the product
  * build): lane 0 of warp 0 (a head warp) and of warp 6 (a tail warp) attribute
  * clock64 intervals to the phase that just ended; summed over CTAs. */
-enum { P_FETCH, P_STAGE, P_CHUNK, P_PH1, P_BAR1, P_PH2, P_BAR2, P_HD, P_N };
+enum { P_FETCH, P_STAGE, P_CHUNK, P_PH1, P_BAR1, P_PH2, P_BAR2, P_HD, P_SLD, P_SB1, P_SG, P_HL, P_HB1, P_HC, P_HB2, P_HDEC,
+       P_FB, P_N };
 #ifdef CRN_PHASE_PROF
 __device__ unsigned long long g_prof[2 * P_N];
 __shared__ unsigned long long s_pacc[2][P_N];
@@ -547,6 +548,45 @@ __device__ __forceinline__ u32 lds_q(u32 qq, int c) {
     return v;
 }
 
+/* ---- asynchronous bulk copies (TMA engine) of a task's input streams into shared
+ * memory, completing on one mbarrier (row a2: the coalesced LLR load) */
+__device__ __forceinline__ void mbar_init(u32 bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u32 bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "CRN_MBW%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra CRN_MBW%=;\n\t}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(u32 dst, const void *src, u32 bytes, u32 bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+/* orders this thread's earlier generic-proxy shared-memory accesses before later async-proxy writes */
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+/* Bulk staging plan of a whole-CTA W = 32 task (crn_decode.cu run_task_fast): copy
+ * c = x * 2NP + e (stream x, CB lane e) of the K + 4 values of CB lane e, widened to
+ * 16-byte boundaries, lands in a slot of BS(K) bytes in one of three regions that
+ * are free until the task's first half-iteration: CH (branch-metric chunks), NII + X
+ * (boundary states, hand-over) and Y (Le1). */
+constexpr int RB0 = 4 * (HW * BLOCK * 2), RB1 = 4 * (S_NII_WORDS + 2 * NS * WMAX), RB2 = 4 * SUMK;   /* region bytes */
+__host__ __device__ constexpr int bulk_slot_bytes(int K) { return (2 * (K + 4) + 28 + 15) & ~15; }
+__host__ __device__ constexpr int bulk_slots(int K) {
+    return RB0 / bulk_slot_bytes(K) + RB1 / bulk_slot_bytes(K) + RB2 / bulk_slot_bytes(K);
+}
+/* shared byte address of copy c's slot */
+__device__ __forceinline__ u32 bulk_slot(u32 smem_base, int K, int c) {
+    const int S = bulk_slot_bytes(K), n0 = RB0 / S, n1 = RB1 / S;
+    return c < n0 ? smem_base + 4u * S_CH + (u32)(c * S)
+         : c < n0 + n1 ? smem_base + 4u * S_NII + (u32)((c - n0) * S)
+                       : smem_base + 4u * S_Y + (u32)((c - n0 - n1) * S);
+}
+
 /* One half-iteration of constituent c (rows a5-a8).  Le -> Y (c = 0, natural
  * order) or Z (c = 1, interleaved order). */
 template <int VAR, int G>
@@ -689,7 +729,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                                               uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok,
                                               uint8_t *__restrict__ iters_used, int16_t *__restrict__ ext_out,
                                               const crn_tables &tab, u32 *sm, u32 tmem, TaskSh sh, Purge pg,
-                                              int sh8) {
+                                              int sh8, int bulk = -1, u32 mbar = 0, const uint8_t *dlt = nullptr) {
     constexpr int W = 32;
     const int M = tk.M, NP = tk.n_pairs, T = NP * M;
     constexpr int GWIN = WMAX / G;              /* windows of the group's task */
@@ -729,11 +769,81 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         const int p = f.p, j = f.j;
         const int clo = sh.cb[2 * p], chi = sh.cb[2 * p + 1];
         const int Flo = sh.F[2 * p], Fhi = sh.F[2 * p + 1];
-        const int64_t olo = clo >= 0 ? desc[clo].llr_off : 0, ohi = chi >= 0 ? desc[chi].llr_off : 0;
-        const int n0 = j * W + f.k0;
         u32 *tmp = sm + S_Z;                  /* natural Ls, window-major, for the interleaved gather
                                                  (the Z plane is first written in DEC2 of iteration 1) */
-        {
+        if (G == 1 && !LLR8 && bulk >= 0) {
+            /* the task's streams were bulk-copied into shared memory (decode_kernel): the QPP
+             * word indices are loaded while the copies land, then every thread transposes
+             * its window's words into the [step][window] planes */
+#pragma unroll
+            for (int s = 0; s < HW; s++) {
+                q1[s] = __ldg(qinv + (f.k0 + s) * M + j);
+                q2[s] = __ldg(qts + (f.k0 + s) * M + j);
+            }
+            const u32 base = smem_addr(sm);
+            const int K = tk.K;
+            u32 rlo[3], rhi[3];                 /* byte address of element 0 of each stream of the pair's CBs */
+#pragma unroll
+            for (int x = 0; x < 3; x++) {
+                rlo[x] = bulk_slot(base, K, x * 2 * NP + 2 * p) + 2u * dlt[2 * p];
+                rhi[x] = bulk_slot(base, K, x * 2 * NP + 2 * p + 1) + 2u * dlt[2 * p + 1];
+            }
+            mbar_wait(mbar, (u32)bulk);
+            if (active) {
+                /* word wi of the window (elements 2 wi, 2 wi + 1) of each stream: the head
+                 * thread takes 8 words, the tail thread the other 8, rotated by lane so that
+                 * a warp's 32 reads (windows 64 bytes apart) hit 32 distinct banks; the
+                 * plane writes (one column per lane) are conflict-free as well */
+                const u32 rot = (u32)(tid >> 1) & 15u;
+#pragma unroll
+                for (int x = 0; x < 3; x++) {
+                    u32 *dst = x == 0 ? tmp : sm + S_LP + (x - 1) * SUMK;
+#pragma unroll
+                    for (int q = 0; q < HW / 2; q++) {
+                        const u32 wi = ((tail_thr ? 8u : 0u) + (u32)q + rot) & 15u;
+                        const u32 off = 4u * (16u * (u32)j + wi);
+                        const u32 a = clo >= 0 ? lds_at(rlo[x] + off) : 0u, b = chi >= 0 ? lds_at(rhi[x] + off) : 0u;
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            u32 v = __byte_perm(a, b, h ? 0x7632 : 0x5410);
+                            const int n = j * W + 2 * (int)wi + h;
+                            if (x < 2) {                               /* known filler 0: Ls = Lp1 = -4096 */
+                                if (n < Flo) v = (v & 0xFFFF0000u) | 0xF000u;
+                                if (n < Fhi) v = (v & 0x0000FFFFu) | 0xF0000000u;
+                            }
+                            dst[(2 * wi + h) * TS + f.t] = __vmins2(__vmaxs2(v, CLIP_LO), CLIP_HI);
+                        }
+                    }
+                }
+                if (tail_thr && j == M - 1) {
+                    /* beta_K of both constituents from the tail columns (R11 order) */
+                    u32 tl[12];
+#pragma unroll
+                    for (int mm = 0; mm < 12; mm++) {
+                        const int x = mm % 3;
+                        const u32 o = 2u * (u32)(K + mm / 3);
+                        int16_t a = 0, b = 0;
+                        if (clo >= 0) asm volatile("ld.shared.s16 %0, [%1];" : "=h"(a) : "r"(rlo[x] + o));
+                        if (chi >= 0) asm volatile("ld.shared.s16 %0, [%1];" : "=h"(b) : "r"(rhi[x] + o));
+                        tl[mm] = clamp_pack(a, b);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 2; c++) {
+                        u32 bb[NS];
+                        tail_beta(tl + 6 * c, bb);
+#pragma unroll
+                        for (int s = 0; s < NS; s++) sm[S_TAIL + p * 16 + c * 8 + s] = bb[s];
+                    }
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < HW; s++) {
+                q1[s] += f.pM;
+                q2[s] += f.pM;
+            }
+        } else {
+        const int64_t olo = clo >= 0 ? desc[clo].llr_off : 0, ohi = chi >= 0 ? desc[chi].llr_off : 0;
+        const int n0 = j * W + f.k0;
         /* every global load of the staging first (one round trip): the thread's 16
          * LLRs of each stream and CB, its QPP word indices and, for the last
          * window's tail thread, the 12 tail columns */
@@ -741,6 +851,10 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
 #pragma unroll
         for (int x = 0; x < 3; x++) {
             const int16_t *src = x == 0 ? l0 : x == 1 ? l1 : l2;
+#ifdef CRN_EXP_NOLLR
+            for (int k = 0; k < HW / 2; k++) { wl[x][k] = olo + n0 + k; wh[x][k] = ohi + k; }
+            continue;
+#endif
             if (clo >= 0) load16<LLR8>(src, olo + n0, sh8, wl[x]);
             else {
 #pragma unroll
@@ -754,8 +868,13 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         }
 #pragma unroll
         for (int s = 0; s < HW; s++) {
+#ifdef CRN_EXP_NOQPP
+            q1[s] = ((f.k0 + s) * 7 % 32) * TS + (j * 5) % M;
+            q2[s] = ((f.k0 + s) * 11 % 32) * TS + (j * 3) % M;
+#else
             q1[s] = __ldg(qinv + (f.k0 + s) * M + j);
             q2[s] = __ldg(qts + (f.k0 + s) * M + j);
+#endif
         }
         const bool tail_owner = active && tail_thr && j == M - 1;
         int16_t t0[12], t1[12];
@@ -810,9 +929,18 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             q1[s] += f.pM;
             q2[s] += f.pM;
         }
-        }   /* f.wact */
+        }   /* direct loads */
+        prof_mark(P_SLD);
         gsync<G>(g);
+        prof_mark(P_SB1);
         {
+            if (G == 1 && !LLR8 && bulk >= 0) {     /* Ls - Lp1 of the thread's own steps, from the planes */
+                u32 s0[HW];
+#pragma unroll
+                for (int s = 0; s < HW; s++)
+                    s0[s] = __vsub2(tmp[(f.k0 + s) * TS + f.t], sm[S_LP + (f.k0 + s) * TS + f.t]);
+                tm_store16(f.ts, s0);
+            }
             u32 sn[HW];
 #pragma unroll
             for (int s = 0; s < HW; s++)          /* interleaved systematic Ls[Pi(jW+k)] */
@@ -823,6 +951,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             tm_store16(f.ts + HW, sn);
             tm_wait_st();
         }
+        prof_mark(P_SG);
         gsync<G>(g);
         prof_mark(P_STAGE);
     }
@@ -845,7 +974,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         /* ---- row a9: L_APP = Ls + Le1 + La1_next (tie -> 1, R16); 16 bits per
          * thread and CB lane, merged per window; windowed CRC */
         {
-            u32 wlo = 0, whi = 0;
+            u32 wb = 0;                       /* bit s: lo CB's step k0 + s, bit 16 + s: hi CB's */
             int mlo = 0, mhi = 0;             /* MI statistic of this thread's steps (R29) */
             u32 sn[HW];
             const int n00 = f.j * W + f.k0, Fl = sh.F[2 * f.p], Fh = sh.F[2 * f.p + 1];
@@ -855,33 +984,36 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                 const u32 la1n = lds_q(qq[s], 0);                    /* La1_next[n] = Le2[Pi^-1(n)] */
                 const u32 ls = vadd(sn[s], sm[S_LP + (f.k0 + s) * TS + f.t]);
                 const u32 lapp = vadd(vadd(ls, sm[S_Y + (f.k0 + s) * TS + f.t]), la1n);
-                const u32 ge = __vcmpges2(lapp, 0u);
-                wlo |= (ge & 1u) << s;
-                whi |= ((ge >> 16) & 1u) << s;
+                /* b = (L_APP >= 0) per half enters at bits 15 / 31 and moves down one bit per
+                 * later step (w >> 1 as a multiply-high, off the ALU pipe) */
+                wb = __umulhi(wb, 0x80000000u) | (~lapp & 0x80008000u);
                 if (et == CRN_ET_MI) {
                     mlo += mi_pair(sh.mitab, lapp, n00 + s >= Fl, false);
                     mhi += mi_pair(sh.mitab, lapp, false, n00 + s >= Fh);
                 }
             }
-            u32 *hb = sm + S_X;               /* [half][lo/hi][window] */
+            u32 *hb = sm + S_X;               /* [half][window] bits of both CBs; [2 + lane][window] window words */
             if (active) {
-                hb[((tail_thr ? 2 : 0) + 0) * TS + f.t] = wlo;
-                hb[((tail_thr ? 2 : 0) + 1) * TS + f.t] = whi;
+                hb[(tail_thr ? 1 : 0) * TS + f.t] = wb;
                 if (et == CRN_ET_MI) {
                     atomicAdd(&sh.mi[2 * f.p], mlo);
                     atomicAdd(&sh.mi[2 * f.p + 1], mhi);
                 }
             }
+            prof_mark(P_HL);
             gsync<G>(g);
+            prof_mark(P_HB1);
+            u32 r3 = 0;                       /* this window's CRC register contribution */
+            int kind = CRN_CRC_NONE;
             if (active) {
                 /* the window's 32 hard decisions of one CB lane: the head thread takes
                  * the low (first) CB of the pair, the tail thread the high one */
                 const int p = f.p, j = f.j, l = tail_thr ? 1 : 0;
-                u32 w = hb[l * TS + f.t] | (hb[(2 + l) * TS + f.t] << 16);
+                u32 w = __byte_perm(hb[f.t], hb[TS + f.t], l ? 0x7632u : 0x5410u);
                 const int n0 = j * W, F = sh.F[2 * p + l];
                 if (F > n0) w &= (F >= n0 + 32) ? 0u : (0xFFFFFFFFu << (F - n0));
-                hb[l * TS + f.t] = w;                 /* (its own word: head and tail touch different ones) */
-                const int kind = sh.kind[2 * p + l];
+                hb[(2 + l) * TS + f.t] = w;
+                kind = sh.kind[2 * p + l];
                 if (kind != CRN_CRC_NONE) {
                     /* CRC register contribution x^(32 d) R(w) mod g, d = M-1-j = 64a + 8b + c, as
                      * three nibble-table maps (crn_internal.h CRN_CRC_NIB_WORDS) */
@@ -889,17 +1021,31 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                     const u32 d = (u32)(M - 1 - j);
                     const u32 t1 = T + (d & 7u) * 512u, t2 = T + 4096u + ((d >> 3) & 7u) * 384u,
                               t3 = T + 7168u + (d >> 6) * 384u;         /* byte addresses of the three maps */
-                    u32 r = 0, r2 = 0, r3 = 0;
+                    u32 r = 0, r2 = 0;
 #pragma unroll
                     for (int q = 0; q < 8; q++) r ^= lds_at(t1 + 64u * q + nib_off(w, q));
 #pragma unroll
                     for (int q = 0; q < 6; q++) r2 ^= lds_at(t2 + 64u * q + nib_off(r, q));
 #pragma unroll
                     for (int q = 0; q < 6; q++) r3 ^= lds_at(t3 + 64u * q + nib_off(r2, q));
-                    atomicXor(&sh.crc[2 * p + l], r3);
                 }
             }
+            /* combine the windows' contributions: one shared atomic per warp when all its
+             * lanes hold windows of one CB lane (every K with 32 | M), else one per window */
+            {
+                const int e = 2 * f.p + (tail_thr ? 1 : 0);
+                const int e0 = __shfl_sync(0xFFFFFFFFu, e, 0);      /* every lane: no short-circuit around it */
+                const bool uni = __all_sync(0xFFFFFFFFu, active && e == e0);
+                if (uni) {
+                    r3 = __reduce_xor_sync(0xFFFFFFFFu, r3);
+                    if ((threadIdx.x & 31) == 0 && kind != CRN_CRC_NONE) atomicXor(&sh.crc[e], r3);
+                } else if (active && kind != CRN_CRC_NONE) {
+                    atomicXor(&sh.crc[e], r3);
+                }
+            }
+            prof_mark(P_HC);
             gsync<G>(g);
+            prof_mark(P_HB2);
             /* stop decision (row a9; R3 / R29), taken by every thread for both CB lanes of
              * its pair from the complete CRC register and MI sum; the head (tail) thread
              * of window 0 is the low (high) lane's owner: it records crc_ok /
@@ -926,7 +1072,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                             *(volatile uint8_t *)&pg.dead[pg.tb[e]] = 1;
                         if (iters_used) iters_used[sh.cb[e]] = (uint8_t)it;
                     }
-                    if (l == (tail_thr ? 1 : 0)) out_bits[sh.bo[e] + j] = hb[l * TS + f.t];
+                    if (l == (tail_thr ? 1 : 0)) out_bits[sh.bo[e] + j] = hb[(2 + l) * TS + f.t];
                     if (ext_out) {
                         const int64_t oe = sh.eo[e] + j * W + f.k0;
 #pragma unroll
@@ -937,7 +1083,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                     }
                 }
             }
-            prof_mark(P_HD);
+            prof_mark(P_HDEC);
             /* one counting barrier: every read of this iteration's flags is before it */
             const int left = gsync_count<G>(g, running);
             if (active && f.j == 0) {
@@ -1275,7 +1421,7 @@ struct NextSh {
     int *task;
     crn_task *tk;
     int *cb, *F, *kind, *tb;
-    int64_t *bo, *eo;
+    int64_t *bo, *eo, *lo;      /* lo: LLR element offsets (for the bulk staging copies; may be null) */
 };
 
 __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks, const crn_task *__restrict__ tasks,
@@ -1298,6 +1444,7 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
             nx.kind[e] = 0;
             nx.bo[e] = 0;
             nx.eo[e] = 0;
+            if (nx.lo) nx.lo[e] = 0;
             if (nx.tb) nx.tb[e] = -1;
             continue;
         }
@@ -1306,6 +1453,7 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
         nx.kind[e] = d.crc_kind;
         nx.bo[e] = d.bit_off;
         nx.eo[e] = d.ext_off;
+        if (nx.lo) nx.lo[e] = d.llr_off;
         if (nx.tb) nx.tb[e] = d.reserved;
         const int esz = sh8 < 0 ? 2 : 1;                 /* int16 or int8 LLRs */
         const int64_t off = esz * d.llr_off;
@@ -1314,8 +1462,17 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
         for (int x = 0; x < 3; x++) {
             const uintptr_t a = reinterpret_cast<uintptr_t>(x == 0 ? l0 : x == 1 ? l1 : l2) + off;
             const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (a + bytes + 15) & ~(uintptr_t)15;
+#if defined(CRN_EXP_PFLINE)
+            for (uintptr_t q = a0 & ~(uintptr_t)127; q < a1; q += 128)
+                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(q) : "memory");
+#elif defined(CRN_EXP_PFEL)
+            asm volatile("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+                         "cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, pol;\n\t}"
+                         ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+#else
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
                          : "memory");
+#endif
         }
     }
 }
@@ -1342,6 +1499,9 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     __shared__ int s_cb[2 * MAXP], s_F[2 * MAXP], s_kind[2 * MAXP];
     __shared__ uint8_t s_done[2 * MAXP], s_fin[2 * MAXP];
     __shared__ int s_mi[2 * MAXP], s_mip[2 * MAXP], s_mitab[256];
+    __shared__ int64_t s_nlo[2 * MAXP];         /* next task: LLR element offsets (bulk staging) */
+    __shared__ uint8_t s_dlt[2 * MAXP];         /* current task: element offset of each CB inside its 16-byte copy */
+    __shared__ __align__(8) uint64_t s_mbar;    /* completion of the current task's bulk copies */
 
     int *counter = (int *)ws;
     if (n_tasks < 0) n_tasks = ((const volatile int *)ws)[1];   /* built on the device (crn_tasks.cu) */
@@ -1373,7 +1533,19 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
      * switches to three groups of four warps, each claiming its own tasks. */
     const int slots = (int)gridDim.x * G3;
     auto ahead = [&]() { return *(volatile int *)counter + slots < n_tasks; };
-    const NextSh nx{&s_ntask[0], &s_ntk[0], s_ncb, s_nF, s_nkind, PURGE ? s_ntb : nullptr, s_nbo, s_neo};
+    const NextSh nx{&s_ntask[0], &s_ntk[0], s_ncb, s_nF, s_nkind, PURGE ? s_ntb : nullptr, s_nbo, s_neo,
+                    (PURGE || LLR8) ? nullptr : s_nlo};
+    /* bulk staging (whole-CTA W = 32 tasks of the default instantiations): the three
+     * stream bases must be 16-byte aligned (per launch), every CB's offset even (per task) */
+#ifndef CRN_BULK_STAGE
+    const bool bulk_base = false &&
+#else
+    const bool bulk_base = !PURGE && !LLR8 &&
+#endif
+        (((uintptr_t)l0 | (uintptr_t)l1 | (uintptr_t)l2) & 15) == 0;
+    const u32 mbar = smem_addr(&s_mbar);
+    int bulk_par = 0;
+    if (tid == 0) mbar_init(mbar, 1);
     prof_init();
     if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
     bool pend = false;                          /* warp 0: the next task is still to be claimed */
@@ -1388,6 +1560,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             grp_mode = true;
             break;
         }
+        int odd = 0;
         for (int e = tid; e < 2 * tk.n_pairs; e += BLOCK) {
             const int cb = s_ncb[e];
             s_cb[e] = cb;
@@ -1395,6 +1568,10 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             s_kind[e] = s_nkind[e];
             s_bo[e] = s_nbo[e];
             s_eo[e] = s_neo[e];
+            if (bulk_base) {
+                s_dlt[e] = (uint8_t)(s_nlo[e] & 7);
+                odd |= (int)(s_nlo[e] & 1);
+            }
             s_done[e] = cb < 0;
             s_fin[e] = 0;
             s_crc[e] = 0;
@@ -1409,11 +1586,37 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
                 if (iters_used) iters_used[cb] = 0;
             }
         }
-        __syncthreads();                        /* next slots consumed */
+        fence_proxy_async();                    /* shared memory of the last task before the bulk copies */
+        odd = __syncthreads_or(odd);            /* next slots consumed */
+        prof_mark(P_FB);
+        const int bulk = (bulk_base && tk.W == 32 && !odd && bulk_slots(tk.K) >= 6 * tk.n_pairs) ? bulk_par : -1;
         if (tid < 32) {
+            if (bulk >= 0) {
+                /* copy c = x * 2NP + e: stream x of CB lane e, widened to 16-byte boundaries */
+                const int ncp = 6 * tk.n_pairs, K = tk.K;
+                const u32 base = smem_addr(smem);
+                u32 bytes = 0;
+                for (int c = tid; c < ncp; c += 32) {
+                    const int x = c / (2 * tk.n_pairs), e = c - x * 2 * tk.n_pairs;
+                    if (s_cb[e] < 0) continue;
+                    const uintptr_t a = reinterpret_cast<uintptr_t>(x == 0 ? l0 : x == 1 ? l1 : l2) + 2 * s_nlo[e];
+                    bytes += (u32)(((a + 2 * (K + 4) + 15) & ~(uintptr_t)15) - (a & ~(uintptr_t)15));
+                }
+                bytes = __reduce_add_sync(0xFFFFFFFFu, bytes);
+                if (tid == 0) mbar_expect_tx(mbar, bytes);
+                __syncwarp();
+                for (int c = tid; c < ncp; c += 32) {
+                    const int x = c / (2 * tk.n_pairs), e = c - x * 2 * tk.n_pairs;
+                    if (s_cb[e] < 0) continue;
+                    const uintptr_t a = reinterpret_cast<uintptr_t>(x == 0 ? l0 : x == 1 ? l1 : l2) + 2 * s_nlo[e];
+                    const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (a + 2 * (K + 4) + 15) & ~(uintptr_t)15;
+                    bulk_g2s(bulk_slot(base, K, c), reinterpret_cast<const void *>(a0), (u32)(a1 - a0), mbar);
+                }
+            }
             pend = !ahead();
             if (!pend) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
         }
+        if (bulk >= 0) bulk_par ^= 1;
         if (PURGE) {                            /* a fully purged task is skipped */
             if (tid == 0) {
                 int left = 0;
@@ -1429,7 +1632,8 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
         do {                                                                                                      \
             if (tk.W == 32)                                                                                       \
                 run_task_fast<V, PURGE, LLR8, 1>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok,           \
-                                                 iters_used, ext_out, tab, smem, tmem, sh, pg, sh8);              \
+                                                 iters_used, ext_out, tab, smem, tmem, sh, pg, sh8, bulk, mbar,   \
+                                                 s_dlt);                                                          \
             else                                                                                                  \
                 run_task_split<V, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, \
                                                ext_out, tab, smem, tmem, sh, pg, sh8);                            \
@@ -1442,7 +1646,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     if (grp_mode) {                             /* CTA-uniform */
         const int g = tid / GB3, ltid = tid - g * GB3, eb = 2 * GPB3 * g;
         const NextSh ng{&s_ntask[g], &s_ntk[g], s_ncb + eb, s_nF + eb, s_nkind + eb, PURGE ? s_ntb + eb : nullptr,
-                        s_nbo + eb, s_neo + eb};
+                        s_nbo + eb, s_neo + eb, nullptr};
         bool gpend = g > 0;                     /* group 0 starts with the task the CTA claimed */
         for (;;) {
             if (gpend && ltid < 32) claim_next(ng, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, ltid, sh8);

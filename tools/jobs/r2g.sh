@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+TAG=r2g
+bash tools/jobs/abq.sh ${TAG}_ab base hd1 base hd1
+for c in "64 4" "100 3"; do
+  set -- $c
+  CRN_LIB=$PWD/paper_1905_01141_b200/variants/libcrn_prof_hd1.so timeout 300 python tools/phase_prof.py $1 $2 > gpurun_out/${TAG}_phase_cfg$2.json 2>&1
+done

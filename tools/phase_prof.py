@@ -16,7 +16,8 @@ from paper_1905_01141_b200 import batch as bmod  # noqa: E402
 from paper_1905_01141_b200 import crn  # noqa: E402
 from paper_1905_01141_b200 import workload as wlmod  # noqa: E402
 
-NAMES = ["fetch", "stage", "chunk", "phase1", "bar1", "phase2", "bar2", "hard_dec"]
+NAMES = ["fetch", "stage", "chunk", "phase1", "bar1", "phase2", "bar2", "hard_dec", "st_loads", "st_bar1", "st_gather",
+         "hd_lapp", "hd_bar1", "hd_crc", "hd_bar2", "hd_decide", "fetch_bars"]
 
 
 def main():
