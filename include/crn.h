@@ -305,6 +305,14 @@ int crn_kpi_iterations(const uint8_t *iters_used, const uint8_t *crc_ok, int32_t
  * desc is HOST memory; info/d0/d1/d2 device memory. */
 int crn_encode_batch(const crn_cb_desc *desc, int32_t n_cb, const uint8_t *info, int32_t attach_crc,
                      uint8_t *d0, uint8_t *d1, uint8_t *d2, void *cuda_stream);
+/* The same with packed bits (bit b of a stream is bit b % 32 of word b / 32,
+ * LSB first; one eighth of the bytes of the form above): CB i's K_i content bits
+ * are bits [ext_off, ext_off + K_i) of info, its K_i + 4 coded bits of stream x
+ * are written to bits [llr_off, llr_off + K_i + 4) of dx.  Offsets need no
+ * alignment: CBs may share a word (such words are merged atomically, bits
+ * outside every CB's range are left as they were).  Errors as crn_encode_batch. */
+int crn_encode_batch_packed(const crn_cb_desc *desc, int32_t n_cb, const uint32_t *info, int32_t attach_crc,
+                            uint32_t *d0, uint32_t *d1, uint32_t *d2, void *cuda_stream);
 
 /* ------------------------------------------------------------------ rate matching */
 
@@ -336,6 +344,13 @@ int crn_rate_dematch_batch(const crn_rm_desc *desc, int32_t n_cb, const int16_t 
  * them) -> its E selected bits e[e_off ..) (one bit per byte). */
 int crn_rate_match_batch(const crn_rm_desc *desc, int32_t n_cb, const uint8_t *d0, const uint8_t *d1,
                          const uint8_t *d2, uint8_t *e, void *cuda_stream);
+/* The same with packed bits (LSB-first words, as crn_encode_batch_packed writes
+ * them): CB i's stream x is bits [llr_off, llr_off + K + 4) of dx, its E selected
+ * bits go to bits [e_off, e_off + E) of e (e_off, llr_off in BITS; no alignment
+ * needed: words shared with neighbouring CBs are merged atomically, bits outside
+ * every CB's range are left as they were).  Errors as crn_rate_match_batch. */
+int crn_rate_match_batch_packed(const crn_rm_desc *desc, int32_t n_cb, const uint32_t *d0, const uint32_t *d1,
+                                const uint32_t *d2, uint32_t *e, void *cuda_stream);
 
 /* ------------------------------------------------------------------ host helpers */
 

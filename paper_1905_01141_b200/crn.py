@@ -75,11 +75,13 @@ _SIGS = {
     "crn_counted_ops": (C.c_int64, [i32p, C.c_int32, u8p, C.c_int32]),
     "crn_kpi_iterations": (C.c_int, [u8p, u8p, C.c_int32, C.c_int32, u8p]),
     "crn_encode_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp]),
+    "crn_encode_batch_packed": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp]),
     "crn_tb_build_cbs": (C.c_int, [u8p, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_int64, u8p, vp,
                                    i32p]),
     "crn_tb_build_cbs_batch": (C.c_int, [i64p, i64p, C.c_int32, vp, C.c_int32, vp, vp, i32p, vp]),
     "crn_rate_dematch_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp]),
     "crn_rate_match_batch": (C.c_int, [vp, C.c_int32, vp, vp, vp, vp, vp]),
+    "crn_rate_match_batch_packed": (C.c_int, [vp, C.c_int32, vp, vp, vp, vp, vp]),
     "crn_tb_verdict_batch": (C.c_int, [vp, C.c_int32, vp, C.c_int32, vp, vp, vp, vp, vp]),
     "crn_tb_reassemble": (C.c_int, [u32p, vp, u8p, C.c_int32, C.c_int64, u8p]),
     "crn_segment_tb": (C.c_int, [C.c_int64, P(Seg)]),
@@ -338,6 +340,22 @@ def encode_batch(desc, info, attach_crc: bool, d0, d1, d2, stream=None) -> None:
                                 _ptr(d2), _stream(stream)), "crn_encode_batch")
 
 
+def encode_batch_packed(desc, info, attach_crc: bool, d0, d1, d2, stream=None) -> None:
+    """crn_encode_batch_packed: info / d* int32 CUDA tensors of packed LSB-first bits;
+    ext_off / llr_off are BIT offsets."""
+    _cuda_dev(info, d0, d1, d2)
+    _need_i32(info, d0, d1, d2)
+    desc = np.ascontiguousarray(desc, DESC_DTYPE)
+    _chk(lib().crn_encode_batch_packed(desc.ctypes.data, desc.size, _ptr(info), int(attach_crc), _ptr(d0), _ptr(d1),
+                                       _ptr(d2), _stream(stream)), "crn_encode_batch_packed")
+
+
+def _need_i32(*ts):
+    for t in ts:
+        if t.dtype != __import__("torch").int32:
+            raise CrnError("packed-bit buffers are int32 tensors")
+
+
 def tb_build_cbs(tb_bits, base_bit: int = 0, base_llr: int = 0, base_word: int = 0, max_cb: int = 64):
     """-> (cb_bits uint8 [sum K], desc array [C])."""
     tb = np.ascontiguousarray(tb_bits, np.uint8)
@@ -391,6 +409,16 @@ def rate_match_batch(desc, d0, d1, d2, e, stream=None) -> None:
     desc = np.ascontiguousarray(desc, RM_DTYPE)
     _chk(lib().crn_rate_match_batch(desc.ctypes.data, desc.size, _ptr(d0), _ptr(d1), _ptr(d2), _ptr(e),
                                     _stream(stream)), "crn_rate_match_batch")
+
+
+def rate_match_batch_packed(desc, d0, d1, d2, e, stream=None) -> None:
+    """crn_rate_match_batch_packed: desc (RM_DTYPE, llr_off / e_off in BITS) host array;
+    d*, e int32 CUDA tensors of packed LSB-first bits."""
+    _cuda_dev(d0, d1, d2, e)
+    _need_i32(d0, d1, d2, e)
+    desc = np.ascontiguousarray(desc, RM_DTYPE)
+    _chk(lib().crn_rate_match_batch_packed(desc.ctypes.data, desc.size, _ptr(d0), _ptr(d1), _ptr(d2), _ptr(e),
+                                           _stream(stream)), "crn_rate_match_batch_packed")
 
 
 TB_DTYPE = np.dtype([("cb0", "<i4"), ("n_cb", "<i4"), ("tbs", "<i8"), ("word_off", "<i8")])

@@ -78,7 +78,7 @@ constexpr int S_OFFS = S_CRCNIB + 2 * CRN_CRC_NIB_WORDS;   /* int64 [4][2 MAXP]:
 static_assert(S_OFFS % 2 == 0, "8-byte aligned");
 constexpr int SMEM_WORDS = S_OFFS + 4 * 2 * MAXP * 2;
 constexpr int YZ_END_BYTES = 4 * (S_Z + SUMK);     /* + static shared memory: must stay < 64 KiB */
-static_assert(SMEM_WORDS * 4 + 10240 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
+static_assert(SMEM_WORDS * 4 + 9728 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
 
 /* ---- optional phase profiler (build with -DCRN_PHASE_PROF; never in the product
  * build): lane 0 of warp 0 (a head warp) and of warp 6 (a tail warp) attribute
@@ -113,6 +113,32 @@ __device__ __forceinline__ void prof_flush() {
 }
 #else
 __device__ __forceinline__ void prof_mark(int) {}
+#endif
+/* ---- optional task trace (build with -DCRN_TASK_TRACE; never in the product build):
+ * per task its start / end %globaltimer (ns), SM and group, tools/task_trace.py */
+#ifdef CRN_TASK_TRACE
+constexpr int TRACE_MAX = 1 << 16;
+__device__ unsigned long long g_trace[4 * TRACE_MAX];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace_task(int task, int which, int g) {
+    if (task < TRACE_MAX) {
+        g_trace[4 * task + which] = gtimer();
+        if (which == 0) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+            g_trace[4 * task + 2] = sm;
+            g_trace[4 * task + 3] = (unsigned long long)g;
+        }
+    }
+}
+#else
+__device__ __forceinline__ void trace_task(int, int, int) {}
+#endif
+#ifndef CRN_PHASE_PROF
 __device__ __forceinline__ void prof_init() {}
 __device__ __forceinline__ void prof_flush() {}
 #endif
@@ -548,45 +574,6 @@ __device__ __forceinline__ u32 lds_q(u32 qq, int c) {
     return v;
 }
 
-/* ---- asynchronous bulk copies (TMA engine) of a task's input streams into shared
- * memory, completing on one mbarrier (row a2: the coalesced LLR load) */
-__device__ __forceinline__ void mbar_init(u32 bar, u32 count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(u32 bar, u32 bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
-    asm volatile("{\n\t.reg .pred p;\n"
-                 "CRN_MBW%=:\n\t"
-                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-                 "@!p bra CRN_MBW%=;\n\t}" ::"r"(bar), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(u32 dst, const void *src, u32 bytes, u32 bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
-}
-/* orders this thread's earlier generic-proxy shared-memory accesses before later async-proxy writes */
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-/* Bulk staging plan of a whole-CTA W = 32 task (crn_decode.cu run_task_fast): copy
- * c = x * 2NP + e (stream x, CB lane e) of the K + 4 values of CB lane e, widened to
- * 16-byte boundaries, lands in a slot of BS(K) bytes in one of three regions that
- * are free until the task's first half-iteration: CH (branch-metric chunks), NII + X
- * (boundary states, hand-over) and Y (Le1). */
-constexpr int RB0 = 4 * (HW * BLOCK * 2), RB1 = 4 * (S_NII_WORDS + 2 * NS * WMAX), RB2 = 4 * SUMK;   /* region bytes */
-__host__ __device__ constexpr int bulk_slot_bytes(int K) { return (2 * (K + 4) + 28 + 15) & ~15; }
-__host__ __device__ constexpr int bulk_slots(int K) {
-    return RB0 / bulk_slot_bytes(K) + RB1 / bulk_slot_bytes(K) + RB2 / bulk_slot_bytes(K);
-}
-/* shared byte address of copy c's slot */
-__device__ __forceinline__ u32 bulk_slot(u32 smem_base, int K, int c) {
-    const int S = bulk_slot_bytes(K), n0 = RB0 / S, n1 = RB1 / S;
-    return c < n0 ? smem_base + 4u * S_CH + (u32)(c * S)
-         : c < n0 + n1 ? smem_base + 4u * S_NII + (u32)((c - n0) * S)
-                       : smem_base + 4u * S_Y + (u32)((c - n0 - n1) * S);
-}
-
 /* One half-iteration of constituent c (rows a5-a8).  Le -> Y (c = 0, natural
  * order) or Z (c = 1, interleaved order). */
 template <int VAR, int G>
@@ -729,7 +716,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                                               uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok,
                                               uint8_t *__restrict__ iters_used, int16_t *__restrict__ ext_out,
                                               const crn_tables &tab, u32 *sm, u32 tmem, TaskSh sh, Purge pg,
-                                              int sh8, int bulk = -1, u32 mbar = 0, const uint8_t *dlt = nullptr) {
+                                              int sh8) {
     constexpr int W = 32;
     const int M = tk.M, NP = tk.n_pairs, T = NP * M;
     constexpr int GWIN = WMAX / G;              /* windows of the group's task */
@@ -771,77 +758,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         const int Flo = sh.F[2 * p], Fhi = sh.F[2 * p + 1];
         u32 *tmp = sm + S_Z;                  /* natural Ls, window-major, for the interleaved gather
                                                  (the Z plane is first written in DEC2 of iteration 1) */
-        if (G == 1 && !LLR8 && bulk >= 0) {
-            /* the task's streams were bulk-copied into shared memory (decode_kernel): the QPP
-             * word indices are loaded while the copies land, then every thread transposes
-             * its window's words into the [step][window] planes */
-#pragma unroll
-            for (int s = 0; s < HW; s++) {
-                q1[s] = __ldg(qinv + (f.k0 + s) * M + j);
-                q2[s] = __ldg(qts + (f.k0 + s) * M + j);
-            }
-            const u32 base = smem_addr(sm);
-            const int K = tk.K;
-            u32 rlo[3], rhi[3];                 /* byte address of element 0 of each stream of the pair's CBs */
-#pragma unroll
-            for (int x = 0; x < 3; x++) {
-                rlo[x] = bulk_slot(base, K, x * 2 * NP + 2 * p) + 2u * dlt[2 * p];
-                rhi[x] = bulk_slot(base, K, x * 2 * NP + 2 * p + 1) + 2u * dlt[2 * p + 1];
-            }
-            mbar_wait(mbar, (u32)bulk);
-            if (active) {
-                /* word wi of the window (elements 2 wi, 2 wi + 1) of each stream: the head
-                 * thread takes 8 words, the tail thread the other 8, rotated by lane so that
-                 * a warp's 32 reads (windows 64 bytes apart) hit 32 distinct banks; the
-                 * plane writes (one column per lane) are conflict-free as well */
-                const u32 rot = (u32)(tid >> 1) & 15u;
-#pragma unroll
-                for (int x = 0; x < 3; x++) {
-                    u32 *dst = x == 0 ? tmp : sm + S_LP + (x - 1) * SUMK;
-#pragma unroll
-                    for (int q = 0; q < HW / 2; q++) {
-                        const u32 wi = ((tail_thr ? 8u : 0u) + (u32)q + rot) & 15u;
-                        const u32 off = 4u * (16u * (u32)j + wi);
-                        const u32 a = clo >= 0 ? lds_at(rlo[x] + off) : 0u, b = chi >= 0 ? lds_at(rhi[x] + off) : 0u;
-#pragma unroll
-                        for (int h = 0; h < 2; h++) {
-                            u32 v = __byte_perm(a, b, h ? 0x7632 : 0x5410);
-                            const int n = j * W + 2 * (int)wi + h;
-                            if (x < 2) {                               /* known filler 0: Ls = Lp1 = -4096 */
-                                if (n < Flo) v = (v & 0xFFFF0000u) | 0xF000u;
-                                if (n < Fhi) v = (v & 0x0000FFFFu) | 0xF0000000u;
-                            }
-                            dst[(2 * wi + h) * TS + f.t] = __vmins2(__vmaxs2(v, CLIP_LO), CLIP_HI);
-                        }
-                    }
-                }
-                if (tail_thr && j == M - 1) {
-                    /* beta_K of both constituents from the tail columns (R11 order) */
-                    u32 tl[12];
-#pragma unroll
-                    for (int mm = 0; mm < 12; mm++) {
-                        const int x = mm % 3;
-                        const u32 o = 2u * (u32)(K + mm / 3);
-                        int16_t a = 0, b = 0;
-                        if (clo >= 0) asm volatile("ld.shared.s16 %0, [%1];" : "=h"(a) : "r"(rlo[x] + o));
-                        if (chi >= 0) asm volatile("ld.shared.s16 %0, [%1];" : "=h"(b) : "r"(rhi[x] + o));
-                        tl[mm] = clamp_pack(a, b);
-                    }
-#pragma unroll
-                    for (int c = 0; c < 2; c++) {
-                        u32 bb[NS];
-                        tail_beta(tl + 6 * c, bb);
-#pragma unroll
-                        for (int s = 0; s < NS; s++) sm[S_TAIL + p * 16 + c * 8 + s] = bb[s];
-                    }
-                }
-            }
-#pragma unroll
-            for (int s = 0; s < HW; s++) {
-                q1[s] += f.pM;
-                q2[s] += f.pM;
-            }
-        } else {
+        {
         const int64_t olo = clo >= 0 ? desc[clo].llr_off : 0, ohi = chi >= 0 ? desc[chi].llr_off : 0;
         const int n0 = j * W + f.k0;
         /* every global load of the staging first (one round trip): the thread's 16
@@ -851,10 +768,6 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
 #pragma unroll
         for (int x = 0; x < 3; x++) {
             const int16_t *src = x == 0 ? l0 : x == 1 ? l1 : l2;
-#ifdef CRN_EXP_NOLLR
-            for (int k = 0; k < HW / 2; k++) { wl[x][k] = olo + n0 + k; wh[x][k] = ohi + k; }
-            continue;
-#endif
             if (clo >= 0) load16<LLR8>(src, olo + n0, sh8, wl[x]);
             else {
 #pragma unroll
@@ -868,13 +781,8 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         }
 #pragma unroll
         for (int s = 0; s < HW; s++) {
-#ifdef CRN_EXP_NOQPP
-            q1[s] = ((f.k0 + s) * 7 % 32) * TS + (j * 5) % M;
-            q2[s] = ((f.k0 + s) * 11 % 32) * TS + (j * 3) % M;
-#else
             q1[s] = __ldg(qinv + (f.k0 + s) * M + j);
             q2[s] = __ldg(qts + (f.k0 + s) * M + j);
-#endif
         }
         const bool tail_owner = active && tail_thr && j == M - 1;
         int16_t t0[12], t1[12];
@@ -929,18 +837,11 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             q1[s] += f.pM;
             q2[s] += f.pM;
         }
-        }   /* direct loads */
+        }
         prof_mark(P_SLD);
         gsync<G>(g);
         prof_mark(P_SB1);
         {
-            if (G == 1 && !LLR8 && bulk >= 0) {     /* Ls - Lp1 of the thread's own steps, from the planes */
-                u32 s0[HW];
-#pragma unroll
-                for (int s = 0; s < HW; s++)
-                    s0[s] = __vsub2(tmp[(f.k0 + s) * TS + f.t], sm[S_LP + (f.k0 + s) * TS + f.t]);
-                tm_store16(f.ts, s0);
-            }
             u32 sn[HW];
 #pragma unroll
             for (int s = 0; s < HW; s++)          /* interleaved systematic Ls[Pi(jW+k)] */
@@ -1421,7 +1322,7 @@ struct NextSh {
     int *task;
     crn_task *tk;
     int *cb, *F, *kind, *tb;
-    int64_t *bo, *eo, *lo;      /* lo: LLR element offsets (for the bulk staging copies; may be null) */
+    int64_t *bo, *eo;
 };
 
 __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks, const crn_task *__restrict__ tasks,
@@ -1444,7 +1345,6 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
             nx.kind[e] = 0;
             nx.bo[e] = 0;
             nx.eo[e] = 0;
-            if (nx.lo) nx.lo[e] = 0;
             if (nx.tb) nx.tb[e] = -1;
             continue;
         }
@@ -1453,7 +1353,6 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
         nx.kind[e] = d.crc_kind;
         nx.bo[e] = d.bit_off;
         nx.eo[e] = d.ext_off;
-        if (nx.lo) nx.lo[e] = d.llr_off;
         if (nx.tb) nx.tb[e] = d.reserved;
         const int esz = sh8 < 0 ? 2 : 1;                 /* int16 or int8 LLRs */
         const int64_t off = esz * d.llr_off;
@@ -1462,17 +1361,8 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
         for (int x = 0; x < 3; x++) {
             const uintptr_t a = reinterpret_cast<uintptr_t>(x == 0 ? l0 : x == 1 ? l1 : l2) + off;
             const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (a + bytes + 15) & ~(uintptr_t)15;
-#if defined(CRN_EXP_PFLINE)
-            for (uintptr_t q = a0 & ~(uintptr_t)127; q < a1; q += 128)
-                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(q) : "memory");
-#elif defined(CRN_EXP_PFEL)
-            asm volatile("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-                         "cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, pol;\n\t}"
-                         ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
-#else
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
                          : "memory");
-#endif
         }
     }
 }
@@ -1499,9 +1389,6 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     __shared__ int s_cb[2 * MAXP], s_F[2 * MAXP], s_kind[2 * MAXP];
     __shared__ uint8_t s_done[2 * MAXP], s_fin[2 * MAXP];
     __shared__ int s_mi[2 * MAXP], s_mip[2 * MAXP], s_mitab[256];
-    __shared__ int64_t s_nlo[2 * MAXP];         /* next task: LLR element offsets (bulk staging) */
-    __shared__ uint8_t s_dlt[2 * MAXP];         /* current task: element offset of each CB inside its 16-byte copy */
-    __shared__ __align__(8) uint64_t s_mbar;    /* completion of the current task's bulk copies */
 
     int *counter = (int *)ws;
     if (n_tasks < 0) n_tasks = ((const volatile int *)ws)[1];   /* built on the device (crn_tasks.cu) */
@@ -1533,19 +1420,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
      * switches to three groups of four warps, each claiming its own tasks. */
     const int slots = (int)gridDim.x * G3;
     auto ahead = [&]() { return *(volatile int *)counter + slots < n_tasks; };
-    const NextSh nx{&s_ntask[0], &s_ntk[0], s_ncb, s_nF, s_nkind, PURGE ? s_ntb : nullptr, s_nbo, s_neo,
-                    (PURGE || LLR8) ? nullptr : s_nlo};
-    /* bulk staging (whole-CTA W = 32 tasks of the default instantiations): the three
-     * stream bases must be 16-byte aligned (per launch), every CB's offset even (per task) */
-#ifndef CRN_BULK_STAGE
-    const bool bulk_base = false &&
-#else
-    const bool bulk_base = !PURGE && !LLR8 &&
-#endif
-        (((uintptr_t)l0 | (uintptr_t)l1 | (uintptr_t)l2) & 15) == 0;
-    const u32 mbar = smem_addr(&s_mbar);
-    int bulk_par = 0;
-    if (tid == 0) mbar_init(mbar, 1);
+    const NextSh nx{&s_ntask[0], &s_ntk[0], s_ncb, s_nF, s_nkind, PURGE ? s_ntb : nullptr, s_nbo, s_neo};
     prof_init();
     if (tid < 32) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
     bool pend = false;                          /* warp 0: the next task is still to be claimed */
@@ -1560,7 +1435,6 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             grp_mode = true;
             break;
         }
-        int odd = 0;
         for (int e = tid; e < 2 * tk.n_pairs; e += BLOCK) {
             const int cb = s_ncb[e];
             s_cb[e] = cb;
@@ -1568,10 +1442,6 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             s_kind[e] = s_nkind[e];
             s_bo[e] = s_nbo[e];
             s_eo[e] = s_neo[e];
-            if (bulk_base) {
-                s_dlt[e] = (uint8_t)(s_nlo[e] & 7);
-                odd |= (int)(s_nlo[e] & 1);
-            }
             s_done[e] = cb < 0;
             s_fin[e] = 0;
             s_crc[e] = 0;
@@ -1586,37 +1456,12 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
                 if (iters_used) iters_used[cb] = 0;
             }
         }
-        fence_proxy_async();                    /* shared memory of the last task before the bulk copies */
-        odd = __syncthreads_or(odd);            /* next slots consumed */
+        __syncthreads();                        /* next slots consumed */
         prof_mark(P_FB);
-        const int bulk = (bulk_base && tk.W == 32 && !odd && bulk_slots(tk.K) >= 6 * tk.n_pairs) ? bulk_par : -1;
         if (tid < 32) {
-            if (bulk >= 0) {
-                /* copy c = x * 2NP + e: stream x of CB lane e, widened to 16-byte boundaries */
-                const int ncp = 6 * tk.n_pairs, K = tk.K;
-                const u32 base = smem_addr(smem);
-                u32 bytes = 0;
-                for (int c = tid; c < ncp; c += 32) {
-                    const int x = c / (2 * tk.n_pairs), e = c - x * 2 * tk.n_pairs;
-                    if (s_cb[e] < 0) continue;
-                    const uintptr_t a = reinterpret_cast<uintptr_t>(x == 0 ? l0 : x == 1 ? l1 : l2) + 2 * s_nlo[e];
-                    bytes += (u32)(((a + 2 * (K + 4) + 15) & ~(uintptr_t)15) - (a & ~(uintptr_t)15));
-                }
-                bytes = __reduce_add_sync(0xFFFFFFFFu, bytes);
-                if (tid == 0) mbar_expect_tx(mbar, bytes);
-                __syncwarp();
-                for (int c = tid; c < ncp; c += 32) {
-                    const int x = c / (2 * tk.n_pairs), e = c - x * 2 * tk.n_pairs;
-                    if (s_cb[e] < 0) continue;
-                    const uintptr_t a = reinterpret_cast<uintptr_t>(x == 0 ? l0 : x == 1 ? l1 : l2) + 2 * s_nlo[e];
-                    const uintptr_t a0 = a & ~(uintptr_t)15, a1 = (a + 2 * (K + 4) + 15) & ~(uintptr_t)15;
-                    bulk_g2s(bulk_slot(base, K, c), reinterpret_cast<const void *>(a0), (u32)(a1 - a0), mbar);
-                }
-            }
             pend = !ahead();
             if (!pend) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
         }
-        if (bulk >= 0) bulk_par ^= 1;
         if (PURGE) {                            /* a fully purged task is skipped */
             if (tid == 0) {
                 int left = 0;
@@ -1627,13 +1472,13 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             if (s_left[0] == 0) continue;
         }
         prof_mark(P_FETCH);
+        if (tid == 0) trace_task(task, 0, 0);
         /* VAR = LOGMAP: its own kernels; otherwise MAXLOG / SCALED chosen per launch */
 #define CRN_RUN(V)                                                                                                \
         do {                                                                                                      \
             if (tk.W == 32)                                                                                       \
                 run_task_fast<V, PURGE, LLR8, 1>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok,           \
-                                                 iters_used, ext_out, tab, smem, tmem, sh, pg, sh8, bulk, mbar,   \
-                                                 s_dlt);                                                          \
+                                                 iters_used, ext_out, tab, smem, tmem, sh, pg, sh8);              \
             else                                                                                                  \
                 run_task_split<V, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, \
                                                ext_out, tab, smem, tmem, sh, pg, sh8);                            \
@@ -1642,11 +1487,12 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
         else if ((variant & 0xFF) == CRN_VARIANT_SCALED) CRN_RUN(CRN_VARIANT_SCALED);
         else CRN_RUN(CRN_VARIANT_MAXLOG);
 #undef CRN_RUN
+        if (tid == 0) trace_task(task, 1, 0);
     }
     if (grp_mode) {                             /* CTA-uniform */
         const int g = tid / GB3, ltid = tid - g * GB3, eb = 2 * GPB3 * g;
         const NextSh ng{&s_ntask[g], &s_ntk[g], s_ncb + eb, s_nF + eb, s_nkind + eb, PURGE ? s_ntb + eb : nullptr,
-                        s_nbo + eb, s_neo + eb, nullptr};
+                        s_nbo + eb, s_neo + eb};
         bool gpend = g > 0;                     /* group 0 starts with the task the CTA claimed */
         for (;;) {
             if (gpend && ltid < 32) claim_next(ng, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, ltid, sh8);
@@ -1688,6 +1534,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
                 gsync<G3>(g);
                 if (s_left[g] == 0) continue;
             }
+            if (ltid == 0) trace_task(task, 0, 1 + g);
             if constexpr (VAR == CRN_VARIANT_LOGMAP)
                 run_task_fast<CRN_VARIANT_LOGMAP, PURGE, LLR8, G3>(tk, desc, l0, l1, l2, max_iters, et, out_bits,
                                                                    crc_ok, iters_used, ext_out, tab, smem, tmem, sh,
@@ -1700,6 +1547,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
                 run_task_fast<CRN_VARIANT_MAXLOG, PURGE, LLR8, G3>(tk, desc, l0, l1, l2, max_iters, et, out_bits,
                                                                    crc_ok, iters_used, ext_out, tab, smem, tmem, sh,
                                                                    pg, sh8);
+            if (ltid == 0) trace_task(task, 1, 1 + g);
         }
     }
     prof_flush();
@@ -1815,6 +1663,15 @@ extern "C" int crn_prof_read(unsigned long long *out) {
     if (cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 2 * P_N) != cudaSuccess) return CRN_ECUDA;
     static const unsigned long long z[2 * P_N] = {};
     cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+    return CRN_OK;
+}
+#endif
+
+#ifdef CRN_TASK_TRACE
+/* task trace readout (tracing builds only): 4 words per task (start ns, end ns, SM, group), then reset */
+extern "C" int crn_trace_read(unsigned long long *out, int32_t n_tasks) {
+    const size_t n = (size_t)(n_tasks < TRACE_MAX ? n_tasks : TRACE_MAX) * 4;
+    if (cudaMemcpyFromSymbol(out, g_trace, n * sizeof(unsigned long long)) != cudaSuccess) return CRN_ECUDA;
     return CRN_OK;
 }
 #endif

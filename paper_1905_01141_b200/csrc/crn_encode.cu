@@ -73,7 +73,7 @@ struct EncShared {
     struct Warp {
         uint32_t c[ENC_WORDS + 2];        /* c, packed LSB-first */
         uint32_t ci[ENC_WORDS];           /* c' = c_{Pi(i)} */
-        uint32_t z1[ENC_WORDS], z2[ENC_WORDS];
+        uint32_t z1[ENC_WORDS + 2], z2[ENC_WORDS + 2];   /* (+ the tail word of the packed write-out) */
     } w[ENC_WARPS];
 };
 
@@ -147,9 +147,54 @@ __device__ __forceinline__ void load_bits(const uint8_t *src, int K, uint32_t *c
     __syncwarp();
 }
 
+/* K bits at bit offset off of a packed LSB-first array -> c[0 .. ceil(K/32)) (bits past K
+ * in the last word are the source's; the caller masks them) */
+__device__ __forceinline__ void load_bits_packed(const uint32_t *src, int64_t off, int K, uint32_t *c, int lane) {
+    const int nw = (K + 31) >> 5, sh = (int)(off & 31);
+    const uint32_t *s = src + (off >> 5);
+    for (int t = lane; t < nw; t += 32) {
+        const uint32_t a = __ldg(s + t);
+        const uint32_t b = (sh && 32 * t + 32 - sh < K) ? __ldg(s + t + 1) : 0u;   /* the next word only if needed */
+        c[t] = __funnelshift_r(a, b, sh);
+    }
+    __syncwarp();
+}
+
+/* src bits [0, nbits) -> dst bits [off, off + nbits) (packed LSB-first); words the
+ * range covers only in part are merged with two atomics (neighbouring CBs share
+ * them), whole words are plain stores.  src must hold ceil(nbits / 32) + 1 words. */
+__device__ __forceinline__ void store_bits_packed(uint32_t *dst, int64_t off, const uint32_t *src, int nbits,
+                                                  int lane) {
+    const int sh = (int)(off & 31), end = (int)((off + nbits) & 31);
+    const int nwd = (sh + nbits + 31) >> 5;                            /* destination words touched */
+    uint32_t *d = dst + (off >> 5);
+    for (int i = lane; i < nwd; i += 32) {
+        const uint32_t v = sh ? __funnelshift_l(i ? src[i - 1] : 0u, src[i], sh) : src[i];  /* dest bit b <- src bit 32 i - sh + b */
+        if (i > 0 && i < nwd - 1) {
+            d[i] = v;                                                  /* interior: a whole word */
+        } else {
+            uint32_t mask = ~0u;
+            if (i == 0) mask &= ~0u << sh;
+            if (i == nwd - 1 && end) mask &= ~0u >> (32 - end);
+            if (mask == ~0u) {
+                d[i] = v;
+            } else {
+                atomicAnd(d + i, ~mask);
+                atomicOr(d + i, v & mask);
+            }
+        }
+    }
+}
+
+/* PACKED = false: one bit per byte in and out (info at ext_off, streams at llr_off);
+ * PACKED = true: packed LSB-first bits (info at bit offset ext_off, each stream's
+ * K + 4 bits at bit offset llr_off). */
+template <bool PACKED>
 __global__ void __launch_bounds__(ENC_THREADS)
-encode_kernel(const crn_cb_desc *__restrict__ desc, int n_cb, const uint8_t *__restrict__ info, int attach,
-              uint8_t *d0, uint8_t *d1, uint8_t *d2) {
+encode_kernel(const crn_cb_desc *__restrict__ desc, int n_cb, const void *__restrict__ info_v, int attach,
+              void *d0_v, void *d1_v, void *d2_v) {
+    const uint8_t *info = static_cast<const uint8_t *>(info_v);
+    uint8_t *d0 = static_cast<uint8_t *>(d0_v), *d1 = static_cast<uint8_t *>(d1_v), *d2 = static_cast<uint8_t *>(d2_v);
     extern __shared__ __align__(16) uint8_t enc_raw[];
     EncShared &S = *reinterpret_cast<EncShared *>(enc_raw);
     build_tables(S);
@@ -158,7 +203,8 @@ encode_kernel(const crn_cb_desc *__restrict__ desc, int n_cb, const uint8_t *__r
     for (int cb = blockIdx.x * ENC_WARPS + warp; cb < n_cb; cb += gridDim.x * ENC_WARPS) {
         const crn_cb_desc d = desc[cb];
         const int K = d.K, F = d.F, nw = (K + 31) >> 5;
-        load_bits(info + d.ext_off, K, W.c, lane);
+        if (PACKED) load_bits_packed(static_cast<const uint32_t *>(info_v), d.ext_off, K, W.c, lane);
+        else load_bits(info + d.ext_off, K, W.c, lane);
         /* fillers read as 0; with attach the last 24 bits are recomputed */
         const int N = attach ? K - 24 : K;
         for (int t = lane; t < nw; t += 32) {
@@ -294,6 +340,40 @@ encode_kernel(const crn_cb_desc *__restrict__ desc, int n_cb, const uint8_t *__r
             s2 = v2 >> 8;
         }
         __syncwarp();
+        if (PACKED) {
+            /* the 4 termination bits of each stream (R11) go to bits K .. K+3 of its
+             * words (K = 0 mod 8: one word), then each stream's K + 4 bits are stored */
+            if (lane == 0) {
+                uint32_t tb[3] = {0u, 0u, 0u};
+                int s = run1;
+                for (int k = 0; k < 3; k++) {
+                    const int r1 = (s >> 2) & 1, r2 = (s >> 1) & 1, r3 = s & 1;
+                    const int m0 = 2 * k, m1 = 2 * k + 1;                /* t[m] -> stream m % 3, bit K + m / 3 */
+                    tb[m0 % 3] |= (uint32_t)(r2 ^ r3) << (m0 / 3);
+                    tb[m1 % 3] |= (uint32_t)(r1 ^ r3) << (m1 / 3);
+                    s = (r1 << 1) | r2;
+                }
+                s = run2;
+                for (int k = 0; k < 3; k++) {
+                    const int r1 = (s >> 2) & 1, r2 = (s >> 1) & 1, r3 = s & 1;
+                    const int m0 = 6 + 2 * k, m1 = 6 + 2 * k + 1;
+                    tb[m0 % 3] |= (uint32_t)(r2 ^ r3) << (m0 / 3);
+                    tb[m1 % 3] |= (uint32_t)(r1 ^ r3) << (m1 / 3);
+                    s = (r1 << 1) | r2;
+                }
+                const int t = K >> 5, sh = K & 31;
+                const uint32_t keep = sh ? (1u << sh) - 1u : 0u;       /* bits below K in the word */
+                W.c[t] = (W.c[t] & keep) | (tb[0] << sh);
+                W.z1[t] = (W.z1[t] & keep) | (tb[1] << sh);
+                W.z2[t] = (W.z2[t] & keep) | (tb[2] << sh);
+            }
+            __syncwarp();
+            store_bits_packed(static_cast<uint32_t *>(d0_v), d.llr_off, W.c, K + 4, lane);
+            store_bits_packed(static_cast<uint32_t *>(d1_v), d.llr_off, W.z1, K + 4, lane);
+            store_bits_packed(static_cast<uint32_t *>(d2_v), d.llr_off, W.z2, K + 4, lane);
+            __syncwarp();                                 /* W is rewritten by the next CB */
+            continue;
+        }
         /* write-out: bit n -> byte n of each stream, four bytes per store */
         uint8_t *o0 = d0 + d.llr_off, *o1 = d1 + d.llr_off, *o2 = d2 + d.llr_off;
         const bool al = ((reinterpret_cast<uintptr_t>(o0) | reinterpret_cast<uintptr_t>(o1) |
@@ -355,8 +435,8 @@ encode_kernel(const crn_cb_desc *__restrict__ desc, int n_cb, const uint8_t *__r
 }
 }  // namespace
 
-extern "C" int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const uint8_t *info, int32_t attach,
-                                 uint8_t *d0, uint8_t *d1, uint8_t *d2, const crn_tables *, void *stream) {
+extern "C" int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const void *info, int32_t attach,
+                                 void *d0, void *d1, void *d2, int32_t packed, const crn_tables *, void *stream) {
     static std::mutex mu;
     static uint64_t done = 0;                   /* bit d: the QPP constants are on device d */
     static int grid_max = 0;
@@ -368,12 +448,14 @@ extern "C" int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const 
             if (cudaMemcpyToSymbol(c_f1, crn_qpp_f1, sizeof(crn_qpp_f1)) != cudaSuccess ||
                 cudaMemcpyToSymbol(c_f2, crn_qpp_f2, sizeof(crn_qpp_f2)) != cudaSuccess)
                 return CRN_ECUDA;
-            if (cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            if (cudaFuncSetAttribute(encode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(EncShared)) != cudaSuccess ||
+                cudaFuncSetAttribute(encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)sizeof(EncShared)) != cudaSuccess)
                 return CRN_ECUDA;
             int sms = 0, per_sm = 0;
             if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, encode_kernel, ENC_THREADS,
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, encode_kernel<false>, ENC_THREADS,
                                                               sizeof(EncShared)) != cudaSuccess)
                 return CRN_ECUDA;
             grid_max = sms * (per_sm > 0 ? per_sm : 1);
@@ -382,7 +464,11 @@ extern "C" int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const 
     }
     const int need = (n_cb + ENC_WARPS - 1) / ENC_WARPS;
     const int grid = need < grid_max ? need : grid_max;
-    encode_kernel<<<grid, ENC_THREADS, sizeof(EncShared), (cudaStream_t)stream>>>(d_desc, n_cb, info, attach, d0, d1,
-                                                                                 d2);
+    if (packed)
+        encode_kernel<true><<<grid, ENC_THREADS, sizeof(EncShared), (cudaStream_t)stream>>>(d_desc, n_cb, info, attach,
+                                                                                           d0, d1, d2);
+    else
+        encode_kernel<false><<<grid, ENC_THREADS, sizeof(EncShared), (cudaStream_t)stream>>>(d_desc, n_cb, info, attach,
+                                                                                            d0, d1, d2);
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
 }

@@ -912,8 +912,8 @@ static int crn_upload1(const void *h, size_t bytes, int dev, cudaStream_t st, vo
     return crn_upload(&h, &bytes, &off, 1, bytes, dev, st, d_out);
 }
 
-extern "C" int crn_encode_batch(const crn_cb_desc *desc, int32_t n_cb, const uint8_t *info, int32_t attach_crc,
-                                uint8_t *d0, uint8_t *d1, uint8_t *d2, void *stream) {
+static int encode_common(const crn_cb_desc *desc, int32_t n_cb, const void *info, int32_t attach_crc, void *d0,
+                         void *d1, void *d2, int32_t packed, void *stream) {
     if (n_cb < 0) return CRN_EINVAL;
     if (n_cb == 0) return CRN_OK;
     if (!desc || !info || !d0 || !d1 || !d2) return CRN_EINVAL;
@@ -928,9 +928,19 @@ extern "C" int crn_encode_batch(const crn_cb_desc *desc, int32_t n_cb, const uin
     cudaStream_t st = (cudaStream_t)stream;
     void *dd = nullptr;
     if ((rc = crn_upload1(desc, sizeof(crn_cb_desc) * (size_t)n_cb, dev, st, &dd))) return rc;
-    rc = crn_launch_encode((const crn_cb_desc *)dd, n_cb, info, attach_crc, d0, d1, d2, &t->tab, (void *)st);
+    rc = crn_launch_encode((const crn_cb_desc *)dd, n_cb, info, attach_crc, d0, d1, d2, packed, &t->tab, (void *)st);
     cudaFreeAsync(dd, st);
     return rc;
+}
+
+extern "C" int crn_encode_batch(const crn_cb_desc *desc, int32_t n_cb, const uint8_t *info, int32_t attach_crc,
+                                uint8_t *d0, uint8_t *d1, uint8_t *d2, void *stream) {
+    return encode_common(desc, n_cb, info, attach_crc, d0, d1, d2, 0, stream);
+}
+
+extern "C" int crn_encode_batch_packed(const crn_cb_desc *desc, int32_t n_cb, const uint32_t *info,
+                                       int32_t attach_crc, uint32_t *d0, uint32_t *d1, uint32_t *d2, void *stream) {
+    return encode_common(desc, n_cb, info, attach_crc, d0, d1, d2, 1, stream);
 }
 
 extern "C" int crn_ubench_int16x2(int32_t op, int64_t *lane_instr, float *ms, int64_t *cycles) {
@@ -1112,6 +1122,23 @@ extern "C" int crn_rate_match_batch(const crn_rm_desc *desc, int32_t n_cb, const
     void *dd = nullptr;
     if ((rc = rm_upload(desc, n_cb, dev, st, &dd))) return rc;
     rc = crn_launch_match((const crn_rm_desc *)dd, n_cb, d0, d1, d2, e, (void *)st);
+    cudaFreeAsync(dd, st);
+    return rc;
+}
+
+extern "C" int crn_rate_match_batch_packed(const crn_rm_desc *desc, int32_t n_cb, const uint32_t *d0,
+                                           const uint32_t *d1, const uint32_t *d2, uint32_t *e, void *stream) {
+    if (n_cb < 0) return CRN_EINVAL;
+    if (n_cb == 0) return CRN_OK;
+    if (!desc || !d0 || !d1 || !d2 || !e || rm_validate(desc, n_cb)) return CRN_EINVAL;
+    int dev;
+    DevTables *t;
+    int rc = crn_get_ctx(&dev, &t);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    void *dd = nullptr;
+    if ((rc = rm_upload(desc, n_cb, dev, st, &dd))) return rc;
+    rc = crn_launch_match_packed((const crn_rm_desc *)dd, n_cb, d0, d1, d2, e, (void *)st);
     cudaFreeAsync(dd, st);
     return rc;
 }

@@ -124,9 +124,8 @@ int crn_launch_tasks_dev(const crn_cb_desc *d_desc, int32_t n_cb, int32_t want_e
                          crn_task **tasks, crn_pair **pairs, uint8_t **dead, uint8_t *crc_ok,
                          uint8_t *iters_used, void *stream);
 /* crn_encode.cu */
-int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const uint8_t *info,
-                      int32_t attach_crc, uint8_t *d0, uint8_t *d1, uint8_t *d2,
-                      const crn_tables *tab, void *stream);
+int crn_launch_encode(const crn_cb_desc *d_desc, int32_t n_cb, const void *info, int32_t attach_crc,
+                      void *d0, void *d1, void *d2, int32_t packed, const crn_tables *tab, void *stream);
 /* crn_tb.cu */
 int crn_launch_tb(const crn_tb_desc *d_tbs, int32_t n_tb, const crn_cb_desc *d_desc, const uint32_t *cb_words,
                   const uint8_t *crc_ok, uint8_t *tb_ok, uint32_t *tb_words, void *stream);
@@ -135,6 +134,9 @@ int crn_launch_dematch(const crn_rm_desc *d_desc, int32_t n_cb, const int16_t *e
                        int16_t *h1, int16_t *h2, void *stream);
 int crn_launch_match(const crn_rm_desc *d_desc, int32_t n_cb, const uint8_t *d0, const uint8_t *d1,
                      const uint8_t *d2, uint8_t *e, void *stream);
+/* packed-bit matching: stream bits at bit offset llr_off, e bits at bit offset e_off */
+int crn_launch_match_packed(const crn_rm_desc *d_desc, int32_t n_cb, const uint32_t *d0, const uint32_t *d1,
+                            const uint32_t *d2, uint32_t *e, void *stream);
 /* crn_tbseg.cu */
 int crn_launch_tbseg(const crn_tbseg *d_tbs, int32_t n_tb, int64_t max_tbs, const uint8_t *payload, uint8_t *cb_bits,
                      void *stream);

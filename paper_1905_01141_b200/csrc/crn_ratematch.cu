@@ -348,6 +348,77 @@ match_kernel(const crn_rm_desc *__restrict__ desc, const uint8_t *__restrict__ d
     }
 }
 
+/* Matching with packed bits (one bit per bit, LSB-first words): CB i's three
+ * streams are bits [llr_off, llr_off + K + 4) of d0 / d1 / d2, its E output bits go
+ * to bits [e_off, e_off + E) of e.  The same walk as match_kernel on byte-wide T
+ * and Q in shared memory; the stream words come in with plain coalesced loads (a
+ * few hundred words), and the output is assembled a word per warp instruction by
+ * a ballot -- whole words stored, the (at most two) words shared with
+ * neighbouring CBs merged with atomics. */
+constexpr int MP_RAW_W = RM_MAXR + 2;                                 /* words covering one stream at any bit offset */
+constexpr int MP_Q = (3 * (6144 + 4) + 15) / 16 * 16;
+constexpr int MP_SMEM = 3 * MP_RAW_W * 4 + MT_T8 + MP_Q;              /* 39,864 B */
+
+__global__ void __launch_bounds__(RM_THREADS)
+match_packed_kernel(const crn_rm_desc *__restrict__ desc, const uint32_t *__restrict__ d0,
+                    const uint32_t *__restrict__ d1, const uint32_t *__restrict__ d2, uint32_t *e) {
+    extern __shared__ __align__(16) uint8_t mp_sm[];
+    __shared__ RankTab tab;
+    const crn_rm_desc d = desc[blockIdx.x];
+    const Geo g = geo(d.K, d.rv);
+    uint32_t *raw = reinterpret_cast<uint32_t *>(mp_sm);             /* [3][MP_RAW_W] */
+    uint8_t *T8 = mp_sm + 3 * MP_RAW_W * 4, *Q = T8 + MT_T8;
+    const int sh = (int)(d.llr_off & 31);
+    const int64_t w0 = d.llr_off >> 5;
+    const int nwr = (sh + g.D + 31) >> 5;                              /* words holding the stream's bits */
+    for (int i = threadIdx.x; i < 3 * nwr; i += RM_THREADS) {
+        const int s = i / nwr, k = i - s * nwr;
+        raw[s * MP_RAW_W + k] = __ldg((s == 0 ? d0 : s == 1 ? d1 : d2) + w0 + k);
+    }
+    build_ranks(g, &tab);                                             /* ends with __syncthreads */
+    const int Rp = pad_rows(g.R, 4);
+    /* stream order: a thread's n advances by RM_THREADS = 512 = 16 rows */
+#pragma unroll 1
+    for (int s = 0; s < 3; s++) {
+        const uint32_t *rw = raw + s * MP_RAW_W;
+        int n = threadIdx.x;
+        if (n >= g.D) continue;
+        for (uint32_t ta = smem_addr(T8) + t_index(g, Rp, s, n); n < g.D; n += RM_THREADS, ta += 16) {
+            const int b = sh + n;
+            st_s8(ta, (rw[b >> 5] >> (b & 31)) & 1u);
+        }
+    }
+    __syncthreads();
+    const uint32_t qa = smem_addr(Q), t8 = smem_addr(T8);
+    for_each_position(g, tab, Rp, [&](int ix, int r, bool, bool real) { st_s8_if(qa + r, ld_s8(t8 + ix), real); });
+    __syncthreads();
+    /* e bit e_off + k = Q[k mod 3D]: a warp per output word, lane = bit (32
+     * consecutive rank bytes: conflict-free), one ballot; the lane's rank advances
+     * by a constant per word, so no division in the loop */
+    const int lane = threadIdx.x & 31, nn = g.nn, sh0 = (int)(d.e_off & 31), E = d.E;
+    const int nwd = (sh0 + E + 31) >> 5;
+    uint32_t *ec = e + (d.e_off >> 5);
+    int k = 32 * (int)(threadIdx.x >> 5) + lane - sh0;
+    int rr = k % nn;
+    if (rr < 0) rr += nn;
+    const int kinc = 32 * (RM_THREADS / 32), rinc = kinc % nn;
+    for (int i = threadIdx.x >> 5; i < nwd; i += RM_THREADS / 32) {
+        const bool in = k >= 0 && k < E;
+        const uint32_t word = __ballot_sync(0xFFFFFFFFu, in && Q[rr] != 0), mask = __ballot_sync(0xFFFFFFFFu, in);
+        if (lane == 0) {
+            if (mask == 0xFFFFFFFFu) {
+                ec[i] = word;
+            } else {
+                atomicAnd(ec + i, ~mask);
+                atomicOr(ec + i, word);
+            }
+        }
+        k += kinc;
+        rr += rinc;
+        if (rr >= nn) rr -= nn;
+    }
+}
+
 /* the kernels' dynamic shared-memory attribute, set once per device (a bit per
  * device id; the attribute is per device context) */
 template <class K>
@@ -378,5 +449,14 @@ extern "C" int crn_launch_match(const crn_rm_desc *d_desc, int32_t n_cb, const u
     const int attr = rm_smem_attr(match_kernel, MT_SMEM, done);
     if (attr) return attr;
     match_kernel<<<n_cb, RM_THREADS, MT_SMEM, (cudaStream_t)stream>>>(d_desc, d0, d1, d2, e);
+    return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
+}
+
+extern "C" int crn_launch_match_packed(const crn_rm_desc *d_desc, int32_t n_cb, const uint32_t *d0, const uint32_t *d1,
+                                       const uint32_t *d2, uint32_t *e, void *stream) {
+    static std::atomic<uint64_t> done{0};
+    const int attr = rm_smem_attr(match_packed_kernel, MP_SMEM, done);
+    if (attr) return attr;
+    match_packed_kernel<<<n_cb, RM_THREADS, MP_SMEM, (cudaStream_t)stream>>>(d_desc, d0, d1, d2, e);
     return cudaGetLastError() == cudaSuccess ? CRN_OK : CRN_ECUDA;
 }

@@ -867,3 +867,122 @@ def test_tb_build_cbs_batch_matches_oracle(orc):
     assert n == desc.size and got.size == bit
     with pytest.raises(crn.CrnError):
         crn.tb_build_cbs_batch(np.array([0], np.int64), np.array([0], np.int64), payload)
+
+
+def test_race_stress_grids_repeats_variants(orc):
+    """Stand-in for a race detector (compute-sanitizer is closed on this GPU pool,
+    DESIGN.md §5b): the single-buffered shared state (NII boundaries, the hard
+    decision's window words, the CRC / MI atomics, the group tasks' named barriers
+    and next-task slots) is exercised under many different interleavings -- one
+    mixed early-terminated batch (whole-CTA W = 32 tasks, split-path tasks, group
+    tasks, dummy partner lanes, fillers) decoded on persistent grids of 1, 2, 3, 5,
+    17, 61 and all CTAs (so every CTA runs a different task sequence) and 12 times
+    on the full grid, each decoder variant and stopping rule.  Every run must equal
+    the oracle's outputs for that variant, element by element."""
+    rng = np.random.default_rng(23)
+    Ks = ([6144] * 9 + [5824] * 4 + [3072] * 5 + [2048] * 7 + [1056] * 11 + [1088] * 3 + [512] * 30 + [64] * 70 +
+          [1008] * 5 + [488] * 7 + [40] * 13 + [104] * 3)
+    K = list(rng.permutation(Ks))
+    F = [int(rng.integers(0, min(64, k - 24))) if i % 5 == 0 else 0 for i, k in enumerate(K)]
+    d = _desc_for(K, F, [crn.CRC24A if i % 7 == 0 else crn.CRC24B for i in range(len(K))])
+    llr = _random_llr(d, rng, 90)
+    n = int((d["llr_off"] + d["K"] + 4).max())
+    lean = np.zeros(n, np.int16)                 # a third lean to the all-zero codeword: early stops
+    for o, k in zip(d["llr_off"][::3], d["K"][::3]):
+        lean[o:o + k + 4] = -70
+    llr = tuple((x + torch.from_numpy(lean).cuda()).clamp(-32767, 32767) for x in llr)
+    b = _B(d, llr)
+    idx = np.arange(d.size)
+    plan = crn.Plan(d)
+    for variant, et, ov, oet in ((crn.VARIANT_MAXLOG, crn.ET_CRC, orc.VAR_MAXLOG, orc.ET_CRC),
+                                 (crn.VARIANT_SCALED, crn.ET_CRC, orc.VAR_SCALED, orc.ET_CRC),
+                                 (crn.VARIANT_MAXLOG, crn.ET_MI, orc.VAR_MAXLOG, orc.ET_MI),
+                                 (crn.VARIANT_LOGMAP, crn.ET_CRC, orc.VAR_LOGMAP, orc.ET_CRC)):
+        plan.set_variant(variant)
+        r = run_oracle(b, idx, 8, oet, variant=ov)
+        runs = [(g, 1) for g in (1, 2, 3, 5, 17, 61)] + [(0, 12)]
+        for grid, reps in runs:
+            plan.set_grid(grid)
+            for _ in range(reps):
+                bits = torch.full((b.n_words,), -1, dtype=torch.int32, device="cuda")
+                ok = torch.full((d.size,), 7, dtype=torch.uint8, device="cuda")
+                it = torch.zeros(d.size, dtype=torch.uint8, device="cuda")
+                ext = torch.zeros(int(d["K"].sum()), dtype=torch.int16, device="cuda")
+                plan.decode(*llr, 8, et, bits, ok, it, ext)
+                torch.cuda.synchronize()
+                g = dict(words=bits.cpu().numpy().view(np.uint32), crc_ok=ok.cpu().numpy(), iters=it.cpu().numpy(),
+                         ext=ext.cpu().numpy())
+                assert_parity(b, g, r, idx)
+        assert 0 < int(r["crc_ok"].sum()) < d.size and len(set(r["iters"].tolist())) > 2
+    plan.set_grid(0)
+
+
+def _bits_to_words(bits, n_words):
+    """uint8 0/1 array -> packed LSB-first uint32 words (numpy), zero-padded."""
+    b = np.zeros(32 * n_words, np.uint8)
+    b[:bits.size] = bits
+    return np.packbits(b, bitorder="little").view(np.uint32).copy()
+
+
+def _words_to_bits(words):
+    return np.unpackbits(np.ascontiguousarray(words).view(np.uint8), bitorder="little")
+
+
+def test_packed_encoder_and_rate_match_parity(orc):
+    """Row f3/f4 packed-bit forms (crn_encode_batch_packed, crn_rate_match_batch_packed):
+    one bit per bit at unaligned BIT offsets with gaps between CBs (neighbouring CBs
+    share words), mixed K over every K mod 32 residue, CRC attach on and off; the
+    coded streams equal the oracle encoder's and the rate-matched bits the oracle's,
+    bit for bit, and every bit outside the CBs' ranges keeps its previous value."""
+    rng = np.random.default_rng(29)
+    Ks = np.array(list(rng.choice(orc.k_table(), 60)) + [6144, 6144, 40, 1056, 1088, 1008, 1024])
+    n = Ks.size
+    kinds = np.where(np.arange(n) % 4 == 0, crn.CRC24A, crn.CRC24B)
+    d = np.zeros(n, crn.DESC_DTYPE)
+    d["K"], d["crc_kind"] = Ks, kinds
+    d["ext_off"] = np.concatenate([[5], np.cumsum(Ks + 3)[:-1] + 5])               # bit offsets, odd gaps
+    d["llr_off"] = np.concatenate([[3], np.cumsum(Ks + 4 + 7)[:-1] + 3])
+    n_info = int((d["ext_off"] + Ks).max()) + 40
+    n_code = int((d["llr_off"] + Ks + 4).max()) + 40
+    info_bits = rng.integers(0, 2, n_info).astype(np.uint8)
+    info = torch.from_numpy(_bits_to_words(info_bits, (n_info + 31) // 32).view(np.int32)).cuda()
+    nw = (n_code + 31) // 32
+    for attach in (False, True):
+        fill = [rng.integers(0, 2, 32 * nw).astype(np.uint8) for _ in range(3)]
+        outs = [torch.from_numpy(_bits_to_words(f, nw).view(np.int32)).cuda() for f in fill]
+        crn.encode_batch_packed(d, info, attach, *outs)
+        torch.cuda.synchronize()
+        got = [_words_to_bits(o.cpu().numpy()) for o in outs]
+        inside = np.zeros(32 * nw, bool)
+        for i in range(n):
+            K, eo, lo = int(Ks[i]), int(d["ext_off"][i]), int(d["llr_off"][i])
+            c = info_bits[eo:eo + K].copy()
+            if attach:
+                c = orc.crc_attach(int(kinds[i]), c[:-24])
+            ref = orc.turbo_encode(c)
+            for s in range(3):
+                assert np.array_equal(got[s][lo:lo + K + 4], ref[s]), (attach, i, s)
+            inside[lo:lo + K + 4] = True
+        for s in range(3):
+            assert np.array_equal(got[s][~inside], fill[s][~inside]), (attach, s)
+    # packed rate matching of random coded streams
+    dm = _rm_case(rng, 70, np.array([40, 48, 56, 104, 112, 120, 248, 512, 1008, 528, 1056, 2112, 4096, 6144]))
+    dm["llr_off"] = np.concatenate([[9], np.cumsum(dm["K"] + 4 + 13)[:-1] + 9])     # bit offsets
+    dm["e_off"] = np.concatenate([[17], np.cumsum(dm["E"] + 5)[:-1] + 17])
+    n_l = int((dm["llr_off"] + dm["K"] + 4).max()) + 40
+    n_e = int((dm["e_off"] + dm["E"]).max()) + 40
+    coded = [rng.integers(0, 2, n_l).astype(np.uint8) for _ in range(3)]
+    cw = [torch.from_numpy(_bits_to_words(x, (n_l + 31) // 32).view(np.int32)).cuda() for x in coded]
+    nwe = (n_e + 31) // 32
+    efill = rng.integers(0, 2, 32 * nwe).astype(np.uint8)
+    eg = torch.from_numpy(_bits_to_words(efill, nwe).view(np.int32)).cuda()
+    crn.rate_match_batch_packed(dm, *cw, eg)
+    torch.cuda.synchronize()
+    got = _words_to_bits(eg.cpu().numpy())
+    inside = np.zeros(32 * nwe, bool)
+    for i in range(dm.size):
+        K, lo, eo, E = int(dm["K"][i]), int(dm["llr_off"][i]), int(dm["e_off"][i]), int(dm["E"][i])
+        ref = orc.rate_match([x[lo:lo + K + 4] for x in coded], E, int(dm["rv"][i]))
+        assert np.array_equal(got[eo:eo + E], ref), i
+        inside[eo:eo + E] = True
+    assert np.array_equal(got[~inside], efill[~inside])

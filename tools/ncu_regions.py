@@ -37,13 +37,14 @@ def func_ranges():
 
 def local_chains():
     cub = "/tmp/crn_decode_regions.cubin"
-    subprocess.check_call([B.NVCC, *B.ARCH, *B.FLAGS, "-cubin", "-o", cub, SRC])
+    defs = [f"-D{d}" for d in os.environ.get("CRN_DEFINES", "").split()]   # the variant's -D flags
+    subprocess.check_call([B.NVCC, *B.ARCH, *B.FLAGS, *defs, "-cubin", "-o", cub, SRC])
     out = subprocess.check_output(["nvdisasm", "-gi", "-fun", "", cub], stderr=subprocess.DEVNULL).decode() \
         if False else subprocess.check_output(["nvdisasm", "-gi", cub]).decode()
     chains, cur, in_kernel, pending = {}, [], False, []
     for l in out.split("\n"):
         if re.match(r"\s*\.text\.", l) or "Function :" in l:
-            in_kernel = "decode_kernel" in l
+            in_kernel = os.environ.get("CRN_KERNEL", "decode_kernelILb0ELb0ELi0E") in l
         m = re.search(r'//## File ".*?crn_decode.cu", line (\d+)(?: inlined at ".*?", line (\d+))?', l)
         if m:
             pending.append(int(m.group(1)))

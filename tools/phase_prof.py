@@ -17,7 +17,7 @@ from paper_1905_01141_b200 import crn  # noqa: E402
 from paper_1905_01141_b200 import workload as wlmod  # noqa: E402
 
 NAMES = ["fetch", "stage", "chunk", "phase1", "bar1", "phase2", "bar2", "hard_dec", "st_loads", "st_bar1", "st_gather",
-         "hd_lapp", "hd_bar1", "hd_crc", "hd_bar2", "hd_decide", "fetch_bars"]
+         "hd_lapp", "hd_bar1", "hd_crc", "hd_bar2", "hd_decide", "fetch_bars", "st_mbar_wait"]
 
 
 def main():
