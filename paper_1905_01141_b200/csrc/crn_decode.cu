@@ -1494,6 +1494,10 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
         const NextSh ng{&s_ntask[g], &s_ntk[g], s_ncb + eb, s_nF + eb, s_nkind + eb, PURGE ? s_ntb + eb : nullptr,
                         s_nbo + eb, s_neo + eb};
         bool gpend = g > 0;                     /* group 0 starts with the task the CTA claimed */
+        /* groups 1 and 2 claim only after every CTA has claimed its first task: a
+         * small batch (one task per CTA, crn_launch_tasks) then stays spread over the SMs */
+        if (g > 0 && ltid < 32)
+            while (*(volatile int *)counter < (int)gridDim.x) __nanosleep(128);
         for (;;) {
             if (gpend && ltid < 32) claim_next(ng, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, ltid, sh8);
             gsync<G3>(g);                       /* next slots filled */
