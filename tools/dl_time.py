@@ -1,6 +1,6 @@
 """Device time of the DL kernels, byte and packed-bit forms, on n_cells cells of
 cfg4 (256 CBs of K=6144 each): CRC24B attach + turbo encode, rate matching to
-E = 3(K+4) at rv 0.  CUDA events around each call on the launching stream, after
+E = 3(K+4) at rv 0, and de-matching of E int16 values.  CUDA events around each call on the launching stream, after
 warm-up; median of 10 (the host-side descriptor staging of a call is inside, as
 for any caller of the C ABI).  usage: python tools/dl_time.py [n_cells]"""
 import json
@@ -32,10 +32,13 @@ def main():
                                           bitorder="little").view(np.int32).copy()).cuda()
     coded_w = tuple(torch.zeros((b.coded[0].numel() + 31) // 32, dtype=torch.int32, device="cuda") for _ in range(3))
     e_w = torch.zeros((e.numel() + 31) // 32, dtype=torch.int32, device="cuda")
+    soft = torch.zeros(e.numel(), dtype=torch.int16, device="cuda")
+    hs = tuple(torch.empty_like(x) for x in b.llr)
     calls = {"encode_byte": lambda: crn.encode_batch(d, b.info, True, *coded, stream=st),
              "rate_match_byte": lambda: crn.rate_match_batch(rm, *coded, e, stream=st),
              "encode_packed": lambda: crn.encode_batch_packed(d, info_w, True, *coded_w, stream=st),
-             "rate_match_packed": lambda: crn.rate_match_batch_packed(rm, *coded_w, e_w, stream=st)}
+             "rate_match_packed": lambda: crn.rate_match_batch_packed(rm, *coded_w, e_w, stream=st),
+             "rate_dematch": lambda: crn.rate_dematch_batch(rm, soft, False, *hs, stream=st)}
     out = {"n_cb": int(d.size)}
     for name, fn in calls.items():
         for _ in range(3):
