@@ -32,6 +32,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "crn_internal.h"
 
 typedef uint32_t u32;
@@ -498,6 +500,15 @@ __device__ __forceinline__ void tm_load16_wait(u32 ta, u32 v[HW]) {
                  : "memory");
 }
 
+/* Loads 4 columns and waits for them (the rolled phase 1's statics, a block at a time). */
+__device__ __forceinline__ void tm_load4_wait(u32 ta, u32 v[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n\t"
+                 "tcgen05.wait::ld.sync.aligned;"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(ta)
+                 : "memory");
+}
+
 /* LLR element idx of a stream: int16, or with sh8 >= 0 (int8 ingest, row f4,
  * crn_plan_set_llr_format) the int8 value x read as the int16 x * 2^sh8. */
 template <bool LLR8>
@@ -576,7 +587,14 @@ __device__ __forceinline__ u32 lds_q(u32 qq, int c) {
 
 /* One half-iteration of constituent c (rows a5-a8).  Le -> Y (c = 0, natural
  * order) or Z (c = 1, interleaved order). */
-template <int VAR, int G>
+/* ROLL (the latency kernels, crn_launch_decode): phase 1 runs as a loop over
+ * blocks of four steps -- the statics come from TMEM a block at a time and the
+ * gather addresses move down a register window -- and the caller runs both
+ * constituents through one call site, so a lone warp's per-iteration code fits
+ * the instruction caches (a step of the fully unrolled phase 1 costs a lone warp
+ * ~120 cycles against ~76 when its code stays cached, tools/ubench/step_lat.cu).
+ * The arithmetic, and so every output, is the unrolled path's. */
+template <int VAR, int G, bool ROLL = false>
 __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, int it, const u32 (&qq)[HW],
                                            bool zero_la) {
     constexpr bool LOGV = VAR == CRN_VARIANT_LOGMAP;
@@ -591,6 +609,84 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
     /* row a4 fused into phase 1: this thread's 16 (Lu+Lp, Lu-Lp) pairs are formed
      * step by step from the TMEM static sums, the parity plane and the a-priori
      * LLRs gathered at its QPP indices, used at once and kept in smem for phase 2 */
+    if constexpr (ROLL) {
+    const u32 lp_s = smem_addr(lp);
+    u32 m[NS], w[HW];
+#pragma unroll
+    for (int k = 0; k < HW; k++) w[k] = qq[k];
+    if (!tail_thr) {
+        if (f.j == 0) {
+            m[0] = M1;
+#pragma unroll
+            for (int s = 1; s < NS; s++) m[s] = FLOORB;
+        } else if (it == 1) {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = M1;
+        } else {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = nii[nii1_ix(c, 0, s, f.t - 1)];
+        }
+        /* the block's steps use w[0..3]; the next step's loads are issued one step
+         * ahead (the last lookahead reads a valid, unused address) */
+        u32 avn = zero_la ? 0u : lds_q(w[0], c), pvn;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pvn) : "r"(lp_s));
+#pragma unroll 1
+        for (int b = 0; b < HW / 4; b++) {
+            u32 s4[4];
+            tm_load4_wait(f.ts + c * HW + 4 * b, s4);
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const int s = 4 * b + t;
+                const u32 av = avn, pv = pvn;
+                avn = zero_la ? 0u : lds_q(w[t + 1], c);
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pvn) : "r"(lp_s + 4 * (s + 1) * TS));
+                const u32 d = vadd(s4[t], av), x = vadd(vadd(d, pv), pv);
+                ch[s * BLOCK] = make_uint2(x, d);
+                tm_store8(f.ta + s * 8, m);
+                alpha_step_d<LOGV>(m, pv, x, d, lut);
+            }
+#pragma unroll
+            for (int k = 0; k < HW - 4; k++) w[k] = w[k + 4];
+        }
+#pragma unroll
+        for (int s = 0; s < NS; s++) X[s * TS + f.t] = m[s];             /* alpha_16 -> tail thread */
+    } else {
+        if (f.j == f.M - 1) {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = f.sm[S_TAIL + f.p * 16 + c * 8 + s];
+        } else if (it == 1) {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = M1;
+        } else {
+#pragma unroll
+            for (int s = 0; s < NS; s++) m[s] = nii[nii1_ix(c, 1, s, f.t + 1)];
+        }
+        /* backward: the block's steps use w[12..15] */
+        u32 avn = zero_la ? 0u : lds_q(w[HW - 1], c), pvn;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pvn) : "r"(lp_s + 4 * (HW - 1) * TS));
+#pragma unroll 1
+        for (int b = HW / 4 - 1; b >= 0; b--) {
+            u32 s4[4];
+            tm_load4_wait(f.ts + c * HW + 4 * b, s4);
+#pragma unroll
+            for (int t = 3; t >= 0; t--) {
+                const int s = 4 * b + t;
+                const u32 av = avn, pv = pvn;
+                avn = zero_la ? 0u : lds_q(w[HW - 5 + t], c);
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pvn) : "r"(lp_s + 4 * (s - 1) * TS));
+                const u32 d = vadd(s4[t], av), x = vadd(vadd(d, pv), pv);
+                ch[s * BLOCK] = make_uint2(x, d);
+                tm_store8(f.ta + s * 8, m);
+                beta_step_d<LOGV>(m, pv, x, d, lut);
+            }
+#pragma unroll
+            for (int k = HW - 1; k >= 4; k--) w[k] = w[k - 4];
+        }
+#pragma unroll
+        for (int s = 0; s < NS; s++) X[(NS + s) * TS + f.t] = m[s];      /* beta_16 -> head thread */
+    }
+    tm_wait_st();
+    } else {
     u32 av[HW], pv[HW], sn[HW];
     tm_load16_wait(f.ts + c * HW, sn);
     /* the 32 shared loads are issued LA steps ahead of their use, in processing
@@ -657,6 +753,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
         for (int s = 0; s < NS; s++) X[(NS + s) * TS + f.t] = m[s];      /* beta_16 -> head thread */
     }
     tm_wait_st();
+    }   /* ROLL */
     }   /* f.wact */
     prof_mark(P_PH1);
     gsync<G>(f.g);          /* hand-over; also orders this half-iteration's NII reads before its writes */
@@ -709,7 +806,7 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
     }
 }
 
-template <int VAR, bool PURGE, bool LLR8, int G>
+template <int VAR, bool PURGE, bool LLR8, int G, bool ROLL = false, bool ETC = false>
 __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
                                               const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
                                               const int16_t *__restrict__ l2, int max_iters, int et,
@@ -858,6 +955,17 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
     }
 
     for (int it = 1; it <= max_iters; it++) {
+        if constexpr (ROLL) {
+            /* both constituents through one call site (one copy of the SISO code) */
+#pragma unroll 1
+            for (int c = 0; c < 2; c++) {
+                prof_mark(P_CHUNK);
+                siso_split<VAR, G, true>(f, tail_thr, c, it, qq, it == 1 && c == 0);
+                prof_mark(P_PH2);
+                gsync<G>(g);
+                prof_mark(P_BAR2);
+            }
+        } else {
         /* DEC1: La1[n] = Le2[Pi^-1(n)] gathered from Z (zero in iteration 1) */
         prof_mark(P_CHUNK);
         siso_split<VAR, G>(f, tail_thr, 0, it, qq, it == 1);
@@ -870,6 +978,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
         prof_mark(P_PH2);
         gsync<G>(g);
         prof_mark(P_BAR2);
+        }
         if (!et && it != max_iters) continue;     /* fixed mode: decide only at the end */
 
         /* ---- row a9: L_APP = Ls + Le1 + La1_next (tie -> 1, R16); 16 bits per
@@ -880,18 +989,33 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
             u32 sn[HW];
             const int n00 = f.j * W + f.k0, Fl = sh.F[2 * f.p], Fh = sh.F[2 * f.p + 1];
             tm_load16_wait(f.ts, sn);
+            /* with the stopping-rule test inside the loop every step is its own basic
+             * block and its three shared loads cannot be issued ahead (~1.7 k cycles
+             * per early-termination iteration) */
+            auto lapp_pass = [&](auto mi_rule) {
 #pragma unroll
-            for (int s = 0; s < HW; s++) {
-                const u32 la1n = lds_q(qq[s], 0);                    /* La1_next[n] = Le2[Pi^-1(n)] */
-                const u32 ls = vadd(sn[s], sm[S_LP + (f.k0 + s) * TS + f.t]);
-                const u32 lapp = vadd(vadd(ls, sm[S_Y + (f.k0 + s) * TS + f.t]), la1n);
-                /* b = (L_APP >= 0) per half enters at bits 15 / 31 and moves down one bit per
-                 * later step (w >> 1 as a multiply-high, off the ALU pipe) */
-                wb = __umulhi(wb, 0x80000000u) | (~lapp & 0x80008000u);
-                if (et == CRN_ET_MI) {
-                    mlo += mi_pair(sh.mitab, lapp, n00 + s >= Fl, false);
-                    mhi += mi_pair(sh.mitab, lapp, false, n00 + s >= Fh);
+                for (int s = 0; s < HW; s++) {
+                    const u32 la1n = lds_q(qq[s], 0);                    /* La1_next[n] = Le2[Pi^-1(n)] */
+                    const u32 ls = vadd(sn[s], sm[S_LP + (f.k0 + s) * TS + f.t]);
+                    const u32 lapp = vadd(vadd(ls, sm[S_Y + (f.k0 + s) * TS + f.t]), la1n);
+                    /* b = (L_APP >= 0) per half enters at bits 15 / 31 and moves down one bit per
+                     * later step (w >> 1 as a multiply-high, off the ALU pipe) */
+                    wb = __umulhi(wb, 0x80000000u) | (~lapp & 0x80008000u);
+                    if (decltype(mi_rule)::value && et == CRN_ET_MI) {
+                        mlo += mi_pair(sh.mitab, lapp, n00 + s >= Fl, false);
+                        mhi += mi_pair(sh.mitab, lapp, false, n00 + s >= Fh);
+                    }
                 }
+            };
+            /* CRC early termination (every iteration): the branch-free copy, in the
+             * CRC kernel (ETC) and the latency kernels; fixed iterations (once per
+             * task) and the MI rule: the copy with the test (the throughput kernel
+             * carries only this one, so its code is unchanged) */
+            if constexpr (ETC || ROLL) {
+                if (ETC || et == CRN_ET_CRC) lapp_pass(std::false_type{});
+                else lapp_pass(std::true_type{});
+            } else {
+                lapp_pass(std::true_type{});
             }
             u32 *hb = sm + S_X;               /* [half][window] bits of both CBs; [2 + lane][window] window words */
             if (active) {
@@ -1140,7 +1264,7 @@ __device__ __forceinline__ void siso_gsplit(const GSplit &g, bool tail_thr, int 
     }
 }
 
-template <int VAR, bool PURGE, bool LLR8>
+template <int VAR, bool PURGE, bool LLR8, int TAG = 0>   /* TAG: one copy per kernel family (ROLL 1, ETC 2) */
 __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
                                             const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
                                             const int16_t *__restrict__ l2, int max_iters, int et,
@@ -1370,7 +1494,7 @@ __device__ __forceinline__ void claim_next(NextSh nx, int *counter, int n_tasks,
 /* One instantiation per (purge?, int8 LLRs?, Log-MAP?): the default
  * <false, false, MAXLOG> (which also runs CRN_VARIANT_SCALED, chosen per launch)
  * has no purge, int8 or Log-MAP code at all. */
-template <bool PURGE, bool LLR8, int VAR>
+template <bool PURGE, bool LLR8, int VAR, bool ROLL = false, bool ETC = false>
 __global__ void __launch_bounds__(BLOCK, 1)
 decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__ tasks, int n_tasks,
               const crn_pair *__restrict__ pairs, const int16_t *__restrict__ l0,
@@ -1477,11 +1601,11 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
 #define CRN_RUN(V)                                                                                                \
         do {                                                                                                      \
             if (tk.W == 32)                                                                                       \
-                run_task_fast<V, PURGE, LLR8, 1>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok,           \
+                run_task_fast<V, PURGE, LLR8, 1, ROLL, ETC>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok,     \
                                                  iters_used, ext_out, tab, smem, tmem, sh, pg, sh8);              \
             else                                                                                                  \
-                run_task_split<V, PURGE, LLR8>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok, iters_used, \
-                                               ext_out, tab, smem, tmem, sh, pg, sh8);                            \
+                run_task_split<V, PURGE, LLR8, ROLL ? 1 : ETC ? 2 : 0>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok,     \
+                                                     iters_used, ext_out, tab, smem, tmem, sh, pg, sh8);          \
         } while (0)
         if constexpr (VAR == CRN_VARIANT_LOGMAP) CRN_RUN(CRN_VARIANT_LOGMAP);
         else if ((variant & 0xFF) == CRN_VARIANT_SCALED) CRN_RUN(CRN_VARIANT_SCALED);
@@ -1540,15 +1664,15 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
             }
             if (ltid == 0) trace_task(task, 0, 1 + g);
             if constexpr (VAR == CRN_VARIANT_LOGMAP)
-                run_task_fast<CRN_VARIANT_LOGMAP, PURGE, LLR8, G3>(tk, desc, l0, l1, l2, max_iters, et, out_bits,
+                run_task_fast<CRN_VARIANT_LOGMAP, PURGE, LLR8, G3, ROLL, ETC>(tk, desc, l0, l1, l2, max_iters, et, out_bits,
                                                                    crc_ok, iters_used, ext_out, tab, smem, tmem, sh,
                                                                    pg, sh8);
             else if ((variant & 0xFF) == CRN_VARIANT_SCALED)
-                run_task_fast<CRN_VARIANT_SCALED, PURGE, LLR8, G3>(tk, desc, l0, l1, l2, max_iters, et, out_bits,
+                run_task_fast<CRN_VARIANT_SCALED, PURGE, LLR8, G3, ROLL, ETC>(tk, desc, l0, l1, l2, max_iters, et, out_bits,
                                                                    crc_ok, iters_used, ext_out, tab, smem, tmem, sh,
                                                                    pg, sh8);
             else
-                run_task_fast<CRN_VARIANT_MAXLOG, PURGE, LLR8, G3>(tk, desc, l0, l1, l2, max_iters, et, out_bits,
+                run_task_fast<CRN_VARIANT_MAXLOG, PURGE, LLR8, G3, ROLL, ETC>(tk, desc, l0, l1, l2, max_iters, et, out_bits,
                                                                    crc_ok, iters_used, ext_out, tab, smem, tmem, sh,
                                                                    pg, sh8);
             if (ltid == 0) trace_task(task, 1, 1 + g);
@@ -1571,14 +1695,17 @@ extern "C" int crn_decode_set_logmap(uint32_t lo, uint32_t hi) {
     return cudaMemcpyToSymbol(c_logmap, w, sizeof(w)) == cudaSuccess ? CRN_OK : CRN_ECUDA;
 }   /* the task counter; all decode state is on chip */
 
-/* the four instantiations: <purge?, int8 LLRs?> */
+/* the instantiations: <purge?, int8 LLRs?, variant> and the two latency (ROLL) kernels */
 template <class F>
 cudaError_t for_each_kernel(F &&f) {
     const void *k[] = {
         (const void *)decode_kernel<false, false, CRN_VARIANT_MAXLOG>, (const void *)decode_kernel<true, false, CRN_VARIANT_MAXLOG>,
         (const void *)decode_kernel<false, true, CRN_VARIANT_MAXLOG>, (const void *)decode_kernel<true, true, CRN_VARIANT_MAXLOG>,
         (const void *)decode_kernel<false, false, CRN_VARIANT_LOGMAP>, (const void *)decode_kernel<true, false, CRN_VARIANT_LOGMAP>,
-        (const void *)decode_kernel<false, true, CRN_VARIANT_LOGMAP>, (const void *)decode_kernel<true, true, CRN_VARIANT_LOGMAP>};
+        (const void *)decode_kernel<false, true, CRN_VARIANT_LOGMAP>, (const void *)decode_kernel<true, true, CRN_VARIANT_LOGMAP>,
+        (const void *)decode_kernel<false, false, CRN_VARIANT_MAXLOG, true>,
+        (const void *)decode_kernel<false, true, CRN_VARIANT_MAXLOG, true>,
+        (const void *)decode_kernel<false, false, CRN_VARIANT_MAXLOG, false, true>};
     cudaError_t e = cudaSuccess;
     for (const void *x : k)
         if (e == cudaSuccess) e = f(x);
@@ -1649,7 +1776,27 @@ extern "C" int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_ta
         if (var == CRN_VARIANT_LOGMAP) CRN_LAUNCH(PG, L8, CRN_VARIANT_LOGMAP);                                     \
         else CRN_LAUNCH(PG, L8, CRN_VARIANT_MAXLOG);   /* MAXLOG or SCALED, chosen inside */                       \
     } while (0)
-    if (tb_dead) {
+    /* a batch that fits one wave (every task its own CTA) runs the latency kernel:
+     * rolled phase 1, one SISO call site (CRN_ROLL=0 / 1 forces it off / on) */
+    static const int roll_env = [] {
+        const char *e = getenv("CRN_ROLL");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    const bool roll = !tb_dead && var != CRN_VARIANT_LOGMAP &&
+                      (roll_env >= 0 ? roll_env == 1 : (n_tasks > 0 && n_tasks <= grid));
+    if (roll) {
+        if (llr8) decode_kernel<false, true, CRN_VARIANT_MAXLOG, true><<<g, BLOCK, smem_bytes(), st>>>(
+            d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits, ok, it, ext, *tab, (uint8_t *)ws,
+            variant, nullptr);
+        else decode_kernel<false, false, CRN_VARIANT_MAXLOG, true><<<g, BLOCK, smem_bytes(), st>>>(
+            d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits, ok, it, ext, *tab, (uint8_t *)ws,
+            variant, nullptr);
+    } else if (!tb_dead && !llr8 && var != CRN_VARIANT_LOGMAP && et == CRN_ET_CRC) {
+        /* CRC early termination, int16 LLRs: the kernel with the branch-free hard decision */
+        decode_kernel<false, false, CRN_VARIANT_MAXLOG, false, true><<<g, BLOCK, smem_bytes(), st>>>(
+            d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits, ok, it, ext, *tab, (uint8_t *)ws,
+            variant, nullptr);
+    } else if (tb_dead) {
         if (llr8) CRN_LAUNCH_V(true, true);
         else CRN_LAUNCH_V(true, false);
     } else {
