@@ -806,14 +806,21 @@ __device__ __forceinline__ void siso_split(const SCtx &f, bool tail_thr, int c, 
     }
 }
 
-template <int VAR, bool PURGE, bool LLR8, int G, bool ROLL = false, bool ETC = false>
+struct NoHook {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+/* hook: called by every thread right after its staging loads are issued (the
+ * CRC-ET and latency kernels run warp 0's claim of the next task there, so the
+ * claim's round trips overlap the staging loads instead of preceding them) */
+template <int VAR, bool PURGE, bool LLR8, int G, bool ROLL = false, bool ETC = false, class Hook = NoHook>
 __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_desc *__restrict__ desc,
                                               const int16_t *__restrict__ l0, const int16_t *__restrict__ l1,
                                               const int16_t *__restrict__ l2, int max_iters, int et,
                                               uint32_t *__restrict__ out_bits, uint8_t *__restrict__ crc_ok,
                                               uint8_t *__restrict__ iters_used, int16_t *__restrict__ ext_out,
                                               const crn_tables &tab, u32 *sm, u32 tmem, TaskSh sh, Purge pg,
-                                              int sh8) {
+                                              int sh8, Hook hook = Hook{}) {
     constexpr int W = 32;
     const int M = tk.M, NP = tk.n_pairs, T = NP * M;
     constexpr int GWIN = WMAX / G;              /* windows of the group's task */
@@ -892,6 +899,7 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                 t1[mm] = chi >= 0 ? ld_llr<LLR8>(src, ohi + col, sh8) : (int16_t)0;
             }
         }
+        hook();
         u32 sn[HW];
 #pragma unroll
         for (int x = 0; x < 3; x++) {
@@ -1582,10 +1590,13 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
         }
         __syncthreads();                        /* next slots consumed */
         prof_mark(P_FB);
-        if (tid < 32) {
-            pend = !ahead();
-            if (!pend) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
-        }
+        auto claim_ahead = [&]() {
+            if (tid < 32) {
+                pend = !ahead();
+                if (!pend) claim_next(nx, counter, n_tasks, tasks, pairs, desc, l0, l1, l2, tid, sh8);
+            }
+        };
+        if constexpr (!(ETC || ROLL)) claim_ahead();
         if (PURGE) {                            /* a fully purged task is skipped */
             if (tid == 0) {
                 int left = 0;
@@ -1600,12 +1611,24 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
         /* VAR = LOGMAP: its own kernels; otherwise MAXLOG / SCALED chosen per launch */
 #define CRN_RUN(V)                                                                                                \
         do {                                                                                                      \
-            if (tk.W == 32)                                                                                       \
-                run_task_fast<V, PURGE, LLR8, 1, ROLL, ETC>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok,     \
+            if constexpr (ETC || ROLL) {                                                                          \
+                if (tk.W == 32) {                                                                                 \
+                    run_task_fast<V, PURGE, LLR8, 1, ROLL, ETC>(tk, desc, l0, l1, l2, max_iters, et, out_bits,    \
+                                                                crc_ok, iters_used, ext_out, tab, smem, tmem, sh, \
+                                                                pg, sh8, claim_ahead);                            \
+                } else {                                                                                          \
+                    claim_ahead();                                                                                \
+                    run_task_split<V, PURGE, LLR8, ROLL ? 1 : 2>(tk, desc, l0, l1, l2, max_iters, et, out_bits,   \
+                                                                 crc_ok, iters_used, ext_out, tab, smem, tmem,    \
+                                                                 sh, pg, sh8);                                    \
+                }                                                                                                 \
+            } else if (tk.W == 32) {                                                                              \
+                run_task_fast<V, PURGE, LLR8, 1>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok,           \
                                                  iters_used, ext_out, tab, smem, tmem, sh, pg, sh8);              \
-            else                                                                                                  \
-                run_task_split<V, PURGE, LLR8, ROLL ? 1 : ETC ? 2 : 0>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok,     \
-                                                     iters_used, ext_out, tab, smem, tmem, sh, pg, sh8);          \
+            } else {                                                                                              \
+                run_task_split<V, PURGE, LLR8, 0>(tk, desc, l0, l1, l2, max_iters, et, out_bits, crc_ok,          \
+                                                  iters_used, ext_out, tab, smem, tmem, sh, pg, sh8);             \
+            }                                                                                                     \
         } while (0)
         if constexpr (VAR == CRN_VARIANT_LOGMAP) CRN_RUN(CRN_VARIANT_LOGMAP);
         else if ((variant & 0xFF) == CRN_VARIANT_SCALED) CRN_RUN(CRN_VARIANT_SCALED);
