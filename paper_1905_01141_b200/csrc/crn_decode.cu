@@ -79,6 +79,16 @@ constexpr int S_CRCNIB = S_WORDS;
 constexpr int S_OFFS = S_CRCNIB + 2 * CRN_CRC_NIB_WORDS;   /* int64 [4][2 MAXP]: bit_off, ext_off (current, next) */
 static_assert(S_OFFS % 2 == 0, "8-byte aligned");
 constexpr int SMEM_WORDS = S_OFFS + 4 * 2 * MAXP * 2;
+/* The CRC-ET and latency kernels keep the nibble tables with every window-
+ * distance table shifted by 4 banks (t1: 132-word stride, t2 / t3: 100): the
+ * lanes of a warp look up tables of 8 different distances at once, which with
+ * 128 / 96-word strides all start on the same bank (3-4 wavefronts per lookup) */
+constexpr int NIBP_T1 = 132, NIBP_T23 = 100, NIBP_O2 = 8 * NIBP_T1, NIBP_O3 = NIBP_O2 + 8 * NIBP_T23;
+constexpr int NIBP_KIND = NIBP_O3 + 3 * NIBP_T23;
+constexpr int S_OFFS_P = S_CRCNIB + 2 * NIBP_KIND;
+static_assert(S_OFFS_P % 2 == 0 && CRN_CRC_NIB_WORDS == 1024 + 768 + 288, "padded nibble-table layout");
+constexpr int SMEM_WORDS_P = S_OFFS_P + 4 * 2 * MAXP * 2;
+static_assert(SMEM_WORDS_P * 4 + 9728 <= 232448, "padded layout over the sm_100 opt-in limit");
 constexpr int YZ_END_BYTES = 4 * (S_Z + SUMK);     /* + static shared memory: must stay < 64 KiB */
 static_assert(SMEM_WORDS * 4 + 9728 <= 232448, "dynamic + static shared memory over the sm_100 opt-in limit");
 
@@ -1050,10 +1060,15 @@ __device__ __forceinline__ void run_task_fast(const crn_task &tk, const crn_cb_d
                 if (kind != CRN_CRC_NONE) {
                     /* CRC register contribution x^(32 d) R(w) mod g, d = M-1-j = 64a + 8b + c, as
                      * three nibble-table maps (crn_internal.h CRN_CRC_NIB_WORDS) */
-                    const u32 T = smem_addr(sh.crcnib) + (kind == CRN_CRC24A ? 0u : 4u * CRN_CRC_NIB_WORDS);
+                    constexpr bool PADNIB = ETC || ROLL;
+                    const u32 T = smem_addr(sh.crcnib) +
+                                  (kind == CRN_CRC24A ? 0u : 4u * (PADNIB ? NIBP_KIND : CRN_CRC_NIB_WORDS));
                     const u32 d = (u32)(M - 1 - j);
-                    const u32 t1 = T + (d & 7u) * 512u, t2 = T + 4096u + ((d >> 3) & 7u) * 384u,
-                              t3 = T + 7168u + (d >> 6) * 384u;         /* byte addresses of the three maps */
+                    const u32 t1 = PADNIB ? T + (d & 7u) * (4u * NIBP_T1) : T + (d & 7u) * 512u,
+                              t2 = PADNIB ? T + 4u * NIBP_O2 + ((d >> 3) & 7u) * (4u * NIBP_T23)
+                                          : T + 4096u + ((d >> 3) & 7u) * 384u,
+                              t3 = PADNIB ? T + 4u * NIBP_O3 + (d >> 6) * (4u * NIBP_T23)
+                                          : T + 7168u + (d >> 6) * 384u;   /* byte addresses of the three maps */
                     u32 r = 0, r2 = 0;
 #pragma unroll
                     for (int q = 0; q < 8; q++) r ^= lds_at(t1 + 64u * q + nib_off(w, q));
@@ -1526,12 +1541,23 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
     if (n_tasks < 0) n_tasks = ((const volatile int *)ws)[1];   /* built on the device (crn_tasks.cu) */
     const int tid = threadIdx.x;
     u32 *s_crcnib = smem + S_CRCNIB;
-    int64_t *s_bo = reinterpret_cast<int64_t *>(smem + S_OFFS), *s_eo = s_bo + 2 * MAXP, *s_nbo = s_eo + 2 * MAXP,
+    int64_t *s_bo = reinterpret_cast<int64_t *>(smem + ((ETC || ROLL) ? S_OFFS_P : S_OFFS)), *s_eo = s_bo + 2 * MAXP,
+            *s_nbo = s_eo + 2 * MAXP,
             *s_neo = s_nbo + 2 * MAXP;
     const TaskSh sh{s_crcnib, s_cb, s_F, s_kind, s_mi, s_mip, s_mitab, s_done, s_fin, s_crc, s_left, s_bo, s_eo};
     const Purge pg{s_tb, tb_dead};
     for (int i = tid; i < 256; i += BLOCK) s_mitab[i] = tab.mi_tab[i];
-    for (int i = tid; i < 2 * CRN_CRC_NIB_WORDS; i += BLOCK) s_crcnib[i] = tab.crc_nib[i];
+    if constexpr (ETC || ROLL) {
+        for (int i = tid; i < 2 * CRN_CRC_NIB_WORDS; i += BLOCK) {
+            const int k = i >= CRN_CRC_NIB_WORDS, r = i - k * CRN_CRC_NIB_WORDS;
+            const int dst = r < 1024 ? (r >> 7) * NIBP_T1 + (r & 127)
+                          : r < 1792 ? NIBP_O2 + (r - 1024) / 96 * NIBP_T23 + (r - 1024) % 96
+                                     : NIBP_O3 + (r - 1792) / 96 * NIBP_T23 + (r - 1792) % 96;
+            s_crcnib[k * NIBP_KIND + dst] = tab.crc_nib[i];
+        }
+    } else {
+        for (int i = tid; i < 2 * CRN_CRC_NIB_WORDS; i += BLOCK) s_crcnib[i] = tab.crc_nib[i];
+    }
 
     /* TMEM: the whole 512 columns (one CTA per SM: the shared-memory footprint guarantees it) */
     if ((tid >> 5) == 0) {
@@ -1708,6 +1734,7 @@ decode_kernel(const crn_cb_desc *__restrict__ desc, const crn_task *__restrict__
 }
 
 size_t smem_bytes() { return (size_t)SMEM_WORDS * 4; }
+size_t smem_bytes_p() { return (size_t)SMEM_WORDS_P * 4; }   /* CRC-ET and latency kernels */
 
 }  // namespace
 
@@ -1743,7 +1770,7 @@ extern "C" int crn_decode_grid(int device) {
     static int configured = -1;
     if (configured != device) {
         cudaError_t e = for_each_kernel([](const void *k) {
-            return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes());
+            return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes_p());
         });
         if (e != cudaSuccess) return -100 - (int)e;
         configured = device;
@@ -1761,7 +1788,7 @@ extern "C" int crn_decode_grid(int device) {
     if (bad) return -400;
     e = for_each_kernel([&](const void *k) {
         int occ = 0;
-        cudaError_t r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, BLOCK, smem_bytes());
+        cudaError_t r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, BLOCK, smem_bytes_p());
         if (r == cudaSuccess && occ != 1) bad = occ ? occ : -1;
         return r;
     });
@@ -1808,15 +1835,15 @@ extern "C" int crn_launch_decode(const crn_cb_desc *d_desc, const crn_task *d_ta
     const bool roll = !tb_dead && var != CRN_VARIANT_LOGMAP &&
                       (roll_env >= 0 ? roll_env == 1 : (n_tasks > 0 && n_tasks <= grid));
     if (roll) {
-        if (llr8) decode_kernel<false, true, CRN_VARIANT_MAXLOG, true><<<g, BLOCK, smem_bytes(), st>>>(
+        if (llr8) decode_kernel<false, true, CRN_VARIANT_MAXLOG, true><<<g, BLOCK, smem_bytes_p(), st>>>(
             d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits, ok, it, ext, *tab, (uint8_t *)ws,
             variant, nullptr);
-        else decode_kernel<false, false, CRN_VARIANT_MAXLOG, true><<<g, BLOCK, smem_bytes(), st>>>(
+        else decode_kernel<false, false, CRN_VARIANT_MAXLOG, true><<<g, BLOCK, smem_bytes_p(), st>>>(
             d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits, ok, it, ext, *tab, (uint8_t *)ws,
             variant, nullptr);
     } else if (!tb_dead && !llr8 && var != CRN_VARIANT_LOGMAP && et == CRN_ET_CRC) {
         /* CRC early termination, int16 LLRs: the kernel with the branch-free hard decision */
-        decode_kernel<false, false, CRN_VARIANT_MAXLOG, false, true><<<g, BLOCK, smem_bytes(), st>>>(
+        decode_kernel<false, false, CRN_VARIANT_MAXLOG, false, true><<<g, BLOCK, smem_bytes_p(), st>>>(
             d_desc, d_tasks, n_tasks, d_pairs, l0, l1, l2, max_iters, et, bits, ok, it, ext, *tab, (uint8_t *)ws,
             variant, nullptr);
     } else if (tb_dead) {
