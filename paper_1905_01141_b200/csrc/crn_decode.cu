@@ -1405,8 +1405,38 @@ __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_des
         u32 blo = 0, bhi = 0;
         int mlo = 0, mhi = 0;                   /* MI statistic (R29) */
         if (working) {                          /* TMEM loads are warp-collective: every lane of a working warp */
+            int s = 0;
+            if constexpr (TAG != 0) {
+                /* latency / CRC-ET kernels, CRC rule: eight steps per batch, their TMEM
+                 * statics (eight x1 loads, one wait) and shared loads all issued first */
+                if (et != CRN_ET_MI) {
+                    for (; s + 8 <= hw; s += 8) {
+                        u32 st8[8], lpv[8], yv[8], zv[8];
+#pragma unroll
+                        for (int u = 0; u < 8; u++)
+                            asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                                         : "=r"(st8[u]) : "r"(g.ts + s + u) : "memory");
+#pragma unroll
+                        for (int u = 0; u < 8; u++) {
+                            const int ix = (k0 + s + u) * Tp + t;
+                            lpv[u] = g.LP[ix];
+                            yv[u] = g.Y[ix];
+                            zv[u] = g.Z[g.Q[(s + u) * st2 + tid]];
+                        }
+                        tm_wait_ld8(st8);
+#pragma unroll
+                        for (int u = 0; u < 8; u++) {
+                            const int n = j * W + k0 + s + u;
+                            const u32 lapp = vadd(vadd(vadd(st8[u], lpv[u]), yv[u]), zv[u]);
+                            const u32 ge = __vcmpges2(lapp, 0u);
+                            blo |= (n < Flo ? 0u : (ge & 1u)) << (s + u);
+                            bhi |= (n < Fhi ? 0u : ((ge >> 16) & 1u)) << (s + u);
+                        }
+                    }
+                }
+            }
 #pragma unroll 1
-            for (int s = 0; s < hw; s++) {
+            for (; s < hw; s++) {
                 const int ix = (k0 + s) * Tp + t, n = j * W + k0 + s;
                 const u32 ls = vadd(tm_load1_wait(g.ts + s), g.LP[ix]);
                 const u32 lapp = vadd(vadd(ls, g.Y[ix]), g.Z[g.Q[s * st2 + tid]]);
@@ -1435,8 +1465,24 @@ __device__ __noinline__ void run_task_split(const crn_task &tk, const crn_cb_des
                 if (kind == CRN_CRC_NONE) continue;
                 const u32 *cb = cbit + (kind == CRN_CRC24A ? 0 : K) + k0 * M;
                 u32 acc = 0;
+                if constexpr (TAG != 0) {
+                    /* the latency / CRC-ET kernels: eight independent constant loads in
+                     * flight (one at a time, each waited for, this loop cost a lone task
+                     * ~2 x 30 L2 round trips per iteration) */
+                    int s = 0;
+                    for (; s + 8 <= hw; s += 8) {
+                        u32 v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; u++) v[u] = __ldg(cb + (s + u) * M);
+#pragma unroll
+                        for (int u = 0; u < 8; u++) acc ^= v[u] & (0u - ((b >> (s + u)) & 1u));
+                    }
+#pragma unroll 1
+                    for (; s < hw; s++) acc ^= __ldg(cb + s * M) & (0u - ((b >> s) & 1u));
+                } else {
 #pragma unroll 1
                 for (int s = 0; s < hw; s++) acc ^= __ldg(cb + s * M) & (0u - ((b >> s) & 1u));
+                }
                 atomicXor(&sh.crc[2 * p + l], acc);
             }
         }
