@@ -17,6 +17,7 @@
  *
  * Nothing here computes the method: all decoding runs in crn_decode.cu.
  */
+#include <cuda.h>            /* types of the one driver entry point used (cuStreamWriteValue32) */
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -75,6 +76,23 @@ void crn_pipe_destroy(HostPipe *p) {
     if (p->s_out) cudaStreamDestroy(p->s_out);
     if (p->mem) cudaFree(p->mem);
     delete p;
+}
+
+/* cuStreamWriteValue32 through the runtime's driver entry point (no -lcuda):
+ * the stream runner's completion flags (nullptr when unavailable) */
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WriteValue32Fn write_value32() {
+    static WriteValue32Fn fn = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            f = nullptr;
+        }
+        return (WriteValue32Fn)f;
+    }();
+    return fn;
 }
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -361,6 +379,35 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
     for (auto &e : ev_in) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     cudaEvent_t ev_dec = nullptr;
     if (merged) cudaEventCreateWithFlags(&ev_dec, cudaEventDisableTiming);
+    /* completion flags in pinned host memory, one per (TTI, group), written by the
+     * group's stream after its download (cuStreamWriteValue32): the completion
+     * thread spins on host memory instead of cudaEventQuery, whose driver lock the
+     * group threads' submissions would otherwise wait on.  Without the entry point
+     * (or CRN_STREAM_EVQ=1) the thread polls the events as before. */
+    static const bool evq_env = [] {
+        const char *e = getenv("CRN_STREAM_EVQ");
+        return e && e[0] == '1';
+    }();
+    WriteValue32Fn wv32 = evq_env || NG == 0 ? nullptr : write_value32();
+    uint32_t *hflag_mem = nullptr;
+    if (wv32 && cudaHostAlloc((void **)&hflag_mem, sizeof(uint32_t) * (size_t)(NG + 1), cudaHostAllocMapped) !=
+                    cudaSuccess) {
+        cudaGetLastError();
+        hflag_mem = nullptr;
+    }
+    if (hflag_mem) {                                /* probe once: stream memory operations usable? */
+        memset(hflag_mem, 0, sizeof(uint32_t) * (size_t)(NG + 1));
+        if (wv32((CUstream)G[0].st, (CUdeviceptr)(uintptr_t)(hflag_mem + NG), 1u, 0) != CUDA_SUCCESS ||
+            cudaStreamSynchronize(G[0].st) != cudaSuccess || ((volatile uint32_t *)hflag_mem)[NG] != 1u) {
+            cudaGetLastError();
+            cudaFreeHost(hflag_mem);
+            hflag_mem = nullptr;
+        }
+    }
+    volatile uint32_t *const hflag = hflag_mem;
+    auto signal_done = [&](int64_t x, cudaStream_t st) {      /* after the download, before ev1[x] */
+        if (hflag) wv32((CUstream)st, (CUdeviceptr)(uintptr_t)(hflag + x), 1u, 0);
+    };
     std::vector<double> done_us(NG, 0.0), rel_us(n_tti, 0.0), sub_us(n_tti, 0.0), gsub_us(NG, 0.0);
     std::vector<std::atomic<int>> submitted(n_groups);       /* per group: TTIs enqueued so far */
     for (auto &a : submitted) a.store(0);
@@ -378,10 +425,22 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
                 if (abort_flag.load()) return;
                 std::this_thread::yield();
             }
-            for (;;) {
-                cudaError_t q = cudaEventQuery(ev1[x]);
-                if (q == cudaSuccess) break;
-                if (q != cudaErrorNotReady || abort_flag.load()) return;
+            if (hflag) {
+                /* spin on host memory; an event query only every 64 k spins (a failed
+                 * stream never writes its flag) */
+                for (uint32_t n = 1; hflag[x] == 0u; n++) {
+                    if ((n & 0xFFFFu) == 0u) {
+                        cudaError_t q = cudaEventQuery(ev1[x]);
+                        if (q == cudaSuccess && hflag[x] == 0u) break;
+                        if ((q != cudaSuccess && q != cudaErrorNotReady) || abort_flag.load()) return;
+                    }
+                }
+            } else {
+                for (;;) {
+                    cudaError_t q = cudaEventQuery(ev1[x]);
+                    if (q == cudaSuccess) break;
+                    if (q != cudaErrorNotReady || abort_flag.load()) return;
+                }
             }
             done_us[x] = us_since(t0, Clock::now());
         }
@@ -397,6 +456,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
         for (auto &ev : ev_in) cudaEventDestroy(ev);
         if (ev_dec) cudaEventDestroy(ev_dec);
         cleanup();
+        if (hflag_mem) cudaFreeHost(hflag_mem);
         return CRN_ENOMEM;
     }
 
@@ -448,6 +508,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
                                        r.ctr + 64 * (size_t)ti, crn_decode_ws_bytes(t->grid), r.st, CRN_VARIANT_MAXLOG,
                                        nullptr, 0, true, units);
                 if (stages) cudaEventRecord(evk1[x], r.st);
+                signal_done(x, r.st);
                 cudaEventRecord(ev1[x], r.st);
                 gsub_us[x] = us_since(t0, Clock::now());
                 submitted[gi].store(ti + 1, std::memory_order_release);
@@ -490,7 +551,8 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             cudaEventRecord(evk0[x], r.st);
             cudaEventRecord(evk1[x], r.st);
         }
-        cudaEventRecord(ev1[x], r.st);
+        signal_done(x, r.st);
+                cudaEventRecord(ev1[x], r.st);
         gsub_us[x] = us_since(t0, Clock::now());
         submitted[gi].store(ti + 1, std::memory_order_release);
         return src;
@@ -609,6 +671,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
                     if (q.iters_used)
                         cudaMemcpyAsync(q.iters_used, dit + cbase[gi], (size_t)q.n_cb, cudaMemcpyDeviceToHost, r.st);
                 }
+                signal_done(x, r.st);
                 cudaEventRecord(ev1[x], r.st);
             }
             for (int gi = 0; gi < n_groups; gi++) submitted[gi].store(ti + 1, std::memory_order_release);
@@ -665,6 +728,7 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
     for (auto &ev : ev_in) cudaEventDestroy(ev);
     if (ev_dec) cudaEventDestroy(ev_dec);
     cleanup();
+    if (hflag_mem) cudaFreeHost(hflag_mem);
     return rc;
 }
 
