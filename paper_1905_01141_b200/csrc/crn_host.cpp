@@ -220,6 +220,21 @@ static uint32_t mulx_mod(uint32_t a, uint32_t poly) { return ((a << 1) ^ ((a & 0
 static int build_tables(int dev, DevTables **out) {
     auto it = g_tables.find(dev);
     if (it != g_tables.end()) { *out = &it->second; return CRN_OK; }
+    {   /* The one-shot batch calls take their descriptor uploads from the device's
+         * default stream-ordered pool (cudaMallocAsync).  With the pool's default
+         * release threshold of 0 every synchronisation hands the freed blocks back
+         * to the driver and the next call pays a fresh allocation (~0.2 ms); keep up
+         * to 256 MiB cached unless the application already asked for more. */
+        cudaMemPool_t mp;
+        uint64_t cur = 0;
+        const uint64_t want = 256ull << 20;
+        if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess &&
+            cudaMemPoolGetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &cur) == cudaSuccess && cur < want) {
+            uint64_t v = want;
+            cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &v);
+        }
+        cudaGetLastError();
+    }
     std::vector<uint32_t> qpp, qts, qin, qiw, cb;
     std::vector<int32_t> qoff(CRN_NUM_K), cboff(CRN_NUM_K);
     for (int ki = 0; ki < CRN_NUM_K; ki++) {

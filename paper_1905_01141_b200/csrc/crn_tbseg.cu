@@ -106,12 +106,32 @@ tbseg_kernel(const crn_tbseg *__restrict__ tbs, int n_tb, const uint8_t *__restr
         const int pad = (int)((32 - (B & 31)) & 31);             /* payload bit i at padded position pad + i */
         const int nwa = (int)((B + pad) >> 5);                    /* words of the padded payload */
         const uint8_t *src = payload + T.payload_off;
-        /* ---- pack: word k holds padded positions 32k..32k+31, MSB first */
-        for (int k = warp; k < nwa; k += SEG_THREADS / 32) {
-            const int64_t i = 32 * (int64_t)k + lane - pad;
-            const bool bit = i >= 0 && (__ldg(src + i) & 1u);
-            const uint32_t w = __ballot_sync(0xFFFFFFFFu, bit);   /* lane l -> bit l */
-            if (lane == 0) S.w[k] = __brev(w);
+        /* ---- pack: word k holds padded positions 32k..32k+31, MSB first.  A thread
+         * packs eight positions into one byte of S.w: two aligned 8-byte loads funnelled
+         * to the payload's byte alignment, the eight 0/1 bytes gathered into eight bits
+         * by one multiply (byte j -> bit 63 - j: no two products share a bit); the groups
+         * at the payload's two ends (positions before it, the last 15 bytes) bit by bit */
+        {
+            uint8_t *wb = reinterpret_cast<uint8_t *>(S.w);
+            const int ng = nwa * 4;
+            for (int q = tid; q < ng; q += SEG_THREADS) {
+                const int64_t i0 = 8 * (int64_t)q - pad;
+                uint32_t b8 = 0;
+                if (i0 >= 0 && i0 + 16 <= B) {
+                    const uintptr_t a = reinterpret_cast<uintptr_t>(src + i0);
+                    const unsigned long long *al = reinterpret_cast<const unsigned long long *>(a & ~(uintptr_t)7);
+                    const int sh = (int)(a & 7) * 8;
+                    const unsigned long long lo = __ldg(al), hi = __ldg(al + 1);
+                    const unsigned long long x = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+                    b8 = (uint32_t)(((x & 0x0101010101010101ull) * 0x8040201008040201ull) >> 56);
+                } else {
+                    for (int j = 0; j < 8; j++) {
+                        const int64_t i = i0 + j;
+                        if (i >= 0 && i < B && (__ldg(src + i) & 1u)) b8 |= 0x80u >> j;
+                    }
+                }
+                wb[q ^ 3] = (uint8_t)b8;                          /* word q/4, its bytes most significant first */
+            }
         }
         __syncthreads();
         /* ---- CRC24A over the padded payload */
@@ -137,6 +157,32 @@ tbseg_kernel(const crn_tbseg *__restrict__ tbs, int n_tb, const uint8_t *__restr
         const int C = T.C, Km = T.Kminus, Kp = T.Kplus, Cm = T.Cminus, F = T.F, L = T.L;
         const int64_t total = (int64_t)Cm * Km + (int64_t)(C - Cm) * Kp;
         uint8_t *dst = cb_bits + T.cb_bit0;
+        if ((reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+            /* K, L and every CB offset are multiples of 8: a thread writes eight bytes
+             * of one CB from eight bits of b (no per-byte division).  Positions before
+             * the payload (CB 0's fillers) read the zero front padding or fall before
+             * word 0 */
+            int64_t cb0 = 0;
+            for (int r = 0; r < C; r++) {
+                const int Kr = r < Cm ? Km : Kp, Fr = r == 0 ? F : 0;
+                const int64_t srcr = (r <= Cm ? (int64_t)r * (Km - L) : (int64_t)Cm * (Km - L) + (int64_t)(r - Cm) * (Kp - L))
+                                     - (r > 0 ? F : 0);
+                unsigned long long *d8 = reinterpret_cast<unsigned long long *>(dst + cb0);
+                for (int k8 = 8 * tid; k8 < Kr - L; k8 += 8 * SEG_THREADS) {
+                    const int64_t P = pad + srcr + (k8 - Fr);
+                    uint32_t b8;                                  /* positions P..P+7, first one in bit 7 */
+                    if (P >= 0) {
+                        const uint32_t hi = S.w[P >> 5], lo = S.w[(P >> 5) + 1];
+                        b8 = __funnelshift_l(lo, hi, (int)(P & 31)) >> 24;
+                    } else
+                        b8 = P > -8 ? (S.w[0] >> 24) >> (int)(-P) : 0u;
+                    const unsigned long long x = (unsigned long long)(__brev(b8) >> 24);      /* byte j's bit in bit j */
+                    const unsigned long long v = (x * 0x0101010101010101ull) & 0x8040201008040201ull;
+                    d8[k8 >> 3] = ((v + 0x7F7F7F7F7F7F7F7Full) >> 7) & 0x0101010101010101ull;
+                }
+                cb0 += Kr;
+            }
+        } else
         for (int64_t p = tid; p < total; p += SEG_THREADS) {
             int r, k;
             if (p < (int64_t)Cm * Km) { r = (int)(p / Km); k = (int)(p - (int64_t)r * Km); }

@@ -865,6 +865,16 @@ def test_tb_build_cbs_batch_matches_oracle(orc):
             word += (K + 31) // 32
             n += 1
     assert n == desc.size and got.size == bit
+    # a CB buffer that is not 8-byte aligned takes the kernel's byte-by-byte write
+    # path; payload bytes with their upper bits set count by bit 0 only (include/crn.h)
+    for shift in (1, 4):
+        raw = torch.full((got.size + 16,), 7, dtype=torch.uint8, device="cuda")
+        d2, cb2 = crn.tb_build_cbs_batch(np.array(tbs, np.int64), np.array(off, np.int64), payload | 0xFE,
+                                         cb_bits=raw[shift:shift + got.size + 8], max_cb=desc.size)
+        torch.cuda.synchronize()
+        assert np.array_equal(d2, desc) and np.array_equal(cb2.cpu().numpy(), got)
+        r = raw.cpu().numpy()
+        assert (r[:shift] == 7).all() and (r[shift + got.size:] == 7).all()
     with pytest.raises(crn.CrnError):
         crn.tb_build_cbs_batch(np.array([0], np.int64), np.array([0], np.int64), payload)
 
