@@ -380,7 +380,15 @@ int crn_tb_build_cbs(const uint8_t *tb_bits, int64_t tbs_bits, int32_t max_cb, i
  * 0, the bits of payload || CRC24A, and each CB's CRC24B when C > 1.  *n_cb
  * receives the CB count.  The segmentation arithmetic (O(1) per TB) runs on
  * the host; CRC24A, the bit placement and CRC24B run in one kernel (a CTA per
- * TB), asynchronously on cuda_stream.  CRN_EINVAL for n_tb < 0, tbs < 1, a
+ * TB), asynchronously on cuda_stream (the first call on a device builds the
+ * kernel's CRC tables and waits for them once).  The kernel writes cb_bits
+ * eight bytes at a time when cb_bits is 8-byte aligned, byte by byte otherwise
+ * (same result).  Like every one-shot batch call here (decode, encode, rate
+ * (de)matching) the descriptor upload comes from the device's default
+ * stream-ordered memory pool; the library raises that pool's release threshold
+ * to 256 MiB once per device (unless it is already higher) so that a
+ * synchronisation between calls does not return the blocks to the driver.
+ * CRN_EINVAL for n_tb < 0, tbs < 1, a
  * negative offset, more than max_cb CBs in total or a TB of more than
  * CRN_TB_MAX_CB CBs. */
 int crn_tb_build_cbs_batch(const int64_t *tbs_bits, const int64_t *payload_off, int32_t n_tb, const uint8_t *payload,

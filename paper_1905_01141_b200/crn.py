@@ -380,15 +380,16 @@ def tb_build_cbs_batch(tbs_bits, payload_off, payload, cb_bits=None, max_cb=None
         raise CrnError("tbs_bits and payload_off differ in length")
     if max_cb is None:
         max_cb = int(sum(segment_tb(int(x))["C"] for x in tb)) if tb.size else 0
-    desc = np.zeros(max(max_cb, 1), DESC_DTYPE)
+    desc = np.empty(max(max_cb, 1), DESC_DTYPE)          # the call writes every field of its n_cb records
     if cb_bits is None:
         cb_bits = torch.empty(max(max_cb, 1) * 6144, dtype=torch.uint8, device=payload.device)
     n = C.c_int32()
     _chk(lib().crn_tb_build_cbs_batch(_np(tb, C.c_int64), _np(po, C.c_int64), tb.size, _ptr(payload), max_cb,
                                       _ptr(cb_bits), desc.ctypes.data, C.byref(n), _stream(stream)),
          "crn_tb_build_cbs_batch")
-    desc = desc[:n.value].copy()
-    return desc, cb_bits[:int(desc["K"].sum())]
+    desc = desc[:n.value]                                # a view: copying a structured array goes field by field
+    n_bytes = int(desc["ext_off"][-1]) + int(desc["K"][-1]) if n.value else 0      # = sum K (dense layout)
+    return desc, cb_bits[:n_bytes]
 
 
 RM_DTYPE = np.dtype([("K", "<i4"), ("E", "<i4"), ("rv", "<i4"), ("reserved", "<i4"), ("e_off", "<i8"),

@@ -9,19 +9,22 @@
  *
  * with the segmentation (C, K+, K-, C-, F, L) from crn_segment_tb on the host
  * (O(1) per TB, like the decoder's bucketing).  One CTA per TB:
+ *   tables   the byte-table CRCs and x^(32 m) mod g: built once per device
+ *            (tbseg_init_kernel), copied into shared memory per CTA;
  *   pack     the payload (one bit per byte) into MSB-first words in shared
  *            memory, front-padded so it ends on a word boundary (leading zeros
- *            do not change a zero-initialised CRC), one coalesced ballot per word;
+ *            do not change a zero-initialised CRC), eight positions per thread;
  *   CRC24A   every thread runs the byte-table CRC over its run of words and
  *            multiplies its register by x^(32 m) mod g (m = words after the run,
  *            square-and-multiply over x^(32 2^k)), XOR-reduced over the CTA;
  *   CBs      all threads write the CB bytes (fillers, b's bits, the CRC24A bits
- *            for C = 1) coalesced;
+ *            for C = 1) coalesced, eight bytes per thread;
  *   CRC24B   a warp per CB: 32-bit segments of the CB's data aligned to its end,
  *            byte-table CRC each, times x^(32 m) (table), XOR-reduced by shuffles.
  * The CB contents are exactly crn_tb_build_cbs's (one bit per byte), ready for
  * crn_encode_batch. */
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include <mutex>
@@ -74,30 +77,43 @@ __device__ __forceinline__ uint32_t xpow32(const uint32_t *xp2, uint32_t m, uint
     return r;
 }
 
-__global__ void __launch_bounds__(SEG_THREADS)
-tbseg_kernel(const crn_tbseg *__restrict__ tbs, int n_tb, const uint8_t *__restrict__ payload,
-             uint8_t *__restrict__ cb_bits) {
-    extern __shared__ __align__(16) uint8_t seg_raw[];
-    SegSmem &S = *reinterpret_cast<SegSmem *>(seg_raw);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    /* per-CTA tables */
+/* SegSmem's leading tables (tab, xp2, xpb: one contiguous run of words), per device */
+constexpr int SEG_TAB_WORDS = 2 * 256 + 2 * XP_LOG + XPB_N;
+__device__ uint32_t g_seg_tab[SEG_TAB_WORDS];
+
+__global__ void __launch_bounds__(SEG_THREADS) tbseg_init_kernel() {
+    __shared__ uint32_t xp2[2][XP_LOG];
+    const int tid = threadIdx.x;
+    uint32_t *tab = g_seg_tab, *gxp2 = g_seg_tab + 2 * 256, *xpb = gxp2 + 2 * XP_LOG;
     for (int e = tid; e < 2 * 256; e += SEG_THREADS) {
         const uint32_t poly = (e >> 8) ? POLY_B : POLY_A;
         uint32_t reg = (uint32_t)(e & 255) << 16;
         for (int k = 0; k < 8; k++) reg = crc_step_bit(reg, poly);
-        S.tab[e >> 8][e & 255] = reg;
+        tab[e] = reg;
     }
     if (tid < 2) {
         const uint32_t poly = tid ? POLY_B : POLY_A;
         uint32_t r = 1;
         for (int k = 0; k < 32; k++) r = crc_step_bit(r, poly);     /* x^32 */
         for (int k = 0; k < XP_LOG; k++) {
-            S.xp2[tid][k] = r;
+            xp2[tid][k] = r;
+            gxp2[tid * XP_LOG + k] = r;
             r = mulmod24(r, r, poly);
         }
     }
     __syncthreads();
-    for (int m = tid; m < XPB_N; m += SEG_THREADS) S.xpb[m] = xpow32(S.xp2[1], (uint32_t)m, POLY_B);
+    for (int m = tid; m < XPB_N; m += SEG_THREADS) xpb[m] = xpow32(xp2[1], (uint32_t)m, POLY_B);
+}
+
+__global__ void __launch_bounds__(SEG_THREADS)
+tbseg_kernel(const crn_tbseg *__restrict__ tbs, int n_tb, const uint8_t *__restrict__ payload,
+             uint8_t *__restrict__ cb_bits) {
+    extern __shared__ __align__(16) uint8_t seg_raw[];
+    SegSmem &S = *reinterpret_cast<SegSmem *>(seg_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    /* the CRC tables: built once per device by tbseg_init_kernel, copied per CTA */
+    static_assert(offsetof(SegSmem, red) == 4 * SEG_TAB_WORDS, "tab, xp2, xpb lead SegSmem");
+    for (int e = tid; e < SEG_TAB_WORDS; e += SEG_THREADS) reinterpret_cast<uint32_t *>(seg_raw)[e] = g_seg_tab[e];
     __syncthreads();
 
     for (int t = blockIdx.x; t < n_tb; t += gridDim.x) {
@@ -253,6 +269,18 @@ extern "C" int crn_launch_tbseg(const crn_tbseg *d_tbs, int32_t n_tb, int64_t ma
                 cudaSuccess)
                 return CRN_ECUDA;
             attr_bytes = 227 * 1024;
+        }
+    }
+    {   /* first use on this device: build the tables and wait for them, so a later
+         * call on any other stream finds them complete */
+        static bool tab_ready[64] = {};
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev < 0 || dev >= 64) return CRN_EINVAL;
+        if (!tab_ready[dev]) {
+            tbseg_init_kernel<<<1, SEG_THREADS, 0, (cudaStream_t)stream>>>();
+            if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
+                return CRN_ECUDA;
+            tab_ready[dev] = true;
         }
     }
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
