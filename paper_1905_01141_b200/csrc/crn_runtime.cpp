@@ -475,6 +475,24 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
         int src = CRN_OK;
         cudaEventRecord(ev0[x], r.st);
         if (q.n_cb > 0) {
+            const int64_t n_llr = g_llr[x], n_words = g_words[x];
+            /* Offsets from the upper bound tasks, pairs <= CBs (the buffers are sized
+             * for it): known before the tasks are built, so the LLR upload -- most of
+             * the bytes -- is enqueued first and the host-side task building and blob
+             * assembly below overlap its DMA. */
+            const Layout L = layout(q.n_cb, q.n_cb, q.n_cb, n_llr, n_words, esz);
+            uint8_t *dm = (uint8_t *)r.dmem;
+            int16_t *dl[3];
+            for (int s = 0; s < 3; s++) dl[s] = (int16_t *)(dm + L.o_l + s * L.bl);
+            if (!zc) {
+                const uint8_t *hs[3] = {(const uint8_t *)q.llr_sys, (const uint8_t *)q.llr_p1,
+                                        (const uint8_t *)q.llr_p2};
+                const size_t sb = (size_t)esz * (size_t)n_llr;             /* bytes per stream */
+                if (hs[1] == hs[0] + sb && hs[2] == hs[1] + sb && L.bl == sb)
+                    cudaMemcpyAsync(dl[0], hs[0], 3 * sb, cudaMemcpyHostToDevice, r.st);
+                else                                            /* the three streams: one copy if contiguous */
+                    for (int s = 0; s < 3; s++) cudaMemcpyAsync(dl[s], hs[s], sb, cudaMemcpyHostToDevice, r.st);
+            }
             std::vector<crn_task> tasks;
             std::vector<crn_pair> pairs;
             std::vector<int> sel(q.n_cb);
@@ -482,8 +500,6 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
             /* the groups' kernels run concurrently: each spreads over its share of the SMs */
             const int units = crn_build_tasks(q.desc, sel.data(), q.n_cb, tasks, pairs,
                                               std::max(1, t->grid / n_groups));
-            const int64_t n_llr = g_llr[x], n_words = g_words[x];
-            const Layout L = layout(q.n_cb, (int)tasks.size(), (int)pairs.size(), n_llr, n_words, esz);
             const int b = ti & 1;
             if (ti >= 2) {                              /* blob slot b was last uploaded by TTI ti-2 */
                 const cudaEvent_t prev = ev1[x - 2 * (int64_t)n_groups];
@@ -514,16 +530,8 @@ extern "C" int crn_stream_run_ex(const crn_tti_group *g, int32_t n_tti, int32_t 
                 submitted[gi].store(ti + 1, std::memory_order_release);
                 return src;
             }
-            uint8_t *dm = (uint8_t *)r.dmem;
-            cudaMemcpyAsync(dm, hb, L.o_l, cudaMemcpyHostToDevice, r.st);
-            const uint8_t *hs[3] = {(const uint8_t *)q.llr_sys, (const uint8_t *)q.llr_p1, (const uint8_t *)q.llr_p2};
-            int16_t *dl[3];
-            for (int s = 0; s < 3; s++) dl[s] = (int16_t *)(dm + L.o_l + s * L.bl);
-            const size_t sb = (size_t)esz * (size_t)n_llr;             /* bytes per stream */
-            if (hs[1] == hs[0] + sb && hs[2] == hs[1] + sb && L.bl == sb)
-                cudaMemcpyAsync(dl[0], hs[0], 3 * sb, cudaMemcpyHostToDevice, r.st);
-            else                                            /* the three streams: one copy if contiguous */
-                for (int s = 0; s < 3; s++) cudaMemcpyAsync(dl[s], hs[s], sb, cudaMemcpyHostToDevice, r.st);
+            /* the blob: counter | descriptors | tasks | pairs, up to the last pair */
+            cudaMemcpyAsync(dm, hb, L.o_pairs + sizeof(crn_pair) * pairs.size(), cudaMemcpyHostToDevice, r.st);
             uint32_t *dbits = (uint32_t *)(dm + L.o_bits);
             uint8_t *dok = dm + L.o_ok, *dit = dm + L.o_it;
             if (stages) {
